@@ -1,0 +1,38 @@
+# Build every native artefact in-tree (the .so files travel to the GPU box with gpurun).
+#   make            all libraries
+#   make clean
+NVCC    ?= nvcc
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -v --expt-relaxed-constexpr
+CC      ?= gcc
+CXX     ?= g++
+
+PKG     := paper_2602_22103_b200
+CSRC    := $(PKG)/csrc
+PASTA_CU  := $(wildcard $(CSRC)/*.cu)
+PASTA_CPP := $(wildcard $(CSRC)/*.cpp)
+PASTA_H   := include/pasta.h $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h)
+
+LIBS := tracegen/libtracegen_host.so oracle/liboracle.so
+ifneq ($(PASTA_CU),)
+LIBS += $(PKG)/libpasta.so tracegen/libtracegen_dev.so
+endif
+
+all: $(LIBS)
+
+tracegen/libtracegen_host.so: tracegen/gen_host.c
+	$(CC) -O2 -std=c11 -fPIC -shared -o $@ $<
+
+tracegen/libtracegen_dev.so: tracegen/gen_dev.cu
+	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC -shared -o $@ $<
+
+oracle/liboracle.so: oracle/oracle.cpp
+	$(CXX) -O2 -std=c++17 -fPIC -shared -o $@ $<
+
+$(PKG)/libpasta.so: $(PASTA_CU) $(PASTA_CPP) $(PASTA_H)
+	$(NVCC) $(NVFLAGS) -Iinclude -I$(CSRC) -shared -o $@ $(PASTA_CU) $(PASTA_CPP) 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
+
+clean:
+	rm -f $(LIBS) build_ptxas.log
+
+.PHONY: all clean

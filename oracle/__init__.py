@@ -1,0 +1,169 @@
+"""oracle -- CPU oracle for the PASTA trace-analysis hot path (TEST INFRASTRUCTURE).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / ``--impl
+reference`` leg may import this package. It shares no code with the CUDA path
+(paper_2602_22103_b200/) and never imports it.
+
+``OracleTrace`` mirrors the handle semantics of include/pasta.h with its own plain
+Python registration bookkeeping (a dict of live ranges, linear overlap checks), and
+delegates the per-record definition to oracle/oracle.cpp (std::map lookup, hash-map
+counts, std::sort top-K). Everything is accumulated in
+numpy uint64 arrays.
+
+Status codes are the ones include/pasta.h documents (values restated, not imported).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+OK, EINVAL, EOVERLAP, ENOENT, ECAPACITY = 0, -1, -2, -3, -4
+U64MAX = (1 << 64) - 1
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_lib = None
+
+
+class _Range(ctypes.Structure):
+    _fields_ = [("base", ctypes.c_uint64), ("size", ctypes.c_uint64), ("id", ctypes.c_uint32),
+                ("pad", ctypes.c_uint32)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run `make` (or __graft_entry__.build())")
+        L = ctypes.CDLL(path)
+        vp, u64, u32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32
+        L.oracle_analyze.restype = ctypes.c_int
+        L.oracle_analyze.argtypes = [vp, u64, vp, u64, vp, u64, u64, u64, u32, u64, vp, vp, vp, vp, vp, vp]
+        L.oracle_bitmap.restype = u64
+        L.oracle_bitmap.argtypes = [vp, u64, vp]
+        L.oracle_footprint.restype = u64
+        L.oracle_footprint.argtypes = [vp, u64, u64, vp, vp]
+        L.oracle_row_popcount.restype = None
+        L.oracle_row_popcount.argtypes = [vp, u64, u64, vp]
+        L.oracle_topk.restype = u64
+        L.oracle_topk.argtypes = [vp, u64, u64, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+class OracleTrace:
+    """Oracle counterpart of a pasta_trace handle (include/pasta.h)."""
+
+    def __init__(self, va_lo: int, va_hi: int, max_live: int, max_ids: int):
+        self.va_lo, self.va_hi = int(va_lo), int(va_hi)
+        self.max_live, self.max_ids = int(max_live), int(max_ids)
+        self.live = {}  # base -> (size, id)
+        self.sizes = []  # id -> registered size (ids are never reused)
+        self.kernel_rows = None
+        self.kun = None
+        self.kernel_pages = None
+        self.page_counts = None
+        self.page_shift = None
+        self.alloc_counts = np.zeros(self.max_ids, dtype=np.uint64)
+        self.totals = np.zeros(3, dtype=np.uint64)  # records, unattributed, out_of_window
+
+    # ---- registration: snapshot semantics, SPEC S:53 (no live overlap), S:210 ----
+    def register_alloc(self, base: int, size: int):
+        base, size = int(base), int(size)
+        if size <= 0 or base < 0 or base + size > U64MAX:
+            return EINVAL, None
+        for b, (s, _) in self.live.items():
+            if base < b + s and b < base + size:  # half-open intervals intersect
+                return EOVERLAP, None
+        if len(self.live) >= self.max_live or len(self.sizes) >= self.max_ids:
+            return ECAPACITY, None
+        i = len(self.sizes)
+        self.sizes.append(size)
+        self.live[base] = (size, i)
+        return OK, i
+
+    def register_free(self, base: int):
+        if int(base) not in self.live:
+            return ENOENT
+        del self.live[int(base)]
+        return OK
+
+    # ---- one analyze call, accumulating ----
+    def analyze(self, addr: np.ndarray, kernel_offsets=None, page_shift: int = 12, kernel_rows: bool = False,
+                kernel_pages: bool = False):
+        addr = np.ascontiguousarray(addr, dtype=np.uint64)
+        n = addr.size
+        P = (self.va_hi - self.va_lo) >> page_shift
+        W = (P + 63) // 64
+        if self.page_counts is None or self.page_shift != page_shift:
+            self.page_counts = np.zeros(P, dtype=np.uint64)
+            self.page_shift = page_shift
+        if kernel_offsets is None:
+            ko = np.array([0, n], dtype=np.uint64)
+        else:
+            ko = np.ascontiguousarray(kernel_offsets, dtype=np.uint64)
+        nk = ko.size - 1
+        kac = kun = kp = None
+        if kernel_rows:
+            if self.kernel_rows is None or self.kernel_rows.shape != (nk, self.max_ids):
+                self.kernel_rows = np.zeros((nk, self.max_ids), dtype=np.uint64)
+                self.kun = np.zeros(nk, dtype=np.uint64)
+            kac, kun = self.kernel_rows, self.kun
+        if kernel_pages:
+            if self.kernel_pages is None or self.kernel_pages.shape != (nk, W):
+                self.kernel_pages = np.zeros((nk, W), dtype=np.uint64)
+            kp = self.kernel_pages
+        live = (_Range * max(1, len(self.live)))()
+        for i, (b, (s, idx)) in enumerate(sorted(self.live.items())):
+            live[i].base, live[i].size, live[i].id = b, s, idx
+        rc = lib().oracle_analyze(ctypes.addressof(live), len(self.live), _ptr(addr), n, _ptr(ko), nk,
+                                  self.va_lo, self.va_hi, page_shift, self.max_ids, _ptr(self.page_counts),
+                                  _ptr(self.alloc_counts), _ptr(self.totals), _ptr(kac), _ptr(kun), _ptr(kp))
+        if rc != 0:
+            raise ValueError(f"oracle_analyze rejected its input ({rc})")
+
+    # ---- derived results ----
+    def bitmap(self):
+        P = self.page_counts.size
+        bm = np.zeros((P + 63) // 64, dtype=np.uint64)
+        u = lib().oracle_bitmap(_ptr(self.page_counts), P, _ptr(bm))
+        return bm, int(u)
+
+    def footprints(self):
+        sizes = np.zeros(self.max_ids, dtype=np.uint64)
+        sizes[: len(self.sizes)] = self.sizes
+        nk = self.kernel_rows.shape[0]
+        fp = np.zeros(nk, dtype=np.uint64)
+        ws = lib().oracle_footprint(_ptr(self.kernel_rows), nk, self.max_ids, _ptr(sizes), _ptr(fp))
+        return fp, int(ws)
+
+    def kernel_unique_pages(self):
+        nk, W = self.kernel_pages.shape
+        out = np.zeros(nk, dtype=np.uint64)
+        lib().oracle_row_popcount(_ptr(self.kernel_pages), nk, W, _ptr(out))
+        return out
+
+    def topk(self, K: int):
+        return topk(self.page_counts, K)
+
+
+def topk(page_counts: np.ndarray, K: int):
+    """(pages[K], counts[K], found) ordered by (count desc, page asc) (R10)."""
+    pc = np.ascontiguousarray(page_counts, dtype=np.uint64)
+    pages = np.empty(K, dtype=np.uint64)
+    counts = np.empty(K, dtype=np.uint64)
+    found = lib().oracle_topk(_ptr(pc), pc.size, K, _ptr(pages), _ptr(counts))
+    return pages, counts, int(found)
+
+
+def bitmap(page_counts: np.ndarray):
+    pc = np.ascontiguousarray(page_counts, dtype=np.uint64)
+    bm = np.zeros((pc.size + 63) // 64, dtype=np.uint64)
+    u = lib().oracle_bitmap(_ptr(pc), pc.size, _ptr(bm))
+    return bm, int(u)

@@ -1,0 +1,197 @@
+// oracle/oracle.cpp -- the CPU ORACLE for the PASTA trace-analysis hot path.
+//
+// TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+// cpu_baseline / --impl reference leg may load this library. It shares no code,
+// header, table or helper with the CUDA path (paper_2602_22103_b200/), and neither
+// side includes or imports the other.
+//
+// It is the plain definition of what the method computes, written out step by step
+// in the order of SURVEY.md section 8(c) (std::map range lookup, hash-map counts,
+// std::set per-kernel pages, full std::sort for top-K). Integer counting only: the
+// method has no approximation, so the oracle is the definition itself.
+//
+// Paper passages followed (/root/reference/PAPER.md line numbers):
+//  * P:843-844 "a map from memory object to access count ... a profiling device
+//    function increments access count for each associated memory object upon each
+//    access ... objects with non-zero access counts are identified as part of the
+//    kernel's working set"                       -> alloc / per-kernel object counts
+//  * P:797-799 "associating memory access addresses with their corresponding
+//    objects, we can compute the memory footprint of each kernel. The maximum of
+//    these footprints across all kernels defines the working set size"
+//                                                -> footprint[k], WS_obj
+//  * P:795 working set = "maximum memory footprint of any single kernel execution"
+//  * P:916 "tracks access hotness over time in the unit of 2MB virtual memory
+//    blocks"                                     -> page histogram (s = 21; s = 12 too)
+//  * P:918-919 hot blocks are prefetch / cudaMemAdvise candidates -> top-K hot pages
+// Readings where the paper is silent are DESIGN.md "Readings" R1-R14.
+//
+// Parity status: every function below is pinned by tests/test_oracle_pins.py
+// (hand-worked golden trace, closed forms, invariants, brute force). None is
+// "parity unpinned".
+#include <algorithm>
+#include <cstdint>
+#include <map>
+#include <set>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+extern "C" {
+
+struct oracle_range {
+  uint64_t base;
+  uint64_t size;
+  uint32_t id;
+  uint32_t pad;
+};
+
+// One analyze call, accumulating (+=) into the caller's arrays.
+//   live[n_live]          registrations live at this call (snapshot semantics, R13)
+//   addr[n]               8-byte address records (R1); attribution by address only (R2)
+//   kernel_offsets        [n_kernels+1] CSR segments (R12); NULL => one kernel
+//   [va_lo, va_hi), s     page window (R7, R8)
+//   page_counts[P]        P = (va_hi - va_lo) >> s
+//   alloc_counts[max_ids] indexed by alloc id
+//   totals[3]             records, unattributed, out_of_window
+//   kac[n_kernels*max_ids], kun[n_kernels]             optional (NULL)
+//   kernel_pages[n_kernels*ceil(P/64)] (bits OR-ed in)  optional (NULL)
+// Returns 0, or -1 if an id is out of range or the offsets are inconsistent.
+int oracle_analyze(const oracle_range* live, uint64_t n_live, const uint64_t* addr, uint64_t n,
+                   const uint64_t* kernel_offsets, uint64_t n_kernels, uint64_t va_lo, uint64_t va_hi,
+                   uint32_t page_shift, uint64_t max_ids, uint64_t* page_counts, uint64_t* alloc_counts,
+                   uint64_t* totals, uint64_t* kac, uint64_t* kun, uint64_t* kernel_pages) {
+  // Step 1: std::map<base, (end, id)> from the live registrations.
+  std::map<uint64_t, std::pair<uint64_t, uint32_t>> ranges;
+  for (uint64_t i = 0; i < n_live; ++i) {
+    if (live[i].id >= max_ids) return -1;
+    ranges[live[i].base] = {live[i].base + live[i].size, live[i].id};
+  }
+  std::vector<uint64_t> offs;
+  if (kernel_offsets) {
+    offs.assign(kernel_offsets, kernel_offsets + n_kernels + 1);
+  } else {
+    n_kernels = 1;
+    offs = {0, n};
+  }
+  if (offs.front() != 0 || offs.back() != n) return -1;
+  for (uint64_t k = 0; k < n_kernels; ++k)
+    if (offs[k] > offs[k + 1]) return -1;
+
+  const uint64_t P = (va_hi - va_lo) >> page_shift;
+  const uint64_t W = (P + 63) / 64;
+  std::unordered_map<uint64_t, uint64_t> page;  // page index -> count (this call)
+  uint64_t unattributed = 0, oow = 0;
+
+  // Step 2: for each record j in kernel segment k.
+  for (uint64_t k = 0; k < n_kernels; ++k) {
+    std::set<uint64_t> kpages;  // pages touched by kernel k
+    for (uint64_t j = offs[k]; j < offs[k + 1]; ++j) {
+      const uint64_t a = addr[j];
+      // 2.1 owner: it = upper_bound(a); owner = prev(it) if a < prev(it).end.
+      bool owned = false;
+      uint32_t owner = 0;
+      auto it = ranges.upper_bound(a);
+      if (it != ranges.begin()) {
+        auto p = std::prev(it);
+        if (a < p->second.first) {
+          owned = true;
+          owner = p->second.second;
+        }
+      }
+      // 2.2 alloc / per-kernel counts, or the unattributed bins (R5).
+      if (owned) {
+        alloc_counts[owner] += 1;
+        if (kac) kac[k * max_ids + owner] += 1;
+      } else {
+        unattributed += 1;
+        if (kun) kun[k] += 1;
+      }
+      // 2.3 page histogram over the window (R7, R8).
+      if (va_lo <= a && a < va_hi) {
+        const uint64_t p = (a - va_lo) >> page_shift;
+        page[p] += 1;
+        kpages.insert(p);
+      } else {
+        oow += 1;
+      }
+    }
+    if (kernel_pages) {
+      for (uint64_t p : kpages) kernel_pages[k * W + p / 64] |= (uint64_t)1 << (p % 64);
+    }
+  }
+  // Step 3 (densify): add the hash-map counts into the dense page array.
+  for (const auto& kv : page) page_counts[kv.first] += kv.second;
+  totals[0] += n;
+  totals[1] += unattributed;
+  totals[2] += oow;
+  return 0;
+}
+
+// Step 3: bitmap bit p = page_counts[p] > 0 (R14: bit p%64 of word p/64, LSB
+// first, tail bits zero); returns unique_pages = number of set bits.
+uint64_t oracle_bitmap(const uint64_t* page_counts, uint64_t P, uint64_t* bitmap) {
+  const uint64_t W = (P + 63) / 64;
+  if (bitmap)
+    for (uint64_t w = 0; w < W; ++w) bitmap[w] = 0;
+  uint64_t unique = 0;
+  for (uint64_t p = 0; p < P; ++p) {
+    if (page_counts[p] > 0) {
+      unique += 1;
+      if (bitmap) bitmap[p / 64] |= (uint64_t)1 << (p % 64);
+    }
+  }
+  return unique;
+}
+
+// Step 3: footprint[k] = sum of size_i over ids with kac[k][i] > 0;
+// returns WS_obj = max_k footprint[k]. id_size[max_ids] = registered sizes.
+uint64_t oracle_footprint(const uint64_t* kac, uint64_t n_kernels, uint64_t max_ids, const uint64_t* id_size,
+                          uint64_t* footprint) {
+  uint64_t ws = 0;
+  for (uint64_t k = 0; k < n_kernels; ++k) {
+    uint64_t f = 0;
+    for (uint64_t i = 0; i < max_ids; ++i)
+      if (kac[k * max_ids + i] > 0) f += id_size[i];
+    if (footprint) footprint[k] = f;
+    ws = std::max(ws, f);
+  }
+  return ws;
+}
+
+// Per-kernel unique pages: |kpages[k]| = popcount of the kernel's bitmap row.
+void oracle_row_popcount(const uint64_t* rows, uint64_t n_rows, uint64_t W, uint64_t* out) {
+  for (uint64_t k = 0; k < n_rows; ++k) {
+    uint64_t c = 0;
+    for (uint64_t w = 0; w < W; ++w) {
+      uint64_t x = rows[k * W + w];
+      for (int b = 0; b < 64; ++b) c += (x >> b) & 1;
+    }
+    out[k] = c;
+  }
+}
+
+// Step 4: collect all (count, p) with count > 0, std::sort by (count desc, p asc),
+// take the first min(K, nnz) (R10). Slots [found, K) get (UINT64_MAX, 0).
+uint64_t oracle_topk(const uint64_t* page_counts, uint64_t P, uint64_t K, uint64_t* out_page,
+                     uint64_t* out_count) {
+  std::vector<std::pair<uint64_t, uint64_t>> v;  // (count, page)
+  for (uint64_t p = 0; p < P; ++p)
+    if (page_counts[p] > 0) v.push_back({page_counts[p], p});
+  std::sort(v.begin(), v.end(), [](const std::pair<uint64_t, uint64_t>& x, const std::pair<uint64_t, uint64_t>& y) {
+    if (x.first != y.first) return x.first > y.first;
+    return x.second < y.second;
+  });
+  const uint64_t found = std::min<uint64_t>(K, v.size());
+  for (uint64_t i = 0; i < K; ++i) {
+    if (i < found) {
+      out_page[i] = v[i].second;
+      out_count[i] = v[i].first;
+    } else {
+      out_page[i] = UINT64_MAX;
+      out_count[i] = 0;
+    }
+  }
+  return found;
+}
+
+}  // extern "C"
