@@ -1,0 +1,199 @@
+/* pasta.h -- C ABI of the B200-native PASTA trace-analysis hot path.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, arxiv 2602.22103):
+ *   "When a kernel is launched, a map from memory object to access count is
+ *    transferred to the GPU. During execution, a profiling device function
+ *    increments access count for each associated memory object upon each access.
+ *    When the kernel completes, the access count map is copied back to the CPU,
+ *    where objects with non-zero access counts are identified as part of the
+ *    kernel's working set."
+ *   working set = "the maximum memory footprint of any single kernel execution"
+ *
+ *   hotness "in the unit of 2MB virtual memory blocks"; hot blocks are prefetch /
+ *   cudaMemAdvise candidates
+ * Here the collected records sit in a device buffer ("the profiling library
+ * records the instruction into a device buffer. A helper device function then
+ * processes many of these events concurrently") and are reduced on the
+ * device into: per-page, per-allocation and per-kernel histograms, the unique-page
+ * bitmap with popcount, per-kernel footprints / working set, and the top-K hot
+ * pages. The readings R1-R14 that fix what the paper leaves open are listed in
+ * DESIGN.md ("Readings"); they are cited below as (Rn).
+ *
+ * Conventions for every call:
+ *   - returns an int status: PASTA_OK (0) or a negative PASTA_E* code; never
+ *     aborts, never throws, never prints;
+ *   - argument validation is synchronous and happens before anything is enqueued;
+ *     a failed call leaves the handle and every output unchanged;
+ *   - device work is asynchronous on the handle's stream (pasta_open_params.stream);
+ *     PASTA_ECUDA reports a launch or copy failure; asynchronous device faults
+ *     surface at the next call or at pasta_sync;
+ *   - "device pointer" = memory the handle's device can dereference (cudaMalloc /
+ *     torch CUDA tensors; pinned host memory also qualifies). The caller owns
+ *     records and outputs; the handle owns its range table and scratch.
+ *   - a handle is not thread-safe; several handles per device are fine.
+ */
+#ifndef PASTA_H
+#define PASTA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PASTA_OK = 0,
+  PASTA_EINVAL = -1,    /* bad argument (null, zero size, misaligned window, ...) */
+  PASTA_EOVERLAP = -2,  /* register_alloc intersects a live range (R4) */
+  PASTA_ENOENT = -3,    /* register_free of a base that is not live */
+  PASTA_ECAPACITY = -4, /* more than max_live live ranges or max_ids ids issued */
+  PASTA_ECUDA = -5,     /* CUDA runtime error (launch, copy, allocation, async fault) */
+  PASTA_ESTATE = -6,    /* call not valid in the handle's current state */
+  PASTA_ENOMEM = -7     /* host allocation failed */
+};
+
+/* Indices into the totals[PASTA_TOTALS] output array (u64 each). */
+enum {
+  PASTA_T_RECORDS = 0,       /* += n per analyze call                                   */
+  PASTA_T_UNATTRIBUTED = 1,  /* += records owned by no live range (R5)                  */
+  PASTA_T_OUT_OF_WINDOW = 2, /* += records outside [va_lo, va_hi) (R8)                  */
+  PASTA_T_UNIQUE_PAGES = 3,  /* = popcount(bitmap) (overwritten by finalize)            */
+  PASTA_T_WS_OBJ = 4,        /* = max_k footprint[k] in bytes (overwritten; R11) */
+  PASTA_TOTALS = 8           /* slots 5..7 reserved (left untouched)                    */
+};
+
+/* Per-kernel stats row: kernel_stats[k * PASTA_KSTATS + i]. */
+enum {
+  PASTA_K_ATTRIBUTED = 0,   /* += records of kernel k owned by some live range          */
+  PASTA_K_UNATTRIBUTED = 1, /* += records of kernel k owned by none                     */
+  PASTA_K_FOOTPRINT = 2,    /* = sum of registered sizes of ids with count > 0  */
+  PASTA_K_UNIQUE_PAGES = 3, /* = popcount of kernel k's page-bitmap row, 0 if absent    */
+  PASTA_KSTATS = 4
+};
+
+typedef struct pasta_trace pasta_trace; /* opaque; one per (process, device, window) */
+
+typedef struct {
+  int32_t device;     /* CUDA device ordinal the handle binds to                        */
+  uint32_t max_live;  /* range-table capacity (simultaneously live ranges), >= 1        */
+  uint32_t max_ids;   /* ids ever issued by this handle (= bins of alloc_counts), >= 1  */
+  uint32_t flags;     /* reserved, must be 0                                            */
+  uint64_t va_lo;     /* page window [va_lo, va_hi): multiples of 4 KiB, va_lo < va_hi  */
+  uint64_t va_hi;
+  uintptr_t stream;   /* cudaStream_t for all device work (0 = legacy default stream)   */
+  uint64_t host_chunk_bytes; /* staging chunk for PASTA_REC_HOST (0 = 256 MiB)          */
+} pasta_open_params;
+
+/* Input records. By default both arrays are DEVICE memory, read-only, never copied
+ * to the host. With PASTA_REC_HOST they are HOST memory (pinned for full speed):
+ * the library streams them to the device in chunks on an internal copy stream
+ * overlapped with the scan (the end-to-end path); the raw trace still never comes
+ * back. Record j is the 8-byte address of one access (R1, R2); segment k of the
+ * CSR offsets is kernel launch k (R12). */
+typedef struct {
+  const uint64_t* addr;           /* [n] records, 8-byte aligned                        */
+  const uint64_t* kernel_offsets; /* [n_kernels+1], o[0]=0, o[n_kernels]=n, non-decreasing;
+                                     NULL => one kernel. Device memory is not checked
+                                     (bad offsets mis-attribute, never write out of
+                                     bounds); host offsets are checked (EINVAL).       */
+  uint32_t n_kernels;
+  uint32_t flags;                 /* PASTA_REC_HOST */
+} pasta_records;
+
+enum { PASTA_REC_HOST = 1u };
+
+/* Outputs: caller-owned DEVICE memory (e.g. torch int64 tensors viewed as u64).
+ * Counts ACCUMULATE (+=) across calls, so a long trace can be analyzed in batches
+ * and shards can be merged by summation. P = (va_hi-va_lo) >> s,
+ * W = ceil(P/64). */
+typedef struct {
+  uint64_t* page_counts;         /* [P]           required  += (R7, R8)                */
+  uint64_t* alloc_counts;        /* [max_ids]     required  +=, indexed by alloc id   */
+  uint64_t* totals;              /* [PASTA_TOTALS] required (see PASTA_T_*)                    */
+  uint64_t* page_bitmap;         /* [W] optional, overwritten: bit p%64 of word p/64 = count>0 (R14) */
+  uint64_t* kernel_alloc_counts; /* [n_kernels*max_ids] optional, row-major +=   */
+  uint64_t* kernel_stats;        /* [n_kernels*PASTA_KSTATS] optional; needs kernel_alloc_counts */
+  uint64_t* kernel_page_bitmap;  /* [n_kernels*W] optional, OR-accumulated; needs kernel_alloc_counts */
+  uint32_t flags;                /* PASTA_NO_FINALIZE */
+  uint32_t reserved;
+} pasta_histograms;
+
+/* Skip the finalize step in pasta_analyze (bitmap, unique pages, footprints, WS);
+ * call pasta_finalize once at the end instead (streaming and multi-GPU merge). */
+enum { PASTA_NO_FINALIZE = 1u };
+
+/* Open a handle: binds to params->device, allocates the device range table for
+ * max_live ranges and max_ids ids. *out is set only on success. */
+int pasta_trace_open(const pasta_open_params* params, pasta_trace** out);
+
+/* Register a live allocation [base, base+size) (R3: half-open). size > 0 and
+ * base + size <= 2^64 - 1, else EINVAL; intersecting a live range => EOVERLAP
+ * (adjacent ranges are legal); ids are issued 0, 1, 2, ... and never reused; more
+ * than max_live live ranges or max_ids ids => ECAPACITY. Takes effect for the
+ * pasta_analyze calls enqueued after it (snapshot semantics, R13: "When a kernel is
+ * launched, a map ... is transferred to the GPU"). */
+int pasta_register_alloc(pasta_trace* h, uint64_t base, uint64_t size, uint32_t* out_id);
+
+/* Remove the live range whose base is exactly `base` (ENOENT otherwise). Its id's
+ * counts stay addressable; the id is never reissued. */
+int pasta_register_free(pasta_trace* h, uint64_t base);
+
+/* Analyze n records at page granularity 2^page_shift (12 <= page_shift <= 30;
+ * va_lo and va_hi must be multiples of 2^page_shift and P < 2^32). Steps, all on the
+ * device in one scan of the records (S1-S3 of DESIGN.md section 1):
+ *   owner(a) = the live range holding a, else unattributed          (R2-R5)
+ *   page_counts[(a - va_lo) >> s] += 1 if va_lo <= a < va_hi, else out_of_window
+ *   alloc_counts[id(owner)] += 1; kernel rows / stats per segment
+ *   kernel_page_bitmap[k] |= bit(page)
+ * then, unless PASTA_NO_FINALIZE, pasta_finalize. n = 0 is legal (finalize only). */
+int pasta_analyze(pasta_trace* h, const pasta_records* trace, uint64_t n, uint32_t page_shift,
+                  pasta_histograms* out);
+
+/* Recompute the derived outputs from the accumulated counts in `out`:
+ * page_bitmap (if non-NULL) and totals[UNIQUE_PAGES] from page_counts; for
+ * n_kernels rows (if kernel_alloc_counts and kernel_stats are non-NULL)
+ * footprint[k] = sum of registered sizes of ids with a non-zero count (P:797-799,
+ * P:844), totals[WS_OBJ] = max_k footprint[k], and unique pages per kernel
+ * from kernel_page_bitmap (if non-NULL). */
+int pasta_finalize(pasta_trace* h, uint32_t page_shift, uint32_t n_kernels, pasta_histograms* out);
+
+/* Top-K hot pages: the first min(k, nnz) pages with a non-zero count,
+ * ordered by count descending then page index ascending (R10). out_page[k],
+ * out_count[k] receive them; slots [found, k) get (UINT64_MAX, 0); *out_found =
+ * min(k, nnz). All three are device pointers (pinned host memory works for
+ * out_found). Radix select on the device; no host synchronization. k >= 1. */
+int pasta_topk(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t k, uint64_t* out_page,
+               uint64_t* out_count, uint64_t* out_found);
+
+/* Multi-GPU merge helper (OR of bitmaps): out_bitmap[w] =
+ * OR over r < g of gathered[r*words + w]; *out_popcount (device u64, may be NULL)
+ * = number of set bits. NCCL has no bitwise-OR reduction, so shards all_gather their
+ * bitmaps and OR them here. out_bitmap may alias gathered (r = 0 row). */
+int pasta_bitmap_or(pasta_trace* h, const uint64_t* gathered, uint32_t g, uint64_t words, uint64_t* out_bitmap,
+                    uint64_t* out_popcount);
+
+/* Block until the handle's stream is idle; reports asynchronous faults (ECUDA). */
+int pasta_sync(pasta_trace* h);
+
+/* Release the handle's device and host resources (synchronizes its stream first).
+ * pasta_close(NULL) is a no-op returning PASTA_OK. */
+int pasta_close(pasta_trace* h);
+
+/* Static string for a status code. */
+const char* pasta_strerror(int status);
+
+/* Instrumentation. With timing enabled every kernel the library launches is
+ * bracketed by CUDA events on the launching stream. pasta_get_timing synchronizes
+ * those events and returns accumulated milliseconds per phase
+ * (out_ms[PASTA_PHASES]) and the number of kernels launched since open (always
+ * counted). pasta_reset_timing zeroes both. */
+enum { PASTA_PH_SCAN = 0, PASTA_PH_FINALIZE = 1, PASTA_PH_TOPK = 2, PASTA_PH_MERGE = 3, PASTA_PH_COPY = 4,
+       PASTA_PHASES = 5 };
+int pasta_set_timing(pasta_trace* h, int enable);
+int pasta_get_timing(pasta_trace* h, double* out_ms, uint64_t* out_launches);
+int pasta_reset_timing(pasta_trace* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PASTA_H */

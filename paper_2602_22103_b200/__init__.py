@@ -1,0 +1,277 @@
+"""paper_2602_22103_b200 -- thin Python binding of the PASTA trace-analysis C ABI.
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels of
+libpasta.so (include/pasta.h). The functions keep the C names; ``PastaError`` is
+raised for a non-zero status. PyTorch supplies device memory and streams only.
+There is no CPU fallback: importing this package fails loudly if libpasta.so is
+missing, and opening a handle fails without a CUDA device.
+
+Convenience layer (still marshalling only):
+  * ``Histograms`` allocates the output arrays as views into ONE packed int64
+    device buffer ``[page_counts | alloc_counts | totals | ...]`` so the multi-GPU
+    merge is a single all_reduce (see .dist);
+  * ``Trace`` wraps a handle with register / analyze / topk methods.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libpasta.so")
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"{_LIB_PATH} is missing: build it with `make` or __graft_entry__.build() "
+                      "(there is no CPU fallback)")
+_lib = ctypes.CDLL(_LIB_PATH)
+
+PASTA_OK, PASTA_EINVAL, PASTA_EOVERLAP, PASTA_ENOENT, PASTA_ECAPACITY, PASTA_ECUDA, PASTA_ESTATE, PASTA_ENOMEM = (
+    0, -1, -2, -3, -4, -5, -6, -7)
+T_RECORDS, T_UNATTRIBUTED, T_OUT_OF_WINDOW, T_UNIQUE_PAGES, T_WS_OBJ, TOTALS = 0, 1, 2, 3, 4, 8
+K_ATTRIBUTED, K_UNATTRIBUTED, K_FOOTPRINT, K_UNIQUE_PAGES, KSTATS = 0, 1, 2, 3, 4
+PASTA_REC_HOST = 1
+PASTA_NO_FINALIZE = 1
+PH_SCAN, PH_FINALIZE, PH_TOPK, PH_MERGE, PH_COPY, PHASES = 0, 1, 2, 3, 4, 5
+PHASE_NAMES = ("scan", "finalize", "topk", "merge", "copy")
+
+
+class pasta_open_params(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("max_live", ctypes.c_uint32), ("max_ids", ctypes.c_uint32),
+                ("flags", ctypes.c_uint32), ("va_lo", ctypes.c_uint64), ("va_hi", ctypes.c_uint64),
+                ("stream", ctypes.c_void_p), ("host_chunk_bytes", ctypes.c_uint64)]
+
+
+class pasta_records(ctypes.Structure):
+    _fields_ = [("addr", ctypes.c_void_p), ("kernel_offsets", ctypes.c_void_p), ("n_kernels", ctypes.c_uint32),
+                ("flags", ctypes.c_uint32)]
+
+
+class pasta_histograms(ctypes.Structure):
+    _fields_ = [("page_counts", ctypes.c_void_p), ("alloc_counts", ctypes.c_void_p), ("totals", ctypes.c_void_p),
+                ("page_bitmap", ctypes.c_void_p), ("kernel_alloc_counts", ctypes.c_void_p),
+                ("kernel_stats", ctypes.c_void_p), ("kernel_page_bitmap", ctypes.c_void_p),
+                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+_vp, _u64, _u32, _int = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
+_SIGS = {
+    "pasta_trace_open": (_int, [ctypes.POINTER(pasta_open_params), ctypes.POINTER(_vp)]),
+    "pasta_register_alloc": (_int, [_vp, _u64, _u64, ctypes.POINTER(_u32)]),
+    "pasta_register_free": (_int, [_vp, _u64]),
+    "pasta_analyze": (_int, [_vp, ctypes.POINTER(pasta_records), _u64, _u32, ctypes.POINTER(pasta_histograms)]),
+    "pasta_finalize": (_int, [_vp, _u32, _u32, ctypes.POINTER(pasta_histograms)]),
+    "pasta_topk": (_int, [_vp, _vp, _u64, _u32, _vp, _vp, _vp]),
+    "pasta_bitmap_or": (_int, [_vp, _vp, _u32, _u64, _vp, _vp]),
+    "pasta_sync": (_int, [_vp]),
+    "pasta_close": (_int, [_vp]),
+    "pasta_strerror": (ctypes.c_char_p, [_int]),
+    "pasta_set_timing": (_int, [_vp, _int]),
+    "pasta_get_timing": (_int, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)]),
+    "pasta_reset_timing": (_int, [_vp]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_SIGS)
+
+
+class PastaError(RuntimeError):
+    def __init__(self, status, what=""):
+        self.status = status
+        super().__init__(f"{what}: {pasta_strerror(status)} ({status})")
+
+
+def _check(status, what):
+    if status != PASTA_OK:
+        raise PastaError(status, what)
+    return status
+
+
+def _ptr(t):
+    """Device (or host) address of a tensor / int / None."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+# ----------------------------- C-name functions -----------------------------
+def pasta_strerror(status: int) -> str:
+    return _lib.pasta_strerror(status).decode()
+
+
+def pasta_trace_open(device: int, va_lo: int, va_hi: int, max_live: int, max_ids: int, stream=0,
+                     host_chunk_bytes: int = 0):
+    p = pasta_open_params(device, max_live, max_ids, 0, va_lo, va_hi, ctypes.c_void_p(stream or 0), host_chunk_bytes)
+    h = ctypes.c_void_p()
+    _check(_lib.pasta_trace_open(ctypes.byref(p), ctypes.byref(h)), "pasta_trace_open")
+    return h
+
+
+def pasta_register_alloc(h, base: int, size: int) -> int:
+    out = _u32()
+    _check(_lib.pasta_register_alloc(h, base, size, ctypes.byref(out)), "pasta_register_alloc")
+    return out.value
+
+
+def pasta_register_free(h, base: int):
+    _check(_lib.pasta_register_free(h, base), "pasta_register_free")
+
+
+def pasta_analyze(h, addr, n: int, page_shift: int, hist, kernel_offsets=None, n_kernels: int = 0, flags: int = 0):
+    rec = pasta_records(_ptr(addr), _ptr(kernel_offsets), n_kernels, flags)
+    _check(_lib.pasta_analyze(h, ctypes.byref(rec), n, page_shift, ctypes.byref(hist)), "pasta_analyze")
+
+
+def pasta_finalize(h, page_shift: int, n_kernels: int, hist):
+    _check(_lib.pasta_finalize(h, page_shift, n_kernels, ctypes.byref(hist)), "pasta_finalize")
+
+
+def pasta_topk(h, page_counts, P: int, k: int, out_page, out_count, out_found):
+    _check(_lib.pasta_topk(h, _ptr(page_counts), P, k, _ptr(out_page), _ptr(out_count), _ptr(out_found)),
+           "pasta_topk")
+
+
+def pasta_bitmap_or(h, gathered, g: int, words: int, out_bitmap, out_popcount=None):
+    _check(_lib.pasta_bitmap_or(h, _ptr(gathered), g, words, _ptr(out_bitmap), _ptr(out_popcount)),
+           "pasta_bitmap_or")
+
+
+def pasta_sync(h):
+    _check(_lib.pasta_sync(h), "pasta_sync")
+
+
+def pasta_close(h):
+    _check(_lib.pasta_close(h), "pasta_close")
+
+
+def pasta_set_timing(h, enable: bool):
+    _check(_lib.pasta_set_timing(h, 1 if enable else 0), "pasta_set_timing")
+
+
+def pasta_get_timing(h):
+    ms = (ctypes.c_double * PHASES)()
+    n = _u64()
+    _check(_lib.pasta_get_timing(h, ms, ctypes.byref(n)), "pasta_get_timing")
+    return dict(zip(PHASE_NAMES, list(ms))), n.value
+
+
+def pasta_reset_timing(h):
+    _check(_lib.pasta_reset_timing(h), "pasta_reset_timing")
+
+
+# ----------------------------- convenience layer -----------------------------
+class Histograms:
+    """Output arrays as int64 CUDA tensors (u64 bit patterns).
+
+    ``packed`` = [page_counts (P) | alloc_counts (max_ids) | totals (8)] is one buffer,
+    so the merge across ranks is one all_reduce(SUM). Per-kernel
+    arrays and the bitmap are separate tensors."""
+
+    def __init__(self, P: int, max_ids: int, device, n_kernels: int = 0, kernel_rows: bool = False,
+                 kernel_pages: bool = False, bitmap: bool = True):
+        import torch
+
+        self.P, self.max_ids, self.n_kernels = P, max_ids, n_kernels
+        self.words = (P + 63) // 64
+        self.packed = torch.zeros(P + max_ids + TOTALS, dtype=torch.int64, device=device)
+        self.page_counts = self.packed[:P]
+        self.alloc_counts = self.packed[P:P + max_ids]
+        self.totals = self.packed[P + max_ids:]
+        self.page_bitmap = torch.zeros(self.words, dtype=torch.int64, device=device) if bitmap else None
+        self.kernel_alloc_counts = self.kernel_stats = self.kernel_page_bitmap = None
+        if kernel_rows:
+            self.kernel_alloc_counts = torch.zeros(n_kernels * max_ids, dtype=torch.int64, device=device)
+            self.kernel_stats = torch.zeros(n_kernels * KSTATS, dtype=torch.int64, device=device)
+        if kernel_pages:
+            self.kernel_page_bitmap = torch.zeros(n_kernels * self.words, dtype=torch.int64, device=device)
+
+    def zero_(self):
+        for t in (self.packed, self.page_bitmap, self.kernel_alloc_counts, self.kernel_stats,
+                  self.kernel_page_bitmap):
+            if t is not None:
+                t.zero_()
+        return self
+
+    def struct(self, flags: int = 0) -> pasta_histograms:
+        return pasta_histograms(_ptr(self.page_counts), _ptr(self.alloc_counts), _ptr(self.totals),
+                                _ptr(self.page_bitmap), _ptr(self.kernel_alloc_counts), _ptr(self.kernel_stats),
+                                _ptr(self.kernel_page_bitmap), flags, 0)
+
+
+class Trace:
+    """A pasta_trace handle bound to one CUDA device and stream."""
+
+    def __init__(self, device, va_lo: int, va_hi: int, max_live: int, max_ids: int, stream=None,
+                 host_chunk_bytes: int = 0):
+        import torch
+
+        self.device = torch.device(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        self.va_lo, self.va_hi, self.max_live, self.max_ids = va_lo, va_hi, max_live, max_ids
+        self.h = pasta_trace_open(self.device.index or 0, va_lo, va_hi, max_live, max_ids, stream.cuda_stream,
+                                  host_chunk_bytes)
+
+    def n_pages(self, page_shift: int) -> int:
+        return (self.va_hi - self.va_lo) >> page_shift
+
+    def register_alloc(self, base: int, size: int) -> int:
+        return pasta_register_alloc(self.h, base, size)
+
+    def register_free(self, base: int):
+        pasta_register_free(self.h, base)
+
+    def histograms(self, page_shift: int, n_kernels: int = 0, kernel_rows=False, kernel_pages=False, bitmap=True):
+        return Histograms(self.n_pages(page_shift), self.max_ids, self.device, n_kernels, kernel_rows, kernel_pages,
+                          bitmap)
+
+    def analyze(self, records, page_shift: int, hist: Histograms, kernel_offsets=None, n: int | None = None,
+                finalize: bool = True, host: bool = False):
+        if n is None:
+            n = records.numel()
+        nk = 0 if kernel_offsets is None else kernel_offsets.numel() - 1
+        pasta_analyze(self.h, records, n, page_shift, hist.struct(0 if finalize else PASTA_NO_FINALIZE),
+                      kernel_offsets, nk, PASTA_REC_HOST if host else 0)
+
+    def finalize(self, page_shift: int, hist: Histograms, n_kernels: int = 0):
+        pasta_finalize(self.h, page_shift, n_kernels, hist.struct())
+
+    def topk(self, page_counts, k: int, out=None):
+        import torch
+
+        if out is None:
+            out = (torch.empty(k, dtype=torch.int64, device=self.device),
+                   torch.empty(k, dtype=torch.int64, device=self.device),
+                   torch.empty(1, dtype=torch.int64, device=self.device))
+        pasta_topk(self.h, page_counts, page_counts.numel(), k, out[0], out[1], out[2])
+        return out
+
+    def bitmap_or(self, gathered, g: int, words: int, out_bitmap, out_popcount=None):
+        pasta_bitmap_or(self.h, gathered, g, words, out_bitmap, out_popcount)
+
+    def sync(self):
+        pasta_sync(self.h)
+
+    def set_timing(self, on: bool):
+        pasta_set_timing(self.h, on)
+
+    def timing(self):
+        return pasta_get_timing(self.h)
+
+    def reset_timing(self):
+        pasta_reset_timing(self.h)
+
+    def close(self):
+        if self.h is not None:
+            pasta_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

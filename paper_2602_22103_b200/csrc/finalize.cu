@@ -1,0 +1,144 @@
+// finalize.cu -- S3: unique-page bitmap + popcount, per-kernel footprint / WS, and
+// the bitmap OR used by the multi-GPU merge (DESIGN.md sections 3-5).
+//
+//  * bitmap: one warp per 64 pages: two coalesced 8-byte loads per lane, two
+//    __ballot_sync(count != 0) make the 64-bit word (low half = first 32 pages), lane
+//    0 stores it and adds __popcll; block reduce, one atomicAdd per block into
+//    totals[UNIQUE_PAGES] (P:795 working set by pages, north star part 3; R14).
+//  * footprint: one warp per kernel row: sum of registered sizes over ids with a
+//    non-zero count; atomicMax of the rows into totals[WS_OBJ]
+//    (P:795); the row's page-bitmap popcount (per-kernel unique pages).
+#include <cstdint>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace pasta {
+namespace {
+
+using namespace dev;
+
+constexpr int kBlock = 256;
+
+__global__ void __launch_bounds__(kBlock) bitmap_kernel(const uint64_t* __restrict__ pc, uint64_t P,
+                                                        uint64_t* __restrict__ bitmap,
+                                                        uint64_t* __restrict__ unique_out) {
+  __shared__ uint64_t part[kBlock / 32];
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t W = (P + 63) / 64;
+  const uint64_t gw = (uint64_t)blockIdx.x * (kBlock / 32) + wib;
+  const uint64_t nw = (uint64_t)gridDim.x * (kBlock / 32);
+  uint64_t local = 0;
+  for (uint64_t w = gw; w < W; w += nw) {
+    const uint64_t p0 = 64 * w + lane, p1 = p0 + 32;
+    const uint64_t c0 = p0 < P ? __ldg(pc + p0) : 0;
+    const uint64_t c1 = p1 < P ? __ldg(pc + p1) : 0;
+    const unsigned b0 = __ballot_sync(kFull, c0 != 0);
+    const unsigned b1 = __ballot_sync(kFull, c1 != 0);
+    if (lane == 0) {
+      const uint64_t word = (uint64_t)b0 | ((uint64_t)b1 << 32);
+      if (bitmap) bitmap[w] = word;
+      local += __popcll(word);
+    }
+  }
+  if (lane == 0) part[wib] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t s = 0;
+    for (int i = 0; i < kBlock / 32; ++i) s += part[i];
+    if (s) red_add_u64(unique_out, s);
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) footprint_kernel(const uint64_t* __restrict__ kac, uint32_t K,
+                                                           uint64_t max_ids, const uint64_t* __restrict__ id_size,
+                                                           const uint64_t* __restrict__ kpb, uint32_t words,
+                                                           uint64_t* __restrict__ kstats,
+                                                           uint64_t* __restrict__ ws_out) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t gw = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * kBlock) >> 5;
+  uint64_t wmax = 0;
+  for (uint64_t k = gw; k < K; k += nw) {
+    const uint64_t* row = kac + k * max_ids;
+    uint64_t f = 0;
+    for (uint64_t i = lane; i < max_ids; i += 32)
+      if (__ldg(row + i) != 0) f += __ldg(id_size + i);
+    f = warp_sum_u64(f);
+    uint64_t up = 0;
+    if (kpb) {
+      const uint64_t* brow = kpb + k * words;
+      for (uint64_t w = lane; w < words; w += 32) up += __popcll(__ldg(brow + w));
+      up = warp_sum_u64(up);
+    }
+    if (lane == 0) {
+      kstats[k * 4 + 2] = f;
+      kstats[k * 4 + 3] = up;
+    }
+    wmax = f > wmax ? f : wmax;
+  }
+  if (lane == 0 && wmax) atomic_max_u64(ws_out, wmax);
+}
+
+__global__ void __launch_bounds__(kBlock) bitmap_or_kernel(const uint64_t* gathered, uint32_t g,
+                                                           uint64_t words, uint64_t* out, uint64_t* popcount) {
+  __shared__ uint64_t part[kBlock / 32];
+  const uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+  const uint64_t nt = (uint64_t)gridDim.x * kBlock;
+  uint64_t local = 0;
+  for (uint64_t w = tid; w < words; w += nt) {
+    uint64_t x = 0;
+    for (uint32_t r = 0; r < g; ++r) x |= gathered[(uint64_t)r * words + w];
+    out[w] = x;
+    local += __popcll(x);
+  }
+  if (!popcount) return;
+  local = warp_sum_u64(local);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t s = 0;
+    for (int i = 0; i < kBlock / 32; ++i) s += part[i];
+    if (s) red_add_u64(popcount, s);
+  }
+}
+
+int grid_for(uint64_t items, int per_block, int max_grid) {
+  uint64_t b = (items + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  if (b > (uint64_t)max_grid) b = max_grid;
+  return (int)b;
+}
+
+}  // namespace
+
+cudaError_t launch_finalize_bitmap(const uint64_t* page_counts, uint64_t P, uint64_t* bitmap, uint64_t* unique_out,
+                                   int grid, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(unique_out, 0, sizeof(uint64_t), st);
+  if (e != cudaSuccess) return e;
+  const uint64_t W = (P + 63) / 64;
+  bitmap_kernel<<<grid_for(W, kBlock / 32, grid), kBlock, 0, st>>>(page_counts, P, bitmap, unique_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_footprint(const uint64_t* kac, uint32_t n_kernels, uint64_t max_ids, const uint64_t* id_size,
+                             const uint64_t* kpb, uint32_t words, uint64_t* kstats, uint64_t* ws_out, int grid,
+                             cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(ws_out, 0, sizeof(uint64_t), st);
+  if (e != cudaSuccess) return e;
+  footprint_kernel<<<grid_for(n_kernels, kBlock / 32, grid), kBlock, 0, st>>>(kac, n_kernels, max_ids, id_size, kpb,
+                                                                             words, kstats, ws_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bitmap_or(const uint64_t* gathered, uint32_t g, uint64_t words, uint64_t* out,
+                             uint64_t* popcount, int grid, cudaStream_t st) {
+  if (popcount) {
+    cudaError_t e = cudaMemsetAsync(popcount, 0, sizeof(uint64_t), st);
+    if (e != cudaSuccess) return e;
+  }
+  bitmap_or_kernel<<<grid_for(words, kBlock, grid), kBlock, 0, st>>>(gathered, g, words, out, popcount);
+  return cudaGetLastError();
+}
+
+}  // namespace pasta

@@ -1,0 +1,63 @@
+// internal.h -- structures shared by the host library (pasta.cpp) and the kernel
+// launchers (*.cu). Not part of the C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pasta {
+
+constexpr uint32_t kOOW = 0xFFFFFFFFu;  // page index sentinel: outside the window
+
+// Everything the fused scan needs.
+struct ScanArgs {
+  const uint64_t* rec;       // body records (16-byte aligned), rec[0] has global index gidx0
+  uint64_t nbody;            // even count of body records
+  uint64_t gidx0;            // global record index of rec[0] (for kernel offsets)
+  const uint64_t* bounds;    // [2A] sorted boundary array of the live ranges
+  const uint32_t* ids;       // [A] alloc id of live range r
+  uint32_t A;                // live ranges
+  uint32_t n_kernels;        // >= 1
+  const uint64_t* koffs;     // [n_kernels+1] or nullptr (one kernel)
+  uint64_t va_lo, va_hi;
+  uint32_t page_shift;
+  uint32_t words;            // ceil(P/64) (kernel page bitmap row length)
+  uint64_t max_ids;
+  uint64_t* page_counts;
+  uint64_t* alloc_counts;
+  uint64_t* totals;
+  uint64_t* kac;             // kernel_alloc_counts or nullptr
+  uint64_t* kstats;          // kernel_stats or nullptr
+  uint64_t* kpb;             // kernel_page_bitmap or nullptr
+  uint64_t add_records;      // added to totals[RECORDS] by block 0
+};
+
+// Extra records that are not part of the 16-byte aligned even body (<= 2).
+struct ExtraArgs {
+  ScanArgs s;
+  const uint64_t* ex_ptr[2];
+  uint64_t ex_gidx[2];
+  int n_ex;
+};
+
+int scan_smem_bytes(uint32_t A, bool big_table);
+cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_scan_extras(const ExtraArgs& a, cudaStream_t st);
+bool scan_table_fits_smem(uint32_t A);
+
+cudaError_t launch_finalize_bitmap(const uint64_t* page_counts, uint64_t P, uint64_t* bitmap, uint64_t* unique_out,
+                                   int grid, cudaStream_t st);
+cudaError_t launch_footprint(const uint64_t* kac, uint32_t n_kernels, uint64_t max_ids, const uint64_t* id_size,
+                             const uint64_t* kpb, uint32_t words, uint64_t* kstats, uint64_t* ws_out, int grid,
+                             cudaStream_t st);
+cudaError_t launch_bitmap_or(const uint64_t* gathered, uint32_t g, uint64_t words, uint64_t* out,
+                             uint64_t* popcount, int grid, cudaStream_t st);
+
+// Top-K scratch layout (device), sized by topk_scratch_bytes(k, grid).
+size_t topk_scratch_bytes(uint64_t k, int grid);
+// Enqueues the whole radix-select + gather + sort pipeline; `launch` is called once
+// per kernel launch with the phase's cudaError_t (for counting / timing hooks).
+typedef void (*launch_hook)(void* ctx, int begin);
+cudaError_t run_topk(const uint64_t* page_counts, uint64_t P, uint32_t k, uint64_t* out_page, uint64_t* out_count,
+                     uint64_t* out_found, void* scratch, int grid, cudaStream_t st, int* n_launches);
+
+}  // namespace pasta

@@ -1,0 +1,554 @@
+// pasta.cpp -- host side of the C ABI (include/pasta.h): handle, range table,
+// argument validation, stream-ordered table upload, kernel launches, the host-record
+// (end-to-end) streaming path and instrumentation.
+//
+// The range table is the paper's "map from memory object to access count ...
+// transferred to the GPU" when a kernel is launched: registrations edit a
+// host std::map; the next pasta_analyze uploads the sorted boundary array
+// B = [base_0, end_0, base_1, end_1, ...] and the range -> id map on the handle's
+// stream (snapshot semantics, R13), so every enqueued call sees the table as it was
+// when it was enqueued.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <new>
+#include <vector>
+
+#include "internal.h"
+#include "pasta.h"
+
+using namespace pasta;
+
+struct TimedLaunch {
+  int phase;
+  cudaEvent_t a, b;
+};
+
+struct pasta_trace {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  uint64_t va_lo = 0, va_hi = 0;
+  uint32_t max_live = 0, max_ids = 0;
+  int sm_count = 148;
+
+  // host registration state
+  std::map<uint64_t, std::pair<uint64_t, uint32_t>> live;  // base -> (size, id)
+  std::vector<uint64_t> id_size;                           // id -> registered size
+  bool dirty = true;
+
+  // device table (capacity max_live / max_ids)
+  uint64_t* d_bounds = nullptr;  // [2*max_live]
+  uint32_t* d_ids = nullptr;     // [max_live]
+  uint64_t* d_id_size = nullptr; // [max_ids]
+  uint32_t A_dev = 0;            // live ranges in the most recently enqueued table
+  unsigned char* h_stage = nullptr;  // pinned staging for table uploads
+  size_t h_stage_bytes = 0;
+  cudaEvent_t upload_done = nullptr;
+  bool upload_pending = false;
+
+  // top-K scratch
+  void* d_topk = nullptr;
+  size_t topk_bytes = 0;
+
+  // host-record streaming path
+  uint64_t host_chunk_bytes = 256ull << 20;
+  uint64_t* d_stage[2] = {nullptr, nullptr};
+  uint64_t* d_koffs = nullptr;
+  size_t d_koffs_cap = 0;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+  cudaEvent_t ev_consumed[2] = {nullptr, nullptr};
+
+  // instrumentation
+  bool timing = false;
+  std::vector<TimedLaunch> pending;
+  std::vector<cudaEvent_t> free_events;
+  double ms[PASTA_PHASES] = {0, 0, 0, 0, 0};
+  uint64_t launches = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+cudaEvent_t take_event(pasta_trace* h) {
+  if (!h->free_events.empty()) {
+    cudaEvent_t e = h->free_events.back();
+    h->free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets device work of one phase with events when timing is on.
+struct Timed {
+  pasta_trace* h;
+  int phase;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  Timed(pasta_trace* h_, int ph, cudaStream_t s) : h(h_), phase(ph), st(s) {
+    if (h->timing) {
+      a = take_event(h);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~Timed() {
+    if (h->timing && a) {
+      cudaEvent_t b = take_event(h);
+      cudaEventRecord(b, st);
+      h->pending.push_back({phase, a, b});
+    }
+  }
+};
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? PASTA_OK : PASTA_ECUDA; }
+
+// Upload the current registration table if it changed (stream-ordered).
+int upload_table(pasta_trace* h) {
+  if (!h->dirty) return PASTA_OK;
+  const uint32_t A = (uint32_t)h->live.size();
+  const size_t nid = h->id_size.size();
+  const size_t need = 16ull * A + 4ull * A + 8ull * nid + 64;
+  if (h->upload_pending) {
+    // the previous upload must have left the staging buffer before we overwrite it
+    if (cudaEventSynchronize(h->upload_done) != cudaSuccess) return PASTA_ECUDA;
+    h->upload_pending = false;
+  }
+  if (need > h->h_stage_bytes) {
+    if (h->h_stage) cudaFreeHost(h->h_stage);
+    h->h_stage = nullptr;
+    size_t cap = std::max<size_t>(need, 4096);
+    if (cudaMallocHost(&h->h_stage, cap) != cudaSuccess) {
+      h->h_stage_bytes = 0;
+      return PASTA_ECUDA;
+    }
+    h->h_stage_bytes = cap;
+  }
+  uint64_t* hb = reinterpret_cast<uint64_t*>(h->h_stage);
+  uint64_t* hs = hb + 2ull * A;
+  uint32_t* hi = reinterpret_cast<uint32_t*>(hs + nid);
+  uint32_t r = 0;
+  for (const auto& kv : h->live) {  // std::map iterates in ascending base order
+    hb[2 * r] = kv.first;
+    hb[2 * r + 1] = kv.first + kv.second.first;
+    hi[r] = kv.second.second;
+    ++r;
+  }
+  for (size_t i = 0; i < nid; ++i) hs[i] = h->id_size[i];
+  cudaError_t e = cudaSuccess;
+  if (A) e = cudaMemcpyAsync(h->d_bounds, hb, 16ull * A, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess && A) e = cudaMemcpyAsync(h->d_ids, hi, 4ull * A, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess && nid) e = cudaMemcpyAsync(h->d_id_size, hs, 8ull * nid, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaEventRecord(h->upload_done, h->stream);
+  if (e != cudaSuccess) return PASTA_ECUDA;
+  h->upload_pending = true;
+  h->A_dev = A;
+  h->dirty = false;
+  return PASTA_OK;
+}
+
+bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7u) == 0; }
+
+// Launch the scan over records [j0, j0 + n) that live at `rec` (device), with global
+// record indices starting at g0 (for kernel offsets). add_records is added once.
+int scan_range(pasta_trace* h, const uint64_t* rec, uint64_t n, uint64_t g0, ScanArgs base, cudaStream_t st,
+               uint64_t add_records) {
+  ExtraArgs ex{};
+  ex.s = base;
+  ex.n_ex = 0;
+  const uint64_t* body = rec;
+  uint64_t gb = g0;
+  uint64_t nb = n;
+  if (nb > 0 && (reinterpret_cast<uintptr_t>(body) & 15u) != 0) {  // 8-aligned, not 16: head record
+    ex.ex_ptr[ex.n_ex] = body;
+    ex.ex_gidx[ex.n_ex] = gb;
+    ++ex.n_ex;
+    ++body;
+    ++gb;
+    --nb;
+  }
+  if (nb & 1) {  // odd tail record
+    ex.ex_ptr[ex.n_ex] = body + nb - 1;
+    ex.ex_gidx[ex.n_ex] = gb + nb - 1;
+    ++ex.n_ex;
+    --nb;
+  }
+  // Per-CTA shared counters are u32: bound the records one launch gives a CTA.
+  const uint64_t per_launch_max = (uint64_t)h->sm_count * (1ull << 31);
+  bool added = false;
+  for (uint64_t off = 0; off < nb; off += per_launch_max) {
+    const uint64_t cnt = std::min<uint64_t>(per_launch_max, nb - off);
+    ScanArgs a = base;
+    a.rec = body + off;
+    a.nbody = cnt;
+    a.gidx0 = gb + off;
+    a.add_records = added ? 0 : add_records;
+    added = true;
+    const uint64_t chunks = (cnt + 4095) / 4096;
+    const int grid = (int)std::min<uint64_t>((uint64_t)h->sm_count, chunks);
+    Timed t(h, PASTA_PH_SCAN, st);
+    cudaError_t e = launch_scan(a, grid, st);
+    ++h->launches;
+    if (e != cudaSuccess) return PASTA_ECUDA;
+  }
+  if (ex.n_ex > 0 || !added) {
+    ex.s.add_records = added ? 0 : add_records;
+    if (ex.n_ex > 0 || ex.s.add_records) {
+      Timed t(h, PASTA_PH_SCAN, st);
+      cudaError_t e = launch_scan_extras(ex, st);
+      ++h->launches;
+      if (e != cudaSuccess) return PASTA_ECUDA;
+    }
+  }
+  return PASTA_OK;
+}
+
+int finalize_impl(pasta_trace* h, uint32_t page_shift, uint32_t n_kernels, pasta_histograms* out) {
+  const uint64_t P = (h->va_hi - h->va_lo) >> page_shift;
+  const uint32_t words = (uint32_t)((P + 63) / 64);
+  const int grid = h->sm_count * 8;
+  {
+    Timed t(h, PASTA_PH_FINALIZE, h->stream);
+    cudaError_t e = launch_finalize_bitmap(out->page_counts, P, out->page_bitmap, out->totals + PASTA_T_UNIQUE_PAGES,
+                                           grid, h->stream);
+    ++h->launches;
+    if (e != cudaSuccess) return PASTA_ECUDA;
+  }
+  if (out->kernel_alloc_counts && out->kernel_stats && n_kernels > 0) {
+    Timed t(h, PASTA_PH_FINALIZE, h->stream);
+    cudaError_t e = launch_footprint(out->kernel_alloc_counts, n_kernels, h->max_ids, h->d_id_size,
+                                     out->kernel_page_bitmap, words, out->kernel_stats,
+                                     out->totals + PASTA_T_WS_OBJ, grid, h->stream);
+    ++h->launches;
+    if (e != cudaSuccess) return PASTA_ECUDA;
+  }
+  return PASTA_OK;
+}
+
+int check_window(const pasta_trace* h, uint32_t page_shift) {
+  if (page_shift < 12 || page_shift > 30) return PASTA_EINVAL;
+  const uint64_t m = (1ull << page_shift) - 1;
+  if ((h->va_lo & m) || (h->va_hi & m)) return PASTA_EINVAL;
+  if (((h->va_hi - h->va_lo) >> page_shift) >= 0xFFFFFFFFull) return PASTA_EINVAL;
+  return PASTA_OK;
+}
+
+int ensure_host_path(pasta_trace* h) {
+  if (h->d_stage[0]) return PASTA_OK;
+  for (int i = 0; i < 2; ++i) {
+    if (cudaMalloc(&h->d_stage[i], h->host_chunk_bytes) != cudaSuccess) return PASTA_ECUDA;
+    if (cudaEventCreateWithFlags(&h->ev_copied[i], cudaEventDisableTiming) != cudaSuccess) return PASTA_ECUDA;
+    if (cudaEventCreateWithFlags(&h->ev_consumed[i], cudaEventDisableTiming) != cudaSuccess) return PASTA_ECUDA;
+  }
+  if (cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return PASTA_ECUDA;
+  return PASTA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pasta_strerror(int s) {
+  switch (s) {
+    case PASTA_OK: return "ok";
+    case PASTA_EINVAL: return "invalid argument";
+    case PASTA_EOVERLAP: return "range overlaps a live range";
+    case PASTA_ENOENT: return "no live range with that base";
+    case PASTA_ECAPACITY: return "capacity exceeded (max_live or max_ids)";
+    case PASTA_ECUDA: return "CUDA error";
+    case PASTA_ESTATE: return "invalid handle state";
+    case PASTA_ENOMEM: return "out of host memory";
+    default: return "unknown status";
+  }
+}
+
+int pasta_trace_open(const pasta_open_params* p, pasta_trace** out) {
+  if (!p || !out) return PASTA_EINVAL;
+  if (p->max_live == 0 || p->max_ids == 0 || p->flags != 0) return PASTA_EINVAL;
+  if (p->va_lo >= p->va_hi || (p->va_lo & 4095) || (p->va_hi & 4095)) return PASTA_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) return PASTA_ECUDA;
+  if (p->device < 0 || p->device >= ndev) return PASTA_EINVAL;
+  pasta_trace* h = new (std::nothrow) pasta_trace();
+  if (!h) return PASTA_ENOMEM;
+  h->device = p->device;
+  h->stream = reinterpret_cast<cudaStream_t>(p->stream);
+  h->va_lo = p->va_lo;
+  h->va_hi = p->va_hi;
+  h->max_live = p->max_live;
+  h->max_ids = p->max_ids;
+  if (p->host_chunk_bytes) h->host_chunk_bytes = (p->host_chunk_bytes + 4095) / 4096 * 4096;
+  DeviceGuard g(h->device);
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device) == cudaSuccess && sms > 0)
+    h->sm_count = sms;
+  bool ok = cudaMalloc(&h->d_bounds, 16ull * h->max_live) == cudaSuccess &&
+            cudaMalloc(&h->d_ids, 4ull * h->max_live) == cudaSuccess &&
+            cudaMalloc(&h->d_id_size, 8ull * h->max_ids) == cudaSuccess &&
+            cudaEventCreateWithFlags(&h->upload_done, cudaEventDisableTiming) == cudaSuccess;
+  if (ok) ok = cudaMemsetAsync(h->d_id_size, 0, 8ull * h->max_ids, h->stream) == cudaSuccess;
+  if (!ok) {
+    pasta_close(h);
+    return PASTA_ECUDA;
+  }
+  *out = h;
+  return PASTA_OK;
+}
+
+int pasta_register_alloc(pasta_trace* h, uint64_t base, uint64_t size, uint32_t* out_id) {
+  if (!h) return PASTA_EINVAL;
+  // size > 0 and base + size <= 2^64 - 1 (the exclusive end is representable)
+  if (size == 0 || base > UINT64_MAX - size) return PASTA_EINVAL;
+  const uint64_t end = base + size;
+  // overlap: the live range with the largest base < end must end at or before base
+  auto it = h->live.lower_bound(end);  // first base >= end
+  if (it != h->live.begin()) {
+    auto pr = std::prev(it);
+    if (pr->first + pr->second.first > base) return PASTA_EOVERLAP;
+  }
+  if (h->live.size() >= h->max_live || h->id_size.size() >= h->max_ids) return PASTA_ECAPACITY;
+  const uint32_t id = (uint32_t)h->id_size.size();
+  h->id_size.push_back(size);
+  h->live.emplace(base, std::make_pair(size, id));
+  h->dirty = true;
+  if (out_id) *out_id = id;
+  return PASTA_OK;
+}
+
+int pasta_register_free(pasta_trace* h, uint64_t base) {
+  if (!h) return PASTA_EINVAL;
+  auto it = h->live.find(base);
+  if (it == h->live.end()) return PASTA_ENOENT;
+  h->live.erase(it);
+  h->dirty = true;
+  return PASTA_OK;
+}
+
+int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t page_shift, pasta_histograms* out) {
+  if (!h || !tr || !out) return PASTA_EINVAL;
+  if (!out->page_counts || !out->alloc_counts || !out->totals) return PASTA_EINVAL;
+  if ((out->kernel_stats || out->kernel_page_bitmap) && !out->kernel_alloc_counts) return PASTA_EINVAL;
+  if (tr->flags & ~PASTA_REC_HOST) return PASTA_EINVAL;
+  int s = check_window(h, page_shift);
+  if (s) return s;
+  if (n > 0 && (!tr->addr || !aligned8(tr->addr))) return PASTA_EINVAL;
+  const uint32_t K = tr->kernel_offsets ? tr->n_kernels : 1;
+  if (tr->kernel_offsets && tr->n_kernels == 0) return PASTA_EINVAL;
+  const bool host = (tr->flags & PASTA_REC_HOST) != 0;
+  if (host && tr->kernel_offsets) {
+    if (tr->kernel_offsets[0] != 0 || tr->kernel_offsets[K] != n) return PASTA_EINVAL;
+    for (uint32_t k = 0; k < K; ++k)
+      if (tr->kernel_offsets[k] > tr->kernel_offsets[k + 1]) return PASTA_EINVAL;
+  }
+  DeviceGuard g(h->device);
+  s = upload_table(h);
+  if (s) return s;
+
+  const uint64_t P = (h->va_hi - h->va_lo) >> page_shift;
+  ScanArgs a{};
+  a.bounds = h->d_bounds;
+  a.ids = h->d_ids;
+  a.A = h->A_dev;
+  a.n_kernels = K;
+  a.koffs = tr->kernel_offsets;
+  a.va_lo = h->va_lo;
+  a.va_hi = h->va_hi;
+  a.page_shift = page_shift;
+  a.words = (uint32_t)((P + 63) / 64);
+  a.max_ids = h->max_ids;
+  a.page_counts = out->page_counts;
+  a.alloc_counts = out->alloc_counts;
+  a.totals = out->totals;
+  a.kac = out->kernel_alloc_counts;
+  a.kstats = out->kernel_stats;
+  a.kpb = out->kernel_page_bitmap;
+
+  if (!host) {
+    s = scan_range(h, tr->addr, n, 0, a, h->stream, n);
+    if (s) return s;
+  } else {
+    s = ensure_host_path(h);
+    if (s) return s;
+    if (tr->kernel_offsets && K > 1) {
+      const size_t kb = 8ull * (K + 1);
+      if (kb > h->d_koffs_cap) {
+        if (h->d_koffs) cudaFree(h->d_koffs);
+        h->d_koffs = nullptr;
+        if (cudaMalloc(&h->d_koffs, kb) != cudaSuccess) return PASTA_ECUDA;
+        h->d_koffs_cap = kb;
+      }
+      // synchronous upload from pageable memory is fine for the small offset array
+      if (cudaMemcpyAsync(h->d_koffs, tr->kernel_offsets, kb, cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+        return PASTA_ECUDA;
+      a.koffs = h->d_koffs;
+    } else {
+      a.n_kernels = 1;
+      a.koffs = nullptr;
+    }
+    const uint64_t chunk = h->host_chunk_bytes / 8;
+    uint64_t done = 0;
+    int buf = 0;
+    bool first = true;
+    // the copy stream must not run ahead of work already queued on the compute stream
+    cudaEventRecord(h->ev_consumed[0], h->stream);
+    cudaEventRecord(h->ev_consumed[1], h->stream);
+    while (done < n || first) {
+      const uint64_t cnt = std::min<uint64_t>(chunk, n - done);
+      if (cnt > 0) {
+        {
+          Timed t(h, PASTA_PH_COPY, h->copy_stream);
+          if (cudaStreamWaitEvent(h->copy_stream, h->ev_consumed[buf], 0) != cudaSuccess) return PASTA_ECUDA;
+          if (cudaMemcpyAsync(h->d_stage[buf], tr->addr + done, cnt * 8, cudaMemcpyHostToDevice, h->copy_stream) !=
+              cudaSuccess)
+            return PASTA_ECUDA;
+          if (cudaEventRecord(h->ev_copied[buf], h->copy_stream) != cudaSuccess) return PASTA_ECUDA;
+        }
+        if (cudaStreamWaitEvent(h->stream, h->ev_copied[buf], 0) != cudaSuccess) return PASTA_ECUDA;
+      }
+      s = scan_range(h, h->d_stage[buf], cnt, done, a, h->stream, first ? n : 0);
+      if (s) return s;
+      if (cudaEventRecord(h->ev_consumed[buf], h->stream) != cudaSuccess) return PASTA_ECUDA;
+      done += cnt;
+      buf ^= 1;
+      first = false;
+    }
+  }
+  if (!(out->flags & PASTA_NO_FINALIZE)) {
+    s = finalize_impl(h, page_shift, K, out);
+    if (s) return s;
+  }
+  return PASTA_OK;
+}
+
+int pasta_finalize(pasta_trace* h, uint32_t page_shift, uint32_t n_kernels, pasta_histograms* out) {
+  if (!h || !out || !out->page_counts || !out->totals) return PASTA_EINVAL;
+  if ((out->kernel_stats || out->kernel_page_bitmap) && !out->kernel_alloc_counts) return PASTA_EINVAL;
+  int s = check_window(h, page_shift);
+  if (s) return s;
+  DeviceGuard g(h->device);
+  s = upload_table(h);  // id sizes must be current for the footprints
+  if (s) return s;
+  return finalize_impl(h, page_shift, n_kernels, out);
+}
+
+int pasta_topk(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t k, uint64_t* out_page,
+               uint64_t* out_count, uint64_t* out_found) {
+  if (!h || !page_counts || !out_page || !out_count || !out_found || k == 0 || P == 0) return PASTA_EINVAL;
+  DeviceGuard g(h->device);
+  const int grid = h->sm_count * 4;
+  const size_t need = topk_scratch_bytes(k, grid);
+  if (need > h->topk_bytes) {
+    if (h->d_topk) {
+      cudaStreamSynchronize(h->stream);
+      cudaFree(h->d_topk);
+    }
+    h->d_topk = nullptr;
+    h->topk_bytes = 0;
+    if (cudaMalloc(&h->d_topk, need) != cudaSuccess) return PASTA_ECUDA;
+    h->topk_bytes = need;
+  }
+  int nl = 0;
+  Timed t(h, PASTA_PH_TOPK, h->stream);
+  cudaError_t e = run_topk(page_counts, P, k, out_page, out_count, out_found, h->d_topk, grid, h->stream, &nl);
+  h->launches += (uint64_t)nl;
+  return cuda_status(e);
+}
+
+int pasta_bitmap_or(pasta_trace* h, const uint64_t* gathered, uint32_t g, uint64_t words, uint64_t* out_bitmap,
+                    uint64_t* out_popcount) {
+  if (!h || !gathered || !out_bitmap || g == 0 || words == 0) return PASTA_EINVAL;
+  DeviceGuard dg(h->device);
+  Timed t(h, PASTA_PH_MERGE, h->stream);
+  cudaError_t e = launch_bitmap_or(gathered, g, words, out_bitmap, out_popcount, h->sm_count * 8, h->stream);
+  ++h->launches;
+  return cuda_status(e);
+}
+
+int pasta_sync(pasta_trace* h) {
+  if (!h) return PASTA_EINVAL;
+  DeviceGuard g(h->device);
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e == cudaSuccess && h->copy_stream) e = cudaStreamSynchronize(h->copy_stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return cuda_status(e);
+}
+
+int pasta_close(pasta_trace* h) {
+  if (!h) return PASTA_OK;
+  DeviceGuard g(h->device);
+  cudaStreamSynchronize(h->stream);
+  if (h->copy_stream) {
+    cudaStreamSynchronize(h->copy_stream);
+    cudaStreamDestroy(h->copy_stream);
+  }
+  for (auto& t : h->pending) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto e : h->free_events) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (h->d_stage[i]) cudaFree(h->d_stage[i]);
+    if (h->ev_copied[i]) cudaEventDestroy(h->ev_copied[i]);
+    if (h->ev_consumed[i]) cudaEventDestroy(h->ev_consumed[i]);
+  }
+  if (h->d_koffs) cudaFree(h->d_koffs);
+  if (h->d_topk) cudaFree(h->d_topk);
+  if (h->d_bounds) cudaFree(h->d_bounds);
+  if (h->d_ids) cudaFree(h->d_ids);
+  if (h->d_id_size) cudaFree(h->d_id_size);
+  if (h->upload_done) cudaEventDestroy(h->upload_done);
+  if (h->h_stage) cudaFreeHost(h->h_stage);
+  delete h;
+  return PASTA_OK;
+}
+
+int pasta_set_timing(pasta_trace* h, int enable) {
+  if (!h) return PASTA_EINVAL;
+  h->timing = enable != 0;
+  return PASTA_OK;
+}
+
+int pasta_get_timing(pasta_trace* h, double* out_ms, uint64_t* out_launches) {
+  if (!h) return PASTA_EINVAL;
+  DeviceGuard g(h->device);
+  int status = PASTA_OK;
+  for (auto& t : h->pending) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(t.b) != cudaSuccess || cudaEventElapsedTime(&ms, t.a, t.b) != cudaSuccess)
+      status = PASTA_ECUDA;
+    else
+      h->ms[t.phase] += ms;
+    h->free_events.push_back(t.a);
+    h->free_events.push_back(t.b);
+  }
+  h->pending.clear();
+  if (out_ms)
+    for (int i = 0; i < PASTA_PHASES; ++i) out_ms[i] = h->ms[i];
+  if (out_launches) *out_launches = h->launches;
+  return status;
+}
+
+int pasta_reset_timing(pasta_trace* h) {
+  if (!h) return PASTA_EINVAL;
+  uint64_t l = 0;
+  pasta_get_timing(h, nullptr, &l);
+  for (int i = 0; i < PASTA_PHASES; ++i) h->ms[i] = 0;
+  h->launches = 0;
+  return PASTA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+"""Multi-GPU merge of per-shard results -- collectives only.
+
+Trace shards are kernel-aligned contiguous record ranges, one per rank; every rank
+registers the identical allocation list. Every count output is a pointwise sum over
+any partition of the records, so:
+
+* page / alloc counts and the additive totals merge with ONE all_reduce(SUM) of the
+  packed int64 buffer [page_counts | alloc_counts | totals] (two's-complement int64
+  sums are bit-identical to u64 modular sums);
+* the page bitmap merges by OR: NCCL has no bitwise-OR reduction (torch refuses
+  ReduceOp.BOR on NCCL), so ranks all_gather their bitmaps and the pasta_bitmap_or
+  kernel ORs them and recounts unique pages;
+* WS_obj (a max over kernels) merges with all_reduce(MAX);
+* per-kernel rows are disjoint across ranks for kernel-aligned shards; for arbitrary
+  cuts merge_kernel_rows sums the straddling rows.
+Compute stays in the CUDA kernels; these helpers only move data.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def merge_counts(packed: torch.Tensor, group=None):
+    """all_reduce(SUM) of the packed count buffer, in place."""
+    dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=group)
+    return packed
+
+
+def gather_bitmaps(bitmap: torch.Tensor, group=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """[world * words] concatenation of every rank's bitmap (rank-major)."""
+    world = dist.get_world_size(group)
+    if out is None:
+        out = torch.empty(world * bitmap.numel(), dtype=bitmap.dtype, device=bitmap.device)
+    dist.all_gather_into_tensor(out, bitmap, group=group)
+    return out
+
+
+def merge_max(x: torch.Tensor, group=None):
+    dist.all_reduce(x, op=dist.ReduceOp.MAX, group=group)
+    return x
+
+
+def merge_kernel_rows(rows_local: torch.Tensor, k0: int, n_kernels_total: int, group=None) -> torch.Tensor:
+    """Global [n_kernels_total, C] rows from each rank's local rows [k1-k0, C] starting at
+    kernel k0 (rows of a kernel cut between ranks are summed)."""
+    C = rows_local.shape[1]
+    full = torch.zeros(n_kernels_total, C, dtype=rows_local.dtype, device=rows_local.device)
+    full[k0:k0 + rows_local.shape[0]] += rows_local
+    dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
+    return full
+
+
+class Merger:
+    """One merge step for a Trace's Histograms after a local analyze (with finalize):
+    SUM of counts, OR of bitmaps (+ unique pages), MAX of WS_obj."""
+
+    def __init__(self, trace, hist, group=None):
+        self.tr, self.hist, self.group = trace, hist, group
+        self.world = dist.get_world_size(group)
+        self.gathered = torch.empty(self.world * hist.words, dtype=torch.int64, device=hist.packed.device)
+        self.ws = torch.empty(1, dtype=torch.int64, device=hist.packed.device)
+
+    def merge(self):
+        from . import T_UNIQUE_PAGES, T_WS_OBJ
+
+        h = self.hist
+        self.ws.copy_(h.totals[T_WS_OBJ:T_WS_OBJ + 1])
+        merge_counts(h.packed, self.group)
+        gather_bitmaps(h.page_bitmap, self.group, out=self.gathered)
+        self.tr.bitmap_or(self.gathered, self.world, h.words, h.page_bitmap,
+                          h.totals[T_UNIQUE_PAGES:T_UNIQUE_PAGES + 1])
+        merge_max(self.ws, self.group)
+        h.totals[T_WS_OBJ:T_WS_OBJ + 1].copy_(self.ws)

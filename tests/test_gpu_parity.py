@@ -1,0 +1,391 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by
+element, on the same seeded inputs. Bit-exact on every output (integer path).
+
+Small cases run the whole oracle; full BASELINE sizes (test_full_configs) run in the
+bench launch configuration and are checked on sampled kernel segments the oracle
+computes one by one, plus invariants that hold at any size.
+"""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2602_22103_b200 as pb  # noqa: E402
+import oracle  # noqa: E402
+import tracegen  # noqa: E402
+from tests.harness import assert_parity, gpu_trace, oracle_trace, run_gpu, run_oracle, u64  # noqa: E402
+
+DEV = torch.device("cuda:0")
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+U64MAX = (1 << 64) - 1
+
+
+def _t(np_u64):
+    return torch.from_numpy(np.ascontiguousarray(np_u64, dtype=np.uint64).view(np.int64)).to(DEV)
+
+
+def _case(ranges, records, va_lo, va_hi, s, ko=None, rows=True, pages=True, topk=(1, 5, 64), max_ids=None,
+          label="", misalign=False):
+    rec = np.asarray(records, dtype=np.uint64)
+    tr = gpu_trace(DEV, va_lo, va_hi, ranges, max_ids=max_ids)
+    o = oracle_trace(va_lo, va_hi, ranges, max_ids=max_ids)
+    if ko is None and (rows or pages):
+        ko = [0, rec.size]
+    if misalign:
+        buf = torch.zeros(rec.size + 1, dtype=torch.int64, device=DEV)
+        buf[1:] = _t(rec) if rec.size else buf[1:]
+        dev_rec = buf[1:]
+        assert dev_rec.data_ptr() % 16 == 8
+    else:
+        dev_rec = _t(rec) if rec.size else torch.zeros(0, dtype=torch.int64, device=DEV)
+    g = run_gpu(tr, dev_rec, s, ko, kernel_rows=rows, kernel_pages=pages and rows, topk=topk)
+    r = run_oracle(o, rec, s, ko, kernel_rows=rows, kernel_pages=pages and rows, topk=topk)
+    assert_parity(g, r, kernel_rows=rows, kernel_pages=pages and rows, label=label)
+    tr.close()
+    return g, r
+
+
+# ------------------------------------------------------------------ generator
+def test_device_generator_matches_host():
+    for name in ["tiny", "rn50", "llama"]:
+        p = tracegen.build_plan(name)
+        dp = tracegen.DevicePlan(p, DEV)
+        rng = random.Random(11)
+        windows = [(0, min(p.n, 1 << 20)), (p.n - 4097, p.n)]
+        windows += [(j, j + 100003) for j in (rng.randrange(0, p.n - 100003) for _ in range(3))]
+        for j0, j1 in windows:
+            out = torch.empty(j1 - j0, dtype=torch.int64, device=DEV)
+            tracegen.device_records(dp, out, j0, j1)
+            torch.cuda.synchronize()
+            assert np.array_equal(u64(out), tracegen.host_records(p, j0, j1)), (name, j0, j1)
+
+
+# ------------------------------------------------------------------ goldens
+def test_hand_worked_golden_on_gpu():
+    with open(os.path.join(GOLD, "hand_worked.json")) as f:
+        gd = json.load(f)
+    e = gd["expect"]
+    g, _ = _case(gd["ranges"], gd["records"], gd["window"][0], gd["window"][1], gd["page_shift"],
+                 ko=gd["kernel_offsets"], topk=(2, 3, 10), label="hand_worked")
+    assert g["page_counts"].tolist() == e["page_counts"]
+    assert g["kac"].tolist() == e["kernel_alloc_counts"]
+    assert int(g["bitmap"][0]) == e["bitmap_word0"]
+    assert g["kstats"][:, 2].tolist() == e["footprint"] and int(g["totals"][4]) == e["ws_obj"]
+    assert g["kstats"][:, 3].tolist() == e["kernel_unique_pages"]
+    p, c, f = g["topk"][3]
+    assert [[int(a), int(b)] for a, b in zip(p, c)] == e["top3"]
+    h = gd["at_2MiB"]
+    g2, _ = _case(gd["ranges"], gd["records"], h["window"][0], h["window"][1], h["page_shift"], topk=(1,),
+                  label="hand_worked_2MiB")
+    assert g2["page_counts"].tolist() == h["page_counts"]
+
+
+def test_snapshot_sequence_on_gpu():
+    with open(os.path.join(GOLD, "snapshot_sequence.json")) as f:
+        gd = json.load(f)
+    tr = pb.Trace(DEV, gd["window"][0], gd["window"][1], 8, 8)
+    hist = tr.histograms(gd["page_shift"])
+    for step in gd["steps"]:
+        if step[0] == "register":
+            if step[3]["status"] == 0:
+                assert tr.register_alloc(step[1], step[2]) == step[3]["id"]
+            else:
+                with pytest.raises(pb.PastaError) as ei:
+                    tr.register_alloc(step[1], step[2])
+                assert ei.value.status == step[3]["status"]
+        elif step[0] == "free":
+            if step[2]["status"] == 0:
+                tr.register_free(step[1])
+            else:
+                with pytest.raises(pb.PastaError) as ei:
+                    tr.register_free(step[1])
+                assert ei.value.status == step[2]["status"]
+        else:
+            tr.analyze(_t(np.array(step[1], dtype=np.uint64)), gd["page_shift"], hist)
+    tr.sync()
+    assert u64(hist.alloc_counts)[:3].tolist() == gd["expect"]["alloc_counts"]
+    assert int(u64(hist.totals)[1]) == gd["expect"]["unattributed"]
+    assert int(u64(hist.totals)[0]) == gd["expect"]["records"]
+
+
+# ------------------------------------------------------------------ tiny config (whole oracle)
+@pytest.mark.parametrize("seed", [42, 7])
+def test_tiny_config_parity(seed):
+    p = tracegen.build_plan("tiny", seed=seed)
+    rec = tracegen.host_records(p)
+    dp = tracegen.DevicePlan(p, DEV)
+    drec = torch.empty(p.n, dtype=torch.int64, device=DEV)
+    tracegen.device_records(dp, drec)
+    tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs)
+    o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
+    ko = [int(x) for x in p.kernel_offsets]
+    g = run_gpu(tr, drec, p.page_shift, ko, kernel_rows=True, kernel_pages=True, topk=(16, 1, 1000))
+    r = run_oracle(o, rec, p.page_shift, ko, kernel_rows=True, kernel_pages=True, topk=(16, 1, 1000))
+    assert_parity(g, r, kernel_rows=True, kernel_pages=True, label=f"tiny/{seed}")
+    tr.close()
+
+
+def test_tiny_at_2mib_and_accumulate():
+    """page_shift 21, and a trace analyzed in two calls (cut inside kernel 3) accumulates
+    exactly like one call: counts are pointwise sums."""
+    p = tracegen.build_plan("tiny", seed=3)
+    rec = tracegen.host_records(p)
+    ko = [int(x) for x in p.kernel_offsets]
+    cut = ko[3] + 12345
+    tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs)
+    h1 = tr.histograms(21, n_kernels=4, kernel_rows=True, kernel_pages=True)
+    run_gpu(tr, _t(rec[:cut]), 21, ko[:4] + [cut], kernel_rows=True, kernel_pages=True, hist=h1, finalize=False)
+    h2 = tr.histograms(21, n_kernels=5, kernel_rows=True, kernel_pages=True)
+    ko2 = [0, ko[4] - cut] + [x - cut for x in ko[5:]]
+    run_gpu(tr, _t(rec[cut:]), 21, ko2, kernel_rows=True, kernel_pages=True, hist=h2, finalize=False)
+    o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
+    r = run_oracle(o, rec, 21, ko, kernel_rows=True, kernel_pages=True)
+    k1 = u64(h1.kernel_alloc_counts).reshape(4, -1)
+    k2 = u64(h2.kernel_alloc_counts).reshape(5, -1)
+    kac = np.concatenate([k1[:3], k1[3:4] + k2[:1], k2[1:]])
+    assert np.array_equal(kac, r["kac"])
+    assert np.array_equal(u64(h1.page_counts) + u64(h2.page_counts), r["page_counts"])
+    assert np.array_equal(u64(h1.alloc_counts) + u64(h2.alloc_counts), r["alloc_counts"])
+    b1 = u64(h1.kernel_page_bitmap).reshape(4, -1)
+    b2 = u64(h2.kernel_page_bitmap).reshape(5, -1)
+    assert np.array_equal(np.concatenate([b1[:3], b1[3:4] | b2[:1], b2[1:]]), r["kpb"])
+    tr.close()
+
+
+# ------------------------------------------------------------------ adversarial small traces
+def _adversarial(rng, n, s, nr, near_top=False, adjacent=0.5):
+    npg = rng.randint(1, 300)
+    if near_top:
+        va_hi = (U64MAX >> 21) << 21
+        va_lo = va_hi - (npg << s)
+    else:
+        va_lo = rng.randrange(0, 1 << 24) << 21
+        va_hi = va_lo + (npg << s)
+    lo = max(0, va_lo - (4 << s))
+    hi = min(U64MAX, va_hi + (4 << s))
+    ranges = []
+    cur = lo + rng.randrange(0, 1 << s)
+    for _ in range(nr):
+        if ranges and rng.random() < adjacent:
+            b = ranges[-1][0] + ranges[-1][1]
+        else:
+            b = cur + rng.randrange(0, 2 << s)
+        sz = rng.randrange(1, 2 << s)
+        if b + sz > min(hi, U64MAX - 1):
+            break
+        ranges.append((b, sz))
+        cur = b + sz
+    pts = [lo, hi, 0, U64MAX, va_lo, va_hi, max(0, va_lo - 1), va_hi - 1]
+    for b, sz in ranges:
+        pts += [max(0, b - 1), b, b + sz - 1, b + sz]
+    rec = []
+    run = 0
+    while len(rec) < n:
+        m = rng.random()
+        if m < 0.3:
+            rec.append(rng.choice(pts))
+        elif m < 0.6:  # coalesced run
+            a = rng.randrange(lo, hi)
+            e = rng.choice([4, 8, 16])
+            ln = rng.randint(1, 200)
+            rec += [min(U64MAX, a + e * i) for i in range(ln)]
+        else:
+            rec.append(rng.randrange(lo, hi + 1))
+        run += 1
+    rec = rec[:n]
+    return ranges, rec, va_lo, va_hi
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_adversarial_random(seed):
+    rng = random.Random(100 + seed)
+    for trial in range(6):
+        s = rng.choice([12, 21])
+        n = rng.choice([0, 1, 2, 3, 31, 4095, 4096, 4097, 8193, 60001, 250_000])
+        nr = rng.choice([0, 1, 5, 40, 300])
+        ranges, rec, va_lo, va_hi = _adversarial(rng, n, s, nr, near_top=rng.random() < 0.3)
+        nk = rng.choice([1, 2, 7, 50])
+        cuts = sorted(rng.randint(0, n) for _ in range(nk - 1))
+        if nk > 2 and n > 10:
+            cuts[0] = cuts[1]  # an empty kernel
+        ko = [0] + cuts + [n]
+        _case(ranges, rec, va_lo, va_hi, s, ko=ko, topk=(1, 7, 300), misalign=rng.random() < 0.4,
+              label=f"adv{seed}/{trial} n={n} A={len(ranges)} s={s}")
+
+
+def test_many_ranges_global_table():
+    """A = 65,536 live ranges: the boundary array no longer fits shared memory."""
+    rng = random.Random(9)
+    va_lo = 1 << 40
+    ranges = []
+    b = va_lo
+    for _ in range(65536):
+        b += rng.randrange(0, 64) * 64
+        sz = rng.randrange(1, 33) * 64
+        ranges.append((b, sz))
+        b += sz
+    va_hi = ((b >> 21) + 1) << 21
+    n = 300_000
+    rec = [rng.randrange(va_lo - 4096, va_hi + 4096) for _ in range(n // 2)]
+    for _ in range(n // 2 // 64):
+        a = rng.randrange(va_lo, va_hi)
+        rec += [a + 8 * i for i in range(64)]
+    ko = [0, n // 3, n // 3, len(rec)]
+    _case(ranges, rec, va_lo, va_hi, 12, ko=ko, topk=(10,), label="A=65536")
+
+
+def test_contention_and_scatter():
+    MiB = 1 << 20
+    va_lo, va_hi = 1 << 41, (1 << 41) + 64 * MiB
+    ranges = [(va_lo + i * MiB, MiB) for i in range(64)]
+    hot = [va_lo + 5 * MiB + 100] * 1_000_003  # one page, maximal contention
+    _case(ranges, hot, va_lo, va_hi, 12, ko=[0, 500_000, len(hot)], topk=(3,), label="hot page")
+    # every record a distinct page (permutation over the window at 4 KiB stride)
+    P = 64 * MiB >> 12
+    j = np.arange(P * 3, dtype=np.uint64)
+    rec = np.uint64(va_lo) + ((j * np.uint64(2654435761)) % np.uint64(P)) * np.uint64(4096)
+    _case(ranges, rec, va_lo, va_hi, 12, ko=[0, P, 2 * P, 3 * P], topk=(1, 100, 5000), label="all distinct")
+
+
+def test_host_records_path_equals_device_path():
+    p = tracegen.build_plan("tiny", seed=5)
+    rec = tracegen.host_records(p)
+    ko = [int(x) for x in p.kernel_offsets]
+    tr = pb.Trace(DEV, p.va_lo, p.va_hi, len(p.allocs), len(p.allocs), host_chunk_bytes=1 << 20)  # 8 chunks
+    for b, s in p.allocs:
+        tr.register_alloc(b, s)
+    host_rec = torch.from_numpy(rec.view(np.int64)).pin_memory()
+    g = run_gpu(tr, host_rec, 12, ko, kernel_rows=True, kernel_pages=True, topk=(16,), host=True)
+    o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
+    r = run_oracle(o, rec, 12, ko, kernel_rows=True, kernel_pages=True, topk=(16,))
+    assert_parity(g, r, kernel_rows=True, kernel_pages=True, label="host path")
+    tr.close()
+
+
+# ------------------------------------------------------------------ top-K edge cases
+@pytest.mark.parametrize("K", [1, 2, 17, 1024, 2048, 4096, 5000, 68266])
+def test_topk_direct(K):
+    rng = np.random.default_rng(K)
+    P = 300_000
+    counts = rng.integers(0, 4, size=P).astype(np.uint64)  # heavy ties, many zeros
+    counts[rng.integers(0, P, 50)] = rng.integers(1 << 33, 1 << 34, 50).astype(np.uint64)  # big values
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    pcnt = _t(counts)
+    p, c, f = tr.topk(pcnt, K)
+    tr.sync()
+    rp, rc, rf = oracle.topk(counts, K)
+    assert int(u64(f)[0]) == rf
+    assert np.array_equal(u64(p), rp) and np.array_equal(u64(c), rc)
+    # K > nnz
+    small = np.zeros(1000, dtype=np.uint64)
+    small[[3, 500, 999]] = [7, 7, 1]
+    p, c, f = tr.topk(_t(small), K)
+    tr.sync()
+    rp, rc, rf = oracle.topk(small, K)
+    assert int(u64(f)[0]) == rf == min(K, 3)
+    assert np.array_equal(u64(p), rp) and np.array_equal(u64(c), rc)
+    # all zero
+    p, c, f = tr.topk(_t(np.zeros(77, dtype=np.uint64)), K)
+    tr.sync()
+    assert int(u64(f)[0]) == 0 and np.all(u64(p) == np.uint64(U64MAX)) and np.all(u64(c) == 0)
+    tr.close()
+
+
+def test_bitmap_or_merge_kernel():
+    rng = np.random.default_rng(4)
+    g, W = 4, 70001
+    bms = rng.integers(0, 1 << 63, size=(g, W), dtype=np.uint64) & rng.integers(0, 1 << 63, size=(g, W), dtype=np.uint64)
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    gathered = _t(bms.reshape(-1))
+    out = torch.empty(W, dtype=torch.int64, device=DEV)
+    pop = torch.zeros(1, dtype=torch.int64, device=DEV)
+    tr.bitmap_or(gathered, g, W, out, pop)
+    tr.sync()
+    ref = np.bitwise_or.reduce(bms, axis=0)
+    assert np.array_equal(u64(out), ref)
+    assert int(u64(pop)[0]) == int(np.unpackbits(ref.view(np.uint8)).sum())
+    tr.close()
+
+
+def test_errors_are_status_codes():
+    tr = pb.Trace(DEV, 0, 1 << 30, 2, 3)
+    with pytest.raises(pb.PastaError) as ei:
+        tr.register_alloc(0x1000, 0)
+    assert ei.value.status == pb.PASTA_EINVAL
+    tr.register_alloc(0x1000, 0x1000)
+    with pytest.raises(pb.PastaError) as ei:
+        tr.register_alloc(0x1800, 0x10)
+    assert ei.value.status == pb.PASTA_EOVERLAP
+    with pytest.raises(pb.PastaError) as ei:
+        tr.register_free(0x1800)
+    assert ei.value.status == pb.PASTA_ENOENT
+    hist = tr.histograms(12)
+    with pytest.raises(pb.PastaError) as ei:  # page_shift out of range
+        tr.analyze(torch.zeros(4, dtype=torch.int64, device=DEV), 11, hist)
+    assert ei.value.status == pb.PASTA_EINVAL
+    with pytest.raises(pb.PastaError) as ei:  # misaligned window for 2^31 pages
+        pb.Trace(DEV, 4096, 1 << 30, 1, 1).analyze(torch.zeros(4, dtype=torch.int64, device=DEV), 21, hist)
+    assert ei.value.status == pb.PASTA_EINVAL
+    tr.close()
+
+
+# ------------------------------------------------------------------ full BASELINE sizes
+FULL = ["rn50", "gpt2m", "uvm", "llama"]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_config_sampled(name):
+    """Full-size config in the bench launch configuration: device-generated records,
+    one analyze; oracle recomputes sampled kernel segments one by one (kernel rows,
+    per-kernel unattributed, per-kernel page bits) from host-generated records; global
+    outputs checked by conservation and bitmap/count invariants."""
+    p = tracegen.build_plan(name)
+    free = torch.cuda.mem_get_info(DEV)[0]
+    if p.n * 8 + (2 << 30) > free:
+        pytest.skip(f"{name} needs {p.n * 8 / 2**30:.1f} GiB")
+    dp = tracegen.DevicePlan(p, DEV)
+    drec = torch.empty(p.n, dtype=torch.int64, device=DEV)
+    tracegen.device_records(dp, drec)
+    tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs)
+    ko = [int(x) for x in p.kernel_offsets]
+    g = run_gpu(tr, drec, p.page_shift, ko, kernel_rows=True, kernel_pages=p.want_kernel_pages,
+                topk=tuple(p.topk))
+    del drec
+    torch.cuda.empty_cache()
+    n = p.n
+    tot = g["totals"]
+    assert int(tot[0]) == n
+    assert int(g["page_counts"].sum()) + int(tot[2]) == n
+    assert int(g["alloc_counts"].sum()) + int(tot[1]) == n
+    assert np.array_equal(g["kac"].sum(axis=0), g["alloc_counts"])
+    assert int(g["kstats"][:, 1].sum()) == int(tot[1])
+    bm, u = oracle.bitmap(g["page_counts"])  # bitmap/unique recomputed from the GPU's counts
+    assert np.array_equal(g["bitmap"], bm) and int(tot[3]) == u
+    for K in p.topk:  # top-K exactly as the oracle selects from the GPU's counts
+        rp, rc, rf = oracle.topk(g["page_counts"], K)
+        gp, gc, gf = g["topk"][K]
+        assert gf == rf and np.array_equal(gp, rp) and np.array_equal(gc, rc)
+    rng = random.Random(1)
+    ks = sorted(set([0, p.n_kernels - 1] + [rng.randrange(p.n_kernels) for _ in range(6)]))
+    sizes = np.array([s for _, s in p.allocs], dtype=np.uint64)
+    for k in ks:
+        j0, j1 = ko[k], ko[k + 1]
+        if j1 - j0 > 60_000_000:
+            continue
+        rec = tracegen.host_records(p, j0, j1)
+        o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
+        o.analyze(rec, [0, j1 - j0], p.page_shift, kernel_rows=True, kernel_pages=p.want_kernel_pages)
+        assert np.array_equal(g["kac"][k], o.kernel_rows[0]), (name, k)
+        assert int(g["kstats"][k, 1]) == int(o.kun[0]), (name, k)
+        assert int(g["kstats"][k, 2]) == int(sizes[o.kernel_rows[0] > 0].sum()), (name, k)
+        if p.want_kernel_pages:
+            assert np.array_equal(g["kpb"][k], o.kernel_pages[0]), (name, k)
+    tr.close()
