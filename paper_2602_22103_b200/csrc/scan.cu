@@ -7,23 +7,29 @@
 // associated memory object upon each access". The paper's lookup / counting
 // method is unstated; this is our sm_100a design:
 //
-//  * persistent grid, one CTA per SM, each CTA owns a contiguous run of 32 KiB
-//    chunks; one producer warp streams chunks global -> shared with 1-D TMA bulk
-//    copies (cp.async.bulk + mbarrier complete_tx, L2 evict_first) into a 4-stage
-//    ring; 16 consumer warps read their records with conflict-free LDS.128;
-//  * each consumer lane owns RPT consecutive records and keeps a *run*: the
-//    interval [lo, lo+span] = (owning range or gap) intersected with (page or
-//    out-of-window region) plus a count. A record inside the run costs one 64-bit
-//    subtract-compare; a warp whose lanes all stay in their runs takes one vote;
-//  * on a miss the lane flushes its run (warp-aggregated: __match_any_sync groups,
-//    __reduce_add_sync sum, one leader atomic per distinct key) and looks the new
-//    address up: page by shift, owner by binary search over the sorted boundary
-//    array held in shared memory (count of boundaries <= a: odd => inside range
-//    (c-1)/2, even => gap);
-//  * owner counts go to a per-CTA shared-memory array (u32 per live range plus the
-//    unattributed slot), flushed to global at kernel-segment boundaries and at the
-//    end; page counts go straight to L2 with red.global.add.u64 (one per distinct
-//    (warp, page) flush), per-kernel page bits with atom.or at the same flush.
+//  * persistent grid, one CTA per SM; each CTA owns a contiguous run of 32 KiB
+//    chunks; one producer warp streams them global -> shared with 1-D TMA bulk copies
+//    (cp.async.bulk + mbarrier complete_tx, L2 evict_first) into a 4-stage ring;
+//  * 16 consumer warps; warp w takes the 256-record slice [256w, 256w+256) of each
+//    chunk with four conflict-free LDS.128 per lane (lane l holds slice positions
+//    64i + 2l + {0,1}, i = 0..3, in position order);
+//  * every address resolves to exactly one *interval* = (live range or gap between
+//    ranges) intersected with (page or out-of-window region); the owner part comes
+//    from a binary search over the sorted boundary array B = [base_0, end_0, ...]
+//    in shared memory (count c of boundaries <= a: odd => range (c-1)/2, even =>
+//    gap), cached per lane; the page part is arithmetic;
+//  * tier W (warp-uniform): A = interval of the slice's first record, B = interval
+//    of its last; if A == B or B starts right after A, and every lane's 8 records are
+//    non-decreasing with a_0 >= A.lo and a_7 <= B.last, then every record is in
+//    A u B and the A-count is #{a <= A.last}: one __reduce_add_sync per slice;
+//  * tier L (per lane): A = interval of the lane's first record, B = interval of its
+//    first record outside A, membership counts; the (page, owner, count) pairs of
+//    the warp are merged by a leader loop (ballot / shfl / __reduce_add_sync);
+//  * tier F (per lane, rare): records in neither A nor B are looked up one by one;
+//  * counts accumulate in warp-uniform registers (current page, current owner) and
+//    are flushed by one lane with red.global.add.u64 when the page / owner changes,
+//    at kernel-segment boundaries (per warp, no CTA barrier) and at the end; the
+//    per-kernel page bit is set with atom.or at the page flush.
 #include <cstdint>
 
 #include "common.cuh"
@@ -34,34 +40,44 @@ namespace {
 
 using namespace dev;
 
-constexpr int kRPT = 8;                       // records per consumer lane per chunk
-constexpr int kVec = kRPT / 2;                // LDS.128 per lane per chunk
 constexpr int kConsWarps = 16;
-constexpr int kCons = kConsWarps * 32;        // consumer threads
-constexpr int kThreads = kCons + 32;          // + one producer warp
-constexpr int kChunk = kCons * kRPT;          // records per chunk (4096 = 32 KiB)
+constexpr int kCons = kConsWarps * 32;  // consumer threads
+constexpr int kThreads = kCons + 32;    // + one producer warp
+constexpr int kSlice = 256;             // records per warp per chunk (8 per lane)
+constexpr int kChunk = kConsWarps * kSlice;  // 4096 records = 32 KiB
 constexpr int kStages = 4;
 constexpr uint32_t kChunkBytes = kChunk * 8;
 constexpr int kRingBytes = kStages * kChunkBytes;
 constexpr int kMiscBytes = 2 * kStages * 8 + 16;
 constexpr int kSmemLimit = 227 * 1024;
 
-struct Lane {
-  uint64_t lo, span;    // current run interval [lo, lo + span]
-  uint64_t olo, ospan;  // owner (range or gap) interval
-  uint32_t cnt;         // records in the run
+struct Ctx {
+  uint64_t va_lo, va_hi, wbytes;  // window, wbytes = va_hi - va_lo
+  uint32_t s;
+  uint32_t A;
+  const uint64_t* B;  // boundary array (shared or global)
+};
+
+struct Ival {           // one interval: [lo, lo + span]
+  uint64_t lo, span;
   uint32_t page;        // page index or kOOW
   uint32_t own;         // live-range index, A = unattributed
-  uint32_t kbit;        // last page whose kernel bit this lane set (KPAGES)
 };
+
+struct OwnCache {       // last owner interval (range or gap) seen by this lane
+  uint64_t olo, ospan;
+  uint32_t own;
+};
+
+__device__ __forceinline__ bool inside(uint64_t a, const Ival& I) { return a - I.lo <= I.span; }
 
 // #{ i < m : B[i] <= a } by bisection.
 template <bool kGlobal>
 __device__ __forceinline__ uint32_t count_le(const uint64_t* __restrict__ B, uint32_t m, uint64_t a) {
   uint32_t lo = 0, len = m;
   while (len > 0) {
-    uint32_t half = len >> 1;
-    uint64_t v = kGlobal ? __ldg(B + lo + half) : B[lo + half];
+    const uint32_t half = len >> 1;
+    const uint64_t v = kGlobal ? __ldg(B + lo + half) : B[lo + half];
     if (v <= a) {
       lo += half + 1;
       len -= half + 1;
@@ -72,44 +88,42 @@ __device__ __forceinline__ uint32_t count_le(const uint64_t* __restrict__ B, uin
   return lo;
 }
 
-struct Ctx {
-  uint64_t va_lo, va_hi;
-  uint32_t s;
-  uint32_t A;
-  const uint64_t* B;  // boundary array (shared or global)
-};
-
 template <bool kBig>
-__device__ __forceinline__ void lookup(Lane& L, uint64_t a, const Ctx& c) {
-  if (a - L.olo > L.ospan) {
+__device__ __forceinline__ Ival lookup(OwnCache& oc, uint64_t a, const Ctx& c) {
+  if (a - oc.olo > oc.ospan) {
     const uint32_t m = 2 * c.A;
     const uint32_t cc = count_le<kBig>(c.B, m, a);
     const uint64_t olo = cc ? (kBig ? __ldg(c.B + cc - 1) : c.B[cc - 1]) : 0ull;
     const uint64_t olast = (cc == m) ? ~0ull : (kBig ? __ldg(c.B + cc) : c.B[cc]) - 1;
-    L.olo = olo;
-    L.ospan = olast - olo;
-    L.own = (cc & 1u) ? (cc >> 1) : c.A;
+    oc.olo = olo;
+    oc.ospan = olast - olo;
+    oc.own = (cc & 1u) ? (cc >> 1) : c.A;
   }
   uint64_t plo, plast;
-  if (a < c.va_lo) {
-    plo = 0;
-    plast = c.va_lo - 1;
-    L.page = kOOW;
-  } else if (a >= c.va_hi) {
-    plo = c.va_hi;
-    plast = ~0ull;
-    L.page = kOOW;
-  } else {
-    const uint64_t p = (a - c.va_lo) >> c.s;
-    L.page = static_cast<uint32_t>(p);
+  uint32_t page;
+  const uint64_t d = a - c.va_lo;
+  if (d < c.wbytes) {
+    const uint64_t p = d >> c.s;
+    page = static_cast<uint32_t>(p);
     plo = c.va_lo + (p << c.s);
     plast = plo + ((1ull << c.s) - 1);
+  } else if (a < c.va_lo) {
+    plo = 0;
+    plast = c.va_lo - 1;
+    page = kOOW;
+  } else {
+    plo = c.va_hi;
+    plast = ~0ull;
+    page = kOOW;
   }
-  const uint64_t olast = L.olo + L.ospan;
-  const uint64_t lo = L.olo > plo ? L.olo : plo;
+  const uint64_t olast = oc.olo + oc.ospan;
+  Ival I;
+  I.lo = oc.olo > plo ? oc.olo : plo;
   const uint64_t last = olast < plast ? olast : plast;
-  L.lo = lo;
-  L.span = last - lo;
+  I.span = last - I.lo;
+  I.page = page;
+  I.own = oc.own;
+  return I;
 }
 
 struct Out {
@@ -122,142 +136,213 @@ struct Out {
   const uint32_t* ids;
   uint64_t max_ids;
   uint32_t words;
-  uint32_t* own_cnt;  // shared (A+1 slots) unless kBig
-  uint32_t* oow;      // shared
+  uint32_t A;
 };
 
-// Owner count of `s` records straight to global (kBig path and the extras kernel).
+// Owner count `v` of kernel k to global (one thread).
 template <bool kRows>
-__device__ __forceinline__ void owner_to_global(const Out& o, uint32_t own, uint32_t A, uint64_t s, uint32_t k) {
-  if (own < A) {
+__device__ __forceinline__ void owner_to_global(const Out& o, uint32_t own, uint64_t v, uint32_t k) {
+  if (v == 0) return;
+  if (own < o.A) {
     const uint32_t id = __ldg(o.ids + own);
-    red_add_u64(o.alloc_counts + id, s);
+    red_add_u64(o.alloc_counts + id, v);
     if (kRows) {
-      red_add_u64(o.kac + (uint64_t)k * o.max_ids + id, s);
-      if (o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 0, s);
+      red_add_u64(o.kac + (uint64_t)k * o.max_ids + id, v);
+      if (o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 0, v);
     }
   } else {
-    red_add_u64(o.totals + 1, s);
-    if (kRows && o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 1, s);
+    red_add_u64(o.totals + 1, v);
+    if (kRows && o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 1, v);
   }
 }
 
-// Warp-collective: lanes with `pred` flush their run. Called by all 32 lanes.
+// Page count `v` of kernel k to global (one thread).
+template <bool kPages>
+__device__ __forceinline__ void page_to_global(const Out& o, uint32_t page, uint64_t v, uint32_t k) {
+  if (v == 0) return;
+  if (page == kOOW) {
+    red_add_u64(o.totals + 2, v);
+  } else {
+    red_add_u64(o.page_counts + page, v);
+    if (kPages) red_or_u64(o.kpb + (uint64_t)k * o.words + (page >> 6), 1ull << (page & 63));
+  }
+}
+
+// Warp-uniform accumulators (every lane holds the same values).
+struct WarpAcc {
+  uint32_t page, own;
+  uint32_t pcnt, ocnt;
+};
+
+template <bool kRows, bool kPages>
+__device__ __forceinline__ void wadd(WarpAcc& w, const Out& o, uint32_t page, uint32_t own, uint32_t c, uint32_t k,
+                                     uint32_t lane) {
+  if (page != w.page) {
+    if (lane == 0) page_to_global<kPages>(o, w.page, w.pcnt, k);
+    w.page = page;
+    w.pcnt = 0;
+  }
+  w.pcnt += c;
+  if (own != w.own) {
+    if (lane == 0) owner_to_global<kRows>(o, w.own, w.ocnt, k);
+    w.own = own;
+    w.ocnt = 0;
+  }
+  w.ocnt += c;
+}
+
+// Per-lane fallback accumulators (tier F).
+struct LaneAcc {
+  uint32_t own, ocnt;
+  uint32_t kbit;  // last page whose kernel bit this lane set
+};
+
+// Tier F: one record, looked up alone; page count straight to L2, owner accumulated.
 template <bool kBig, bool kRows, bool kPages>
-__device__ __forceinline__ void flush_runs(bool pred, Lane& L, const Out& o, uint32_t A, uint32_t k) {
-  const unsigned m = __ballot_sync(kFull, pred);
-  if (m == 0) return;
-  if (pred) {
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned g1 = __match_any_sync(m, L.own);
-    const uint32_t s1 = __reduce_add_sync(g1, L.cnt);
-    if (lane == (unsigned)(__ffs(g1) - 1)) {
-      if (kBig) owner_to_global<kRows>(o, L.own, A, s1, k);
-      else atomicAdd(o.own_cnt + L.own, s1);
+__device__ __forceinline__ void fallback_record(uint64_t x, OwnCache& oc, LaneAcc& la, const Ctx& c, const Out& o,
+                                             uint32_t k) {
+  const Ival I = lookup<kBig>(oc, x, c);
+  if (I.page == kOOW) {
+    red_add_u64(o.totals + 2, 1);
+  } else {
+    red_add_u64(o.page_counts + I.page, 1);
+    if (kPages && la.kbit != I.page) {
+      red_or_u64(o.kpb + (uint64_t)k * o.words + (I.page >> 6), 1ull << (I.page & 63));
+      la.kbit = I.page;
     }
-    const unsigned g2 = __match_any_sync(m, L.page);
-    const uint32_t s2 = __reduce_add_sync(g2, L.cnt);
-    if (lane == (unsigned)(__ffs(g2) - 1)) {
-      if (L.page == kOOW) {
-        atomicAdd(o.oow, s2);
-      } else {
-        red_add_u64(o.page_counts + L.page, s2);
-        if (kPages && L.kbit != L.page)
-          red_or_u64(o.kpb + (uint64_t)k * o.words + (L.page >> 6), 1ull << (L.page & 63));
-      }
-    }
-    if (kPages) L.kbit = L.page;
+  }
+  if (I.own != la.own) {
+    owner_to_global<kRows>(o, la.own, la.ocnt, k);
+    la.own = I.own;
+    la.ocnt = 0;
+  }
+  la.ocnt += 1;
+}
+
+// Warp-collective: merge every lane's up to two (page, owner, count) entries into the
+// warp accumulators (leader loop; one __reduce_add_sync per distinct key).
+template <bool kRows, bool kPages>
+__device__ __forceinline__ void merge_entries(WarpAcc& w, const Out& o, uint32_t k, uint32_t lane, bool pa,
+                                              uint32_t pA, uint32_t oA, uint32_t cA, bool pb, uint32_t pB,
+                                              uint32_t oB, uint32_t cB) {
+  for (;;) {
+    const unsigned m = __ballot_sync(kFull, pa || pb);
+    if (m == 0) break;
+    const int leader = __ffs(m) - 1;
+    const uint32_t kp = __shfl_sync(kFull, pa ? pA : pB, leader);
+    const uint32_t ko = __shfl_sync(kFull, pa ? oA : oB, leader);
+    const bool mA = pa && pA == kp && oA == ko;
+    const bool mB = pb && pB == kp && oB == ko;
+    const uint32_t sum = __reduce_add_sync(kFull, (mA ? cA : 0u) + (mB ? cB : 0u));
+    wadd<kRows, kPages>(w, o, kp, ko, sum, k, lane);
+    pa = pa && !mA;
+    pb = pb && !mB;
   }
 }
 
-// CTA-collective (consumer threads): flush every lane's run, then the shared owner
-// counts of kernel segment k.
+// Tier L + F for this lane's records selected by `valid` (bit i <-> a[i]).
 template <bool kBig, bool kRows, bool kPages>
-__device__ void segment_flush(Lane& L, const Out& o, uint32_t A, uint32_t k) {
-  flush_runs<kBig, kRows, kPages>(L.cnt > 0, L, o, A, k);
-  L.cnt = 0;
-  if (kPages) L.kbit = kOOW;
-  named_bar_sync(1, kCons);
-  uint64_t attributed = 0;
-  if (!kBig) {
-    for (uint32_t r = threadIdx.x; r <= A; r += kCons) {
-      const uint32_t v = o.own_cnt[r];
-      if (v == 0) continue;
-      o.own_cnt[r] = 0;
-      if (r < A) {
-        const uint32_t id = __ldg(o.ids + r);
-        red_add_u64(o.alloc_counts + id, v);
-        if (kRows) red_add_u64(o.kac + (uint64_t)k * o.max_ids + id, v);
-        attributed += v;
-      } else {
-        red_add_u64(o.totals + 1, v);
-        if (kRows && o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 1, v);
-      }
+__device__ __forceinline__ void process_lane(const uint64_t (&a)[8], uint32_t valid, OwnCache& oc, LaneAcc& la,
+                                             WarpAcc& w, const Ctx& c, const Out& o, uint32_t k, uint32_t lane) {
+  // seed A: first valid record
+  uint64_t x = a[7];
+#pragma unroll
+  for (int i = 6; i >= 0; --i)
+    if ((valid >> i) & 1u) x = a[i];
+  Ival IA{};
+  uint32_t cA = 0, inA = 0;
+  if (valid) {
+    IA = lookup<kBig>(oc, x, c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (((valid >> i) & 1u) && inside(a[i], IA)) inA |= 1u << i;
+    cA = __popc(inA);
+  }
+  uint32_t miss = valid & ~inA;
+  Ival IB{};
+  uint32_t cB = 0;
+  if (__any_sync(kFull, miss != 0)) {
+    if (miss) {
+      uint64_t y = a[7];
+#pragma unroll
+      for (int i = 6; i >= 0; --i)
+        if ((miss >> i) & 1u) y = a[i];
+      IB = lookup<kBig>(oc, y, c);
+      uint32_t inB = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (((miss >> i) & 1u) && inside(a[i], IB)) inB |= 1u << i;
+      cB = __popc(inB);
+      miss &= ~inB;
     }
-    if (kRows && o.kstats) {
-      attributed = warp_sum_u64(attributed);
-      if ((threadIdx.x & 31) == 0 && attributed) red_add_u64(o.kstats + (uint64_t)k * 4 + 0, attributed);
+    if (__any_sync(kFull, miss != 0)) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if ((miss >> i) & 1u) fallback_record<kBig, kRows, kPages>(a[i], oc, la, c, o, k);
     }
   }
-  if (threadIdx.x == 0) {
-    const uint32_t v = *o.oow;
-    if (v) {
-      *o.oow = 0;
-      red_add_u64(o.totals + 2, v);
-    }
-  }
-  named_bar_sync(1, kCons);
+  merge_entries<kRows, kPages>(w, o, k, lane, cA > 0, IA.page, IA.own, cA, cB > 0, IB.page, IB.own, cB);
 }
 
-// Process this lane's records of the current chunk whose chunk positions lie in
-// [r0, r1). a[2i], a[2i+1] are the records at positions base + 2*rot(i) (+1).
-template <bool kMasked, bool kBig, bool kRows, bool kPages>
-__device__ __forceinline__ void process(const uint64_t (&a)[kRPT], uint32_t base, uint32_t rsh, uint32_t r0,
-                                        uint32_t r1, Lane& L, const Ctx& c, const Out& o, uint32_t k) {
-  uint32_t need = 0, hits = 0;
+// Full 256-record slice: tier W, else tier L/F.
+template <bool kBig, bool kRows, bool kPages>
+__device__ __forceinline__ void process_full(const uint64_t (&a)[8], OwnCache& oc, LaneAcc& la, WarpAcc& w,
+                                             const Ctx& c, const Out& o, uint32_t k, uint32_t lane) {
+  const uint64_t xf = __shfl_sync(kFull, a[0], 0);
+  const uint64_t xl = __shfl_sync(kFull, a[7], 31);
+  const Ival IA = lookup<kBig>(oc, xf, c);
+  const bool same = inside(xl, IA);
+  Ival IB = IA;
+  if (!same) IB = lookup<kBig>(oc, xl, c);
+  const uint64_t alast = IA.lo + IA.span;
+  const bool ok = same || (IB.lo - 1 == alast);
+  bool lane_ok = ok && a[0] >= IA.lo && a[7] <= IB.lo + IB.span;
 #pragma unroll
-  for (int i = 0; i < kVec; ++i) {
+  for (int i = 0; i < 7; ++i) lane_ok = lane_ok && (a[i] <= a[i + 1]);
+  if (__all_sync(kFull, lane_ok)) {
+    if (same) {
+      wadd<kRows, kPages>(w, o, IA.page, IA.own, kSlice, k, lane);
+    } else {
+      uint32_t cA = 0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      bool v = true;
-      if (kMasked) {
-        const uint32_t pos = base + 2 * ((i + rsh) % kVec) + h;
-        v = pos >= r0 && pos < r1;
-      }
-      const bool hit = (a[2 * i + h] - L.lo) <= L.span;
-      need += v;
-      hits += (v && hit);
+      for (int i = 0; i < 8; ++i) cA += (a[i] <= alast) ? 1u : 0u;
+      const uint32_t sA = __reduce_add_sync(kFull, cA);
+      wadd<kRows, kPages>(w, o, IA.page, IA.own, sA, k, lane);
+      wadd<kRows, kPages>(w, o, IB.page, IB.own, kSlice - sA, k, lane);
     }
-  }
-  if (__all_sync(kFull, hits == need)) {
-    L.cnt += need;
     return;
   }
-#pragma unroll
-  for (int i = 0; i < kVec; ++i) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      bool v = true;
-      if (kMasked) {
-        const uint32_t pos = base + 2 * ((i + rsh) % kVec) + h;
-        v = pos >= r0 && pos < r1;
-      }
-      const uint64_t x = a[2 * i + h];
-      const bool miss = v && ((x - L.lo) > L.span);
-      if (__any_sync(kFull, miss)) {
-        flush_runs<kBig, kRows, kPages>(miss && L.cnt > 0, L, o, c.A, k);
-        if (miss) {
-          lookup<kBig>(L, x, c);
-          L.cnt = 0;
-        }
-      }
-      L.cnt += v;
-    }
+  process_lane<kBig, kRows, kPages>(a, 0xFFu, oc, la, w, c, o, k, lane);
+}
+
+// Warp-local flush of everything accumulated for kernel segment k.
+template <bool kRows, bool kPages>
+__device__ __forceinline__ void warp_flush(WarpAcc& w, LaneAcc& la, const Out& o, uint32_t k, uint32_t lane) {
+  if (lane == 0) {
+    page_to_global<kPages>(o, w.page, w.pcnt, k);
+    owner_to_global<kRows>(o, w.own, w.ocnt, k);
   }
+  w.pcnt = 0;
+  w.ocnt = 0;
+  w.page = kOOW - 1;  // no page: forces the next wadd to (re)set the kernel bit
+  // lane fallback owner counts: warp-aggregate by owner
+  bool pend = la.ocnt > 0;
+  for (;;) {
+    const unsigned m = __ballot_sync(kFull, pend);
+    if (m == 0) break;
+    const int leader = __ffs(m) - 1;
+    const uint32_t key = __shfl_sync(kFull, la.own, leader);
+    const bool mine = pend && la.own == key;
+    const uint32_t sum = __reduce_add_sync(kFull, mine ? la.ocnt : 0u);
+    if (lane == (uint32_t)leader) owner_to_global<kRows>(o, key, sum, k);
+    pend = pend && !mine;
+  }
+  la.ocnt = 0;
+  la.kbit = kOOW;
 }
 
 __device__ __forceinline__ uint32_t kernel_of(const uint64_t* __restrict__ koffs, uint32_t K, uint64_t g) {
-  // largest k with koffs[k] <= g among k in [0, K-1]
+  // largest k in [0, K-1] with koffs[k] <= g
   uint32_t lo = 0, hi = K - 1;
   while (lo < hi) {
     const uint32_t mid = (lo + hi + 1) >> 1;
@@ -273,34 +358,30 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args) 
   uint64_t* ring = reinterpret_cast<uint64_t*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
   uint64_t* empty = full + kStages;
-  uint32_t* oow = reinterpret_cast<uint32_t*>(empty + kStages);
   uint64_t* sB = reinterpret_cast<uint64_t*>(smem + kRingBytes + kMiscBytes);
-  uint32_t* own_cnt = reinterpret_cast<uint32_t*>(sB + 2 * (size_t)args.A);
 
   const uint32_t A = args.A;
   const uint64_t nchunks = (args.nbody + kChunk - 1) / kChunk;
   const uint64_t c0 = (uint64_t)blockIdx.x * nchunks / gridDim.x;
   const uint64_t c1 = (uint64_t)(blockIdx.x + 1) * nchunks / gridDim.x;
   const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, kConsWarps);
     }
-    *oow = 0;
     fence_mbar_init();
     if (blockIdx.x == 0 && args.add_records) red_add_u64(args.totals + 0, args.add_records);
   }
-  if (!kBig) {
+  if (!kBig)
     for (uint32_t i = threadIdx.x; i < 2 * A; i += kThreads) sB[i] = args.bounds[i];
-    for (uint32_t i = threadIdx.x; i <= A; i += kThreads) own_cnt[i] = 0;
-  }
   __syncthreads();
 
   if (warp == kConsWarps) {
     // ---------------- producer warp: TMA bulk copies into the ring ----------------
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
       uint32_t it = 0;
       for (uint64_t ch = c0; ch < c1; ++ch, ++it) {
@@ -319,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args) 
   Ctx c;
   c.va_lo = args.va_lo;
   c.va_hi = args.va_hi;
+  c.wbytes = args.va_hi - args.va_lo;
   c.s = args.page_shift;
   c.A = A;
   c.B = kBig ? args.bounds : sB;
@@ -332,64 +414,78 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args) 
   o.ids = args.ids;
   o.max_ids = args.max_ids;
   o.words = args.words;
-  o.own_cnt = own_cnt;
-  o.oow = oow;
+  o.A = A;
 
-  Lane L;
-  L.olo = 1;
-  L.ospan = 0;  // forces a search on the first lookup
-  L.cnt = 0;
-  L.kbit = kOOW;
-  lookup<kBig>(L, 0ull, c);
+  OwnCache oc;
+  oc.olo = 1;
+  oc.ospan = 0;  // forces a search on the first lookup
+  oc.own = A;
+  WarpAcc w;
+  w.page = kOOW - 1;
+  w.own = A;
+  w.pcnt = 0;
+  w.ocnt = 0;
+  LaneAcc la;
+  la.own = A;
+  la.ocnt = 0;
+  la.kbit = kOOW;
 
   const uint32_t K = args.n_kernels;
   uint32_t k = 0;
   uint64_t kend = ~0ull;
   if (kRows && K > 1 && c0 < c1) {
-    k = kernel_of(args.koffs, K, args.gidx0 + c0 * kChunk);
+    k = kernel_of(args.koffs, K, args.gidx0 + c0 * kChunk + (uint64_t)warp * kSlice);
     kend = (k + 1 < K) ? __ldg(args.koffs + k + 1) : ~0ull;
   }
-
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t base = threadIdx.x * kRPT;         // chunk position of my first record
-  const uint32_t rsh = lane / (8 / kVec);           // LDS.128 rotation (bank-conflict free)
 
   uint32_t it = 0;
   for (uint64_t ch = c0; ch < c1; ++ch, ++it) {
     const uint32_t st = it % kStages;
     mbar_wait(full + st, (it / kStages) & 1u);
-    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(ring + (size_t)st * kChunk + base);
-    uint64_t a[kRPT];
+    const ulonglong2* src =
+        reinterpret_cast<const ulonglong2*>(ring + (size_t)st * kChunk + (size_t)warp * kSlice) + lane;
+    uint64_t a[8];
 #pragma unroll
-    for (int i = 0; i < kVec; ++i) {
-      const ulonglong2 v = src[(i + rsh) % kVec];
+    for (int i = 0; i < 4; ++i) {
+      const ulonglong2 v = src[32 * i];
       a[2 * i] = v.x;
       a[2 * i + 1] = v.y;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
 
-    const uint64_t g0 = args.gidx0 + ch * kChunk;
     const uint64_t remc = args.nbody - ch * kChunk;
     const uint32_t valid = (uint32_t)(remc < (uint64_t)kChunk ? remc : (uint64_t)kChunk);
+    const uint32_t wbase = (uint32_t)warp * kSlice;
+    if (valid <= wbase) continue;
+    const uint32_t wvalid = (valid - wbase) < (uint32_t)kSlice ? (valid - wbase) : (uint32_t)kSlice;
+    const uint64_t gw = args.gidx0 + ch * kChunk + wbase;
     uint32_t r0 = 0;
     for (;;) {
-      if (kRows && g0 + r0 >= kend) {
-        segment_flush<kBig, kRows, kPages>(L, o, A, k);
-        while (k + 1 < K && __ldg(args.koffs + k + 1) <= g0 + r0) ++k;
+      if (kRows && gw + r0 >= kend) {
+        warp_flush<kRows, kPages>(w, la, o, k, lane);
+        while (k + 1 < K && __ldg(args.koffs + k + 1) <= gw + r0) ++k;
         kend = (k + 1 < K) ? __ldg(args.koffs + k + 1) : ~0ull;
       }
-      uint32_t r1 = valid;
-      if (kRows && kend - g0 < (uint64_t)r1) r1 = (uint32_t)(kend - g0);
-      if (r0 == 0 && r1 == (uint32_t)kChunk)
-        process<false, kBig, kRows, kPages>(a, base, rsh, r0, r1, L, c, o, k);
-      else
-        process<true, kBig, kRows, kPages>(a, base, rsh, r0, r1, L, c, o, k);
+      uint32_t r1 = wvalid;
+      if (kRows && kend - gw < (uint64_t)r1) r1 = (uint32_t)(kend - gw);
+      if (r0 == 0 && r1 == (uint32_t)kSlice) {
+        process_full<kBig, kRows, kPages>(a, oc, la, w, c, o, k, lane);
+      } else {
+        // positions of a[2i+h] in the slice: 64i + 2*lane + h
+        uint32_t vm = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t pos = 64u * (i >> 1) + 2u * lane + (i & 1);
+          if (pos >= r0 && pos < r1) vm |= 1u << i;
+        }
+        process_lane<kBig, kRows, kPages>(a, vm, oc, la, w, c, o, k, lane);
+      }
       r0 = r1;
-      if (r0 >= valid) break;
+      if (r0 >= wvalid) break;
     }
   }
-  segment_flush<kBig, kRows, kPages>(L, o, A, k);
+  warp_flush<kRows, kPages>(w, la, o, k, lane);
 }
 
 // The <= 2 records outside the aligned even body (unaligned head, odd tail): one
@@ -407,28 +503,30 @@ __global__ void scan_extras_kernel(const ExtraArgs ea) {
   Ctx c;
   c.va_lo = s.va_lo;
   c.va_hi = s.va_hi;
+  c.wbytes = s.va_hi - s.va_lo;
   c.s = s.page_shift;
   c.A = s.A;
   c.B = s.bounds;
-  Lane L;
-  L.olo = 1;
-  L.ospan = 0;
-  lookup<true>(L, a, c);
+  OwnCache oc;
+  oc.olo = 1;
+  oc.ospan = 0;
+  oc.own = s.A;
+  const Ival I = lookup<true>(oc, a, c);
   Out o{};
+  o.page_counts = s.page_counts;
   o.alloc_counts = s.alloc_counts;
   o.totals = s.totals;
   o.kac = s.kac;
   o.kstats = s.kstats;
+  o.kpb = s.kpb;
   o.ids = s.ids;
   o.max_ids = s.max_ids;
-  if (rows) owner_to_global<true>(o, L.own, s.A, 1, k);
-  else owner_to_global<false>(o, L.own, s.A, 1, k);
-  if (L.page == kOOW) {
-    red_add_u64(s.totals + 2, 1);
-  } else {
-    red_add_u64(s.page_counts + L.page, 1);
-    if (s.kpb) red_or_u64(s.kpb + (uint64_t)k * s.words + (L.page >> 6), 1ull << (L.page & 63));
-  }
+  o.words = s.words;
+  o.A = s.A;
+  if (rows) owner_to_global<true>(o, I.own, 1, k);
+  else owner_to_global<false>(o, I.own, 1, k);
+  if (s.kpb) page_to_global<true>(o, I.page, 1, k);
+  else page_to_global<false>(o, I.page, 1, k);
 }
 
 template <bool kBig, bool kRows, bool kPages>
@@ -444,12 +542,12 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
 }  // namespace
 
 bool scan_table_fits_smem(uint32_t A) {
-  return (size_t)kRingBytes + kMiscBytes + 16ull * A + 4ull * (A + 1) + 64 <= (size_t)kSmemLimit;
+  return (size_t)kRingBytes + kMiscBytes + 16ull * A + 64 <= (size_t)kSmemLimit;
 }
 
 int scan_smem_bytes(uint32_t A, bool big_table) {
   if (big_table) return kRingBytes + kMiscBytes;
-  return (int)(kRingBytes + kMiscBytes + 16ull * A + 4ull * (A + 1));
+  return (int)(kRingBytes + kMiscBytes + 16ull * A);
 }
 
 cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st) {
@@ -470,7 +568,5 @@ cudaError_t launch_scan_extras(const ExtraArgs& a, cudaStream_t st) {
   scan_extras_kernel<<<1, 32, 0, st>>>(a);
   return cudaGetLastError();
 }
-
-int scan_chunk_records() { return kChunk; }
 
 }  // namespace pasta
