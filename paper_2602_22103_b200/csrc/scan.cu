@@ -7,24 +7,31 @@
 // associated memory object upon each access". The paper's lookup / counting
 // method is unstated; this is our sm_100a design:
 //
-//  * persistent grid, one CTA per SM; each CTA owns a contiguous run of 32 KiB
-//    chunks; one producer warp streams them global -> shared with 1-D TMA bulk copies
-//    (cp.async.bulk + mbarrier complete_tx, L2 evict_first) into a 4-stage ring;
-//  * 16 consumer warps; warp w takes the 256-record slice [256w, 256w+256) of each
-//    chunk with four conflict-free LDS.128 per lane (lane l holds slice positions
-//    64i + 2l + {0,1}, i = 0..3, in position order);
+//  * persistent grid, one CTA of 16 warps per SM; the records are cut into 2 KiB
+//    slices (256 records) and every warp owns a contiguous run of slices; each warp
+//    runs its own TMA pipeline: lane 0 keeps S-1 slices in flight with 1-D bulk
+//    copies (cp.async.bulk + mbarrier complete_tx, L2 evict_first) into the warp's
+//    S-slot shared-memory ring (S = 6 or 7 by the table size), so warps never wait
+//    on each other;
+//  * a slice is read with four conflict-free LDS.128 per lane (lane l holds slice
+//    positions 64i + 2l + {0,1}, i = 0..3, in position order);
 //  * every address resolves to exactly one *interval* = (live range or gap between
 //    ranges) intersected with (page or out-of-window region); the owner part comes
 //    from a binary search over the sorted boundary array B = [base_0, end_0, ...]
 //    in shared memory (count c of boundaries <= a: odd => range (c-1)/2, even =>
 //    gap), cached per lane; the page part is arithmetic;
-//  * tier W (warp-uniform): A = interval of the slice's first record, B = interval
-//    of its last; if A == B or B starts right after A, and every lane's 8 records are
-//    non-decreasing with a_0 >= A.lo and a_7 <= B.last, then every record is in
-//    A u B and the A-count is #{a <= A.last}: one __reduce_add_sync per slice;
-//  * tier L (per lane): A = interval of the lane's first record, B = interval of its
-//    first record outside A, membership counts; the (page, owner, count) pairs of
-//    the warp are merged by a leader loop (ballot / shfl / __reduce_add_sync);
+//  * tier W (warp-uniform): A = interval of the slice's first record (usually the
+//    warp's cached interval), B = interval of its last; if A == B or B starts right
+//    after A, and every lane's 8 records are non-decreasing with a_0 >= A.lo and
+//    a_7 <= B.last, then every record is in A u B and the A-count is #{a <= A.last}:
+//    one __reduce_add_sync per slice;
+//  * tier W2 (warp-uniform): same A and B, per-record membership (tile jumps, row
+//    switches: two intervals that are not adjacent);
+//  * tier L (per lane): the slice is re-read lane-contiguously (8 consecutive
+//    records per lane, rotated LDS.128 order); A = interval of the lane's first
+//    record, B = interval of its first record outside A, membership counts; the
+//    (page, owner, count) pairs of the warp are merged by a leader loop (ballot /
+//    shfl / __reduce_add_sync);
 //  * tier F (per lane, rare): records in neither A nor B are looked up one by one;
 //  * counts accumulate in warp-uniform registers (current page, current owner) and
 //    are flushed by one lane with red.global.add.u64 when the page / owner changes,
@@ -40,16 +47,16 @@ namespace {
 
 using namespace dev;
 
-constexpr int kConsWarps = 16;
-constexpr int kCons = kConsWarps * 32;  // consumer threads
-constexpr int kThreads = kCons + 32;    // + one producer warp
-constexpr int kSlice = 256;             // records per warp per chunk (8 per lane)
-constexpr int kChunk = kConsWarps * kSlice;  // 4096 records = 32 KiB
-constexpr int kStages = 4;
-constexpr uint32_t kChunkBytes = kChunk * 8;
-constexpr int kRingBytes = kStages * kChunkBytes;
-constexpr int kMiscBytes = 2 * kStages * 8 + 16;
+constexpr int kWarps = 16;
+constexpr int kThreads = kWarps * 32;
+constexpr int kSlice = 256;                 // records per slice (8 per lane)
+constexpr uint32_t kSliceBytes = kSlice * 8;  // 2 KiB
+constexpr int kMaxStages = 8;
+constexpr int kMinStages = 3;
+constexpr int kBarBytes = kWarps * kMaxStages * 8;
 constexpr int kSmemLimit = 227 * 1024;
+
+__host__ __device__ constexpr int ring_bytes(int stages) { return kWarps * stages * (int)kSliceBytes; }
 
 struct Ctx {
   uint64_t va_lo, va_hi, wbytes;  // window, wbytes = va_hi - va_lo
@@ -276,43 +283,115 @@ __device__ __forceinline__ void process_lane(const uint64_t (&a)[8], uint32_t va
       miss &= ~inB;
     }
     if (__any_sync(kFull, miss != 0)) {
+      // a rolled loop over the remaining records keeps the compiler from hoisting the
+      // per-record address arithmetic of the rare path into every slice
+#pragma unroll 1
+      while (miss) {
+        const int i = __ffs(miss) - 1;
+        miss &= miss - 1;
+        uint64_t z = a[0];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if ((miss >> i) & 1u) fallback_record<kBig, kRows, kPages>(a[i], oc, la, c, o, k);
+        for (int j = 1; j < 8; ++j) z = (i == j) ? a[j] : z;
+        fallback_record<kBig, kRows, kPages>(z, oc, la, c, o, k);
+      }
     }
   }
   merge_entries<kRows, kPages>(w, o, k, lane, cA > 0, IA.page, IA.own, cA, cB > 0, IB.page, IB.own, cB);
 }
 
-// Full 256-record slice: tier W, else tier L/F.
+__device__ __forceinline__ uint32_t lo32(uint64_t x) { return static_cast<uint32_t>(x); }
+__device__ __forceinline__ uint32_t hi32(uint64_t x) { return static_cast<uint32_t>(x >> 32); }
+
+// #{ i : v[i] <= t } for non-decreasing v[0..7] (three probes + the top element).
+__device__ __forceinline__ uint32_t count_sorted8(const uint32_t (&v)[8], uint32_t t) {
+  uint32_t c = (v[3] <= t) ? 4u : 0u;
+  const uint32_t x = c ? v[5] : v[1];
+  c += (x <= t) ? 2u : 0u;
+  const uint32_t y = (c & 4u) ? ((c & 2u) ? v[6] : v[4]) : ((c & 2u) ? v[2] : v[0]);
+  c += (y <= t) ? 1u : 0u;
+  return (v[7] <= t) ? 8u : c;
+}
+
+// Full 256-record slice. `a` holds the strided view (lane l: positions 64i + 2l + h);
+// `slot` is the slice's shared-memory address (for the lane-contiguous re-read).
 template <bool kBig, bool kRows, bool kPages>
-__device__ __forceinline__ void process_full(const uint64_t (&a)[8], OwnCache& oc, LaneAcc& la, WarpAcc& w,
-                                             const Ctx& c, const Out& o, uint32_t k, uint32_t lane) {
+__device__ __forceinline__ void process_full(const uint64_t (&a)[8], uint32_t slot, Ival& cur, OwnCache& oc,
+                                             LaneAcc& la, WarpAcc& w, const Ctx& c, const Out& o, uint32_t k,
+                                             uint32_t lane) {
   const uint64_t xf = __shfl_sync(kFull, a[0], 0);
   const uint64_t xl = __shfl_sync(kFull, a[7], 31);
-  const Ival IA = lookup<kBig>(oc, xf, c);
+  Ival IA = cur;
+  if (!inside(xf, IA)) IA = lookup<kBig>(oc, xf, c);
   const bool same = inside(xl, IA);
   Ival IB = IA;
   if (!same) IB = lookup<kBig>(oc, xl, c);
+  cur = IB;
   const uint64_t alast = IA.lo + IA.span;
-  const bool ok = same || (IB.lo - 1 == alast);
-  bool lane_ok = ok && a[0] >= IA.lo && a[7] <= IB.lo + IB.span;
+  const uint64_t blast = IB.lo + IB.span;
+  const uint32_t H = hi32(IA.lo);
+  // ---- tier W: A u B is one 32-bit-addressable range and every lane is sorted ----
+  if ((same || IB.lo - 1 == alast) && hi32(blast) == H) {
+    uint32_t v[8];
+    bool ok = true;
 #pragma unroll
-  for (int i = 0; i < 7; ++i) lane_ok = lane_ok && (a[i] <= a[i + 1]);
-  if (__all_sync(kFull, lane_ok)) {
-    if (same) {
-      wadd<kRows, kPages>(w, o, IA.page, IA.own, kSlice, k, lane);
+    for (int i = 0; i < 8; ++i) {
+      v[i] = lo32(a[i]);
+      ok = ok && hi32(a[i]) == H;
+    }
+    ok = ok && v[0] >= lo32(IA.lo) && v[7] <= lo32(blast);
+#pragma unroll
+    for (int i = 0; i < 7; ++i) ok = ok && v[i] <= v[i + 1];
+    if (__all_sync(kFull, ok)) {
+      if (same) {
+        wadd<kRows, kPages>(w, o, IA.page, IA.own, kSlice, k, lane);
+      } else {
+        const uint32_t sA = __reduce_add_sync(kFull, count_sorted8(v, lo32(alast)));
+        wadd<kRows, kPages>(w, o, IA.page, IA.own, sA, k, lane);
+        wadd<kRows, kPages>(w, o, IB.page, IB.own, kSlice - sA, k, lane);
+      }
+      return;
+    }
+  }
+  // ---- tier W2: every record in A or B, any order ----
+  {
+    uint32_t cA = 0;
+    bool ok = true;
+    if (hi32(alast) == H && hi32(IB.lo) == hi32(blast)) {
+      const uint32_t HB = hi32(IB.lo), LA = lo32(IA.lo), LB = lo32(IB.lo);
+      const uint32_t SA = lo32(IA.span), SB = lo32(IB.span);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool inA = hi32(a[i]) == H && lo32(a[i]) - LA <= SA;
+        const bool inB = hi32(a[i]) == HB && lo32(a[i]) - LB <= SB;
+        cA += inA ? 1u : 0u;
+        ok = ok && (inA || inB);
+      }
     } else {
-      uint32_t cA = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) cA += (a[i] <= alast) ? 1u : 0u;
+      for (int i = 0; i < 8; ++i) {
+        const bool inA = inside(a[i], IA);
+        cA += inA ? 1u : 0u;
+        ok = ok && (inA || inside(a[i], IB));
+      }
+    }
+    if (__all_sync(kFull, ok)) {
       const uint32_t sA = __reduce_add_sync(kFull, cA);
       wadd<kRows, kPages>(w, o, IA.page, IA.own, sA, k, lane);
-      wadd<kRows, kPages>(w, o, IB.page, IB.own, kSlice - sA, k, lane);
+      if (sA != (uint32_t)kSlice) wadd<kRows, kPages>(w, o, IB.page, IB.own, kSlice - sA, k, lane);
+      return;
     }
-    return;
   }
-  process_lane<kBig, kRows, kPages>(a, 0xFFu, oc, la, w, c, o, k, lane);
+  // ---- tier L: lane-contiguous re-read (8 consecutive records, rotated order) ----
+  uint64_t b[8];
+  const uint32_t rsh = (lane >> 1) & 3u;
+  const uint32_t base = slot + 64u * lane;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const ulonglong2 x = lds128(base + 16u * ((i + rsh) & 3u));
+    b[2 * i] = x.x;
+    b[2 * i + 1] = x.y;
+  }
+  process_lane<kBig, kRows, kPages>(b, 0xFFu, oc, la, w, c, o, k, lane);
 }
 
 // Warp-local flush of everything accumulated for kernel segment k.
@@ -353,50 +432,47 @@ __device__ __forceinline__ uint32_t kernel_of(const uint64_t* __restrict__ koffs
 }
 
 template <bool kBig, bool kRows, bool kPages>
-__global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args) {
+__global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* ring = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* sB = reinterpret_cast<uint64_t*>(smem + kRingBytes + kMiscBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages));
+  uint64_t* sB = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages) + kBarBytes);
 
   const uint32_t A = args.A;
-  const uint64_t nchunks = (args.nbody + kChunk - 1) / kChunk;
-  const uint64_t c0 = (uint64_t)blockIdx.x * nchunks / gridDim.x;
-  const uint64_t c1 = (uint64_t)(blockIdx.x + 1) * nchunks / gridDim.x;
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  // contiguous slice range [s0, s1) of this warp
+  const uint64_t nsl = (args.nbody + kSlice - 1) / kSlice;
+  const uint64_t gwarp = (uint64_t)blockIdx.x * kWarps + warp;
+  const uint64_t nwarp = (uint64_t)gridDim.x * kWarps;
+  const uint64_t s0 = gwarp * nsl / nwarp, s1 = (gwarp + 1) * nsl / nwarp;
+  const uint32_t nmy = (uint32_t)(s1 - s0);
+  // the last slice of the trace may be partial
+  const uint32_t tail_valid = (uint32_t)(args.nbody - (nsl - 1) * kSlice);
+  const uint32_t nfull = (s1 == nsl && tail_valid != (uint32_t)kSlice) ? nmy - 1 : nmy;
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, kConsWarps);
-    }
+  const uint32_t ring_u32 = smem_u32(smem) + (uint32_t)(warp * stages) * kSliceBytes;
+  const uint32_t bar_u32 = smem_u32(bars + warp * kMaxStages);
+
+  if (lane == 0) {
+    for (int j = 0; j < stages; ++j) mbar_init(bars + warp * kMaxStages + j, 1);
     fence_mbar_init();
-    if (blockIdx.x == 0 && args.add_records) red_add_u64(args.totals + 0, args.add_records);
+    if (blockIdx.x == 0 && warp == 0 && args.add_records) red_add_u64(args.totals + 0, args.add_records);
   }
   if (!kBig)
     for (uint32_t i = threadIdx.x; i < 2 * A; i += kThreads) sB[i] = args.bounds[i];
   __syncthreads();
 
-  if (warp == kConsWarps) {
-    // ---------------- producer warp: TMA bulk copies into the ring ----------------
-    if (lane == 0) {
-      const uint64_t pol = l2_evict_first_policy();
-      uint32_t it = 0;
-      for (uint64_t ch = c0; ch < c1; ++ch, ++it) {
-        const uint32_t st = it % kStages;
-        if (it >= kStages) mbar_wait(empty + st, ((it / kStages) & 1u) ^ 1u);
-        const uint64_t rem = args.nbody - ch * kChunk;
-        const uint32_t bytes = (uint32_t)((rem < (uint64_t)kChunk ? rem : (uint64_t)kChunk) * 8);
-        mbar_arrive_expect_tx(full + st, bytes);
-        tma_load_1d(ring + (size_t)st * kChunk, args.rec + ch * kChunk, bytes, full + st, pol);
-      }
-    }
-    return;
-  }
+  const uint64_t pol = l2_evict_first_policy();
+  const uint64_t* wrec = args.rec + s0 * kSlice;  // this warp's first record
+  // TMA for relative slice j into ring slot `slot` (lane 0 only)
+  auto issue = [&](uint32_t j, uint32_t slot) {
+    const uint32_t bytes = j < nfull ? kSliceBytes : tail_valid * 8u;
+    mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, bytes);
+    tma_load_1d_u32(ring_u32 + slot * kSliceBytes, wrec + (uint64_t)j * kSlice, bytes, bar_u32 + 8u * slot, pol);
+  };
+  if (lane == 0)
+    for (uint32_t j = 0; j < (uint32_t)stages && j < nmy; ++j) issue(j, j);
 
-  // ---------------- consumer warps ----------------
   Ctx c;
   c.va_lo = args.va_lo;
   c.va_hi = args.va_hi;
@@ -420,6 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args) 
   oc.olo = 1;
   oc.ospan = 0;  // forces a search on the first lookup
   oc.own = A;
+  Ival cur = lookup<kBig>(oc, 0ull, c);  // a valid interval (the one holding address 0)
   WarpAcc w;
   w.page = kOOW - 1;
   w.own = A;
@@ -430,59 +507,77 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args) 
   la.ocnt = 0;
   la.kbit = kOOW;
 
+  // Kernel segments: records are global index gbase + r, r = 256 j + position.
+  const uint64_t gbase = args.gidx0 + s0 * kSlice;
   const uint32_t K = args.n_kernels;
   uint32_t k = 0;
-  uint64_t kend = ~0ull;
-  if (kRows && K > 1 && c0 < c1) {
-    k = kernel_of(args.koffs, K, args.gidx0 + c0 * kChunk + (uint64_t)warp * kSlice);
+  uint64_t kend = ~0ull;  // global index where segment k ends
+  if (kRows && K > 1 && nmy > 0) {
+    k = kernel_of(args.koffs, K, gbase);
     kend = (k + 1 < K) ? __ldg(args.koffs + k + 1) : ~0ull;
   }
+  // first relative slice that is not a plain full slice inside segment k
+  auto next_event = [&]() -> uint32_t {
+    uint64_t e = nfull;
+    if (kRows && kend != ~0ull) {
+      const uint64_t kb = (kend - gbase) / kSlice;  // slice holding record kend (or starting at it)
+      if (kb < e) e = kb;
+    }
+    return (uint32_t)e;
+  };
+  uint32_t jev = next_event();
 
-  uint32_t it = 0;
-  for (uint64_t ch = c0; ch < c1; ++ch, ++it) {
-    const uint32_t st = it % kStages;
-    mbar_wait(full + st, (it / kStages) & 1u);
-    const ulonglong2* src =
-        reinterpret_cast<const ulonglong2*>(ring + (size_t)st * kChunk + (size_t)warp * kSlice) + lane;
+  uint32_t slot = 0, phase = 0;
+  for (uint32_t j = 0; j < nmy; ++j) {
+    const uint32_t sa = ring_u32 + slot * kSliceBytes;
+    mbar_wait_u32(bar_u32 + 8u * slot, phase);
     uint64_t a[8];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const ulonglong2 v = src[32 * i];
+      const ulonglong2 v = lds128(sa + 16u * lane + 512u * i);
       a[2 * i] = v.x;
       a[2 * i + 1] = v.y;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + st);
-
-    const uint64_t remc = args.nbody - ch * kChunk;
-    const uint32_t valid = (uint32_t)(remc < (uint64_t)kChunk ? remc : (uint64_t)kChunk);
-    const uint32_t wbase = (uint32_t)warp * kSlice;
-    if (valid <= wbase) continue;
-    const uint32_t wvalid = (valid - wbase) < (uint32_t)kSlice ? (valid - wbase) : (uint32_t)kSlice;
-    const uint64_t gw = args.gidx0 + ch * kChunk + wbase;
-    uint32_t r0 = 0;
-    for (;;) {
-      if (kRows && gw + r0 >= kend) {
-        warp_flush<kRows, kPages>(w, la, o, k, lane);
-        while (k + 1 < K && __ldg(args.koffs + k + 1) <= gw + r0) ++k;
-        kend = (k + 1 < K) ? __ldg(args.koffs + k + 1) : ~0ull;
-      }
-      uint32_t r1 = wvalid;
-      if (kRows && kend - gw < (uint64_t)r1) r1 = (uint32_t)(kend - gw);
-      if (r0 == 0 && r1 == (uint32_t)kSlice) {
-        process_full<kBig, kRows, kPages>(a, oc, la, w, c, o, k, lane);
-      } else {
-        // positions of a[2i+h] in the slice: 64i + 2*lane + h
-        uint32_t vm = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint32_t pos = 64u * (i >> 1) + 2u * lane + (i & 1);
-          if (pos >= r0 && pos < r1) vm |= 1u << i;
+    if (j != jev) {
+      process_full<kBig, kRows, kPages>(a, sa, cur, oc, la, w, c, o, k, lane);
+    } else {
+      // kernel boundary in or at this slice, or the partial tail slice
+      const uint32_t valid = j < nfull ? (uint32_t)kSlice : tail_valid;
+      const uint64_t g0 = gbase + (uint64_t)j * kSlice;
+      uint32_t r0 = 0;
+      for (;;) {
+        if (kRows && g0 + r0 >= kend) {
+          warp_flush<kRows, kPages>(w, la, o, k, lane);
+          while (k + 1 < K && __ldg(args.koffs + k + 1) <= g0 + r0) ++k;
+          kend = (k + 1 < K) ? __ldg(args.koffs + k + 1) : ~0ull;
         }
-        process_lane<kBig, kRows, kPages>(a, vm, oc, la, w, c, o, k, lane);
+        uint32_t r1 = valid;
+        if (kRows && kend - g0 < (uint64_t)r1) r1 = (uint32_t)(kend - g0);
+        if (r0 == 0 && r1 == (uint32_t)kSlice) {
+          process_full<kBig, kRows, kPages>(a, sa, cur, oc, la, w, c, o, k, lane);
+        } else {
+          uint32_t vm = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t pos = 64u * (i >> 1) + 2u * lane + (i & 1);
+            if (pos >= r0 && pos < r1) vm |= 1u << i;
+          }
+          process_lane<kBig, kRows, kPages>(a, vm, oc, la, w, c, o, k, lane);
+        }
+        r0 = r1;
+        if (r0 >= valid) break;
       }
-      r0 = r1;
-      if (r0 >= wvalid) break;
+      jev = next_event();  // > j: kend now lies beyond every record of this slice
+    }
+    // the slot is free again: refill it with the slice `stages` ahead
+    __syncwarp();
+    if (lane == 0 && j + stages < nmy) {
+      fence_proxy_async_smem();
+      issue(j + stages, slot);
+    }
+    if (++slot == (uint32_t)stages) {
+      slot = 0;
+      phase ^= 1u;
     }
   }
   warp_flush<kRows, kPages>(w, la, o, k, lane);
@@ -529,25 +624,31 @@ __global__ void scan_extras_kernel(const ExtraArgs ea) {
   else page_to_global<false>(o, I.page, 1, k);
 }
 
+int stages_for(uint32_t A, bool big) {
+  const long table = big ? 0 : 16l * A;
+  const long avail = (long)kSmemLimit - kBarBytes - table;
+  long st = avail / ring_bytes(1);
+  if (st > kMaxStages) st = kMaxStages;
+  return (int)st;
+}
+
 template <bool kBig, bool kRows, bool kPages>
 cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
+  const int stages = stages_for(a.A, kBig);
   const int smem = scan_smem_bytes(a.A, kBig);
   auto fn = scan_kernel<kBig, kRows, kPages>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  fn<<<grid, kThreads, smem, st>>>(a);
+  fn<<<grid, kThreads, smem, st>>>(a, stages);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-bool scan_table_fits_smem(uint32_t A) {
-  return (size_t)kRingBytes + kMiscBytes + 16ull * A + 64 <= (size_t)kSmemLimit;
-}
+bool scan_table_fits_smem(uint32_t A) { return stages_for(A, false) >= kMinStages; }
 
 int scan_smem_bytes(uint32_t A, bool big_table) {
-  if (big_table) return kRingBytes + kMiscBytes;
-  return (int)(kRingBytes + kMiscBytes + 16ull * A);
+  return ring_bytes(stages_for(A, big_table)) + kBarBytes + (big_table ? 0 : (int)(16ull * A));
 }
 
 cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st) {
