@@ -32,6 +32,13 @@ oracle/liboracle.so: oracle/oracle.cpp
 $(PKG)/libpasta.so: $(PASTA_CU) $(PASTA_CPP) $(PASTA_H)
 	$(NVCC) $(NVFLAGS) -Iinclude -I$(CSRC) -shared -o $@ $(PASTA_CU) $(PASTA_CPP) 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
 
+# A/B variants of the scan (same ABI): make variants VARIANTS="name:-DFLAG=1 ..."
+variants: $(PASTA_CU) $(PASTA_CPP) $(PASTA_H)
+	mkdir -p build/variants
+	@for v in $(VARIANTS); do n=$${v%%:*}; f=$$(echo $${v#*:} | tr ',' ' '); \
+	  echo "variant $$n: $$f"; \
+	  $(NVCC) $(NVFLAGS) $$f -Iinclude -I$(CSRC) -shared -o build/variants/libpasta_$$n.so $(PASTA_CU) $(PASTA_CPP) 2>/dev/null || exit 1; done
+
 clean:
 	rm -f $(LIBS) build_ptxas.log
 

@@ -18,7 +18,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libpasta.so")
+# PASTA_LIB selects an alternative build of the same C ABI (A/B performance runs).
+_LIB_PATH = os.environ.get("PASTA_LIB") or os.path.join(_HERE, "libpasta.so")
 if not os.path.exists(_LIB_PATH):
     raise ImportError(f"{_LIB_PATH} is missing: build it with `make` or __graft_entry__.build() "
                       "(there is no CPU fallback)")

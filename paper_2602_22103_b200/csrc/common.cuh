@@ -89,6 +89,12 @@ __device__ __forceinline__ ulonglong2 lds128(uint32_t a) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+
 // Order this thread's prior generic-proxy shared-memory accesses before later
 // async-proxy (TMA) writes to the same buffer.
 __device__ __forceinline__ void fence_proxy_async_smem() {

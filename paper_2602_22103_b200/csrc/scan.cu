@@ -42,6 +42,13 @@
 #include "common.cuh"
 #include "internal.h"
 
+#ifndef PASTA_SWPIPE
+#define PASTA_SWPIPE 0
+#endif
+#ifndef PASTA_XFL_LDS
+#define PASTA_XFL_LDS 1
+#endif
+
 namespace pasta {
 namespace {
 
@@ -318,8 +325,13 @@ template <bool kBig, bool kRows, bool kPages>
 __device__ __forceinline__ void process_full(const uint64_t (&a)[8], uint32_t slot, Ival& cur, OwnCache& oc,
                                              LaneAcc& la, WarpAcc& w, const Ctx& c, const Out& o, uint32_t k,
                                              uint32_t lane) {
+#if PASTA_XFL_LDS
+  const uint64_t xf = lds64(slot);
+  const uint64_t xl = lds64(slot + 8u * (kSlice - 1));
+#else
   const uint64_t xf = __shfl_sync(kFull, a[0], 0);
   const uint64_t xl = __shfl_sync(kFull, a[7], 31);
+#endif
   Ival IA = cur;
   if (!inside(xf, IA)) IA = lookup<kBig>(oc, xf, c);
   const bool same = inside(xl, IA);
@@ -527,6 +539,32 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   };
   uint32_t jev = next_event();
 
+#if PASTA_SWPIPE
+  // Software pipeline: the registers of slice j+1 are loaded (LDS) before slice j is
+  // processed, so the shared-memory latency hides behind the processing.
+  uint64_t nxt[8];
+  auto load_slice = [&](uint32_t slot_, uint32_t phase_) {
+    const uint32_t sa_ = ring_u32 + slot_ * kSliceBytes;
+    mbar_wait_u32(bar_u32 + 8u * slot_, phase_);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const ulonglong2 v = lds128(sa_ + 16u * lane + 512u * i);
+      nxt[2 * i] = v.x;
+      nxt[2 * i + 1] = v.y;
+    }
+  };
+  if (nmy > 0) load_slice(0, 0);
+  uint32_t slot = 0, phase = 0;
+  for (uint32_t j = 0; j < nmy; ++j) {
+    const uint32_t sa = ring_u32 + slot * kSliceBytes;
+    uint64_t a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = nxt[i];
+    if (j + 1 < nmy) {
+      const uint32_t ns = slot + 1 == (uint32_t)stages ? 0u : slot + 1;
+      load_slice(ns, ns == 0 ? phase ^ 1u : phase);
+    }
+#else
   uint32_t slot = 0, phase = 0;
   for (uint32_t j = 0; j < nmy; ++j) {
     const uint32_t sa = ring_u32 + slot * kSliceBytes;
@@ -538,6 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
       a[2 * i] = v.x;
       a[2 * i + 1] = v.y;
     }
+#endif
     if (j != jev) {
       process_full<kBig, kRows, kPages>(a, sa, cur, oc, la, w, c, o, k, lane);
     } else {
@@ -569,12 +608,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
       }
       jev = next_event();  // > j: kend now lies beyond every record of this slice
     }
-    // the slot is free again: refill it with the slice `stages` ahead
+    // the slot is free again (every lane has consumed its values): refill it with the
+    // slice `stages` ahead
     __syncwarp();
-    if (lane == 0 && j + stages < nmy) {
-      fence_proxy_async_smem();
-      issue(j + stages, slot);
-    }
+    if (lane == 0 && j + stages < nmy) issue(j + stages, slot);
     if (++slot == (uint32_t)stages) {
       slot = 0;
       phase ^= 1u;
