@@ -389,3 +389,40 @@ def test_full_config_sampled(name):
         if p.want_kernel_pages:
             assert np.array_equal(g["kpb"][k], o.kernel_pages[0]), (name, k)
     tr.close()
+
+
+def test_merger_world1_nccl():
+    """The NCCL merge path (all_reduce SUM of the packed counts, all_gather + the
+    pasta_bitmap_or kernel, all_reduce MAX of WS) at world size 1 leaves a finalized
+    result unchanged; its OR output equals the bitmap recomputed from the counts."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2602_22103_b200 import dist as pdist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=DEV)
+    try:
+        p = tracegen.build_plan("tiny", seed=9)
+        drec = torch.empty(p.n, dtype=torch.int64, device=DEV)
+        tracegen.device_records(tracegen.DevicePlan(p, DEV), drec)
+        tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs)
+        ko = torch.from_numpy(p.kernel_offsets.view(np.int64).copy()).to(DEV)
+        hist = tr.histograms(p.page_shift, n_kernels=p.n_kernels, kernel_rows=True)
+        tr.analyze(drec, p.page_shift, hist, kernel_offsets=ko)
+        tr.sync()
+        before = (u64(hist.packed).copy(), u64(hist.page_bitmap).copy())
+        pdist.Merger(tr, hist).merge()
+        tr.sync()
+        after = u64(hist.packed)
+        assert np.array_equal(after, before[0])
+        assert np.array_equal(u64(hist.page_bitmap), before[1])
+        bm, uq = oracle.bitmap(u64(hist.page_counts))
+        assert np.array_equal(u64(hist.page_bitmap), bm) and int(u64(hist.totals)[3]) == uq
+        tr.close()
+    finally:
+        dist.destroy_process_group()
