@@ -43,6 +43,7 @@ int scan_smem_bytes(uint32_t A, bool big_table);
 cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_scan_extras(const ExtraArgs& a, cudaStream_t st);
 bool scan_table_fits_smem(uint32_t A);
+int scan_warps();
 
 cudaError_t launch_finalize_bitmap(const uint64_t* page_counts, uint64_t P, uint64_t* bitmap, uint64_t* unique_out,
                                    int grid, cudaStream_t st);

@@ -198,8 +198,9 @@ int scan_range(pasta_trace* h, const uint64_t* rec, uint64_t n, uint64_t g0, Sca
     a.gidx0 = gb + off;
     a.add_records = added ? 0 : add_records;
     added = true;
-    const uint64_t slices = (cnt + 255) / 256;  // 2 KiB slices, 16 warps per CTA
-    const int grid = (int)std::min<uint64_t>((uint64_t)h->sm_count, (slices + 15) / 16);
+    const uint64_t slices = (cnt + 255) / 256;  // 2 KiB slices, scan_warps() warps per CTA
+    const uint64_t wpc = (uint64_t)scan_warps();
+    const int grid = (int)std::min<uint64_t>((uint64_t)h->sm_count, (slices + wpc - 1) / wpc);
     Timed t(h, PASTA_PH_SCAN, st);
     cudaError_t e = launch_scan(a, grid, st);
     ++h->launches;

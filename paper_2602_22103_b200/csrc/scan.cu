@@ -54,7 +54,10 @@ namespace {
 
 using namespace dev;
 
-constexpr int kWarps = 16;
+#ifndef PASTA_WARPS
+#define PASTA_WARPS 24
+#endif
+constexpr int kWarps = PASTA_WARPS;
 constexpr int kThreads = kWarps * 32;
 constexpr int kSlice = 256;                 // records per slice (8 per lane)
 constexpr uint32_t kSliceBytes = kSlice * 8;  // 2 KiB
@@ -681,6 +684,8 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
 }
 
 }  // namespace
+
+int scan_warps() { return kWarps; }
 
 bool scan_table_fits_smem(uint32_t A) { return stages_for(A, false) >= kMinStages; }
 
