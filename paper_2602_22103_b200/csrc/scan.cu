@@ -45,6 +45,12 @@
 #ifndef PASTA_SWPIPE
 #define PASTA_SWPIPE 0
 #endif
+#ifndef PASTA_TREE
+#define PASTA_TREE 0
+#endif
+#ifndef PASTA_FLAT_FLUSH
+#define PASTA_FLAT_FLUSH 0
+#endif
 #ifndef PASTA_XFL_LDS
 #define PASTA_XFL_LDS 1
 #endif
@@ -195,7 +201,15 @@ template <bool kRows, bool kPages>
 __device__ __forceinline__ void wadd(WarpAcc& w, const Out& o, uint32_t page, uint32_t own, uint32_t c, uint32_t k,
                                      uint32_t lane) {
   if (page != w.page) {
+#if PASTA_FLAT_FLUSH
+    // one predicated RED (no divergent branch): out-of-window counts go to totals[2]
+    uint64_t* dst = (w.page == kOOW) ? o.totals + 2 : o.page_counts + w.page;
+    if (lane == 0 && w.pcnt != 0) red_add_u64(dst, w.pcnt);
+    if (kPages && lane == 0 && w.pcnt != 0 && w.page != kOOW)
+      red_or_u64(o.kpb + (uint64_t)k * o.words + (w.page >> 6), 1ull << (w.page & 63));
+#else
     if (lane == 0) page_to_global<kPages>(o, w.page, w.pcnt, k);
+#endif
     w.page = page;
     w.pcnt = 0;
   }
@@ -347,15 +361,24 @@ __device__ __forceinline__ void process_full(const uint64_t (&a)[8], uint32_t sl
   // ---- tier W: A u B is one 32-bit-addressable range and every lane is sorted ----
   if ((same || IB.lo - 1 == alast) && hi32(blast) == H) {
     uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = lo32(a[i]);
+#if PASTA_TREE
+    // independent predicates combined by a balanced tree (short dependency chains)
+    const bool h01 = (hi32(a[0]) == H) & (hi32(a[1]) == H), h23 = (hi32(a[2]) == H) & (hi32(a[3]) == H);
+    const bool h45 = (hi32(a[4]) == H) & (hi32(a[5]) == H), h67 = (hi32(a[6]) == H) & (hi32(a[7]) == H);
+    const bool m03 = (v[0] <= v[1]) & (v[1] <= v[2]) & (v[2] <= v[3]);
+    const bool m37 = (v[3] <= v[4]) & (v[4] <= v[5]) & (v[5] <= v[6]) & (v[6] <= v[7]);
+    const bool ends = (v[0] >= lo32(IA.lo)) & (v[7] <= lo32(blast));
+    const bool ok = ((h01 & h23) & (h45 & h67)) & (m03 & m37) & ends;
+#else
     bool ok = true;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      v[i] = lo32(a[i]);
-      ok = ok && hi32(a[i]) == H;
-    }
+    for (int i = 0; i < 8; ++i) ok = ok && hi32(a[i]) == H;
     ok = ok && v[0] >= lo32(IA.lo) && v[7] <= lo32(blast);
 #pragma unroll
     for (int i = 0; i < 7; ++i) ok = ok && v[i] <= v[i + 1];
+#endif
     if (__all_sync(kFull, ok)) {
       if (same) {
         wadd<kRows, kPages>(w, o, IA.page, IA.own, kSlice, k, lane);
@@ -374,6 +397,16 @@ __device__ __forceinline__ void process_full(const uint64_t (&a)[8], uint32_t sl
     if (hi32(alast) == H && hi32(IB.lo) == hi32(blast)) {
       const uint32_t HB = hi32(IB.lo), LA = lo32(IA.lo), LB = lo32(IB.lo);
       const uint32_t SA = lo32(IA.span), SB = lo32(IB.span);
+#if PASTA_TREE
+      uint32_t mA = 0, mB = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        mA |= ((hi32(a[i]) == H) & (lo32(a[i]) - LA <= SA)) ? (1u << i) : 0u;
+        mB |= ((hi32(a[i]) == HB) & (lo32(a[i]) - LB <= SB)) ? (1u << i) : 0u;
+      }
+      cA = __popc(mA);
+      ok = (mA | mB) == 0xFFu;
+#else
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const bool inA = hi32(a[i]) == H && lo32(a[i]) - LA <= SA;
@@ -381,6 +414,7 @@ __device__ __forceinline__ void process_full(const uint64_t (&a)[8], uint32_t sl
         cA += inA ? 1u : 0u;
         ok = ok && (inA || inB);
       }
+#endif
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
