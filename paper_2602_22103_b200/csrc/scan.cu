@@ -51,6 +51,9 @@
 #ifndef PASTA_FLAT_FLUSH
 #define PASTA_FLAT_FLUSH 0
 #endif
+#ifndef PASTA_WADD2
+#define PASTA_WADD2 1
+#endif
 #ifndef PASTA_XFL_LDS
 #define PASTA_XFL_LDS 1
 #endif
@@ -222,6 +225,38 @@ __device__ __forceinline__ void wadd(WarpAcc& w, const Out& o, uint32_t page, ui
   w.ocnt += c;
 }
 
+// One predicated RED for a finished page run (out-of-window runs go to totals[2]).
+template <bool kPages>
+__device__ __forceinline__ void flush_page_run(const Out& o, uint32_t page, uint32_t v, uint32_t k, uint32_t lane) {
+  uint64_t* dst = (page == kOOW) ? o.totals + 2 : o.page_counts + page;
+  if (lane == 0) red_add_u64(dst, v);
+  if (kPages && lane == 0 && page != kOOW)
+    red_or_u64(o.kpb + (uint64_t)k * o.words + (page >> 6), 1ull << (page & 63));
+}
+
+// Accumulate sA records of interval A then sB of interval B (sB may be 0). Fast path:
+// A continues the warp's current page and owner and B has the same owner, so page A
+// is complete: one RED, no owner flush.
+template <bool kRows, bool kPages>
+__device__ __forceinline__ void wadd2(WarpAcc& w, const Out& o, const Ival& IA, uint32_t sA, const Ival& IB,
+                                      uint32_t sB, uint32_t k, uint32_t lane) {
+#if PASTA_WADD2
+  if (IA.page == w.page && IA.own == w.own && (sB == 0 || (IB.own == IA.own && IB.page != IA.page))) {
+    w.ocnt += sA + sB;
+    if (sB == 0) {
+      w.pcnt += sA;
+    } else {
+      flush_page_run<kPages>(o, IA.page, w.pcnt + sA, k, lane);
+      w.page = IB.page;
+      w.pcnt = sB;
+    }
+    return;
+  }
+#endif
+  wadd<kRows, kPages>(w, o, IA.page, IA.own, sA, k, lane);
+  if (sB) wadd<kRows, kPages>(w, o, IB.page, IB.own, sB, k, lane);
+}
+
 // Per-lane fallback accumulators (tier F).
 struct LaneAcc {
   uint32_t own, ocnt;
@@ -380,13 +415,8 @@ __device__ __forceinline__ void process_full(const uint64_t (&a)[8], uint32_t sl
     for (int i = 0; i < 7; ++i) ok = ok && v[i] <= v[i + 1];
 #endif
     if (__all_sync(kFull, ok)) {
-      if (same) {
-        wadd<kRows, kPages>(w, o, IA.page, IA.own, kSlice, k, lane);
-      } else {
-        const uint32_t sA = __reduce_add_sync(kFull, count_sorted8(v, lo32(alast)));
-        wadd<kRows, kPages>(w, o, IA.page, IA.own, sA, k, lane);
-        wadd<kRows, kPages>(w, o, IB.page, IB.own, kSlice - sA, k, lane);
-      }
+      const uint32_t sA = same ? (uint32_t)kSlice : __reduce_add_sync(kFull, count_sorted8(v, lo32(alast)));
+      wadd2<kRows, kPages>(w, o, IA, sA, IB, kSlice - sA, k, lane);
       return;
     }
   }
@@ -425,8 +455,7 @@ __device__ __forceinline__ void process_full(const uint64_t (&a)[8], uint32_t sl
     }
     if (__all_sync(kFull, ok)) {
       const uint32_t sA = __reduce_add_sync(kFull, cA);
-      wadd<kRows, kPages>(w, o, IA.page, IA.own, sA, k, lane);
-      if (sA != (uint32_t)kSlice) wadd<kRows, kPages>(w, o, IB.page, IB.own, kSlice - sA, k, lane);
+      wadd2<kRows, kPages>(w, o, IA, sA, IB, kSlice - sA, k, lane);
       return;
     }
   }
