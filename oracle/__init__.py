@@ -5,7 +5,8 @@ reference`` leg may import this package. It shares no code with the CUDA path
 (paper_2602_22103_b200/) and never imports it.
 
 ``OracleTrace`` mirrors the handle semantics of include/pasta.h with its own plain
-Python registration bookkeeping (a dict of live ranges, linear overlap checks), and
+Python registration bookkeeping (a dict of live ranges and a bisect-sorted list of
+bases for the overlap check), and
 delegates the per-record definition to oracle/oracle.cpp (std::map lookup, hash-map
 counts, std::sort top-K; SURVEY.md section 8(c)). Everything is accumulated in
 numpy uint64 arrays.
@@ -14,6 +15,7 @@ Status codes are the ones include/pasta.h documents (values restated, not import
 """
 from __future__ import annotations
 
+import bisect
 import ctypes
 import os
 
@@ -64,6 +66,7 @@ class OracleTrace:
         self.va_lo, self.va_hi = int(va_lo), int(va_hi)
         self.max_live, self.max_ids = int(max_live), int(max_ids)
         self.live = {}  # base -> (size, id)
+        self.bases = []  # sorted live bases
         self.sizes = []  # id -> registered size (ids are never reused)
         self.kernel_rows = None
         self.kun = None
@@ -78,7 +81,12 @@ class OracleTrace:
         base, size = int(base), int(size)
         if size <= 0 or base < 0 or base + size > U64MAX:
             return EINVAL, None
-        for b, (s, _) in self.live.items():
+        # intersecting live ranges: the nearest live base at or below base+size-1 is
+        # the only candidate (live ranges never overlap); a sorted list of bases
+        i = bisect.bisect_right(self.bases, base + size - 1) - 1
+        if i >= 0:
+            b = self.bases[i]
+            s = self.live[b][0]
             if base < b + s and b < base + size:  # half-open intervals intersect
                 return EOVERLAP, None
         if len(self.live) >= self.max_live or len(self.sizes) >= self.max_ids:
@@ -86,12 +94,14 @@ class OracleTrace:
         i = len(self.sizes)
         self.sizes.append(size)
         self.live[base] = (size, i)
+        bisect.insort(self.bases, base)
         return OK, i
 
     def register_free(self, base: int):
         if int(base) not in self.live:
             return ENOENT
         del self.live[int(base)]
+        self.bases.pop(bisect.bisect_left(self.bases, int(base)))
         return OK
 
     # ---- one analyze call, accumulating ----

@@ -34,16 +34,24 @@ constexpr int kBlock = 256;
 constexpr int kTile = 2048;  // bitonic shared-memory tile (elements)
 
 struct State {
-  unsigned long long nnz, maxc, kprime, remaining, prefix, mask;
-  long long shift;
-  unsigned long long done;  // 0 running, 1 nothing to select, 2 threshold found
-  unsigned long long T, need, gt_slots;
+  unsigned long long nnz, kprime;
+  unsigned long long lo;         // selected bin: counts in [lo, lo + 2^(shift+width) - 1]
+  unsigned long long above;      // pages with a count above the bin (all taken)
+  unsigned long long remaining;  // pages still to take from the bin
+  long long shift;               // low bit of the next digit
+  long long width;               // bits in the next digit
+  unsigned long long done;       // 0 refining, 1 nothing to select, 2 threshold fixed
+  unsigned long long T, need;    // take every count > T and the first `need` pages with count == T
+  unsigned long long gt_slots;
   unsigned long long pad[5];
 };
 
+constexpr int kDigitBits = 11;
+constexpr int kBins = 1 << kDigitBits;
+
 struct Scratch {
   State* st;
-  unsigned* hist;              // [256]
+  unsigned* hist;              // [kBins]
   unsigned long long* blkcnt;  // [grid]
   uint64_t* key_c;             // [Kp] counts
   uint64_t* key_p;             // [Kp] pages
@@ -53,92 +61,126 @@ __device__ __forceinline__ bool before(uint64_t c1, uint64_t p1, uint64_t c2, ui
   return c1 > c2 || (c1 == c2 && p1 < p2);
 }
 
-__global__ void __launch_bounds__(kBlock) stats_kernel(const uint64_t* __restrict__ pc, uint64_t P, State* st) {
-  uint64_t nz = 0, mx = 0;
-  for (uint64_t p = (uint64_t)blockIdx.x * kBlock + threadIdx.x; p < P; p += (uint64_t)gridDim.x * kBlock) {
-    const uint64_t c = __ldg(pc + p);
-    nz += (c != 0);
-    mx = c > mx ? c : mx;
+// Pass 1: histogram of the bit length of every non-zero count (65 bins).
+__global__ void __launch_bounds__(kBlock) bitlen_kernel(const uint64_t* __restrict__ pc, uint64_t P, unsigned* hist) {
+  __shared__ unsigned h[65];
+  for (int i = threadIdx.x; i < 65; i += kBlock) h[i] = 0;
+  __syncthreads();
+  const uint64_t n2 = P / 2;
+  const ulonglong2* pc2 = reinterpret_cast<const ulonglong2*>(pc);
+  for (uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (uint64_t)gridDim.x * kBlock) {
+    const ulonglong2 v = __ldg(pc2 + i);
+    if (v.x) atomicAdd(&h[64 - __clzll((long long)v.x)], 1u);
+    if (v.y) atomicAdd(&h[64 - __clzll((long long)v.y)], 1u);
   }
-  nz = warp_sum_u64(nz);
-  mx = warp_max_u64(mx);
-  if ((threadIdx.x & 31) == 0) {
-    if (nz) atomicAdd(&st->nnz, (unsigned long long)nz);
-    if (mx) atomicMax(&st->maxc, (unsigned long long)mx);
+  if ((P & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint64_t c = pc[P - 1];
+    if (c) atomicAdd(&h[64 - __clzll((long long)c)], 1u);
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 65; i += kBlock)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
-__global__ void plan_kernel(State* st, uint64_t K) {
+// Pick the bit length holding the K'-th largest count.
+__global__ void select_len_kernel(State* st, unsigned* hist, uint64_t K) {
   if (threadIdx.x != 0) return;
-  const uint64_t kp = st->nnz < K ? st->nnz : K;
+  unsigned long long nnz = 0;
+  for (int b = 1; b <= 64; ++b) nnz += hist[b];
+  const unsigned long long kp = nnz < K ? nnz : K;
+  st->nnz = nnz;
   st->kprime = kp;
-  st->remaining = kp;
-  st->prefix = 0;
-  st->mask = 0;
   st->gt_slots = 0;
+  st->need = 0;
   if (kp == 0) {
     st->done = 1;
     st->T = ~0ull;
-    st->need = 0;
-    return;
-  }
-  const int msb = 63 - __clzll((long long)st->maxc);
-  st->shift = (msb / 8) * 8;
-  st->done = 0;
-}
-
-__global__ void __launch_bounds__(kBlock) hist_kernel(const uint64_t* __restrict__ pc, uint64_t P, State* st,
-                                                      unsigned* hist) {
-  if (st->done) return;
-  __shared__ unsigned h[256];
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  const uint64_t prefix = st->prefix, mask = st->mask;
-  const int shift = (int)st->shift;
-  for (uint64_t p = (uint64_t)blockIdx.x * kBlock + threadIdx.x; p < P; p += (uint64_t)gridDim.x * kBlock) {
-    const uint64_t c = __ldg(pc + p);
-    if (c != 0 && (c & mask) == prefix) atomicAdd(&h[(c >> shift) & 0xFF], 1u);
-  }
-  __syncthreads();
-  if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
-}
-
-__global__ void select_kernel(State* st, unsigned* hist) {
-  __shared__ unsigned long long suf[256];  // suf[d] = sum of hist[d'] for d' > d
-  if (st->done) return;
-  const int t = threadIdx.x;
-  // inclusive suffix sums by a simple serial pass in thread 0 (256 entries)
-  if (t == 0) {
-    unsigned long long acc = 0;
-    for (int d = 255; d >= 0; --d) {
-      suf[d] = acc;
-      acc += hist[d];
+  } else {
+    unsigned long long above = 0;
+    int L = 64;
+    for (; L >= 1; --L) {
+      if (above + hist[L] >= kp) break;
+      above += hist[L];
     }
-  }
-  __syncthreads();
-  const unsigned long long rem = st->remaining;
-  const unsigned long long above = suf[t], here = hist[t];
-  __syncthreads();
-  if (above < rem && rem <= above + here) {
-    const int shift = (int)st->shift;
-    st->remaining = rem - above;
-    st->prefix |= (unsigned long long)t << shift;
-    st->mask |= 0xFFull << shift;
-    if (shift == 0) {
-      st->T = st->prefix;
-      st->need = rem - above;
+    st->above = above;
+    st->remaining = kp - above;
+    st->lo = 1ull << (L - 1);
+    if (st->remaining == hist[L]) {  // the whole bit-length class is taken
       st->done = 2;
+      st->T = st->lo - 1;
+    } else if (L == 1) {  // the class is the single value 1
+      st->done = 2;
+      st->T = 1;
+      st->need = st->remaining;
     } else {
-      st->shift = shift - 8;
+      const int w = (L - 1) < kDigitBits ? (L - 1) : kDigitBits;
+      st->width = w;
+      st->shift = (L - 1) - w;
+      st->done = 0;
     }
   }
-  hist[t] = 0;
+  for (int i = 0; i <= 64; ++i) hist[i] = 0;
 }
 
-// Pages with count == T per CTA over a contiguous page range.
+// One radix digit among the counts of the selected bin.
+__global__ void __launch_bounds__(kBlock) digit_kernel(const uint64_t* __restrict__ pc, uint64_t P, State* st,
+                                                       unsigned* hist) {
+  if (st->done) return;
+  __shared__ unsigned h[kBins];
+  for (int i = threadIdx.x; i < kBins; i += kBlock) h[i] = 0;
+  __syncthreads();
+  const uint64_t lo = st->lo;
+  const int shift = (int)st->shift, width = (int)st->width;
+  const uint64_t span = (1ull << (shift + width)) - 1;  // bin = [lo, lo + span]
+  const uint64_t n2 = P / 2;
+  const ulonglong2* pc2 = reinterpret_cast<const ulonglong2*>(pc);
+  for (uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (uint64_t)gridDim.x * kBlock) {
+    const ulonglong2 v = __ldg(pc2 + i);
+    if (v.x - lo <= span) atomicAdd(&h[(v.x - lo) >> shift], 1u);
+    if (v.y - lo <= span) atomicAdd(&h[(v.y - lo) >> shift], 1u);
+  }
+  if ((P & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint64_t c = pc[P - 1];
+    if (c - lo <= span) atomicAdd(&h[(c - lo) >> shift], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < (1 << width); i += kBlock)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+__global__ void select_digit_kernel(State* st, unsigned* hist) {
+  if (st->done || threadIdx.x != 0) return;
+  const int shift = (int)st->shift, width = (int)st->width;
+  unsigned long long rem = st->remaining, above = st->above;
+  int d = (1 << width) - 1;
+  for (; d > 0; --d) {
+    if (hist[d] >= rem) break;
+    rem -= hist[d];
+    above += hist[d];
+  }
+  const unsigned long long here = hist[d];
+  st->lo += (unsigned long long)d << shift;
+  st->above = above;
+  st->remaining = rem;
+  if (rem == here) {  // the whole bin is taken: no ties to break
+    st->done = 2;
+    st->T = st->lo - 1;
+  } else if (shift == 0) {  // exact value: take the first `rem` pages with this count
+    st->done = 2;
+    st->T = st->lo;
+    st->need = rem;
+  } else {
+    const int w = shift < kDigitBits ? shift : kDigitBits;
+    st->width = w;
+    st->shift = shift - w;
+  }
+  for (int i = 0; i < (1 << width); ++i) hist[i] = 0;
+}
+
+// Pages with count == T per CTA over a contiguous page range (only when ties are cut).
 __global__ void __launch_bounds__(kBlock) eq_count_kernel(const uint64_t* __restrict__ pc, uint64_t P, State* st,
                                                           unsigned long long* blkcnt) {
-  if (st->done != 2) return;
+  if (st->done != 2 || st->need == 0) return;
   const uint64_t T = st->T;
   const uint64_t b0 = (uint64_t)blockIdx.x * P / gridDim.x, b1 = (uint64_t)(blockIdx.x + 1) * P / gridDim.x;
   uint64_t n = 0;
@@ -154,28 +196,33 @@ __global__ void __launch_bounds__(kBlock) eq_count_kernel(const uint64_t* __rest
   }
 }
 
+// Every page with count > T to an atomically reserved slot (the sort fixes the order);
+// pages with count == T ranked in page order, the first `need` kept. A block whose
+// preceding blocks already supply `need` ties only looks for counts > T.
 __global__ void __launch_bounds__(kBlock) gather_kernel(const uint64_t* __restrict__ pc, uint64_t P, State* st,
                                                         const unsigned long long* blkcnt, uint64_t* key_c,
                                                         uint64_t* key_p) {
   if (st->done != 2) return;
   const uint64_t T = st->T, need = st->need, kp = st->kprime;
   const uint64_t eq_base_slot = kp - need;
+  const uint64_t b0 = (uint64_t)blockIdx.x * P / gridDim.x, b1 = (uint64_t)(blockIdx.x + 1) * P / gridDim.x;
   __shared__ unsigned long long part[kBlock / 32];
   __shared__ unsigned long long running;
-  // exclusive prefix of the ==T counts of the CTAs before this one
   unsigned long long pre = 0;
-  for (unsigned i = threadIdx.x; i < blockIdx.x; i += kBlock) pre += blkcnt[i];
-  pre = warp_sum_u64(pre);
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = pre;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long s = 0;
-    for (int i = 0; i < kBlock / 32; ++i) s += part[i];
-    running = s;
+  if (need) {
+    for (unsigned i = threadIdx.x; i < blockIdx.x; i += kBlock) pre += blkcnt[i];
+    pre = warp_sum_u64(pre);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = pre;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long s2 = 0;
+      for (int i = 0; i < kBlock / 32; ++i) s2 += part[i];
+      running = s2;
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  const uint64_t b0 = (uint64_t)blockIdx.x * P / gridDim.x, b1 = (uint64_t)(blockIdx.x + 1) * P / gridDim.x;
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  bool ties = need && running < need;  // block-uniform
   for (uint64_t t0 = b0; t0 < b1; t0 += kBlock) {
     const uint64_t p = t0 + threadIdx.x;
     const uint64_t c = p < b1 ? __ldg(pc + p) : 0;
@@ -184,6 +231,7 @@ __global__ void __launch_bounds__(kBlock) gather_kernel(const uint64_t* __restri
       key_c[slot] = c;
       key_p[slot] = p;
     }
+    if (!ties) continue;
     const bool eq = p < b1 && c == T;
     const unsigned bal = __ballot_sync(kFull, eq);
     const unsigned long long rank_w = __popc(bal & ((1u << lane) - 1));
@@ -201,11 +249,12 @@ __global__ void __launch_bounds__(kBlock) gather_kernel(const uint64_t* __restri
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      unsigned long long s = 0;
-      for (int i = 0; i < kBlock / 32; ++i) s += part[i];
-      running += s;
+      unsigned long long s2 = 0;
+      for (int i = 0; i < kBlock / 32; ++i) s2 += part[i];
+      running += s2;
     }
     __syncthreads();
+    ties = running < need;
   }
 }
 
@@ -307,7 +356,7 @@ Scratch carve(void* base, uint64_t Kp, int grid) {
   s.st = reinterpret_cast<State*>(b);
   b += 256;
   s.hist = reinterpret_cast<unsigned*>(b);
-  b += 256 * sizeof(unsigned);
+  b += kBins * sizeof(unsigned);
   s.blkcnt = reinterpret_cast<unsigned long long*>(b);
   b += ((size_t)grid * 8 + 255) / 256 * 256;
   s.key_c = reinterpret_cast<uint64_t*>(b);
@@ -320,7 +369,7 @@ Scratch carve(void* base, uint64_t Kp, int grid) {
 
 size_t topk_scratch_bytes(uint64_t k, int grid) {
   const uint64_t Kp = pow2_ceil(k < 2 ? 2 : k);
-  return 256 + 256 * sizeof(unsigned) + ((size_t)grid * 8 + 255) / 256 * 256 + 2 * Kp * 8;
+  return 256 + kBins * sizeof(unsigned) + ((size_t)grid * 8 + 255) / 256 * 256 + 2 * Kp * 8;
 }
 
 #define PASTA_TRY(x)                         \
@@ -334,19 +383,19 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
                      uint64_t* out_found, void* scratch, int grid, cudaStream_t st, int* n_launches) {
   const uint64_t Kp = pow2_ceil(k < 2 ? 2 : k);
   Scratch s = carve(scratch, Kp, grid);
-  cudaError_t e = cudaMemsetAsync(scratch, 0, 256 + 256 * sizeof(unsigned), st);
+  cudaError_t e = cudaMemsetAsync(scratch, 0, 256 + kBins * sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
-  int g = (int)((P + kBlock - 1) / kBlock);
+  int g = (int)((P / 2 + kBlock - 1) / kBlock);
   if (g > grid) g = grid;
   if (g < 1) g = 1;
-  stats_kernel<<<g, kBlock, 0, st>>>(pc, P, s.st);
+  bitlen_kernel<<<g, kBlock, 0, st>>>(pc, P, s.hist);
   PASTA_TRY(cudaGetLastError());
-  plan_kernel<<<1, 32, 0, st>>>(s.st, k);
+  select_len_kernel<<<1, 32, 0, st>>>(s.st, s.hist, k);
   PASTA_TRY(cudaGetLastError());
-  for (int pass = 0; pass < 8; ++pass) {
-    hist_kernel<<<g, kBlock, 0, st>>>(pc, P, s.st, s.hist);
+  for (int pass = 0; pass < (63 + kDigitBits - 1) / kDigitBits; ++pass) {  // <= 6 digits below the MSB
+    digit_kernel<<<g, kBlock, 0, st>>>(pc, P, s.st, s.hist);
     PASTA_TRY(cudaGetLastError());
-    select_kernel<<<1, 256, 0, st>>>(s.st, s.hist);
+    select_digit_kernel<<<1, 32, 0, st>>>(s.st, s.hist);
     PASTA_TRY(cudaGetLastError());
   }
   eq_count_kernel<<<grid, kBlock, 0, st>>>(pc, P, s.st, s.blkcnt);
