@@ -29,18 +29,27 @@ __global__ void __launch_bounds__(kBlock) bitmap_kernel(const uint64_t* __restri
   const uint64_t gw = (uint64_t)blockIdx.x * (kBlock / 32) + wib;
   const uint64_t nw = (uint64_t)gridDim.x * (kBlock / 32);
   uint64_t local = 0;
-  for (uint64_t w = gw; w < W; w += nw) {
-    const uint64_t p0 = 64 * w + lane, p1 = p0 + 32;
-    const uint64_t c0 = p0 < P ? __ldg(pc + p0) : 0;
-    const uint64_t c1 = p1 < P ? __ldg(pc + p1) : 0;
-    const unsigned b0 = __ballot_sync(kFull, c0 != 0);
-    const unsigned b1 = __ballot_sync(kFull, c1 != 0);
-    if (lane == 0) {
+  constexpr int kU = 4;  // bitmap words per warp iteration (8 loads per lane in flight)
+  for (uint64_t w0 = gw * kU; w0 < W; w0 += nw * kU) {
+    uint64_t c[2 * kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t p0 = 64 * (w0 + u) + lane, p1 = p0 + 32;
+      c[2 * u] = p0 < P ? __ldg(pc + p0) : 0;
+      c[2 * u + 1] = p1 < P ? __ldg(pc + p1) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const unsigned b0 = __ballot_sync(kFull, c[2 * u] != 0);
+      const unsigned b1 = __ballot_sync(kFull, c[2 * u + 1] != 0);
       const uint64_t word = (uint64_t)b0 | ((uint64_t)b1 << 32);
-      if (bitmap) bitmap[w] = word;
-      local += __popcll(word);
+      if (lane == u && w0 + u < W) {
+        if (bitmap) bitmap[w0 + u] = word;
+        local += __popcll(word);
+      }
     }
   }
+  local = warp_sum_u64(local);
   if (lane == 0) part[wib] = local;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -62,8 +71,14 @@ __global__ void __launch_bounds__(kBlock) footprint_kernel(const uint64_t* __res
   for (uint64_t k = gw; k < K; k += nw) {
     const uint64_t* row = kac + k * max_ids;
     uint64_t f = 0;
-    for (uint64_t i = lane; i < max_ids; i += 32)
-      if (__ldg(row + i) != 0) f += __ldg(id_size + i);
+    for (uint64_t i0 = lane; i0 < max_ids; i0 += 32 * 4) {
+      uint64_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = i0 + 32 * u < max_ids ? __ldg(row + i0 + 32 * u) : 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (v[u] != 0) f += __ldg(id_size + i0 + 32 * u);
+    }
     f = warp_sum_u64(f);
     uint64_t up = 0;
     if (kpb) {

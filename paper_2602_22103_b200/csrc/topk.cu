@@ -22,8 +22,12 @@
 //     compare-exchange steps for the larger strides; sentinels fill slots [K', K).
 #include <cstdint>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace pasta {
 namespace {
@@ -61,18 +65,45 @@ __device__ __forceinline__ bool before(uint64_t c1, uint64_t p1, uint64_t c2, ui
   return c1 > c2 || (c1 == c2 && p1 < p2);
 }
 
+// Warp-aggregated shared-memory histogram increment: lanes with equal bins are grouped
+// with __match_any_sync and the group leader adds the group size (counts are heavily
+// tied, so plain per-lane atomics would serialize on one bin).
+// Shared-memory histogram increment.
+__device__ __forceinline__ void hist_add(unsigned* h, bool valid, unsigned bin) {
+  if (valid) atomicAdd(&h[bin], 1u);
+}
+
+// Streaming helper: visit every pair index i < n2 of this grid with kU 16-byte loads in
+// flight per thread (enough memory-level parallelism to stream P x 8 bytes at HBM speed).
+constexpr int kU = 8;
+template <typename F>
+__device__ __forceinline__ void stream_pairs(const ulonglong2* __restrict__ pc2, uint64_t n2, F f) {
+  const uint64_t stride = (uint64_t)gridDim.x * kBlock * kU;
+  for (uint64_t base = (uint64_t)blockIdx.x * kBlock * kU + threadIdx.x; base < n2; base += stride) {
+    ulonglong2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t i = base + (uint64_t)u * kBlock;
+      v[u] = i < n2 ? __ldg(pc2 + i) : make_ulonglong2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t i = base + (uint64_t)u * kBlock;
+      if (i < n2) f(i, v[u]);
+    }
+  }
+}
+
+// ---- selection passes (device functions of the one cooperative selection kernel) ----
+
 // Pass 1: histogram of the bit length of every non-zero count (65 bins).
-__global__ void __launch_bounds__(kBlock) bitlen_kernel(const uint64_t* __restrict__ pc, uint64_t P, unsigned* hist) {
-  __shared__ unsigned h[65];
+__device__ void dev_bitlen(const uint64_t* __restrict__ pc, uint64_t P, unsigned* h, unsigned* hist) {
   for (int i = threadIdx.x; i < 65; i += kBlock) h[i] = 0;
   __syncthreads();
-  const uint64_t n2 = P / 2;
-  const ulonglong2* pc2 = reinterpret_cast<const ulonglong2*>(pc);
-  for (uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (uint64_t)gridDim.x * kBlock) {
-    const ulonglong2 v = __ldg(pc2 + i);
-    if (v.x) atomicAdd(&h[64 - __clzll((long long)v.x)], 1u);
-    if (v.y) atomicAdd(&h[64 - __clzll((long long)v.y)], 1u);
-  }
+  stream_pairs(reinterpret_cast<const ulonglong2*>(pc), P / 2, [&](uint64_t, const ulonglong2& v) {
+    hist_add(h, v.x != 0, 64 - __clzll((long long)v.x));
+    hist_add(h, v.y != 0, 64 - __clzll((long long)v.y));
+  });
   if ((P & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const uint64_t c = pc[P - 1];
     if (c) atomicAdd(&h[64 - __clzll((long long)c)], 1u);
@@ -82,9 +113,8 @@ __global__ void __launch_bounds__(kBlock) bitlen_kernel(const uint64_t* __restri
     if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
-// Pick the bit length holding the K'-th largest count.
-__global__ void select_len_kernel(State* st, unsigned* hist, uint64_t K) {
-  if (threadIdx.x != 0) return;
+// Pick the bit length holding the K'-th largest count (one thread).
+__device__ void dev_select_len(volatile State* st, unsigned* hist, uint64_t K) {
   unsigned long long nnz = 0;
   for (int b = 1; b <= 64; ++b) nnz += hist[b];
   const unsigned long long kp = nnz < K ? nnz : K;
@@ -102,16 +132,17 @@ __global__ void select_len_kernel(State* st, unsigned* hist, uint64_t K) {
       if (above + hist[L] >= kp) break;
       above += hist[L];
     }
+    const unsigned long long rem = kp - above;
     st->above = above;
-    st->remaining = kp - above;
+    st->remaining = rem;
     st->lo = 1ull << (L - 1);
-    if (st->remaining == hist[L]) {  // the whole bit-length class is taken
+    if (rem == hist[L]) {  // the whole bit-length class is taken
       st->done = 2;
-      st->T = st->lo - 1;
+      st->T = (1ull << (L - 1)) - 1;
     } else if (L == 1) {  // the class is the single value 1
       st->done = 2;
       st->T = 1;
-      st->need = st->remaining;
+      st->need = rem;
     } else {
       const int w = (L - 1) < kDigitBits ? (L - 1) : kDigitBits;
       st->width = w;
@@ -123,22 +154,17 @@ __global__ void select_len_kernel(State* st, unsigned* hist, uint64_t K) {
 }
 
 // One radix digit among the counts of the selected bin.
-__global__ void __launch_bounds__(kBlock) digit_kernel(const uint64_t* __restrict__ pc, uint64_t P, State* st,
-                                                       unsigned* hist) {
-  if (st->done) return;
-  __shared__ unsigned h[kBins];
-  for (int i = threadIdx.x; i < kBins; i += kBlock) h[i] = 0;
-  __syncthreads();
+__device__ void dev_digit(const uint64_t* __restrict__ pc, uint64_t P, volatile State* st, unsigned* h,
+                          unsigned* hist) {
   const uint64_t lo = st->lo;
   const int shift = (int)st->shift, width = (int)st->width;
+  for (int i = threadIdx.x; i < (1 << width); i += kBlock) h[i] = 0;
+  __syncthreads();
   const uint64_t span = (1ull << (shift + width)) - 1;  // bin = [lo, lo + span]
-  const uint64_t n2 = P / 2;
-  const ulonglong2* pc2 = reinterpret_cast<const ulonglong2*>(pc);
-  for (uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (uint64_t)gridDim.x * kBlock) {
-    const ulonglong2 v = __ldg(pc2 + i);
-    if (v.x - lo <= span) atomicAdd(&h[(v.x - lo) >> shift], 1u);
-    if (v.y - lo <= span) atomicAdd(&h[(v.y - lo) >> shift], 1u);
-  }
+  stream_pairs(reinterpret_cast<const ulonglong2*>(pc), P / 2, [&](uint64_t, const ulonglong2& v) {
+    hist_add(h, v.x - lo <= span, (unsigned)((v.x - lo) >> shift));
+    hist_add(h, v.y - lo <= span, (unsigned)((v.y - lo) >> shift));
+  });
   if ((P & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const uint64_t c = pc[P - 1];
     if (c - lo <= span) atomicAdd(&h[(c - lo) >> shift], 1u);
@@ -148,68 +174,95 @@ __global__ void __launch_bounds__(kBlock) digit_kernel(const uint64_t* __restric
     if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
-__global__ void select_digit_kernel(State* st, unsigned* hist) {
-  if (st->done || threadIdx.x != 0) return;
+// Choose the digit (block 0, all threads): chunked suffix sums from the top bin down.
+__device__ void dev_select_digit(volatile State* st, unsigned* hist, unsigned long long* sm) {
   const int shift = (int)st->shift, width = (int)st->width;
-  unsigned long long rem = st->remaining, above = st->above;
-  int d = (1 << width) - 1;
-  for (; d > 0; --d) {
-    if (hist[d] >= rem) break;
-    rem -= hist[d];
-    above += hist[d];
+  const int nb = 1 << width;
+  const int per = (nb + kBlock - 1) / kBlock;  // bins per thread (<= 8)
+  const int t = threadIdx.x;
+  unsigned long long mine = 0;
+  for (int j = 0; j < per; ++j) {
+    const int d = t * per + j;
+    if (d < nb) mine += hist[d];
   }
-  const unsigned long long here = hist[d];
-  st->lo += (unsigned long long)d << shift;
-  st->above = above;
-  st->remaining = rem;
-  if (rem == here) {  // the whole bin is taken: no ties to break
-    st->done = 2;
-    st->T = st->lo - 1;
-  } else if (shift == 0) {  // exact value: take the first `rem` pages with this count
-    st->done = 2;
-    st->T = st->lo;
-    st->need = rem;
-  } else {
-    const int w = shift < kDigitBits ? shift : kDigitBits;
-    st->width = w;
-    st->shift = shift - w;
+  sm[t] = mine;
+  __syncthreads();
+  if (t == 0) {
+    // thread chunks from the top: find the chunk where the running sum reaches rem
+    unsigned long long rem = st->remaining, above = st->above;
+    int c = kBlock - 1;
+    for (; c > 0; --c) {
+      if (sm[c] >= rem) break;
+      rem -= sm[c];
+      above += sm[c];
+    }
+    int d = c * per + per - 1;
+    if (d > nb - 1) d = nb - 1;
+    for (; d > c * per; --d) {
+      if (hist[d] >= rem) break;
+      rem -= hist[d];
+      above += hist[d];
+    }
+    const unsigned long long here = hist[d];
+    const unsigned long long lo = st->lo + ((unsigned long long)d << shift);
+    st->lo = lo;
+    st->above = above;
+    st->remaining = rem;
+    if (rem == here) {  // the whole bin is taken: no ties to break
+      st->done = 2;
+      st->T = lo - 1;
+    } else if (shift == 0) {  // exact value: take the first `rem` pages with this count
+      st->done = 2;
+      st->T = lo;
+      st->need = rem;
+    } else {
+      const int w = shift < kDigitBits ? shift : kDigitBits;
+      st->width = w;
+      st->shift = shift - w;
+    }
   }
-  for (int i = 0; i < (1 << width); ++i) hist[i] = 0;
+  __syncthreads();
+  for (int i = t; i < nb; i += kBlock) hist[i] = 0;
 }
 
-// Pages with count == T per CTA over a contiguous page range (only when ties are cut).
-__global__ void __launch_bounds__(kBlock) eq_count_kernel(const uint64_t* __restrict__ pc, uint64_t P, State* st,
-                                                          unsigned long long* blkcnt) {
-  if (st->done != 2 || st->need == 0) return;
-  const uint64_t T = st->T;
+// Pages with count == T in this CTA's contiguous page range.
+__device__ void dev_eq_count(const uint64_t* __restrict__ pc, uint64_t P, uint64_t T, unsigned long long* blkcnt,
+                             unsigned long long* part) {
   const uint64_t b0 = (uint64_t)blockIdx.x * P / gridDim.x, b1 = (uint64_t)(blockIdx.x + 1) * P / gridDim.x;
   uint64_t n = 0;
-  for (uint64_t p = b0 + threadIdx.x; p < b1; p += kBlock) n += (__ldg(pc + p) == T);
+  for (uint64_t p0 = b0 + threadIdx.x; p0 < b1; p0 += (uint64_t)kBlock * kU) {
+    uint64_t v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t p = p0 + (uint64_t)u * kBlock;
+      v[u] = p < b1 ? __ldg(pc + p) : ~T;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) n += (v[u] == T);
+  }
   n = warp_sum_u64(n);
-  __shared__ unsigned long long part[kBlock / 32];
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = n;
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned long long s = 0;
-    for (int i = 0; i < kBlock / 32; ++i) s += part[i];
-    blkcnt[blockIdx.x] = s;
+    unsigned long long s2 = 0;
+    for (int i = 0; i < kBlock / 32; ++i) s2 += part[i];
+    blkcnt[blockIdx.x] = s2;
   }
+  __syncthreads();
 }
 
 // Every page with count > T to an atomically reserved slot (the sort fixes the order);
-// pages with count == T ranked in page order, the first `need` kept. A block whose
-// preceding blocks already supply `need` ties only looks for counts > T.
-__global__ void __launch_bounds__(kBlock) gather_kernel(const uint64_t* __restrict__ pc, uint64_t P, State* st,
-                                                        const unsigned long long* blkcnt, uint64_t* key_c,
-                                                        uint64_t* key_p) {
-  if (st->done != 2) return;
+// pages with count == T ranked in page order, the first `need` kept; a block whose own
+// range holds no such page, or whose predecessors already supply `need`, skips ranking.
+__device__ void dev_gather(const uint64_t* __restrict__ pc, uint64_t P, volatile State* st,
+                           const unsigned long long* blkcnt, uint64_t* key_c, uint64_t* key_p,
+                           unsigned long long* part, unsigned long long* running_s) {
   const uint64_t T = st->T, need = st->need, kp = st->kprime;
   const uint64_t eq_base_slot = kp - need;
   const uint64_t b0 = (uint64_t)blockIdx.x * P / gridDim.x, b1 = (uint64_t)(blockIdx.x + 1) * P / gridDim.x;
-  __shared__ unsigned long long part[kBlock / 32];
-  __shared__ unsigned long long running;
-  unsigned long long pre = 0;
-  if (need) {
+  bool ties = false;
+  if (need && blkcnt[blockIdx.x] != 0) {
+    unsigned long long pre = 0;
     for (unsigned i = threadIdx.x; i < blockIdx.x; i += kBlock) pre += blkcnt[i];
     pre = warp_sum_u64(pre);
     if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = pre;
@@ -217,17 +270,36 @@ __global__ void __launch_bounds__(kBlock) gather_kernel(const uint64_t* __restri
     if (threadIdx.x == 0) {
       unsigned long long s2 = 0;
       for (int i = 0; i < kBlock / 32; ++i) s2 += part[i];
-      running = s2;
+      *running_s = s2;
     }
     __syncthreads();
+    ties = *running_s < need;
   }
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  bool ties = need && running < need;  // block-uniform
+  if (!ties) {  // only counts > T are wanted from this range: batched streaming
+    for (uint64_t p0 = b0 + threadIdx.x; p0 < b1; p0 += (uint64_t)kBlock * kU) {
+      uint64_t v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint64_t p = p0 + (uint64_t)u * kBlock;
+        v[u] = p < b1 ? __ldg(pc + p) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (v[u] > T) {
+          const unsigned long long slot = atomicAdd((unsigned long long*)&st->gt_slots, 1ull);
+          key_c[slot] = v[u];
+          key_p[slot] = p0 + (uint64_t)u * kBlock;
+        }
+      }
+    }
+    return;
+  }
   for (uint64_t t0 = b0; t0 < b1; t0 += kBlock) {
     const uint64_t p = t0 + threadIdx.x;
     const uint64_t c = p < b1 ? __ldg(pc + p) : 0;
     if (p < b1 && c > T) {
-      const unsigned long long slot = atomicAdd(&st->gt_slots, 1ull);
+      const unsigned long long slot = atomicAdd((unsigned long long*)&st->gt_slots, 1ull);
       key_c[slot] = c;
       key_p[slot] = p;
     }
@@ -238,7 +310,7 @@ __global__ void __launch_bounds__(kBlock) gather_kernel(const uint64_t* __restri
     __syncthreads();
     if (lane == 0) part[wib] = __popc(bal);
     __syncthreads();
-    unsigned long long off = running;
+    unsigned long long off = *running_s;
     for (unsigned i = 0; i < wib; ++i) off += part[i];
     if (eq) {
       const unsigned long long r = off + rank_w;
@@ -251,11 +323,42 @@ __global__ void __launch_bounds__(kBlock) gather_kernel(const uint64_t* __restri
     if (threadIdx.x == 0) {
       unsigned long long s2 = 0;
       for (int i = 0; i < kBlock / 32; ++i) s2 += part[i];
-      running += s2;
+      *running_s += s2;
     }
     __syncthreads();
-    ties = running < need;
+    ties = *running_s < need;
   }
+}
+
+// The whole selection in ONE cooperative launch: bit-length pass, up to six 11-bit digit
+// passes (stopping as soon as the threshold is fixed), the tie count and the gather,
+// separated by grid-wide barriers.
+__global__ void __launch_bounds__(kBlock) select_coop_kernel(const uint64_t* __restrict__ pc, uint64_t P,
+                                                             uint64_t K, State* st_, unsigned* hist,
+                                                             unsigned long long* blkcnt, uint64_t* key_c,
+                                                             uint64_t* key_p) {
+  cg::grid_group grid = cg::this_grid();
+  volatile State* st = st_;
+  __shared__ unsigned h[kBins];
+  __shared__ unsigned long long sm[kBlock];
+  __shared__ unsigned long long running_s;
+  dev_bitlen(pc, P, h, hist);
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) dev_select_len(st, hist, K);
+  grid.sync();
+  for (int pass = 0; pass < (63 + kDigitBits - 1) / kDigitBits; ++pass) {
+    if (st->done) break;  // grid-uniform: read after the barrier
+    dev_digit(pc, P, st, h, hist);
+    grid.sync();
+    if (blockIdx.x == 0) dev_select_digit(st, hist, sm);
+    grid.sync();
+  }
+  if (st->done != 2) return;
+  if (st->need) {
+    dev_eq_count(pc, P, st->T, blkcnt, sm);
+    grid.sync();
+  }
+  dev_gather(pc, P, st, blkcnt, key_c, key_p, sm, &running_s);
 }
 
 __global__ void pad_kernel(State* st, uint64_t* key_c, uint64_t* key_p, uint64_t Kp) {
@@ -385,23 +488,26 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
   Scratch s = carve(scratch, Kp, grid);
   cudaError_t e = cudaMemsetAsync(scratch, 0, 256 + kBins * sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
-  int g = (int)((P / 2 + kBlock - 1) / kBlock);
-  if (g > grid) g = grid;
-  if (g < 1) g = 1;
-  bitlen_kernel<<<g, kBlock, 0, st>>>(pc, P, s.hist);
-  PASTA_TRY(cudaGetLastError());
-  select_len_kernel<<<1, 32, 0, st>>>(s.st, s.hist, k);
-  PASTA_TRY(cudaGetLastError());
-  for (int pass = 0; pass < (63 + kDigitBits - 1) / kDigitBits; ++pass) {  // <= 6 digits below the MSB
-    digit_kernel<<<g, kBlock, 0, st>>>(pc, P, s.st, s.hist);
-    PASTA_TRY(cudaGetLastError());
-    select_digit_kernel<<<1, 32, 0, st>>>(s.st, s.hist);
-    PASTA_TRY(cudaGetLastError());
+  {
+    static int coop_blocks = 0;  // co-resident blocks per SM for the cooperative launch
+    if (coop_blocks == 0) {
+      int nb = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, select_coop_kernel, kBlock, 0) != cudaSuccess || nb < 1)
+        nb = 1;
+      coop_blocks = nb;
+    }
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int g = sms * (coop_blocks < 4 ? coop_blocks : 4);
+    const uint64_t need_blocks = (P + kBlock - 1) / kBlock;
+    if ((uint64_t)g > need_blocks) g = (int)(need_blocks < 1 ? 1 : need_blocks);
+    if (g > grid) g = grid;
+    uint64_t K64 = k;
+    void* args[] = {(void*)&pc, (void*)&P, (void*)&K64, (void*)&s.st, (void*)&s.hist, (void*)&s.blkcnt,
+                    (void*)&s.key_c, (void*)&s.key_p};
+    PASTA_TRY(cudaLaunchCooperativeKernel((void*)select_coop_kernel, dim3(g), dim3(kBlock), args, 0, st));
   }
-  eq_count_kernel<<<grid, kBlock, 0, st>>>(pc, P, s.st, s.blkcnt);
-  PASTA_TRY(cudaGetLastError());
-  gather_kernel<<<grid, kBlock, 0, st>>>(pc, P, s.st, s.blkcnt, s.key_c, s.key_p);
-  PASTA_TRY(cudaGetLastError());
   const int pg = (int)((Kp + 1023) / 1024 < 1024 ? (Kp + 1023) / 1024 : 1024);
   pad_kernel<<<pg, 1024, 0, st>>>(s.st, s.key_c, s.key_p, Kp);
   PASTA_TRY(cudaGetLastError());
