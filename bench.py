@@ -336,7 +336,9 @@ def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, d
         avail = psutil.virtual_memory().available
     except Exception:
         avail = 16 << 30
-    n_e = max(1, min(n_loc, args.e2e_records, int(avail * 0.4) // 8))
+    # every rank of this node pins its own host copy: share 40 % of the node's free RAM
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    n_e = max(1, min(n_loc, args.e2e_records, int(avail * 0.4) // max(1, local_world) // 8))
     # the e2e trace is the kernel-aligned prefix of this rank's shard that fits in RAM
     ko_loc_np = ko_loc.cpu().numpy()
     kcut = int(np.searchsorted(ko_loc_np, n_e, side="right")) - 1

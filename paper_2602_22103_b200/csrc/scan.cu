@@ -73,6 +73,10 @@ constexpr uint32_t kSliceBytes = kSlice * 8;  // 2 KiB
 constexpr int kMaxStages = 8;
 constexpr int kMinStages = 3;
 constexpr int kBarBytes = kWarps * kMaxStages * 8;
+#ifndef PASTA_LA_SMEM
+#define PASTA_LA_SMEM 1
+#endif
+constexpr int kLaBytes = PASTA_LA_SMEM ? kThreads * 12 : 0;  // LaneAcc per thread
 constexpr int kSmemLimit = 227 * 1024;
 
 __host__ __device__ constexpr int ring_bytes(int stages) { return kWarps * stages * (int)kSliceBytes; }
@@ -513,7 +517,7 @@ template <bool kBig, bool kRows, bool kPages>
 __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages));
-  uint64_t* sB = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages) + kBarBytes);
+  uint64_t* sB = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages) + kBarBytes + kLaBytes);
 
   const uint32_t A = args.A;
   const int warp = threadIdx.x >> 5;
@@ -580,7 +584,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   w.own = A;
   w.pcnt = 0;
   w.ocnt = 0;
+#if PASTA_LA_SMEM
+  // the rarely used tier-F accumulators live in shared memory (fewer live registers)
+  LaneAcc& la = reinterpret_cast<LaneAcc*>(smem + ring_bytes(stages) + kBarBytes)[threadIdx.x];
+#else
   LaneAcc la;
+#endif
   la.own = A;
   la.ocnt = 0;
   la.kbit = kOOW;
@@ -729,7 +738,7 @@ __global__ void scan_extras_kernel(const ExtraArgs ea) {
 
 int stages_for(uint32_t A, bool big) {
   const long table = big ? 0 : 16l * A;
-  const long avail = (long)kSmemLimit - kBarBytes - table;
+  const long avail = (long)kSmemLimit - kBarBytes - kLaBytes - table;
   long st = avail / ring_bytes(1);
   if (st > kMaxStages) st = kMaxStages;
   return (int)st;
@@ -753,7 +762,7 @@ int scan_warps() { return kWarps; }
 bool scan_table_fits_smem(uint32_t A) { return stages_for(A, false) >= kMinStages; }
 
 int scan_smem_bytes(uint32_t A, bool big_table) {
-  return ring_bytes(stages_for(A, big_table)) + kBarBytes + (big_table ? 0 : (int)(16ull * A));
+  return ring_bytes(stages_for(A, big_table)) + kBarBytes + kLaBytes + (big_table ? 0 : (int)(16ull * A));
 }
 
 cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st) {
