@@ -232,8 +232,9 @@ def run_ours(args):
     for b, s in plan.allocs:
         tr.register_alloc(b, s)
     hist = tr.histograms(plan.page_shift, n_kernels=nk_loc, kernel_rows=plan.want_kernel_rows,
-                         kernel_pages=plan.want_kernel_pages)
-    merger = pdist.Merger(tr, hist, group) if world > 1 else None
+                         kernel_pages=plan.want_kernel_pages, pad_pages_to=64 * world)
+    # N > 1: page counts reduce-scattered, top-K from shard candidates (dist.ShardedMerger)
+    merger = pdist.ShardedMerger(tr, hist, plan.topk, group) if world > 1 else None
     K = max(plan.topk)
     top_out = (torch.empty(K, dtype=torch.int64, device=dev), torch.empty(K, dtype=torch.int64, device=dev),
                torch.empty(1, dtype=torch.int64, device=dev))
@@ -243,8 +244,9 @@ def run_ours(args):
         tr.analyze(rec, plan.page_shift, hist, kernel_offsets=ko_loc, n=n_loc, finalize=True)
         if merger is not None:
             merger.merge()
-        for k in plan.topk:
-            tr.topk(hist.page_counts, k, out=top_out)
+        else:
+            for k in plan.topk:
+                tr.topk(hist.page_counts, k, out=top_out)
 
     def barrier():
         if world > 1:
@@ -351,10 +353,10 @@ def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, d
     host.copy_(rec[:n_e])
     ko_h = torch.from_numpy(ko_e.astype(np.int64)).pin_memory()
     h_e = tr.histograms(plan.page_shift, n_kernels=len(ko_e) - 1, kernel_rows=plan.want_kernel_rows,
-                        kernel_pages=plan.want_kernel_pages)
+                        kernel_pages=plan.want_kernel_pages, pad_pages_to=64 * world)
     from paper_2602_22103_b200 import dist as pdist
 
-    merger = pdist.Merger(tr, h_e, group) if world > 1 else None
+    merger = pdist.ShardedMerger(tr, h_e, plan.topk, group) if world > 1 else None
     res_host = torch.empty(8 + 2 * top_out[0].numel() + 1, dtype=torch.int64, pin_memory=True)
     K = top_out[0].numel()
 
@@ -362,13 +364,16 @@ def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, d
         h_e.zero_()
         tr.analyze(host, plan.page_shift, h_e, kernel_offsets=ko_h, n=n_e, host=True)
         if merger is not None:
-            merger.merge()
-        for k in plan.topk:
-            tr.topk(h_e.page_counts, k, out=top_out)
+            outs = merger.merge()
+            res = outs[max(plan.topk)]
+        else:
+            for k in plan.topk:
+                tr.topk(h_e.page_counts, k, out=top_out)
+            res = top_out
         res_host[:8].copy_(h_e.totals, non_blocking=True)
-        res_host[8:8 + K].copy_(top_out[0], non_blocking=True)
-        res_host[8 + K:8 + 2 * K].copy_(top_out[1], non_blocking=True)
-        res_host[8 + 2 * K:].copy_(top_out[2], non_blocking=True)
+        res_host[8:8 + K].copy_(res[0], non_blocking=True)
+        res_host[8 + K:8 + 2 * K].copy_(res[1], non_blocking=True)
+        res_host[8 + 2 * K:].copy_(res[2], non_blocking=True)
 
     steps = max(2, min(args.steps, 5))
     for _ in range(2):

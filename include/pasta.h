@@ -172,6 +172,15 @@ int pasta_topk(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t
 int pasta_bitmap_or(pasta_trace* h, const uint64_t* gathered, uint32_t g, uint64_t words, uint64_t* out_bitmap,
                     uint64_t* out_popcount);
 
+/* Multi-GPU top-K merge: g shard-local top-k lists, rank-major
+ * (cand_page[r*k + i], cand_count[r*k + i], device pointers; pages relative to shard r,
+ * empty slots have count 0), shard r covering global pages [r*shard_pages,
+ * (r+1)*shard_pages). Writes the global top-k by (count desc, page asc) with global page
+ * ids, (UINT64_MAX, 0) in slots [found, k), and *out_found = min(k, non-empty
+ * candidates). Exact: a page in the global top-k is in its own shard's top-k. */
+int pasta_topk_merge(pasta_trace* h, const uint64_t* cand_page, const uint64_t* cand_count, uint32_t g, uint32_t k,
+                     uint64_t shard_pages, uint64_t* out_page, uint64_t* out_count, uint64_t* out_found);
+
 /* Block until the handle's stream is idle; reports asynchronous faults (ECUDA). */
 int pasta_sync(pasta_trace* h);
 

@@ -62,6 +62,7 @@ _SIGS = {
     "pasta_finalize": (_int, [_vp, _u32, _u32, ctypes.POINTER(pasta_histograms)]),
     "pasta_topk": (_int, [_vp, _vp, _u64, _u32, _vp, _vp, _vp]),
     "pasta_bitmap_or": (_int, [_vp, _vp, _u32, _u64, _vp, _vp]),
+    "pasta_topk_merge": (_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp]),
     "pasta_sync": (_int, [_vp]),
     "pasta_close": (_int, [_vp]),
     "pasta_strerror": (ctypes.c_char_p, [_int]),
@@ -140,6 +141,11 @@ def pasta_bitmap_or(h, gathered, g: int, words: int, out_bitmap, out_popcount=No
            "pasta_bitmap_or")
 
 
+def pasta_topk_merge(h, cand_page, cand_count, g: int, k: int, shard_pages: int, out_page, out_count, out_found):
+    _check(_lib.pasta_topk_merge(h, _ptr(cand_page), _ptr(cand_count), g, k, shard_pages, _ptr(out_page),
+                                 _ptr(out_count), _ptr(out_found)), "pasta_topk_merge")
+
+
 def pasta_sync(h):
     _check(_lib.pasta_sync(h), "pasta_sync")
 
@@ -172,15 +178,20 @@ class Histograms:
     arrays and the bitmap are separate tensors."""
 
     def __init__(self, P: int, max_ids: int, device, n_kernels: int = 0, kernel_rows: bool = False,
-                 kernel_pages: bool = False, bitmap: bool = True):
+                 kernel_pages: bool = False, bitmap: bool = True, pad_pages_to: int = 1):
         import torch
 
         self.P, self.max_ids, self.n_kernels = P, max_ids, n_kernels
         self.words = (P + 63) // 64
-        self.packed = torch.zeros(P + max_ids + TOTALS, dtype=torch.int64, device=device)
+        # the page part is padded with zero pages to a multiple of `pad_pages_to` so it
+        # can be reduce-scattered in equal shards (dist.ShardedMerger)
+        self.P_pad = (P + pad_pages_to - 1) // pad_pages_to * pad_pages_to
+        self.packed = torch.zeros(self.P_pad + max_ids + TOTALS, dtype=torch.int64, device=device)
         self.page_counts = self.packed[:P]
-        self.alloc_counts = self.packed[P:P + max_ids]
-        self.totals = self.packed[P + max_ids:]
+        self.pages_padded = self.packed[:self.P_pad]
+        self.small = self.packed[self.P_pad:]  # [alloc_counts | totals]
+        self.alloc_counts = self.packed[self.P_pad:self.P_pad + max_ids]
+        self.totals = self.packed[self.P_pad + max_ids:]
         self.page_bitmap = torch.zeros(self.words, dtype=torch.int64, device=device) if bitmap else None
         self.kernel_alloc_counts = self.kernel_stats = self.kernel_page_bitmap = None
         if kernel_rows:
@@ -226,9 +237,10 @@ class Trace:
     def register_free(self, base: int):
         pasta_register_free(self.h, base)
 
-    def histograms(self, page_shift: int, n_kernels: int = 0, kernel_rows=False, kernel_pages=False, bitmap=True):
+    def histograms(self, page_shift: int, n_kernels: int = 0, kernel_rows=False, kernel_pages=False, bitmap=True,
+                   pad_pages_to: int = 1):
         return Histograms(self.n_pages(page_shift), self.max_ids, self.device, n_kernels, kernel_rows, kernel_pages,
-                          bitmap)
+                          bitmap, pad_pages_to)
 
     def analyze(self, records, page_shift: int, hist: Histograms, kernel_offsets=None, n: int | None = None,
                 finalize: bool = True, host: bool = False):
@@ -253,6 +265,10 @@ class Trace:
 
     def bitmap_or(self, gathered, g: int, words: int, out_bitmap, out_popcount=None):
         pasta_bitmap_or(self.h, gathered, g, words, out_bitmap, out_popcount)
+
+    def topk_merge(self, cand_page, cand_count, g: int, k: int, shard_pages: int, out):
+        pasta_topk_merge(self.h, cand_page, cand_count, g, k, shard_pages, out[0], out[1], out[2])
+        return out
 
     def sync(self):
         pasta_sync(self.h)

@@ -61,4 +61,8 @@ typedef void (*launch_hook)(void* ctx, int begin);
 cudaError_t run_topk(const uint64_t* page_counts, uint64_t P, uint32_t k, uint64_t* out_page, uint64_t* out_count,
                      uint64_t* out_found, void* scratch, int grid, cudaStream_t st, int* n_launches);
 
+cudaError_t run_topk_merge(const uint64_t* cand_page, const uint64_t* cand_count, uint32_t g, uint32_t k,
+                           uint64_t shard_pages, uint64_t* out_page, uint64_t* out_count, uint64_t* out_found,
+                           void* scratch, int grid, cudaStream_t st, int* n_launches);
+
 }  // namespace pasta

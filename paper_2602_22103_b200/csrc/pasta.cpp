@@ -469,6 +469,31 @@ int pasta_topk(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t
   return cuda_status(e);
 }
 
+int pasta_topk_merge(pasta_trace* h, const uint64_t* cand_page, const uint64_t* cand_count, uint32_t g, uint32_t k,
+                     uint64_t shard_pages, uint64_t* out_page, uint64_t* out_count, uint64_t* out_found) {
+  if (!h || !cand_page || !cand_count || !out_page || !out_count || !out_found || g == 0 || k == 0)
+    return PASTA_EINVAL;
+  DeviceGuard dg(h->device);
+  const int grid = h->sm_count * 4;
+  const size_t need = topk_scratch_bytes((uint64_t)g * k, grid);
+  if (need > h->topk_bytes) {
+    if (h->d_topk) {
+      cudaStreamSynchronize(h->stream);
+      cudaFree(h->d_topk);
+    }
+    h->d_topk = nullptr;
+    h->topk_bytes = 0;
+    if (cudaMalloc(&h->d_topk, need) != cudaSuccess) return PASTA_ECUDA;
+    h->topk_bytes = need;
+  }
+  int nl = 0;
+  Timed t(h, PASTA_PH_MERGE, h->stream);
+  cudaError_t e = run_topk_merge(cand_page, cand_count, g, k, shard_pages, out_page, out_count, out_found, h->d_topk,
+                                 grid, h->stream, &nl);
+  h->launches += (uint64_t)nl;
+  return cuda_status(e);
+}
+
 int pasta_bitmap_or(pasta_trace* h, const uint64_t* gathered, uint32_t g, uint64_t words, uint64_t* out_bitmap,
                     uint64_t* out_popcount) {
   if (!h || !gathered || !out_bitmap || g == 0 || words == 0) return PASTA_EINVAL;

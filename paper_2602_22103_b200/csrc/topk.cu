@@ -433,8 +433,8 @@ __global__ void __launch_bounds__(kBlock) bitonic_global_kernel(uint64_t* key_c,
 }
 
 __global__ void write_kernel(const State* st, const uint64_t* key_c, const uint64_t* key_p, uint64_t K,
-                             uint64_t* out_page, uint64_t* out_count, uint64_t* out_found) {
-  const uint64_t kp = st->kprime;
+                             uint64_t* out_page, uint64_t* out_count, uint64_t* out_found, int from_nnz) {
+  const uint64_t kp = from_nnz ? (st->nnz < K ? st->nnz : K) : st->kprime;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K; i += (uint64_t)gridDim.x * blockDim.x) {
     if (i < kp) {
       out_page[i] = key_p[i];
@@ -445,6 +445,27 @@ __global__ void write_kernel(const State* st, const uint64_t* key_c, const uint6
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *out_found = kp;
+}
+
+// Candidates of g shard-local top-K lists (rank-major, k entries each) -> sort keys with
+// global page ids (page + r * shard_pages); empty slots (count 0) become sentinels.
+__global__ void merge_load_kernel(const uint64_t* __restrict__ cand_page, const uint64_t* __restrict__ cand_count,
+                                  uint32_t g, uint32_t k, uint64_t shard_pages, State* st, uint64_t* key_c,
+                                  uint64_t* key_p, uint64_t Kp) {
+  uint64_t nz = 0;
+  const uint64_t n = (uint64_t)g * k;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Kp; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = 0, p = ~0ull;
+    if (i < n) {
+      c = cand_count[i];
+      if (c) p = cand_page[i] + (i / k) * shard_pages;
+    }
+    key_c[i] = c;
+    key_p[i] = c ? p : ~0ull;
+    nz += (c != 0);
+  }
+  nz = warp_sum_u64(nz);
+  if ((threadIdx.x & 31) == 0 && nz) atomicAdd(&st->nnz, (unsigned long long)nz);
 }
 
 uint64_t pow2_ceil(uint64_t x) {
@@ -482,6 +503,25 @@ size_t topk_scratch_bytes(uint64_t k, int grid) {
     if (n_launches) ++*n_launches;           \
   } while (0)
 
+// Bitonic sort of Kp (power of two) keys by (count desc, page asc).
+cudaError_t sort_keys(uint64_t* key_c, uint64_t* key_p, uint64_t Kp, int grid, cudaStream_t st, int* n_launches) {
+  const uint64_t tile = Kp < (uint64_t)kTile ? Kp : (uint64_t)kTile;
+  const int tiles = (int)((Kp + kTile - 1) / kTile);
+  bitonic_tile_kernel<<<tiles, 1024, 0, st>>>(key_c, key_p, Kp, 2, tile, ~0ull);
+  PASTA_TRY(cudaGetLastError());
+  for (uint64_t size = 2 * (uint64_t)kTile; size <= Kp; size <<= 1) {
+    for (uint64_t stride = size >> 1; stride >= (uint64_t)kTile; stride >>= 1) {
+      int gg = (int)((Kp / 2 + kBlock - 1) / kBlock);
+      if (gg > grid) gg = grid;
+      bitonic_global_kernel<<<gg, kBlock, 0, st>>>(key_c, key_p, Kp, size, stride);
+      PASTA_TRY(cudaGetLastError());
+    }
+    bitonic_tile_kernel<<<tiles, 1024, 0, st>>>(key_c, key_p, Kp, size, size, kTile / 2);
+    PASTA_TRY(cudaGetLastError());
+  }
+  return cudaSuccess;
+}
+
 cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_page, uint64_t* out_count,
                      uint64_t* out_found, void* scratch, int grid, cudaStream_t st, int* n_launches) {
   const uint64_t Kp = pow2_ceil(k < 2 ? 2 : k);
@@ -511,24 +551,32 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
   const int pg = (int)((Kp + 1023) / 1024 < 1024 ? (Kp + 1023) / 1024 : 1024);
   pad_kernel<<<pg, 1024, 0, st>>>(s.st, s.key_c, s.key_p, Kp);
   PASTA_TRY(cudaGetLastError());
-  // bitonic sort of Kp keys
-  const uint64_t tile = Kp < (uint64_t)kTile ? Kp : (uint64_t)kTile;
-  const int tiles = (int)((Kp + kTile - 1) / kTile);
-  bitonic_tile_kernel<<<tiles, 1024, 0, st>>>(s.key_c, s.key_p, Kp, 2, tile, ~0ull);
-  PASTA_TRY(cudaGetLastError());
-  for (uint64_t size = 2 * (uint64_t)kTile; size <= Kp; size <<= 1) {
-    for (uint64_t stride = size >> 1; stride >= (uint64_t)kTile; stride >>= 1) {
-      int gg = (int)((Kp / 2 + kBlock - 1) / kBlock);
-      if (gg > grid) gg = grid;
-      bitonic_global_kernel<<<gg, kBlock, 0, st>>>(s.key_c, s.key_p, Kp, size, stride);
-      PASTA_TRY(cudaGetLastError());
-    }
-    bitonic_tile_kernel<<<tiles, 1024, 0, st>>>(s.key_c, s.key_p, Kp, size, size, kTile / 2);
-    PASTA_TRY(cudaGetLastError());
-  }
+  e = sort_keys(s.key_c, s.key_p, Kp, grid, st, n_launches);
+  if (e != cudaSuccess) return e;
   int wg = (int)((k + 255) / 256);
   if (wg > grid) wg = grid;
-  write_kernel<<<wg, 256, 0, st>>>(s.st, s.key_c, s.key_p, k, out_page, out_count, out_found);
+  write_kernel<<<wg, 256, 0, st>>>(s.st, s.key_c, s.key_p, k, out_page, out_count, out_found, 0);
+  PASTA_TRY(cudaGetLastError());
+  return cudaSuccess;
+}
+
+cudaError_t run_topk_merge(const uint64_t* cand_page, const uint64_t* cand_count, uint32_t g, uint32_t k,
+                           uint64_t shard_pages, uint64_t* out_page, uint64_t* out_count, uint64_t* out_found,
+                           void* scratch, int grid, cudaStream_t st, int* n_launches) {
+  const uint64_t n = (uint64_t)g * k;
+  const uint64_t Kp = pow2_ceil(n < 2 ? 2 : n);
+  Scratch s = carve(scratch, Kp, grid);
+  cudaError_t e = cudaMemsetAsync(scratch, 0, 256, st);
+  if (e != cudaSuccess) return e;
+  int lg = (int)((Kp + 255) / 256);
+  if (lg > grid) lg = grid;
+  merge_load_kernel<<<lg, 256, 0, st>>>(cand_page, cand_count, g, k, shard_pages, s.st, s.key_c, s.key_p, Kp);
+  PASTA_TRY(cudaGetLastError());
+  e = sort_keys(s.key_c, s.key_p, Kp, grid, st, n_launches);
+  if (e != cudaSuccess) return e;
+  int wg = (int)((k + 255) / 256);
+  if (wg > grid) wg = grid;
+  write_kernel<<<wg, 256, 0, st>>>(s.st, s.key_c, s.key_p, k, out_page, out_count, out_found, 1);
   PASTA_TRY(cudaGetLastError());
   return cudaSuccess;
 }

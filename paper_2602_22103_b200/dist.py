@@ -51,6 +51,21 @@ def merge_kernel_rows(rows_local: torch.Tensor, k0: int, n_kernels_total: int, g
     return full
 
 
+def reduce_scatter_counts(pages_padded: torch.Tensor, out: torch.Tensor, group=None) -> torch.Tensor:
+    """SUM of every rank's padded page counts; rank r receives shard r (pages
+    [r*S, (r+1)*S), S = len(pages_padded) / world)."""
+    dist.reduce_scatter_tensor(out, pages_padded, op=dist.ReduceOp.SUM, group=group)
+    return out
+
+
+def gather_candidates(pages: torch.Tensor, counts: torch.Tensor, out_pages: torch.Tensor, out_counts: torch.Tensor,
+                      group=None):
+    """[world * k] rank-major concatenation of every rank's local top-k candidates."""
+    dist.all_gather_into_tensor(out_pages, pages, group=group)
+    dist.all_gather_into_tensor(out_counts, counts, group=group)
+    return out_pages, out_counts
+
+
 class Merger:
     """One merge step for a Trace's Histograms after a local analyze (with finalize):
     SUM of counts, OR of bitmaps (+ unique pages), MAX of WS_obj."""
@@ -72,3 +87,53 @@ class Merger:
                           h.totals[T_UNIQUE_PAGES:T_UNIQUE_PAGES + 1])
         merge_max(self.ws, self.group)
         h.totals[T_WS_OBJ:T_WS_OBJ + 1].copy_(self.ws)
+
+
+class ShardedMerger:
+    """Merge with the page counts left sharded (strong scaling):
+
+    * all_reduce(SUM) of the small part [alloc_counts | totals], all_reduce(MAX) of WS;
+    * reduce_scatter(SUM) of the page counts: rank r holds the merged counts of pages
+      [r*S, (r+1)*S) (half the bytes of an all_reduce, and no rank holds all P);
+    * all_gather of the local page bitmaps + pasta_bitmap_or -> the global bitmap and
+      unique pages on every rank (NCCL has no OR);
+    * top-K: each rank selects the top-k of its shard (pasta_topk), the candidates are
+      all_gathered and pasta_topk_merge picks the global top-k (exact: a page of the
+      global top-k is in its own shard's top-k).
+    Histograms must be allocated with pad_pages_to = world * 64."""
+
+    def __init__(self, trace, hist, ks, group=None):
+        self.tr, self.hist, self.group = trace, hist, group
+        self.world = dist.get_world_size(group)
+        assert hist.P_pad % (self.world * 64) == 0, "allocate Histograms with pad_pages_to = world * 64"
+        dev = hist.packed.device
+        self.S = hist.P_pad // self.world
+        self.shard = torch.empty(self.S, dtype=torch.int64, device=dev)
+        self.gathered = torch.empty(self.world * hist.words, dtype=torch.int64, device=dev)
+        self.ws = torch.empty(1, dtype=torch.int64, device=dev)
+        self.ks = tuple(ks)
+        self.loc = {k: (torch.empty(k, dtype=torch.int64, device=dev), torch.empty(k, dtype=torch.int64, device=dev),
+                        torch.empty(1, dtype=torch.int64, device=dev)) for k in self.ks}
+        self.cand = {k: (torch.empty(self.world * k, dtype=torch.int64, device=dev),
+                         torch.empty(self.world * k, dtype=torch.int64, device=dev)) for k in self.ks}
+        self.out = {k: (torch.empty(k, dtype=torch.int64, device=dev), torch.empty(k, dtype=torch.int64, device=dev),
+                        torch.empty(1, dtype=torch.int64, device=dev)) for k in self.ks}
+
+    def merge(self):
+        from . import T_UNIQUE_PAGES, T_WS_OBJ
+
+        h = self.hist
+        self.ws.copy_(h.totals[T_WS_OBJ:T_WS_OBJ + 1])
+        dist.all_reduce(h.small, op=dist.ReduceOp.SUM, group=self.group)
+        reduce_scatter_counts(h.pages_padded, self.shard, self.group)
+        gather_bitmaps(h.page_bitmap, self.group, out=self.gathered)
+        self.tr.bitmap_or(self.gathered, self.world, h.words, h.page_bitmap,
+                          h.totals[T_UNIQUE_PAGES:T_UNIQUE_PAGES + 1])
+        merge_max(self.ws, self.group)
+        h.totals[T_WS_OBJ:T_WS_OBJ + 1].copy_(self.ws)
+        for k in self.ks:
+            lp, lc, _ = self.tr.topk(self.shard, k, out=self.loc[k])
+            cp, cc = self.cand[k]
+            gather_candidates(lp, lc, cp, cc, self.group)
+            self.tr.topk_merge(cp, cc, self.world, k, self.S, self.out[k])
+        return self.out

@@ -138,3 +138,62 @@ def test_shard_plan_is_kernel_aligned_and_covering():
                 if name == "llama":  # balanced within one kernel's worth of records
                     assert abs((j1 - j0) - p.n / world) <= max(np.diff(ko)) + 1
             assert prev == p.n
+
+
+def _worker_sharded(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_22103_b200 import dist as pdist
+
+        p = tracegen.build_plan("tiny", seed=5, n=1 << 17)
+        j0, j1, k0, k1 = p.shard(rank, world)
+        o, _, _ = _oracle_shard(p, j0, j1, k0, k1, True)
+        P = o.page_counts.size
+        P_pad = (P + 64 * world - 1) // (64 * world) * (64 * world)
+        pages = torch.zeros(P_pad, dtype=torch.int64)
+        pages[:P] = torch.from_numpy(o.page_counts.view(np.int64))
+        S = P_pad // world
+        shard = torch.empty(S, dtype=torch.int64)
+        pdist.reduce_scatter_counts(pages, shard)
+        K = 16
+        lp, lc, _ = oracle.topk(shard.numpy().view(np.uint64), K)  # stands in for pasta_topk on the shard
+        cp = torch.empty(world * K, dtype=torch.int64)
+        cc = torch.empty(world * K, dtype=torch.int64)
+        pdist.gather_candidates(torch.from_numpy(lp.view(np.int64).copy()), torch.from_numpy(lc.view(np.int64).copy()),
+                                cp, cc)
+        if rank == 0:
+            out_q.put({"shard0": shard.numpy().copy(), "cp": cp.numpy().copy(), "cc": cc.numpy().copy(), "S": S})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_sharded_topk_flow(world):
+    """reduce_scatter of the page counts + shard-local top-K + all_gather of candidates:
+    the best K of the union (global page ids) is the global top-K."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_sharded, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    p = tracegen.build_plan("tiny", seed=5, n=1 << 17)
+    o = oracle.OracleTrace(p.va_lo, p.va_hi, len(p.allocs), len(p.allocs))
+    for b, s in p.allocs:
+        o.register_alloc(b, s)
+    o.analyze(tracegen.host_records(p), p.kernel_offsets, p.page_shift)
+    S = res["S"]
+    assert np.array_equal(res["shard0"].view(np.uint64)[: min(S, o.page_counts.size)], o.page_counts[:S])
+    K = 16
+    cp, cc = res["cp"].view(np.uint64), res["cc"].view(np.uint64)
+    cand = [(int(c), int(pg) + (i // K) * S) for i, (pg, c) in enumerate(zip(cp, cc)) if c]
+    cand.sort(key=lambda x: (-x[0], x[1]))
+    rp, rc, rf = oracle.topk(o.page_counts, K)
+    assert [pg for _, pg in cand[:K]] == [int(x) for x in rp[:rf]]
+    assert [c for c, _ in cand[:K]] == [int(x) for x in rc[:rf]]

@@ -426,3 +426,65 @@ def test_merger_world1_nccl():
         tr.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("g,K", [(1, 16), (3, 100), (8, 1024)])
+def test_topk_merge_of_shard_candidates(g, K):
+    """pasta_topk_merge over g shard-local top-K lists equals the global top-K."""
+    rng = np.random.default_rng(g * 7 + K)
+    S = 50_000
+    counts = rng.integers(0, 6, size=g * S).astype(np.uint64)
+    counts[rng.integers(0, g * S, 300)] = rng.integers(10, 1000, 300).astype(np.uint64)
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    cp = torch.empty(g * K, dtype=torch.int64, device=DEV)
+    cc = torch.empty(g * K, dtype=torch.int64, device=DEV)
+    for r in range(g):
+        p, c, _ = tr.topk(_t(counts[r * S:(r + 1) * S]), K)
+        cp[r * K:(r + 1) * K] = p
+        cc[r * K:(r + 1) * K] = c
+    out = (torch.empty(K, dtype=torch.int64, device=DEV), torch.empty(K, dtype=torch.int64, device=DEV),
+           torch.empty(1, dtype=torch.int64, device=DEV))
+    tr.topk_merge(cp, cc, g, K, S, out)
+    tr.sync()
+    rp, rc, rf = oracle.topk(counts, K)
+    assert int(u64(out[2])[0]) == rf
+    assert np.array_equal(u64(out[0]), rp) and np.array_equal(u64(out[1]), rc)
+    tr.close()
+
+
+def test_sharded_merger_world1_nccl():
+    """dist.ShardedMerger at world size 1: the shard is the whole page array, and the merged
+    top-K / bitmap / totals equal the single-GPU results."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2602_22103_b200 import dist as pdist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=DEV)
+    try:
+        p = tracegen.build_plan("tiny", seed=13)
+        drec = torch.empty(p.n, dtype=torch.int64, device=DEV)
+        tracegen.device_records(tracegen.DevicePlan(p, DEV), drec)
+        tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs)
+        ko = torch.from_numpy(p.kernel_offsets.view(np.int64).copy()).to(DEV)
+        hist = tr.histograms(p.page_shift, n_kernels=p.n_kernels, kernel_rows=True, pad_pages_to=64)
+        tr.analyze(drec, p.page_shift, hist, kernel_offsets=ko)
+        ref = tr.topk(hist.page_counts, 16)
+        tr.sync()
+        ref = tuple(u64(x).copy() for x in ref)
+        totals = u64(hist.totals).copy()
+        outs = pdist.ShardedMerger(tr, hist, (16, 3), None).merge()
+        tr.sync()
+        assert np.array_equal(u64(outs[16][0]), ref[0]) and np.array_equal(u64(outs[16][1]), ref[1])
+        assert int(u64(outs[16][2])[0]) == int(ref[2][0])
+        assert np.array_equal(u64(hist.totals), totals)
+        rp, rc, rf = oracle.topk(u64(hist.page_counts), 3)
+        assert np.array_equal(u64(outs[3][0]), rp)
+        tr.close()
+    finally:
+        dist.destroy_process_group()
