@@ -115,7 +115,10 @@ typedef struct {
   uint64_t* kernel_stats;        /* [n_kernels*PASTA_KSTATS] optional; needs kernel_alloc_counts */
   uint64_t* kernel_page_bitmap;  /* [n_kernels*W] optional, OR-accumulated; needs kernel_alloc_counts */
   uint32_t flags;                /* PASTA_NO_FINALIZE */
-  uint32_t reserved;
+  uint32_t window_kernels;       /* kernels per hotness window (>= 1 when hotness != NULL) */
+  uint64_t* hotness;             /* [ceil(n_kernels/window_kernels) * P] optional +=, needs
+                                    kernel_alloc_counts: time-windowed page hotness, row
+                                    w = kernel k / window_kernels (NEXT f1)   */
 } pasta_histograms;
 
 /* Skip the finalize step in pasta_analyze (bitmap, unique pages, footprints, WS);

@@ -42,7 +42,7 @@ def lib():
         L = ctypes.CDLL(path)
         vp, u64, u32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32
         L.oracle_analyze.restype = ctypes.c_int
-        L.oracle_analyze.argtypes = [vp, u64, vp, u64, vp, u64, u64, u64, u32, u64, vp, vp, vp, vp, vp, vp]
+        L.oracle_analyze.argtypes = [vp, u64, vp, u64, vp, u64, u64, u64, u32, u64, vp, vp, vp, vp, vp, vp, vp, u64]
         L.oracle_bitmap.restype = u64
         L.oracle_bitmap.argtypes = [vp, u64, vp]
         L.oracle_footprint.restype = u64
@@ -71,6 +71,7 @@ class OracleTrace:
         self.kernel_rows = None
         self.kun = None
         self.kernel_pages = None
+        self.hotness = None
         self.page_counts = None
         self.page_shift = None
         self.alloc_counts = np.zeros(self.max_ids, dtype=np.uint64)
@@ -106,7 +107,7 @@ class OracleTrace:
 
     # ---- one analyze call, accumulating ----
     def analyze(self, addr: np.ndarray, kernel_offsets=None, page_shift: int = 12, kernel_rows: bool = False,
-                kernel_pages: bool = False):
+                kernel_pages: bool = False, window_kernels: int = 0):
         addr = np.ascontiguousarray(addr, dtype=np.uint64)
         n = addr.size
         P = (self.va_hi - self.va_lo) >> page_shift
@@ -129,12 +130,19 @@ class OracleTrace:
             if self.kernel_pages is None or self.kernel_pages.shape != (nk, W):
                 self.kernel_pages = np.zeros((nk, W), dtype=np.uint64)
             kp = self.kernel_pages
+        hot = None
+        if window_kernels:
+            nw = (nk + window_kernels - 1) // window_kernels
+            if self.hotness is None or self.hotness.shape != (nw, P):
+                self.hotness = np.zeros((nw, P), dtype=np.uint64)
+            hot = self.hotness
         live = (_Range * max(1, len(self.live)))()
         for i, (b, (s, idx)) in enumerate(sorted(self.live.items())):
             live[i].base, live[i].size, live[i].id = b, s, idx
         rc = lib().oracle_analyze(ctypes.addressof(live), len(self.live), _ptr(addr), n, _ptr(ko), nk,
                                   self.va_lo, self.va_hi, page_shift, self.max_ids, _ptr(self.page_counts),
-                                  _ptr(self.alloc_counts), _ptr(self.totals), _ptr(kac), _ptr(kun), _ptr(kp))
+                                  _ptr(self.alloc_counts), _ptr(self.totals), _ptr(kac), _ptr(kun), _ptr(kp),
+                                  _ptr(hot), window_kernels)
         if rc != 0:
             raise ValueError(f"oracle_analyze rejected its input ({rc})")
 

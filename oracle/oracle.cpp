@@ -23,6 +23,7 @@
 //  * P:916 "tracks access hotness over time in the unit of 2MB virtual memory
 //    blocks"                                     -> page histogram (s = 21; s = 12 too)
 //  * P:918-919 hot blocks are prefetch / cudaMemAdvise candidates -> top-K hot pages
+//  * P:912-920 hotness "over time" -> time-windowed page matrix (R17)
 // Readings where the paper is silent are DESIGN.md "Readings" R1-R14.
 //
 // Parity status: every function below is pinned by tests/test_oracle_pins.py
@@ -55,11 +56,15 @@ struct oracle_range {
 //   totals[3]             records, unattributed, out_of_window
 //   kac[n_kernels*max_ids], kun[n_kernels]             optional (NULL)
 //   kernel_pages[n_kernels*ceil(P/64)] (bits OR-ed in)  optional (NULL)
+//   hot[ceil(n_kernels/window_kernels)*P]  optional (NULL): time-windowed hotness, the
+//     count of page p in window w = k / window_kernels ("tracks access hotness
+//     over time in the unit of 2MB virtual memory blocks")
 // Returns 0, or -1 if an id is out of range or the offsets are inconsistent.
 int oracle_analyze(const oracle_range* live, uint64_t n_live, const uint64_t* addr, uint64_t n,
                    const uint64_t* kernel_offsets, uint64_t n_kernels, uint64_t va_lo, uint64_t va_hi,
                    uint32_t page_shift, uint64_t max_ids, uint64_t* page_counts, uint64_t* alloc_counts,
-                   uint64_t* totals, uint64_t* kac, uint64_t* kun, uint64_t* kernel_pages) {
+                   uint64_t* totals, uint64_t* kac, uint64_t* kun, uint64_t* kernel_pages, uint64_t* hot,
+                   uint64_t window_kernels) {
   // Step 1: std::map<base, (end, id)> from the live registrations.
   std::map<uint64_t, std::pair<uint64_t, uint32_t>> ranges;
   for (uint64_t i = 0; i < n_live; ++i) {
@@ -74,6 +79,7 @@ int oracle_analyze(const oracle_range* live, uint64_t n_live, const uint64_t* ad
     offs = {0, n};
   }
   if (offs.front() != 0 || offs.back() != n) return -1;
+  if (hot && window_kernels == 0) return -1;
   for (uint64_t k = 0; k < n_kernels; ++k)
     if (offs[k] > offs[k + 1]) return -1;
 
@@ -111,6 +117,7 @@ int oracle_analyze(const oracle_range* live, uint64_t n_live, const uint64_t* ad
         const uint64_t p = (a - va_lo) >> page_shift;
         page[p] += 1;
         kpages.insert(p);
+        if (hot) hot[(k / window_kernels) * P + p] += 1;
       } else {
         oow += 1;
       }

@@ -50,7 +50,7 @@ class pasta_histograms(ctypes.Structure):
     _fields_ = [("page_counts", ctypes.c_void_p), ("alloc_counts", ctypes.c_void_p), ("totals", ctypes.c_void_p),
                 ("page_bitmap", ctypes.c_void_p), ("kernel_alloc_counts", ctypes.c_void_p),
                 ("kernel_stats", ctypes.c_void_p), ("kernel_page_bitmap", ctypes.c_void_p),
-                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("window_kernels", ctypes.c_uint32), ("hotness", ctypes.c_void_p)]
 
 
 _vp, _u64, _u32, _int = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
@@ -178,7 +178,7 @@ class Histograms:
     arrays and the bitmap are separate tensors."""
 
     def __init__(self, P: int, max_ids: int, device, n_kernels: int = 0, kernel_rows: bool = False,
-                 kernel_pages: bool = False, bitmap: bool = True, pad_pages_to: int = 1):
+                 kernel_pages: bool = False, bitmap: bool = True, pad_pages_to: int = 1, window_kernels: int = 0):
         import torch
 
         self.P, self.max_ids, self.n_kernels = P, max_ids, n_kernels
@@ -199,10 +199,15 @@ class Histograms:
             self.kernel_stats = torch.zeros(n_kernels * KSTATS, dtype=torch.int64, device=device)
         if kernel_pages:
             self.kernel_page_bitmap = torch.zeros(n_kernels * self.words, dtype=torch.int64, device=device)
+        self.window_kernels = window_kernels
+        self.hotness = None
+        if window_kernels:
+            self.n_windows = (n_kernels + window_kernels - 1) // window_kernels
+            self.hotness = torch.zeros(self.n_windows * P, dtype=torch.int64, device=device)
 
     def zero_(self):
         for t in (self.packed, self.page_bitmap, self.kernel_alloc_counts, self.kernel_stats,
-                  self.kernel_page_bitmap):
+                  self.kernel_page_bitmap, self.hotness):
             if t is not None:
                 t.zero_()
         return self
@@ -210,7 +215,7 @@ class Histograms:
     def struct(self, flags: int = 0) -> pasta_histograms:
         return pasta_histograms(_ptr(self.page_counts), _ptr(self.alloc_counts), _ptr(self.totals),
                                 _ptr(self.page_bitmap), _ptr(self.kernel_alloc_counts), _ptr(self.kernel_stats),
-                                _ptr(self.kernel_page_bitmap), flags, 0)
+                                _ptr(self.kernel_page_bitmap), flags, self.window_kernels, _ptr(self.hotness))
 
 
 class Trace:
@@ -238,9 +243,9 @@ class Trace:
         pasta_register_free(self.h, base)
 
     def histograms(self, page_shift: int, n_kernels: int = 0, kernel_rows=False, kernel_pages=False, bitmap=True,
-                   pad_pages_to: int = 1):
+                   pad_pages_to: int = 1, window_kernels: int = 0):
         return Histograms(self.n_pages(page_shift), self.max_ids, self.device, n_kernels, kernel_rows, kernel_pages,
-                          bitmap, pad_pages_to)
+                          bitmap, pad_pages_to, window_kernels)
 
     def analyze(self, records, page_shift: int, hist: Histograms, kernel_offsets=None, n: int | None = None,
                 finalize: bool = True, host: bool = False):

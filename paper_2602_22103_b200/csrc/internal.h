@@ -29,6 +29,9 @@ struct ScanArgs {
   uint64_t* kstats;          // kernel_stats or nullptr
   uint64_t* kpb;             // kernel_page_bitmap or nullptr
   uint64_t add_records;      // added to totals[RECORDS] by block 0
+  uint64_t* hot;             // hotness [windows x P] or nullptr
+  uint64_t P;                // pages in the window
+  uint32_t window_kernels;   // kernels per hotness window (>= 1)
 };
 
 // Extra records that are not part of the 16-byte aligned even body (<= 2).

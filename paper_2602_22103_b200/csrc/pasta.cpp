@@ -342,7 +342,8 @@ int pasta_register_free(pasta_trace* h, uint64_t base) {
 int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t page_shift, pasta_histograms* out) {
   if (!h || !tr || !out) return PASTA_EINVAL;
   if (!out->page_counts || !out->alloc_counts || !out->totals) return PASTA_EINVAL;
-  if ((out->kernel_stats || out->kernel_page_bitmap) && !out->kernel_alloc_counts) return PASTA_EINVAL;
+  if ((out->kernel_stats || out->kernel_page_bitmap || out->hotness) && !out->kernel_alloc_counts) return PASTA_EINVAL;
+  if (out->hotness && out->window_kernels == 0) return PASTA_EINVAL;
   if (tr->flags & ~PASTA_REC_HOST) return PASTA_EINVAL;
   int s = check_window(h, page_shift);
   if (s) return s;
@@ -377,6 +378,9 @@ int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t 
   a.kac = out->kernel_alloc_counts;
   a.kstats = out->kernel_stats;
   a.kpb = out->kernel_page_bitmap;
+  a.hot = out->hotness;
+  a.P = P;
+  a.window_kernels = out->window_kernels ? out->window_kernels : 1;
 
   if (!host) {
     s = scan_range(h, tr->addr, n, 0, a, h->stream, n);

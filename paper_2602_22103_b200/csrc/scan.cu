@@ -167,7 +167,15 @@ struct Out {
   uint64_t max_ids;
   uint32_t words;
   uint32_t A;
+  uint64_t* hot;    // hotness matrix [windows x P] or nullptr (NEXT f1)
+  uint64_t P;
+  uint32_t wk;      // kernels per hotness window
 };
+
+// Time-windowed hotness: the page run's count also goes to row k / wk.
+__device__ __forceinline__ void hot_add(const Out& o, uint32_t page, uint64_t v, uint32_t k) {
+  if (o.hot != nullptr && page != kOOW) red_add_u64(o.hot + (uint64_t)(k / o.wk) * o.P + page, v);
+}
 
 // Owner count `v` of kernel k to global (one thread).
 template <bool kRows>
@@ -195,6 +203,7 @@ __device__ __forceinline__ void page_to_global(const Out& o, uint32_t page, uint
   } else {
     red_add_u64(o.page_counts + page, v);
     if (kPages) red_or_u64(o.kpb + (uint64_t)k * o.words + (page >> 6), 1ull << (page & 63));
+    hot_add(o, page, v, k);
   }
 }
 
@@ -236,6 +245,7 @@ __device__ __forceinline__ void flush_page_run(const Out& o, uint32_t page, uint
   if (lane == 0) red_add_u64(dst, v);
   if (kPages && lane == 0 && page != kOOW)
     red_or_u64(o.kpb + (uint64_t)k * o.words + (page >> 6), 1ull << (page & 63));
+  if (lane == 0) hot_add(o, page, v, k);
 }
 
 // Accumulate sA records of interval A then sB of interval B (sB may be 0). Fast path:
@@ -276,6 +286,7 @@ __device__ __forceinline__ void fallback_record(uint64_t x, OwnCache& oc, LaneAc
     red_add_u64(o.totals + 2, 1);
   } else {
     red_add_u64(o.page_counts + I.page, 1);
+    hot_add(o, I.page, 1, k);
     if (kPages && la.kbit != I.page) {
       red_or_u64(o.kpb + (uint64_t)k * o.words + (I.page >> 6), 1ull << (I.page & 63));
       la.kbit = I.page;
@@ -573,6 +584,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   o.max_ids = args.max_ids;
   o.words = args.words;
   o.A = A;
+  o.hot = args.hot;
+  o.P = args.P;
+  o.wk = args.window_kernels;
 
   OwnCache oc;
   oc.olo = 1;
@@ -730,6 +744,9 @@ __global__ void scan_extras_kernel(const ExtraArgs ea) {
   o.max_ids = s.max_ids;
   o.words = s.words;
   o.A = s.A;
+  o.hot = s.hot;
+  o.P = s.P;
+  o.wk = s.window_kernels;
   if (rows) owner_to_global<true>(o, I.own, 1, k);
   else owner_to_global<false>(o, I.own, 1, k);
   if (s.kpb) page_to_global<true>(o, I.page, 1, k);

@@ -20,7 +20,7 @@ def owner_of(a, live):
     return hit
 
 
-def analyze(live, records, kernel_offsets, va_lo, va_hi, s, max_ids):
+def analyze(live, records, kernel_offsets, va_lo, va_hi, s, max_ids, window_kernels=1):
     P = (va_hi - va_lo) >> s
     page = [0] * P
     alloc = [0] * max_ids
@@ -28,6 +28,8 @@ def analyze(live, records, kernel_offsets, va_lo, va_hi, s, max_ids):
     kac = [[0] * max_ids for _ in range(nk)]
     kun = [0] * nk
     kpages = [[0] * P for _ in range(nk)]
+    nw = (nk + window_kernels - 1) // window_kernels
+    hot = [[0] * P for _ in range(nw)]
     unattr = 0
     oow = 0
     for k in range(nk):
@@ -48,9 +50,10 @@ def analyze(live, records, kernel_offsets, va_lo, va_hi, s, max_ids):
                     p += 1
                 page[p] += 1
                 kpages[k][p] = 1
+                hot[k // window_kernels][p] += 1
             else:
                 oow += 1
-    return dict(page=page, alloc=alloc, kac=kac, kun=kun, kpages=kpages, unattr=unattr, oow=oow)
+    return dict(page=page, alloc=alloc, kac=kac, kun=kun, kpages=kpages, unattr=unattr, oow=oow, hot=hot)
 
 
 def bitmap_words(page):

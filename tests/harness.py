@@ -36,13 +36,14 @@ def oracle_trace(va_lo, va_hi, ranges, max_ids=None, max_live=None):
 
 
 def run_gpu(tr, records, page_shift, kernel_offsets=None, kernel_rows=False, kernel_pages=False, topk=(),
-            hist=None, finalize=True, host=False, n=None):
+            hist=None, finalize=True, host=False, n=None, window_kernels=0):
     """records: CUDA int64 tensor (or pinned CPU tensor with host=True)."""
     import torch
 
     nk = 0 if kernel_offsets is None else len(kernel_offsets) - 1
     if hist is None:
-        hist = tr.histograms(page_shift, n_kernels=nk, kernel_rows=kernel_rows, kernel_pages=kernel_pages)
+        hist = tr.histograms(page_shift, n_kernels=nk, kernel_rows=kernel_rows, kernel_pages=kernel_pages,
+                             window_kernels=window_kernels)
     ko = None
     if kernel_offsets is not None:
         ko = torch.tensor(np.asarray(kernel_offsets, dtype=np.uint64).view(np.int64), dtype=torch.int64)
@@ -64,12 +65,16 @@ def run_gpu(tr, records, page_shift, kernel_offsets=None, kernel_rows=False, ker
         out["kstats"] = u64(hist.kernel_stats).reshape(hist.n_kernels, 4)[:nk]
     if hist.kernel_page_bitmap is not None:
         out["kpb"] = u64(hist.kernel_page_bitmap).reshape(hist.n_kernels, -1)[:nk]
+    if hist.hotness is not None:
+        out["hot"] = u64(hist.hotness).reshape(hist.n_windows, -1)
     out["topk"] = {K: (u64(p), u64(c), int(u64(f)[0])) for K, (p, c, f) in tops.items()}
     return out
 
 
-def run_oracle(o, records_np, page_shift, kernel_offsets=None, kernel_rows=False, kernel_pages=False, topk=()):
-    o.analyze(records_np, kernel_offsets, page_shift, kernel_rows=kernel_rows, kernel_pages=kernel_pages)
+def run_oracle(o, records_np, page_shift, kernel_offsets=None, kernel_rows=False, kernel_pages=False, topk=(),
+               window_kernels=0):
+    o.analyze(records_np, kernel_offsets, page_shift, kernel_rows=kernel_rows, kernel_pages=kernel_pages,
+              window_kernels=window_kernels)
     out = {"page_counts": o.page_counts.copy(), "alloc_counts": o.alloc_counts.copy(), "totals3": o.totals.copy()}
     bm, u = o.bitmap()
     out["bitmap"], out["unique"] = bm, u
@@ -81,6 +86,8 @@ def run_oracle(o, records_np, page_shift, kernel_offsets=None, kernel_rows=False
     if kernel_pages:
         out["kpb"] = o.kernel_pages.copy()
         out["kup"] = o.kernel_unique_pages()
+    if window_kernels:
+        out["hot"] = o.hotness.copy()
     out["topk"] = {K: o.topk(K) for K in topk}
     return out
 
@@ -105,6 +112,8 @@ def assert_parity(g, r, kernel_rows=False, kernel_pages=False, label=""):
     if kernel_pages:
         assert np.array_equal(g["kpb"], r["kpb"]), f"{label}: kernel_page_bitmap"
         assert np.array_equal(g["kstats"][:, 3], r["kup"]), f"{label}: kernel unique pages"
+    if "hot" in g or "hot" in r:
+        assert np.array_equal(g["hot"], r["hot"]), f"{label}: hotness"
     for K, (p, c, f) in g["topk"].items():
         rp, rc, rf = r["topk"][K]
         assert f == rf, f"{label}: top{K} found {f} != {rf}"

@@ -33,7 +33,7 @@ def _t(np_u64):
 
 
 def _case(ranges, records, va_lo, va_hi, s, ko=None, rows=True, pages=True, topk=(1, 5, 64), max_ids=None,
-          label="", misalign=False):
+          label="", misalign=False, window_kernels=0):
     rec = np.asarray(records, dtype=np.uint64)
     tr = gpu_trace(DEV, va_lo, va_hi, ranges, max_ids=max_ids)
     o = oracle_trace(va_lo, va_hi, ranges, max_ids=max_ids)
@@ -46,8 +46,9 @@ def _case(ranges, records, va_lo, va_hi, s, ko=None, rows=True, pages=True, topk
         assert dev_rec.data_ptr() % 16 == 8
     else:
         dev_rec = _t(rec) if rec.size else torch.zeros(0, dtype=torch.int64, device=DEV)
-    g = run_gpu(tr, dev_rec, s, ko, kernel_rows=rows, kernel_pages=pages and rows, topk=topk)
-    r = run_oracle(o, rec, s, ko, kernel_rows=rows, kernel_pages=pages and rows, topk=topk)
+    wk = window_kernels if rows else 0
+    g = run_gpu(tr, dev_rec, s, ko, kernel_rows=rows, kernel_pages=pages and rows, topk=topk, window_kernels=wk)
+    r = run_oracle(o, rec, s, ko, kernel_rows=rows, kernel_pages=pages and rows, topk=topk, window_kernels=wk)
     assert_parity(g, r, kernel_rows=rows, kernel_pages=pages and rows, label=label)
     tr.close()
     return g, r
@@ -127,9 +128,12 @@ def test_tiny_config_parity(seed):
     tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs)
     o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
     ko = [int(x) for x in p.kernel_offsets]
-    g = run_gpu(tr, drec, p.page_shift, ko, kernel_rows=True, kernel_pages=True, topk=(16, 1, 1000))
-    r = run_oracle(o, rec, p.page_shift, ko, kernel_rows=True, kernel_pages=True, topk=(16, 1, 1000))
+    g = run_gpu(tr, drec, p.page_shift, ko, kernel_rows=True, kernel_pages=True, topk=(16, 1, 1000),
+                window_kernels=3)
+    r = run_oracle(o, rec, p.page_shift, ko, kernel_rows=True, kernel_pages=True, topk=(16, 1, 1000),
+                   window_kernels=3)
     assert_parity(g, r, kernel_rows=True, kernel_pages=True, label=f"tiny/{seed}")
+    assert g["hot"].shape == (3, p.n_pages) and int(g["hot"].sum()) == int(g["page_counts"].sum())
     tr.close()
 
 
@@ -218,7 +222,7 @@ def test_adversarial_random(seed):
             cuts[0] = cuts[1]  # an empty kernel
         ko = [0] + cuts + [n]
         _case(ranges, rec, va_lo, va_hi, s, ko=ko, topk=(1, 7, 300), misalign=rng.random() < 0.4,
-              label=f"adv{seed}/{trial} n={n} A={len(ranges)} s={s}")
+              label=f"adv{seed}/{trial} n={n} A={len(ranges)} s={s}", window_kernels=rng.choice([0, 1, 3]))
 
 
 def test_many_ranges_global_table():

@@ -331,8 +331,10 @@ def test_brute_force_agreement():
         for b, sz, i in live:
             st, got = o.register_alloc(b, sz)
             assert st == oracle.OK and got == i, (case, b, sz)
-        o.analyze(np.array(recs, dtype=np.uint64), ko, s, kernel_rows=True, kernel_pages=True)
-        bf = brute.analyze(live, recs, ko, va_lo, va_hi, s, max_ids)
+        wk = rng.randint(1, 3)
+        o.analyze(np.array(recs, dtype=np.uint64), ko, s, kernel_rows=True, kernel_pages=True, window_kernels=wk)
+        bf = brute.analyze(live, recs, ko, va_lo, va_hi, s, max_ids, window_kernels=wk)
+        assert o.hotness.tolist() == bf["hot"], case
         assert o.page_counts.tolist() == bf["page"], case
         assert o.alloc_counts.tolist() == bf["alloc"], case
         assert o.kernel_rows.tolist() == bf["kac"], case
@@ -367,3 +369,35 @@ def test_registration_errors():
     assert o.register_alloc(0x3000, 0x10) == (oracle.OK, 2)
     assert o.register_free(0x3000) == oracle.OK
     assert o.register_alloc(0x3000, 0x10)[0] == oracle.ECAPACITY  # max_ids = 3, ids never reused
+
+
+# ---------------- time-windowed hotness (NEXT f1) ----------------
+def test_spec_hotness_matrix_examples():
+    """one access at block 3 in window 0 -> a matrix with a single 1; the matrix
+    sums to the in-window access count; a persistent tensor's block row has no zero window
+    while a transient burst's row is zero outside its burst."""
+    MiB = 1 << 20
+    o = OracleTrace(0, 64 * MiB, 4, 4)
+    o.analyze(np.array([3 * 2 * MiB + 5], dtype=np.uint64), [0, 1, 1], 21, kernel_rows=True, window_kernels=1)
+    assert o.hotness.shape == (2, 32)
+    assert int(o.hotness.sum()) == 1 and int(o.hotness[0, 3]) == 1
+    # 10 kernels: block 1 (weights) read in every kernel, block 7 (a transient buffer) in kernels 3-4
+    rec, ko = [], [0]
+    for k in range(10):
+        rec += [1 * 2 * MiB + 64 * i for i in range(50)]
+        if k in (3, 4):
+            rec += [7 * 2 * MiB + 8 * i for i in range(200)]
+        rec += [100 * MiB + 8]  # out of window: not in the matrix
+        ko.append(len(rec))
+    o2 = OracleTrace(0, 64 * MiB, 4, 4)
+    o2.analyze(np.array(rec, dtype=np.uint64), ko, 21, kernel_rows=True, window_kernels=1)
+    h = o2.hotness
+    assert np.all(h[:, 1] == 50)
+    assert h[3, 7] == 200 and h[4, 7] == 200 and int(h[:, 7].sum()) == 400
+    assert int(h.sum()) == len(rec) - 10
+    # windows of 3 kernels sum rows of the per-kernel matrix
+    o3 = OracleTrace(0, 64 * MiB, 4, 4)
+    o3.analyze(np.array(rec, dtype=np.uint64), ko, 21, kernel_rows=True, window_kernels=3)
+    assert o3.hotness.shape == (4, 32)
+    for w in range(4):
+        assert np.array_equal(o3.hotness[w], h[3 * w:3 * w + 3].sum(axis=0))
