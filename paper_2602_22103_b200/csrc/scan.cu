@@ -173,8 +173,11 @@ struct Out {
 };
 
 // Time-windowed hotness: the page run's count also goes to row k / wk.
+// Compiled in only for the hotness variants: kPages is a mode, bit 0 = per-kernel page
+// bits, bit 1 = hotness.
+template <int kMode>
 __device__ __forceinline__ void hot_add(const Out& o, uint32_t page, uint64_t v, uint32_t k) {
-  if (o.hot != nullptr && page != kOOW) red_add_u64(o.hot + (uint64_t)(k / o.wk) * o.P + page, v);
+  if ((kMode & 2) && page != kOOW) red_add_u64(o.hot + (uint64_t)(k / o.wk) * o.P + page, v);
 }
 
 // Owner count `v` of kernel k to global (one thread).
@@ -195,15 +198,15 @@ __device__ __forceinline__ void owner_to_global(const Out& o, uint32_t own, uint
 }
 
 // Page count `v` of kernel k to global (one thread).
-template <bool kPages>
+template <int kPages>
 __device__ __forceinline__ void page_to_global(const Out& o, uint32_t page, uint64_t v, uint32_t k) {
   if (v == 0) return;
   if (page == kOOW) {
     red_add_u64(o.totals + 2, v);
   } else {
     red_add_u64(o.page_counts + page, v);
-    if (kPages) red_or_u64(o.kpb + (uint64_t)k * o.words + (page >> 6), 1ull << (page & 63));
-    hot_add(o, page, v, k);
+    if (kPages & 1) red_or_u64(o.kpb + (uint64_t)k * o.words + (page >> 6), 1ull << (page & 63));
+    hot_add<kPages>(o, page, v, k);
   }
 }
 
@@ -213,7 +216,7 @@ struct WarpAcc {
   uint32_t pcnt, ocnt;
 };
 
-template <bool kRows, bool kPages>
+template <bool kRows, int kPages>
 __device__ __forceinline__ void wadd(WarpAcc& w, const Out& o, uint32_t page, uint32_t own, uint32_t c, uint32_t k,
                                      uint32_t lane) {
   if (page != w.page) {
@@ -221,7 +224,7 @@ __device__ __forceinline__ void wadd(WarpAcc& w, const Out& o, uint32_t page, ui
     // one predicated RED (no divergent branch): out-of-window counts go to totals[2]
     uint64_t* dst = (w.page == kOOW) ? o.totals + 2 : o.page_counts + w.page;
     if (lane == 0 && w.pcnt != 0) red_add_u64(dst, w.pcnt);
-    if (kPages && lane == 0 && w.pcnt != 0 && w.page != kOOW)
+    if ((kPages & 1) && lane == 0 && w.pcnt != 0 && w.page != kOOW)
       red_or_u64(o.kpb + (uint64_t)k * o.words + (w.page >> 6), 1ull << (w.page & 63));
 #else
     if (lane == 0) page_to_global<kPages>(o, w.page, w.pcnt, k);
@@ -239,19 +242,19 @@ __device__ __forceinline__ void wadd(WarpAcc& w, const Out& o, uint32_t page, ui
 }
 
 // One predicated RED for a finished page run (out-of-window runs go to totals[2]).
-template <bool kPages>
+template <int kPages>
 __device__ __forceinline__ void flush_page_run(const Out& o, uint32_t page, uint32_t v, uint32_t k, uint32_t lane) {
   uint64_t* dst = (page == kOOW) ? o.totals + 2 : o.page_counts + page;
   if (lane == 0) red_add_u64(dst, v);
-  if (kPages && lane == 0 && page != kOOW)
+  if ((kPages & 1) && lane == 0 && page != kOOW)
     red_or_u64(o.kpb + (uint64_t)k * o.words + (page >> 6), 1ull << (page & 63));
-  if (lane == 0) hot_add(o, page, v, k);
+  if ((kPages & 2) && lane == 0) hot_add<kPages>(o, page, v, k);
 }
 
 // Accumulate sA records of interval A then sB of interval B (sB may be 0). Fast path:
 // A continues the warp's current page and owner and B has the same owner, so page A
 // is complete: one RED, no owner flush.
-template <bool kRows, bool kPages>
+template <bool kRows, int kPages>
 __device__ __forceinline__ void wadd2(WarpAcc& w, const Out& o, const Ival& IA, uint32_t sA, const Ival& IB,
                                       uint32_t sB, uint32_t k, uint32_t lane) {
 #if PASTA_WADD2
@@ -278,7 +281,7 @@ struct LaneAcc {
 };
 
 // Tier F: one record, looked up alone; page count straight to L2, owner accumulated.
-template <bool kBig, bool kRows, bool kPages>
+template <bool kBig, bool kRows, int kPages>
 __device__ __forceinline__ void fallback_record(uint64_t x, OwnCache& oc, LaneAcc& la, const Ctx& c, const Out& o,
                                              uint32_t k) {
   const Ival I = lookup<kBig>(oc, x, c);
@@ -286,8 +289,8 @@ __device__ __forceinline__ void fallback_record(uint64_t x, OwnCache& oc, LaneAc
     red_add_u64(o.totals + 2, 1);
   } else {
     red_add_u64(o.page_counts + I.page, 1);
-    hot_add(o, I.page, 1, k);
-    if (kPages && la.kbit != I.page) {
+    hot_add<kPages>(o, I.page, 1, k);
+    if ((kPages & 1) && la.kbit != I.page) {
       red_or_u64(o.kpb + (uint64_t)k * o.words + (I.page >> 6), 1ull << (I.page & 63));
       la.kbit = I.page;
     }
@@ -302,7 +305,7 @@ __device__ __forceinline__ void fallback_record(uint64_t x, OwnCache& oc, LaneAc
 
 // Warp-collective: merge every lane's up to two (page, owner, count) entries into the
 // warp accumulators (leader loop; one __reduce_add_sync per distinct key).
-template <bool kRows, bool kPages>
+template <bool kRows, int kPages>
 __device__ __forceinline__ void merge_entries(WarpAcc& w, const Out& o, uint32_t k, uint32_t lane, bool pa,
                                               uint32_t pA, uint32_t oA, uint32_t cA, bool pb, uint32_t pB,
                                               uint32_t oB, uint32_t cB) {
@@ -322,7 +325,7 @@ __device__ __forceinline__ void merge_entries(WarpAcc& w, const Out& o, uint32_t
 }
 
 // Tier L + F for this lane's records selected by `valid` (bit i <-> a[i]).
-template <bool kBig, bool kRows, bool kPages>
+template <bool kBig, bool kRows, int kPages>
 __device__ __forceinline__ void process_lane(const uint64_t (&a)[8], uint32_t valid, OwnCache& oc, LaneAcc& la,
                                              WarpAcc& w, const Ctx& c, const Out& o, uint32_t k, uint32_t lane) {
   // seed A: first valid record
@@ -388,7 +391,7 @@ __device__ __forceinline__ uint32_t count_sorted8(const uint32_t (&v)[8], uint32
 
 // Full 256-record slice. `a` holds the strided view (lane l: positions 64i + 2l + h);
 // `slot` is the slice's shared-memory address (for the lane-contiguous re-read).
-template <bool kBig, bool kRows, bool kPages>
+template <bool kBig, bool kRows, int kPages>
 __device__ __forceinline__ void process_full(const uint64_t (&a)[8], uint32_t slot, Ival& cur, OwnCache& oc,
                                              LaneAcc& la, WarpAcc& w, const Ctx& c, const Out& o, uint32_t k,
                                              uint32_t lane) {
@@ -488,7 +491,7 @@ __device__ __forceinline__ void process_full(const uint64_t (&a)[8], uint32_t sl
 }
 
 // Warp-local flush of everything accumulated for kernel segment k.
-template <bool kRows, bool kPages>
+template <bool kRows, int kPages>
 __device__ __forceinline__ void warp_flush(WarpAcc& w, LaneAcc& la, const Out& o, uint32_t k, uint32_t lane) {
   if (lane == 0) {
     page_to_global<kPages>(o, w.page, w.pcnt, k);
@@ -524,7 +527,7 @@ __device__ __forceinline__ uint32_t kernel_of(const uint64_t* __restrict__ koffs
   return lo;
 }
 
-template <bool kBig, bool kRows, bool kPages>
+template <bool kBig, bool kRows, int kPages>
 __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages));
@@ -749,8 +752,11 @@ __global__ void scan_extras_kernel(const ExtraArgs ea) {
   o.wk = s.window_kernels;
   if (rows) owner_to_global<true>(o, I.own, 1, k);
   else owner_to_global<false>(o, I.own, 1, k);
-  if (s.kpb) page_to_global<true>(o, I.page, 1, k);
-  else page_to_global<false>(o, I.page, 1, k);
+  const int mode = (s.kpb ? 1 : 0) | (s.hot ? 2 : 0);
+  if (mode == 3) page_to_global<3>(o, I.page, 1, k);
+  else if (mode == 2) page_to_global<2>(o, I.page, 1, k);
+  else if (mode == 1) page_to_global<1>(o, I.page, 1, k);
+  else page_to_global<0>(o, I.page, 1, k);
 }
 
 int stages_for(uint32_t A, bool big) {
@@ -761,7 +767,7 @@ int stages_for(uint32_t A, bool big) {
   return (int)st;
 }
 
-template <bool kBig, bool kRows, bool kPages>
+template <bool kBig, bool kRows, int kPages>
 cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
   const int stages = stages_for(a.A, kBig);
   const int smem = scan_smem_bytes(a.A, kBig);
@@ -784,16 +790,24 @@ int scan_smem_bytes(uint32_t A, bool big_table) {
 
 cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st) {
   const bool big = !scan_table_fits_smem(a.A);
-  const bool rows = a.kac != nullptr;
-  const bool pages = a.kpb != nullptr;
+  const bool rows = a.kac != nullptr;  // per-kernel outputs all require kernel rows
+  const int mode = (a.kpb != nullptr ? 1 : 0) | (a.hot != nullptr ? 2 : 0);
   if (big) {
-    if (!rows) return launch_variant<true, false, false>(a, grid, st);
-    if (!pages) return launch_variant<true, true, false>(a, grid, st);
-    return launch_variant<true, true, true>(a, grid, st);
+    if (!rows) return launch_variant<true, false, 0>(a, grid, st);
+    switch (mode) {
+      case 0: return launch_variant<true, true, 0>(a, grid, st);
+      case 1: return launch_variant<true, true, 1>(a, grid, st);
+      case 2: return launch_variant<true, true, 2>(a, grid, st);
+      default: return launch_variant<true, true, 3>(a, grid, st);
+    }
   }
-  if (!rows) return launch_variant<false, false, false>(a, grid, st);
-  if (!pages) return launch_variant<false, true, false>(a, grid, st);
-  return launch_variant<false, true, true>(a, grid, st);
+  if (!rows) return launch_variant<false, false, 0>(a, grid, st);
+  switch (mode) {
+    case 0: return launch_variant<false, true, 0>(a, grid, st);
+    case 1: return launch_variant<false, true, 1>(a, grid, st);
+    case 2: return launch_variant<false, true, 2>(a, grid, st);
+    default: return launch_variant<false, true, 3>(a, grid, st);
+  }
 }
 
 cudaError_t launch_scan_extras(const ExtraArgs& a, cudaStream_t st) {

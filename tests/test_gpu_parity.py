@@ -43,7 +43,7 @@ def _case(ranges, records, va_lo, va_hi, s, ko=None, rows=True, pages=True, topk
         buf = torch.zeros(rec.size + 1, dtype=torch.int64, device=DEV)
         buf[1:] = _t(rec) if rec.size else buf[1:]
         dev_rec = buf[1:]
-        assert dev_rec.data_ptr() % 16 == 8
+        assert rec.size == 0 or dev_rec.data_ptr() % 16 == 8
     else:
         dev_rec = _t(rec) if rec.size else torch.zeros(0, dtype=torch.int64, device=DEV)
     wk = window_kernels if rows else 0
