@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--e2e-records", type=int, default=1 << 31, help="cap of the pinned host trace for e2e")
     ap.add_argument("--cpu-sample", type=int, default=1 << 28, help="records in the oracle's bounded sample")
     ap.add_argument("--ref-sample", type=int, default=1 << 24, help="records per --impl reference step")
+    ap.add_argument("--stream-batch", type=int, default=0,
+                    help="also time streaming mode: one pasta_analyze per batch of this many records "
+                         "(524288 = the paper's 4 MB buffer), captured in a CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -286,6 +289,9 @@ def run_ours(args):
     value = plan.n * args.steps / (ms_max / 1e3) / 1e9
 
     # ---- e2e: same metric through the C ABI from pinned HOST memory ----
+    stream_res = None
+    if args.stream_batch:
+        stream_res = run_stream(args, plan, rec, n_loc, ko_loc, nk_loc, dev, int(hist.totals[0].item()))
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, dev, top_out)
@@ -320,10 +326,68 @@ def run_ours(args):
             "e2e": e2e,
             "frac_of_8TBs_spec": (achieved / 8000.0) if achieved else None,
         }
+        if stream_res is not None:
+            line["stream"] = stream_res
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier(device_ids=[local])
         torch.distributed.destroy_process_group()
+
+
+def run_stream(args, plan, rec, n_loc, ko_loc, nk_loc, dev, expect_records):
+    """Streaming mode (NEXT f2): the same records analyzed as fixed-size batches, one
+    pasta_analyze (NO_FINALIZE) per batch plus one pasta_finalize, on a dedicated stream;
+    timed eagerly and as one CUDA-graph replay of all the calls."""
+    import torch
+
+    import paper_2602_22103_b200 as pb
+    from paper_2602_22103_b200.stream import BatchRunner
+
+    s = torch.cuda.Stream(dev)
+    A = len(plan.allocs)
+    tr = pb.Trace(dev, plan.va_lo, plan.va_hi, A, A, stream=s)
+    for b, sz in plan.allocs:
+        tr.register_alloc(b, sz)
+    h = tr.histograms(plan.page_shift, n_kernels=nk_loc, kernel_rows=plan.want_kernel_rows,
+                      kernel_pages=plan.want_kernel_pages)
+    runner = BatchRunner(tr, h, rec, ko_loc.cpu().numpy(), n_loc, args.stream_batch, plan.page_shift)
+
+    def once():
+        h.zero_()
+        runner.run()
+        tr.finalize(plan.page_shift, h, n_kernels=nk_loc)
+
+    with torch.cuda.stream(s):
+        once()  # also uploads the range table
+    s.synchronize()
+    assert int(h.totals[0].item()) == expect_records
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    with torch.cuda.stream(s):
+        e0.record(s)
+        for _ in range(reps):
+            once()
+        e1.record(s)
+    s.synchronize()
+    eager_ms = e0.elapsed_time(e1) / reps
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        once()
+    with torch.cuda.stream(s):
+        g.replay()
+        e0.record(s)
+        for _ in range(reps):
+            g.replay()
+        e1.record(s)
+    s.synchronize()
+    graph_ms = e0.elapsed_time(e1) / reps
+    assert int(h.totals[0].item()) == expect_records
+    calls = len(runner.calls)
+    tr.close()
+    return {"batch_records": args.stream_batch, "calls": calls, "unit": "G rec/s",
+            "graph_value": n_loc / (graph_ms / 1e3) / 1e9, "graph_ms": graph_ms,
+            "eager_value": n_loc / (eager_ms / 1e3) / 1e9, "eager_ms": eager_ms,
+            "graph_us_per_call": graph_ms * 1e3 / calls}
 
 
 def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, dev, top_out):

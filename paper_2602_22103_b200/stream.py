@@ -1,0 +1,67 @@
+"""Streaming / in-situ mode: a trace analyzed as a sequence
+of fixed-size batches, the paper's operating point being a "4MB" device buffer (P:323,
+P:971) = 524,288 records per call.
+
+Every batch is one pasta_analyze call with PASTA_NO_FINALIZE over records [a, b). Its
+kernel offsets are the global kernel offsets clipped to [a, b) and rebased, and its
+per-kernel output pointers start at row k0 (the kernel holding record a), so kernels
+cut between batches simply accumulate into the same global row (counts are sums over
+any partition of the records). One pasta_finalize at the end derives
+the bitmap, unique pages, footprints and WS. Host-side planning only; the calls can be
+captured once into a CUDA graph and replayed (see bench.py --stream-batch).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def plan_batches(kernel_offsets, n: int, batch: int):
+    """[(a, b, k0, sub_offsets)] covering [0, n) in batches of `batch` records.
+
+    sub_offsets (int64, len = kernels overlapping [a, b) + 1) are the kernel offsets of
+    the batch relative to a; k0 is the global index of its first kernel."""
+    ko = np.asarray(kernel_offsets, dtype=np.int64)
+    out = []
+    for a in range(0, n, batch):
+        b = min(n, a + batch)
+        k0 = int(np.searchsorted(ko, a, side="right")) - 1
+        k1 = int(np.searchsorted(ko, b, side="left"))  # first kernel starting at or after b
+        inner = np.clip(ko[k0 + 1:k1] - a, 0, b - a)
+        sub = np.concatenate([[0], inner, [b - a]]).astype(np.int64)
+        out.append((a, b, k0, sub))
+    return out
+
+
+class BatchRunner:
+    """Issues the batch calls of plan_batches on a Trace's stream (all device memory)."""
+
+    def __init__(self, trace, hist, records, kernel_offsets, n: int, batch: int, page_shift: int):
+        import torch
+
+        from . import PASTA_NO_FINALIZE, pasta_analyze, pasta_histograms
+
+        self.tr, self.hist, self.page_shift = trace, hist, page_shift
+        self.batches = plan_batches(kernel_offsets, n, batch)
+        dev = records.device
+        flat = np.concatenate([s for _, _, _, s in self.batches])
+        self.offs = torch.from_numpy(flat).to(dev)
+        self.calls = []
+        pos = 0
+        W = hist.words
+        for a, b, k0, sub in self.batches:
+            hs = pasta_histograms(
+                hist.page_counts.data_ptr(), hist.alloc_counts.data_ptr(), hist.totals.data_ptr(),
+                hist.page_bitmap.data_ptr() if hist.page_bitmap is not None else None,
+                hist.kernel_alloc_counts.data_ptr() + 8 * k0 * hist.max_ids
+                if hist.kernel_alloc_counts is not None else None,
+                hist.kernel_stats.data_ptr() + 8 * 4 * k0 if hist.kernel_stats is not None else None,
+                hist.kernel_page_bitmap.data_ptr() + 8 * W * k0 if hist.kernel_page_bitmap is not None else None,
+                PASTA_NO_FINALIZE, 0, None)
+            self.calls.append((records.data_ptr() + 8 * a, b - a, self.offs.data_ptr() + 8 * pos, len(sub) - 1, hs))
+            pos += len(sub)
+        self._analyze = pasta_analyze
+
+    def run(self):
+        """Enqueue every batch (graph-capturable: no host synchronization)."""
+        for addr, nrec, offs, nk, hs in self.calls:
+            self._analyze(self.tr.h, addr, nrec, self.page_shift, hs, offs, nk)

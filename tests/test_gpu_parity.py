@@ -492,3 +492,29 @@ def test_sharded_merger_world1_nccl():
         tr.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("batch", [4096, 10_001 * 2])
+def test_streaming_batches_equal_oracle(batch):
+    """NEXT f2: the trace analyzed as batches (one NO_FINALIZE call each, kernels cut
+    between batches accumulating into the same rows) + one finalize == the oracle."""
+    from paper_2602_22103_b200.stream import BatchRunner
+
+    p = tracegen.build_plan("tiny", seed=21)
+    drec = torch.empty(p.n, dtype=torch.int64, device=DEV)
+    tracegen.device_records(tracegen.DevicePlan(p, DEV), drec)
+    tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs)
+    hist = tr.histograms(p.page_shift, n_kernels=p.n_kernels, kernel_rows=True, kernel_pages=True)
+    runner = BatchRunner(tr, hist, drec, p.kernel_offsets, p.n, batch, p.page_shift)
+    runner.run()
+    tr.finalize(p.page_shift, hist, n_kernels=p.n_kernels)
+    tr.sync()
+    o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
+    ko = [int(x) for x in p.kernel_offsets]
+    r = run_oracle(o, tracegen.host_records(p), p.page_shift, ko, kernel_rows=True, kernel_pages=True)
+    g = {"page_counts": u64(hist.page_counts), "alloc_counts": u64(hist.alloc_counts), "totals": u64(hist.totals),
+         "bitmap": u64(hist.page_bitmap), "kac": u64(hist.kernel_alloc_counts).reshape(p.n_kernels, -1),
+         "kstats": u64(hist.kernel_stats).reshape(p.n_kernels, 4),
+         "kpb": u64(hist.kernel_page_bitmap).reshape(p.n_kernels, -1), "topk": {}}
+    assert_parity(g, r, kernel_rows=True, kernel_pages=True, label=f"stream/{batch}")
+    tr.close()
