@@ -32,6 +32,8 @@ struct ScanArgs {
   uint64_t* hot;             // hotness [windows x P] or nullptr
   uint64_t P;                // pages in the window
   uint32_t window_kernels;   // kernels per hotness window (>= 1)
+  const ulonglong2* chunk_k; // [chunks] (k, koffs[k+1]) of each interleaved chunk's first record (scratch)
+  uint32_t log_ic;           // log2 slices per interleaved chunk (scan_log_chunk)
 };
 
 // Extra records that are not part of the 16-byte aligned even body (<= 2).
@@ -43,10 +45,14 @@ struct ExtraArgs {
 };
 
 int scan_smem_bytes(uint32_t A, bool big_table);
-cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st);
+// Enqueues the scan of a (the chunk map pre-pass first when it is needed); adds the
+// number of kernels launched to *launches.
+cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st, int* launches);
 cudaError_t launch_scan_extras(const ExtraArgs& a, cudaStream_t st);
 bool scan_table_fits_smem(uint32_t A);
 int scan_warps();
+uint32_t scan_log_chunk(uint64_t nbody, int grid);
+size_t scan_scratch_bytes(uint64_t nbody, uint32_t log_ic);
 
 cudaError_t launch_finalize_bitmap(const uint64_t* page_counts, uint64_t P, uint64_t* bitmap, uint64_t* unique_out,
                                    int grid, cudaStream_t st);

@@ -54,6 +54,10 @@ struct pasta_trace {
   void* d_topk = nullptr;
   size_t topk_bytes = 0;
 
+  // scan scratch (interleaved schedule: chunk -> kernel map)
+  unsigned char* d_scan = nullptr;
+  size_t scan_bytes = 0;
+
   // host-record streaming path
   uint64_t host_chunk_bytes = 256ull << 20;
   uint64_t* d_stage[2] = {nullptr, nullptr};
@@ -201,9 +205,23 @@ int scan_range(pasta_trace* h, const uint64_t* rec, uint64_t n, uint64_t g0, Sca
     const uint64_t slices = (cnt + 255) / 256;  // 2 KiB slices, scan_warps() warps per CTA
     const uint64_t wpc = (uint64_t)scan_warps();
     const int grid = (int)std::min<uint64_t>((uint64_t)h->sm_count, (slices + wpc - 1) / wpc);
+    a.log_ic = scan_log_chunk(cnt, grid);
+    const size_t sneed = scan_scratch_bytes(cnt, a.log_ic);
+    if (sneed > h->scan_bytes) {
+      if (h->d_scan) {
+        cudaStreamSynchronize(st);
+        cudaFree(h->d_scan);
+      }
+      h->d_scan = nullptr;
+      h->scan_bytes = 0;
+      if (cudaMalloc(&h->d_scan, sneed) != cudaSuccess) return PASTA_ECUDA;
+      h->scan_bytes = sneed;
+    }
+    a.chunk_k = reinterpret_cast<const ulonglong2*>(h->d_scan);
     Timed t(h, PASTA_PH_SCAN, st);
-    cudaError_t e = launch_scan(a, grid, st);
-    ++h->launches;
+    int nl = 0;
+    cudaError_t e = launch_scan(a, grid, st, &nl);
+    h->launches += nl;
     if (e != cudaSuccess) return PASTA_ECUDA;
   }
   if (ex.n_ex > 0 || !added) {
@@ -294,12 +312,17 @@ int pasta_trace_open(const pasta_open_params* p, pasta_trace** out) {
   h->max_ids = p->max_ids;
   if (p->host_chunk_bytes) h->host_chunk_bytes = (p->host_chunk_bytes + 4095) / 4096 * 4096;
   DeviceGuard g(h->device);
+  // the scan's chunk map: 4 MiB covers every launch up to ~4.3e9 records, so calls
+  // captured into a CUDA graph never allocate
+  constexpr size_t kScanScratch0 = 4u << 20;
+  h->scan_bytes = kScanScratch0;
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device) == cudaSuccess && sms > 0)
     h->sm_count = sms;
   bool ok = cudaMalloc(&h->d_bounds, 16ull * h->max_live) == cudaSuccess &&
             cudaMalloc(&h->d_ids, 4ull * h->max_live) == cudaSuccess &&
             cudaMalloc(&h->d_id_size, 8ull * h->max_ids) == cudaSuccess &&
+            cudaMalloc(&h->d_scan, kScanScratch0) == cudaSuccess &&
             cudaEventCreateWithFlags(&h->upload_done, cudaEventDisableTiming) == cudaSuccess;
   if (ok) ok = cudaMemsetAsync(h->d_id_size, 0, 8ull * h->max_ids, h->stream) == cudaSuccess;
   if (!ok) {
@@ -537,6 +560,7 @@ int pasta_close(pasta_trace* h) {
   }
   if (h->d_koffs) cudaFree(h->d_koffs);
   if (h->d_topk) cudaFree(h->d_topk);
+  if (h->d_scan) cudaFree(h->d_scan);
   if (h->d_bounds) cudaFree(h->d_bounds);
   if (h->d_ids) cudaFree(h->d_ids);
   if (h->d_id_size) cudaFree(h->d_id_size);

@@ -42,6 +42,18 @@
 #include "common.cuh"
 #include "internal.h"
 
+#ifndef PASTA_TRACE_TIMING
+#define PASTA_TRACE_TIMING 0
+#endif
+#if PASTA_TRACE_TIMING
+// debug: per-warp globaltimer stamps {start, first data, 1/4, end} (ns)
+__device__ unsigned long long g_warp_times[148 * 64 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 #ifndef PASTA_SWPIPE
 #define PASTA_SWPIPE 0
 #endif
@@ -69,6 +81,16 @@ using namespace dev;
 constexpr int kWarps = PASTA_WARPS;
 constexpr int kThreads = kWarps * 32;
 constexpr int kSlice = 256;                 // records per slice (8 per lane)
+#ifndef PASTA_TIER_S
+#define PASTA_TIER_S 1  // tier S (one owner, scattered pages) before tier L
+#endif
+#ifndef PASTA_ICHUNK
+#define PASTA_ICHUNK -1  // max log2 slices per interleaved chunk; -1 = contiguous per-warp ranges
+#endif
+#ifndef PASTA_CHUNKS_PER_WARP
+#define PASTA_CHUNKS_PER_WARP 16  // the chunk shrinks until every warp holds this many
+#endif
+constexpr bool kInterleave = PASTA_ICHUNK >= 0;
 constexpr uint32_t kSliceBytes = kSlice * 8;  // 2 KiB
 constexpr int kMaxStages = 8;
 constexpr int kMinStages = 3;
@@ -119,7 +141,7 @@ __device__ __forceinline__ uint32_t count_le(const uint64_t* __restrict__ B, uin
 }
 
 template <bool kBig>
-__device__ __forceinline__ Ival lookup(OwnCache& oc, uint64_t a, const Ctx& c) {
+__device__ __forceinline__ void own_lookup(OwnCache& oc, uint64_t a, const Ctx& c) {
   if (a - oc.olo > oc.ospan) {
     const uint32_t m = 2 * c.A;
     const uint32_t cc = count_le<kBig>(c.B, m, a);
@@ -129,6 +151,13 @@ __device__ __forceinline__ Ival lookup(OwnCache& oc, uint64_t a, const Ctx& c) {
     oc.ospan = olast - olo;
     oc.own = (cc & 1u) ? (cc >> 1) : c.A;
   }
+}
+
+// The interval holding address a: its owner interval (range or gap) cut to its page
+// (or to the out-of-window region below / above the window).
+template <bool kBig>
+__device__ __forceinline__ Ival lookup(OwnCache& oc, uint64_t a, const Ctx& c) {
+  own_lookup<kBig>(oc, a, c);
   uint64_t plo, plast;
   uint32_t page;
   const uint64_t d = a - c.va_lo;
@@ -303,15 +332,36 @@ __device__ __forceinline__ void fallback_record(uint64_t x, OwnCache& oc, LaneAc
   la.ocnt += 1;
 }
 
-// Warp-collective: merge every lane's up to two (page, owner, count) entries into the
-// warp accumulators (leader loop; one __reduce_add_sync per distinct key).
+// One lane's own (page, owner, count) entry straight to L2 (page) and to its LaneAcc
+// (owner), as tier F does for a single record.
 template <bool kRows, int kPages>
-__device__ __forceinline__ void merge_entries(WarpAcc& w, const Out& o, uint32_t k, uint32_t lane, bool pa,
-                                              uint32_t pA, uint32_t oA, uint32_t cA, bool pb, uint32_t pB,
+__device__ __forceinline__ void lane_entry(LaneAcc& la, const Out& o, uint32_t page, uint32_t own, uint32_t cnt,
+                                           uint32_t k) {
+  page_to_global<kPages>(o, page, cnt, k);
+  if (own != la.own) {
+    owner_to_global<kRows>(o, la.own, la.ocnt, k);
+    la.own = own;
+    la.ocnt = 0;
+  }
+  la.ocnt += cnt;
+}
+
+// Warp-collective: merge every lane's up to two (page, owner, count) entries into the
+// warp accumulators (leader loop; one __reduce_add_sync per distinct key). After
+// PASTA_MERGE_ITERS distinct keys the entries are scattered (random pages): every lane
+// then sends its remaining entries itself instead of serialising one key per step.
+#ifndef PASTA_MERGE_ITERS
+#define PASTA_MERGE_ITERS 2
+#endif
+template <bool kRows, int kPages>
+__device__ __forceinline__ void merge_entries(WarpAcc& w, LaneAcc& la, const Out& o, uint32_t k, uint32_t lane,
+                                              bool pa, uint32_t pA, uint32_t oA, uint32_t cA, bool pb, uint32_t pB,
                                               uint32_t oB, uint32_t cB) {
-  for (;;) {
+#pragma unroll 1
+  for (int it = 0;; ++it) {
     const unsigned m = __ballot_sync(kFull, pa || pb);
-    if (m == 0) break;
+    if (m == 0) return;
+    if (it == PASTA_MERGE_ITERS) break;
     const int leader = __ffs(m) - 1;
     const uint32_t kp = __shfl_sync(kFull, pa ? pA : pB, leader);
     const uint32_t ko = __shfl_sync(kFull, pa ? oA : oB, leader);
@@ -322,6 +372,8 @@ __device__ __forceinline__ void merge_entries(WarpAcc& w, const Out& o, uint32_t
     pa = pa && !mA;
     pb = pb && !mB;
   }
+  if (pa) lane_entry<kRows, kPages>(la, o, pA, oA, cA, k);
+  if (pb) lane_entry<kRows, kPages>(la, o, pB, oB, cB, k);
 }
 
 // Tier L + F for this lane's records selected by `valid` (bit i <-> a[i]).
@@ -373,7 +425,7 @@ __device__ __forceinline__ void process_lane(const uint64_t (&a)[8], uint32_t va
       }
     }
   }
-  merge_entries<kRows, kPages>(w, o, k, lane, cA > 0, IA.page, IA.own, cA, cB > 0, IB.page, IB.own, cB);
+  merge_entries<kRows, kPages>(w, la, o, k, lane, cA > 0, IA.page, IA.own, cA, cB > 0, IB.page, IB.own, cB);
 }
 
 __device__ __forceinline__ uint32_t lo32(uint64_t x) { return static_cast<uint32_t>(x); }
@@ -477,6 +529,38 @@ __device__ __forceinline__ void process_full(const uint64_t (&a)[8], uint32_t sl
       return;
     }
   }
+#if PASTA_TIER_S
+  // ---- tier S: every record in one owner interval and in the window, pages scattered
+  // (random or strided access inside one allocation): owner count warp-uniform, each
+  // lane sends its own page runs, no per-record lookup ----
+  {
+    own_lookup<kBig>(oc, xf, c);  // xf's owner interval: the same in every lane
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ok = ok && (a[i] - oc.olo <= oc.ospan) && (a[i] - c.va_lo < c.wbytes);
+    if (__all_sync(kFull, ok)) {
+      if (oc.own != w.own) {
+        if (lane == 0) owner_to_global<kRows>(o, w.own, w.ocnt, k);
+        w.own = oc.own;
+        w.ocnt = 0;
+      }
+      w.ocnt += kSlice;
+      uint32_t pp = (uint32_t)((a[0] - c.va_lo) >> c.s), n = 1;
+#pragma unroll
+      for (int i = 1; i < 8; ++i) {
+        const uint32_t p = (uint32_t)((a[i] - c.va_lo) >> c.s);
+        if (p != pp) {
+          page_to_global<kPages>(o, pp, n, k);
+          pp = p;
+          n = 0;
+        }
+        ++n;
+      }
+      page_to_global<kPages>(o, pp, n, k);
+      return;
+    }
+  }
+#endif
   // ---- tier L: lane-contiguous re-read (8 consecutive records, rotated order) ----
   uint64_t b[8];
   const uint32_t rsh = (lane >> 1) & 3u;
@@ -536,15 +620,31 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   const uint32_t A = args.A;
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
-  // contiguous slice range [s0, s1) of this warp
   const uint64_t nsl = (args.nbody + kSlice - 1) / kSlice;
   const uint64_t gwarp = (uint64_t)blockIdx.x * kWarps + warp;
   const uint64_t nwarp = (uint64_t)gridDim.x * kWarps;
-  const uint64_t s0 = gwarp * nsl / nwarp, s1 = (gwarp + 1) * nsl / nwarp;
-  const uint32_t nmy = (uint32_t)(s1 - s0);
   // the last slice of the trace may be partial
   const uint32_t tail_valid = (uint32_t)(args.nbody - (nsl - 1) * kSlice);
-  const uint32_t nfull = (s1 == nsl && tail_valid != (uint32_t)kSlice) ? nmy - 1 : nmy;
+#if PASTA_ICHUNK >= 0
+  // Interleaved schedule: chunks of 2^lc slices, warp gw takes chunks gw, gw + W, ...,
+  // so every warp samples the whole trace (cheap sweeps, tiled jumps and scattered
+  // records alike) and no warp straggles. Relative slice j -> global slice gsl(j).
+  const uint32_t lc = args.log_ic, icm = (1u << lc) - 1u;
+  const uint64_t nch = (nsl + icm) >> lc;
+  const uint64_t nct = gwarp < nch ? (nch - gwarp + nwarp - 1) / nwarp : 0;  // my chunks
+  const bool own_last = nct > 0 && (gwarp + (nct - 1) * nwarp == nch - 1);
+  const uint32_t nmy = (uint32_t)((nct << lc) - (own_last ? (nch << lc) - nsl : 0));
+  auto gsl = [&](uint32_t j) -> uint64_t { return (((uint64_t)(j >> lc) * nwarp + gwarp) << lc) + (j & icm); };
+  const uint64_t s0 = 0;
+  const bool tail_mine = own_last;
+#else
+  // contiguous slice range [s0, s1) of this warp
+  const uint64_t s0 = gwarp * nsl / nwarp, s1 = (gwarp + 1) * nsl / nwarp;
+  const uint32_t nmy = (uint32_t)(s1 - s0);
+  auto gsl = [&](uint32_t j) -> uint64_t { return s0 + j; };
+  const bool tail_mine = s1 == nsl;
+#endif
+  const uint32_t nfull = (tail_mine && nmy > 0 && tail_valid != (uint32_t)kSlice) ? nmy - 1 : nmy;
 
   const uint32_t ring_u32 = smem_u32(smem) + (uint32_t)(warp * stages) * kSliceBytes;
   const uint32_t bar_u32 = smem_u32(bars + warp * kMaxStages);
@@ -557,14 +657,17 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   if (!kBig)
     for (uint32_t i = threadIdx.x; i < 2 * A; i += kThreads) sB[i] = args.bounds[i];
   __syncthreads();
+#if PASTA_TRACE_TIMING
+  const uint32_t tslot = (blockIdx.x * kWarps + warp) * 4;
+  if (lane == 0) g_warp_times[tslot] = gtimer();
+#endif
 
   const uint64_t pol = l2_evict_first_policy();
-  const uint64_t* wrec = args.rec + s0 * kSlice;  // this warp's first record
   // TMA for relative slice j into ring slot `slot` (lane 0 only)
   auto issue = [&](uint32_t j, uint32_t slot) {
     const uint32_t bytes = j < nfull ? kSliceBytes : tail_valid * 8u;
     mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, bytes);
-    tma_load_1d_u32(ring_u32 + slot * kSliceBytes, wrec + (uint64_t)j * kSlice, bytes, bar_u32 + 8u * slot, pol);
+    tma_load_1d_u32(ring_u32 + slot * kSliceBytes, args.rec + gsl(j) * kSlice, bytes, bar_u32 + 8u * slot, pol);
   };
   if (lane == 0)
     for (uint32_t j = 0; j < (uint32_t)stages && j < nmy; ++j) issue(j, j);
@@ -611,11 +714,54 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   la.ocnt = 0;
   la.kbit = kOOW;
 
-  // Kernel segments: records are global index gbase + r, r = 256 j + position.
-  const uint64_t gbase = args.gidx0 + s0 * kSlice;
+  // Kernel segments: slice j holds global records gidx0 + 256 gsl(j) + position.
   const uint32_t K = args.n_kernels;
   uint32_t k = 0;
   uint64_t kend = ~0ull;  // global index where segment k ends
+#if PASTA_ICHUNK >= 0
+  // chunk starts are events: the chunk's kernel comes from the pre-pass table
+  // (k, kend) of the next chunk is loaded one chunk ahead, off the critical path
+  ulonglong2 pf = make_ulonglong2(0ull, ~0ull);
+  auto prefetch_chunk = [&](uint32_t j) {
+    if (kRows && K > 1 && j < nmy) pf = __ldg(args.chunk_k + (gsl(j) >> lc));
+  };
+  auto enter_chunk = [&](uint32_t j) {
+    if (kRows && K > 1) {
+      const uint32_t nk = (uint32_t)pf.x;
+      if (nk != k) {
+        warp_flush<kRows, kPages>(w, la, o, k, lane);
+        k = nk;
+      }
+      kend = pf.y;
+      prefetch_chunk(j + icm + 1);
+    }
+  };
+  // first relative slice after j that needs the general path: the next chunk start, the
+  // slice holding record kend, or the partial tail slice
+  auto next_event_after = [&](uint32_t j) -> uint32_t {
+    const uint32_t jb = j & ~icm;
+    uint64_t e = (kRows && K > 1) ? (uint64_t)jb + icm + 1 : nfull;
+    if (nfull < e) e = nfull;
+    if (kRows && kend != ~0ull) {
+      const uint64_t gb = args.gidx0 + gsl(jb) * kSlice;
+      if (kend >= gb) {
+        const uint64_t kb = jb + (kend - gb) / kSlice;
+        if (kb < e && kb > j) e = kb;
+      }
+    }
+    return (uint32_t)e;
+  };
+  prefetch_chunk(0);
+  if (nmy > 0) enter_chunk(0);
+  uint32_t jev = nmy > 0 ? next_event_after(0) : 0;
+  if (kRows && K > 1 && nmy > 0) {
+    // the first slice itself may hold a boundary
+    const uint64_t gb = args.gidx0 + gsl(0) * kSlice;
+    if (kend < gb + kSlice) jev = 0;
+  }
+  if (nfull == 0) jev = 0;
+#else
+  const uint64_t gbase = args.gidx0 + s0 * kSlice;
   if (kRows && K > 1 && nmy > 0) {
     k = kernel_of(args.koffs, K, gbase);
     kend = (k + 1 < K) ? __ldg(args.koffs + k + 1) : ~0ull;
@@ -630,6 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
     return (uint32_t)e;
   };
   uint32_t jev = next_event();
+#endif
 
 #if PASTA_SWPIPE
   // Software pipeline: the registers of slice j+1 are loaded (LDS) before slice j is
@@ -661,6 +808,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   for (uint32_t j = 0; j < nmy; ++j) {
     const uint32_t sa = ring_u32 + slot * kSliceBytes;
     mbar_wait_u32(bar_u32 + 8u * slot, phase);
+#if PASTA_TRACE_TIMING
+    if (lane == 0 && j == 0) g_warp_times[tslot + 1] = gtimer();
+    if (lane == 0 && j == nmy / 4) g_warp_times[tslot + 2] = gtimer();
+#endif
     uint64_t a[8];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -672,9 +823,13 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
     if (j != jev) {
       process_full<kBig, kRows, kPages>(a, sa, cur, oc, la, w, c, o, k, lane);
     } else {
-      // kernel boundary in or at this slice, or the partial tail slice
+      // kernel boundary in or at this slice, or the partial tail slice (or, in the
+      // interleaved schedule, the first slice of a chunk)
+#if PASTA_ICHUNK >= 0
+      if ((j & icm) == 0 && j > 0) enter_chunk(j);
+#endif
       const uint32_t valid = j < nfull ? (uint32_t)kSlice : tail_valid;
-      const uint64_t g0 = gbase + (uint64_t)j * kSlice;
+      const uint64_t g0 = args.gidx0 + gsl(j) * kSlice;
       uint32_t r0 = 0;
       for (;;) {
         if (kRows && g0 + r0 >= kend) {
@@ -698,7 +853,11 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
         r0 = r1;
         if (r0 >= valid) break;
       }
+#if PASTA_ICHUNK >= 0
+      jev = next_event_after(j);
+#else
       jev = next_event();  // > j: kend now lies beyond every record of this slice
+#endif
     }
     // the slot is free again (every lane has consumed its values): refill it with the
     // slice `stages` ahead
@@ -710,6 +869,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
     }
   }
   warp_flush<kRows, kPages>(w, la, o, k, lane);
+#if PASTA_TRACE_TIMING
+  if (lane == 0) g_warp_times[tslot + 3] = gtimer();
+#endif
 }
 
 // The <= 2 records outside the aligned even body (unaligned head, odd tail): one
@@ -767,6 +929,14 @@ int stages_for(uint32_t A, bool big) {
   return (int)st;
 }
 
+// chunk_k[c] = (kernel segment k of interleaved chunk c's first record, koffs[k + 1]).
+__global__ void chunk_kernel_map(const __grid_constant__ ScanArgs a, ulonglong2* chunk_k, uint64_t nch) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nch) return;
+  const uint32_t k = kernel_of(a.koffs, a.n_kernels, a.gidx0 + (i << a.log_ic) * kSlice);
+  chunk_k[i] = make_ulonglong2(k, k + 1 < a.n_kernels ? a.koffs[k + 1] : ~0ull);
+}
+
 template <bool kBig, bool kRows, int kPages>
 cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
   const int stages = stages_for(a.A, kBig);
@@ -782,15 +952,49 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
 
 int scan_warps() { return kWarps; }
 
+uint32_t scan_log_chunk(uint64_t nbody, int grid) {
+  if (!kInterleave) return 0;
+  const uint64_t nsl = (nbody + kSlice - 1) / kSlice;
+  const uint64_t per = (uint64_t)grid * kWarps * PASTA_CHUNKS_PER_WARP;
+  uint32_t lc = 0;
+  while ((int)lc < PASTA_ICHUNK && (nsl >> (lc + 1)) >= per) ++lc;
+  return lc;
+}
+
+size_t scan_scratch_bytes(uint64_t nbody, uint32_t log_ic) {
+  const uint64_t nsl = (nbody + kSlice - 1) / kSlice;
+  const uint64_t nch = (nsl + (1ull << log_ic) - 1) >> log_ic;
+  return kInterleave ? 16 * nch + 256 : 256;
+}
+
+extern "C" int pasta_debug_warp_times(unsigned long long* out, int n) {
+#if PASTA_TRACE_TIMING
+  return cudaMemcpyFromSymbol(out, g_warp_times, sizeof(unsigned long long) * n) == cudaSuccess ? n : -1;
+#else
+  (void)out;
+  (void)n;
+  return 0;
+#endif
+}
+
 bool scan_table_fits_smem(uint32_t A) { return stages_for(A, false) >= kMinStages; }
 
 int scan_smem_bytes(uint32_t A, bool big_table) {
   return ring_bytes(stages_for(A, big_table)) + kBarBytes + kLaBytes + (big_table ? 0 : (int)(16ull * A));
 }
 
-cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st, int* launches) {
   const bool big = !scan_table_fits_smem(a.A);
   const bool rows = a.kac != nullptr;  // per-kernel outputs all require kernel rows
+  if (kInterleave && rows && a.n_kernels > 1 && a.nbody > 0) {
+    const uint64_t nsl = (a.nbody + kSlice - 1) / kSlice;
+    const uint64_t nch = (nsl + (1ull << a.log_ic) - 1) >> a.log_ic;
+    chunk_kernel_map<<<(unsigned)((nch + 255) / 256), 256, 0, st>>>(a, const_cast<ulonglong2*>(a.chunk_k), nch);
+    const cudaError_t e0 = cudaGetLastError();
+    if (e0 != cudaSuccess) return e0;
+    ++*launches;
+  }
+  ++*launches;
   const int mode = (a.kpb != nullptr ? 1 : 0) | (a.hot != nullptr ? 2 : 0);
   if (big) {
     if (!rows) return launch_variant<true, false, 0>(a, grid, st);
