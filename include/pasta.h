@@ -77,12 +77,19 @@ typedef struct {
   int32_t device;     /* CUDA device ordinal the handle binds to                        */
   uint32_t max_live;  /* range-table capacity (simultaneously live ranges), >= 1        */
   uint32_t max_ids;   /* ids ever issued by this handle (= bins of alloc_counts), >= 1  */
-  uint32_t flags;     /* reserved, must be 0                                            */
+  uint32_t flags;     /* 0, or one PASTA_SCHED_* schedule override (tuning / testing)   */
   uint64_t va_lo;     /* page window [va_lo, va_hi): multiples of 4 KiB, va_lo < va_hi  */
   uint64_t va_hi;
   uintptr_t stream;   /* cudaStream_t for all device work (0 = legacy default stream)   */
   uint64_t host_chunk_bytes; /* staging chunk for PASTA_REC_HOST (0 = 256 MiB)          */
 } pasta_open_params;
+
+/* Scan schedule (pasta_open_params.flags). By default a launch over few records per
+ * warp gives each warp one contiguous range of 2 KiB slices, and a long launch
+ * (>= ~0.9e9 records on 148 SMs) interleaves chunks of 64 slices across warps so that
+ * no warp straggles behind an expensive region of the trace. Results are identical
+ * under every schedule; the flags force one (for tests and tuning). */
+enum { PASTA_SCHED_CONTIGUOUS = 1u, PASTA_SCHED_INTERLEAVED = 2u };
 
 /* Input records. By default both arrays are DEVICE memory, read-only, never copied
  * to the host. With PASTA_REC_HOST they are HOST memory (pinned for full speed):

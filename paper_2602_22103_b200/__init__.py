@@ -31,6 +31,9 @@ T_RECORDS, T_UNATTRIBUTED, T_OUT_OF_WINDOW, T_UNIQUE_PAGES, T_WS_OBJ, TOTALS = 0
 K_ATTRIBUTED, K_UNATTRIBUTED, K_FOOTPRINT, K_UNIQUE_PAGES, KSTATS = 0, 1, 2, 3, 4
 PASTA_REC_HOST = 1
 PASTA_NO_FINALIZE = 1
+PASTA_SCHED_CONTIGUOUS = 1
+PASTA_SCHED_INTERLEAVED = 2
+_SCHED = {"auto": 0, "contiguous": PASTA_SCHED_CONTIGUOUS, "interleaved": PASTA_SCHED_INTERLEAVED}
 PH_SCAN, PH_FINALIZE, PH_TOPK, PH_MERGE, PH_COPY, PHASES = 0, 1, 2, 3, 4, 5
 PHASE_NAMES = ("scan", "finalize", "topk", "merge", "copy")
 
@@ -105,8 +108,9 @@ def pasta_strerror(status: int) -> str:
 
 
 def pasta_trace_open(device: int, va_lo: int, va_hi: int, max_live: int, max_ids: int, stream=0,
-                     host_chunk_bytes: int = 0):
-    p = pasta_open_params(device, max_live, max_ids, 0, va_lo, va_hi, ctypes.c_void_p(stream or 0), host_chunk_bytes)
+                     host_chunk_bytes: int = 0, flags: int = 0):
+    p = pasta_open_params(device, max_live, max_ids, flags, va_lo, va_hi, ctypes.c_void_p(stream or 0),
+                          host_chunk_bytes)
     h = ctypes.c_void_p()
     _check(_lib.pasta_trace_open(ctypes.byref(p), ctypes.byref(h)), "pasta_trace_open")
     return h
@@ -222,7 +226,7 @@ class Trace:
     """A pasta_trace handle bound to one CUDA device and stream."""
 
     def __init__(self, device, va_lo: int, va_hi: int, max_live: int, max_ids: int, stream=None,
-                 host_chunk_bytes: int = 0):
+                 host_chunk_bytes: int = 0, schedule: str = "auto"):
         import torch
 
         self.device = torch.device(device)
@@ -231,7 +235,7 @@ class Trace:
         self.stream = stream
         self.va_lo, self.va_hi, self.max_live, self.max_ids = va_lo, va_hi, max_live, max_ids
         self.h = pasta_trace_open(self.device.index or 0, va_lo, va_hi, max_live, max_ids, stream.cuda_stream,
-                                  host_chunk_bytes)
+                                  host_chunk_bytes, _SCHED[schedule])
 
     def n_pages(self, page_shift: int) -> int:
         return (self.va_hi - self.va_lo) >> page_shift

@@ -33,7 +33,7 @@ struct ScanArgs {
   uint64_t P;                // pages in the window
   uint32_t window_kernels;   // kernels per hotness window (>= 1)
   const ulonglong2* chunk_k; // [chunks] (k, koffs[k+1]) of each interleaved chunk's first record (scratch)
-  uint32_t log_ic;           // log2 slices per interleaved chunk (scan_log_chunk)
+  int32_t log_ic;            // log2 slices per interleaved chunk, -1 = contiguous (scan_schedule)
 };
 
 // Extra records that are not part of the 16-byte aligned even body (<= 2).
@@ -51,8 +51,11 @@ cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st, int* launc
 cudaError_t launch_scan_extras(const ExtraArgs& a, cudaStream_t st);
 bool scan_table_fits_smem(uint32_t A);
 int scan_warps();
-uint32_t scan_log_chunk(uint64_t nbody, int grid);
-size_t scan_scratch_bytes(uint64_t nbody, uint32_t log_ic);
+// Scan schedule of a launch over nbody records on `grid` CTAs: log2 slices per
+// interleaved chunk, or -1 for contiguous per-warp ranges; and the chunk map scratch.
+// force: 0 = automatic, else PASTA_SCHED_CONTIGUOUS / PASTA_SCHED_INTERLEAVED.
+int scan_schedule(uint64_t nbody, int grid, uint32_t force);
+size_t scan_scratch_bytes(uint64_t nbody, int log_ic);
 
 cudaError_t launch_finalize_bitmap(const uint64_t* page_counts, uint64_t P, uint64_t* bitmap, uint64_t* unique_out,
                                    int grid, cudaStream_t st);

@@ -29,6 +29,7 @@ struct TimedLaunch {
 
 struct pasta_trace {
   int device = 0;
+  uint32_t sched = 0;  // PASTA_SCHED_* override, 0 = automatic
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
   uint64_t va_lo = 0, va_hi = 0;
@@ -205,7 +206,7 @@ int scan_range(pasta_trace* h, const uint64_t* rec, uint64_t n, uint64_t g0, Sca
     const uint64_t slices = (cnt + 255) / 256;  // 2 KiB slices, scan_warps() warps per CTA
     const uint64_t wpc = (uint64_t)scan_warps();
     const int grid = (int)std::min<uint64_t>((uint64_t)h->sm_count, (slices + wpc - 1) / wpc);
-    a.log_ic = scan_log_chunk(cnt, grid);
+    a.log_ic = scan_schedule(cnt, grid, h->sched);
     const size_t sneed = scan_scratch_bytes(cnt, a.log_ic);
     if (sneed > h->scan_bytes) {
       if (h->d_scan) {
@@ -297,7 +298,9 @@ const char* pasta_strerror(int s) {
 
 int pasta_trace_open(const pasta_open_params* p, pasta_trace** out) {
   if (!p || !out) return PASTA_EINVAL;
-  if (p->max_live == 0 || p->max_ids == 0 || p->flags != 0) return PASTA_EINVAL;
+  if (p->max_live == 0 || p->max_ids == 0) return PASTA_EINVAL;
+  if (p->flags != 0 && p->flags != PASTA_SCHED_CONTIGUOUS && p->flags != PASTA_SCHED_INTERLEAVED)
+    return PASTA_EINVAL;
   if (p->va_lo >= p->va_hi || (p->va_lo & 4095) || (p->va_hi & 4095)) return PASTA_EINVAL;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess) return PASTA_ECUDA;
@@ -307,6 +310,7 @@ int pasta_trace_open(const pasta_open_params* p, pasta_trace** out) {
   h->device = p->device;
   h->stream = reinterpret_cast<cudaStream_t>(p->stream);
   h->va_lo = p->va_lo;
+  h->sched = p->flags;
   h->va_hi = p->va_hi;
   h->max_live = p->max_live;
   h->max_ids = p->max_ids;

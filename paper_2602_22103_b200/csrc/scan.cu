@@ -41,6 +41,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "pasta.h"
 
 #ifndef PASTA_TRACE_TIMING
 #define PASTA_TRACE_TIMING 0
@@ -84,13 +85,15 @@ constexpr int kSlice = 256;                 // records per slice (8 per lane)
 #ifndef PASTA_TIER_S
 #define PASTA_TIER_S 1  // tier S (one owner, scattered pages) before tier L
 #endif
-#ifndef PASTA_ICHUNK
-#define PASTA_ICHUNK -1  // max log2 slices per interleaved chunk; -1 = contiguous per-warp ranges
+#ifndef PASTA_IL
+#define PASTA_IL 1  // interleaved chunk schedule for long launches (0 = always contiguous)
 #endif
-#ifndef PASTA_CHUNKS_PER_WARP
-#define PASTA_CHUNKS_PER_WARP 16  // the chunk shrinks until every warp holds this many
+#ifndef PASTA_IL_LOG_CHUNK
+#define PASTA_IL_LOG_CHUNK 6  // log2 slices per interleaved chunk
 #endif
-constexpr bool kInterleave = PASTA_ICHUNK >= 0;
+#ifndef PASTA_IL_MIN_CHUNKS
+#define PASTA_IL_MIN_CHUNKS 16  // interleave only when every warp gets this many chunks
+#endif
 constexpr uint32_t kSliceBytes = kSlice * 8;  // 2 KiB
 constexpr int kMaxStages = 8;
 constexpr int kMinStages = 3;
@@ -99,6 +102,7 @@ constexpr int kBarBytes = kWarps * kMaxStages * 8;
 #define PASTA_LA_SMEM 1
 #endif
 constexpr int kLaBytes = PASTA_LA_SMEM ? kThreads * 12 : 0;  // LaneAcc per thread
+constexpr int kPfBytes = kWarps * 16;                        // per-warp chunk map slot
 constexpr int kSmemLimit = 227 * 1024;
 
 __host__ __device__ constexpr int ring_bytes(int stages) { return kWarps * stages * (int)kSliceBytes; }
@@ -611,11 +615,11 @@ __device__ __forceinline__ uint32_t kernel_of(const uint64_t* __restrict__ koffs
   return lo;
 }
 
-template <bool kBig, bool kRows, int kPages>
+template <bool kBig, bool kRows, int kPages, bool kIL>
 __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages));
-  uint64_t* sB = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages) + kBarBytes + kLaBytes);
+  uint64_t* sB = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages) + kBarBytes + kLaBytes + kPfBytes);
 
   const uint32_t A = args.A;
   const int warp = threadIdx.x >> 5;
@@ -625,25 +629,32 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   const uint64_t nwarp = (uint64_t)gridDim.x * kWarps;
   // the last slice of the trace may be partial
   const uint32_t tail_valid = (uint32_t)(args.nbody - (nsl - 1) * kSlice);
-#if PASTA_ICHUNK >= 0
-  // Interleaved schedule: chunks of 2^lc slices, warp gw takes chunks gw, gw + W, ...,
-  // so every warp samples the whole trace (cheap sweeps, tiled jumps and scattered
-  // records alike) and no warp straggles. Relative slice j -> global slice gsl(j).
-  const uint32_t lc = args.log_ic, icm = (1u << lc) - 1u;
-  const uint64_t nch = (nsl + icm) >> lc;
-  const uint64_t nct = gwarp < nch ? (nch - gwarp + nwarp - 1) / nwarp : 0;  // my chunks
-  const bool own_last = nct > 0 && (gwarp + (nct - 1) * nwarp == nch - 1);
-  const uint32_t nmy = (uint32_t)((nct << lc) - (own_last ? (nch << lc) - nsl : 0));
-  auto gsl = [&](uint32_t j) -> uint64_t { return (((uint64_t)(j >> lc) * nwarp + gwarp) << lc) + (j & icm); };
-  const uint64_t s0 = 0;
-  const bool tail_mine = own_last;
-#else
-  // contiguous slice range [s0, s1) of this warp
-  const uint64_t s0 = gwarp * nsl / nwarp, s1 = (gwarp + 1) * nsl / nwarp;
-  const uint32_t nmy = (uint32_t)(s1 - s0);
-  auto gsl = [&](uint32_t j) -> uint64_t { return s0 + j; };
-  const bool tail_mine = s1 == nsl;
-#endif
+  // Relative slice j of this warp -> global slice gsl(j).
+  //  * contiguous schedule: slices [s0, s1) (short launches, where every warp holds few
+  //    slices and a straggler costs little);
+  //  * interleaved schedule (kIL): chunks of 2^lc slices, warp gw takes chunks gw,
+  //    gw + W, ..., so every warp samples the whole trace (cheap sweeps, tiled jumps and
+  //    scattered records alike) and no warp straggles behind an expensive region.
+  uint32_t lc = 0, icm = 0, nmy;
+  uint64_t s0 = 0;
+  bool tail_mine;
+  if constexpr (kIL) {
+    lc = args.log_ic;
+    icm = (1u << lc) - 1u;
+    const uint64_t nch = (nsl + icm) >> lc;
+    const uint64_t nct = gwarp < nch ? (nch - gwarp + nwarp - 1) / nwarp : 0;  // my chunks
+    tail_mine = nct > 0 && (gwarp + (nct - 1) * nwarp == nch - 1);            // I own the last chunk
+    nmy = (uint32_t)((nct << lc) - (tail_mine ? (nch << lc) - nsl : 0));
+  } else {
+    s0 = gwarp * nsl / nwarp;
+    const uint64_t s1 = (gwarp + 1) * nsl / nwarp;
+    nmy = (uint32_t)(s1 - s0);
+    tail_mine = s1 == nsl;
+  }
+  auto gsl = [&](uint32_t j) -> uint64_t {
+    if constexpr (kIL) return (((uint64_t)(j >> lc) * nwarp + gwarp) << lc) + (j & icm);
+    else return s0 + j;
+  };
   const uint32_t nfull = (tail_mine && nmy > 0 && tail_valid != (uint32_t)kSlice) ? nmy - 1 : nmy;
 
   const uint32_t ring_u32 = smem_u32(smem) + (uint32_t)(warp * stages) * kSliceBytes;
@@ -663,11 +674,19 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
 #endif
 
   const uint64_t pol = l2_evict_first_policy();
-  // TMA for relative slice j into ring slot `slot` (lane 0 only)
+  // TMA for relative slice j into ring slot `slot` (lane 0 only). Slices are issued in
+  // order; the interleaved schedule advances its global slice is_gs incrementally.
+  uint32_t is_gs = kIL ? (uint32_t)gsl(0) : 0u;  // < 2^32: a launch holds at most 148 * 2^31 records
   auto issue = [&](uint32_t j, uint32_t slot) {
     const uint32_t bytes = j < nfull ? kSliceBytes : tail_valid * 8u;
     mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, bytes);
-    tma_load_1d_u32(ring_u32 + slot * kSliceBytes, args.rec + gsl(j) * kSlice, bytes, bar_u32 + 8u * slot, pol);
+    if constexpr (kIL) {
+      tma_load_1d_u32(ring_u32 + slot * kSliceBytes, args.rec + (uint64_t)is_gs * kSlice, bytes,
+                      bar_u32 + 8u * slot, pol);
+      is_gs = (((j + 1) & icm) == 0) ? (uint32_t)gsl(j + 1) : is_gs + 1;
+    } else {
+      tma_load_1d_u32(ring_u32 + slot * kSliceBytes, args.rec + gsl(j) * kSlice, bytes, bar_u32 + 8u * slot, pol);
+    }
   };
   if (lane == 0)
     for (uint32_t j = 0; j < (uint32_t)stages && j < nmy; ++j) issue(j, j);
@@ -718,15 +737,19 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   const uint32_t K = args.n_kernels;
   uint32_t k = 0;
   uint64_t kend = ~0ull;  // global index where segment k ends
-#if PASTA_ICHUNK >= 0
-  // chunk starts are events: the chunk's kernel comes from the pre-pass table
-  // (k, kend) of the next chunk is loaded one chunk ahead, off the critical path
-  ulonglong2 pf = make_ulonglong2(0ull, ~0ull);
+  // interleaved: chunk starts are events, the chunk's (k, kend) comes from the pre-pass
+  // table, copied to this warp's shared slot one chunk ahead (cp.async), off the critical
+  // path and out of the register file
+  const uint32_t pf_u32 = smem_u32(smem) + ring_bytes(stages) + kBarBytes + kLaBytes + 16u * warp;
   auto prefetch_chunk = [&](uint32_t j) {
-    if (kRows && K > 1 && j < nmy) pf = __ldg(args.chunk_k + (gsl(j) >> lc));
+    if (kRows && K > 1 && j < nmy && lane == 0) cp_async_16(pf_u32, args.chunk_k + (gsl(j) >> lc));
   };
   auto enter_chunk = [&](uint32_t j) {
     if (kRows && K > 1) {
+      if (lane == 0) cp_async_wait_all();
+      __syncwarp();
+      const ulonglong2 pf = lds128(pf_u32);
+      __syncwarp();
       const uint32_t nk = (uint32_t)pf.x;
       if (nk != k) {
         warp_flush<kRows, kPages>(w, la, o, k, lane);
@@ -736,74 +759,49 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
       prefetch_chunk(j + icm + 1);
     }
   };
-  // first relative slice after j that needs the general path: the next chunk start, the
-  // slice holding record kend, or the partial tail slice
+  // first relative slice after j that is not a plain full slice inside segment k: the
+  // slice holding record kend, the partial tail slice, or (interleaved) the next chunk
   auto next_event_after = [&](uint32_t j) -> uint32_t {
-    const uint32_t jb = j & ~icm;
-    uint64_t e = (kRows && K > 1) ? (uint64_t)jb + icm + 1 : nfull;
-    if (nfull < e) e = nfull;
-    if (kRows && kend != ~0ull) {
-      const uint64_t gb = args.gidx0 + gsl(jb) * kSlice;
-      if (kend >= gb) {
-        const uint64_t kb = jb + (kend - gb) / kSlice;
-        if (kb < e && kb > j) e = kb;
+    if constexpr (kIL) {
+      const uint32_t jb = j & ~icm;
+      uint64_t e = (kRows && K > 1) ? (uint64_t)jb + icm + 1 : nfull;
+      if (nfull < e) e = nfull;
+      if (kRows && kend != ~0ull) {
+        const uint64_t gb = args.gidx0 + gsl(jb) * kSlice;
+        if (kend >= gb) {
+          const uint64_t kb = jb + (kend - gb) / kSlice;
+          if (kb < e && kb > j) e = kb;
+        }
       }
+      return (uint32_t)e;
+    } else {
+      uint64_t e = nfull;
+      if (kRows && kend != ~0ull) {
+        const uint64_t kb = (kend - args.gidx0) / kSlice - s0;  // slice holding record kend (or starting at it)
+        if (kb < e) e = kb;
+      }
+      return (uint32_t)e;
     }
-    return (uint32_t)e;
   };
-  prefetch_chunk(0);
-  if (nmy > 0) enter_chunk(0);
-  uint32_t jev = nmy > 0 ? next_event_after(0) : 0;
-  if (kRows && K > 1 && nmy > 0) {
-    // the first slice itself may hold a boundary
-    const uint64_t gb = args.gidx0 + gsl(0) * kSlice;
-    if (kend < gb + kSlice) jev = 0;
-  }
-  if (nfull == 0) jev = 0;
-#else
-  const uint64_t gbase = args.gidx0 + s0 * kSlice;
-  if (kRows && K > 1 && nmy > 0) {
-    k = kernel_of(args.koffs, K, gbase);
-    kend = (k + 1 < K) ? __ldg(args.koffs + k + 1) : ~0ull;
-  }
-  // first relative slice that is not a plain full slice inside segment k
-  auto next_event = [&]() -> uint32_t {
-    uint64_t e = nfull;
-    if (kRows && kend != ~0ull) {
-      const uint64_t kb = (kend - gbase) / kSlice;  // slice holding record kend (or starting at it)
-      if (kb < e) e = kb;
+  uint32_t jev;
+  if constexpr (kIL) {
+    prefetch_chunk(0);
+    if (nmy > 0) enter_chunk(0);
+    jev = nmy > 0 ? next_event_after(0) : 0;
+    if (kRows && K > 1 && nmy > 0) {
+      // the first slice itself may hold a boundary
+      const uint64_t gb = args.gidx0 + gsl(0) * kSlice;
+      if (kend < gb + kSlice) jev = 0;
     }
-    return (uint32_t)e;
-  };
-  uint32_t jev = next_event();
-#endif
+    if (nfull == 0) jev = 0;
+  } else {
+    if (kRows && K > 1 && nmy > 0) {
+      k = kernel_of(args.koffs, K, args.gidx0 + s0 * kSlice);
+      kend = (k + 1 < K) ? __ldg(args.koffs + k + 1) : ~0ull;
+    }
+    jev = next_event_after(0);
+  }
 
-#if PASTA_SWPIPE
-  // Software pipeline: the registers of slice j+1 are loaded (LDS) before slice j is
-  // processed, so the shared-memory latency hides behind the processing.
-  uint64_t nxt[8];
-  auto load_slice = [&](uint32_t slot_, uint32_t phase_) {
-    const uint32_t sa_ = ring_u32 + slot_ * kSliceBytes;
-    mbar_wait_u32(bar_u32 + 8u * slot_, phase_);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const ulonglong2 v = lds128(sa_ + 16u * lane + 512u * i);
-      nxt[2 * i] = v.x;
-      nxt[2 * i + 1] = v.y;
-    }
-  };
-  if (nmy > 0) load_slice(0, 0);
-  uint32_t slot = 0, phase = 0;
-  for (uint32_t j = 0; j < nmy; ++j) {
-    const uint32_t sa = ring_u32 + slot * kSliceBytes;
-    uint64_t a[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) a[i] = nxt[i];
-    if (j + 1 < nmy) {
-      const uint32_t ns = slot + 1 == (uint32_t)stages ? 0u : slot + 1;
-      load_slice(ns, ns == 0 ? phase ^ 1u : phase);
-    }
-#else
   uint32_t slot = 0, phase = 0;
   for (uint32_t j = 0; j < nmy; ++j) {
     const uint32_t sa = ring_u32 + slot * kSliceBytes;
@@ -819,15 +817,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
       a[2 * i] = v.x;
       a[2 * i + 1] = v.y;
     }
-#endif
     if (j != jev) {
       process_full<kBig, kRows, kPages>(a, sa, cur, oc, la, w, c, o, k, lane);
     } else {
       // kernel boundary in or at this slice, or the partial tail slice (or, in the
       // interleaved schedule, the first slice of a chunk)
-#if PASTA_ICHUNK >= 0
-      if ((j & icm) == 0 && j > 0) enter_chunk(j);
-#endif
+      if (kIL && (j & icm) == 0 && j > 0) enter_chunk(j);
       const uint32_t valid = j < nfull ? (uint32_t)kSlice : tail_valid;
       const uint64_t g0 = args.gidx0 + gsl(j) * kSlice;
       uint32_t r0 = 0;
@@ -853,11 +848,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
         r0 = r1;
         if (r0 >= valid) break;
       }
-#if PASTA_ICHUNK >= 0
-      jev = next_event_after(j);
-#else
-      jev = next_event();  // > j: kend now lies beyond every record of this slice
-#endif
+      jev = next_event_after(j);  // > j: kend now lies beyond every record of this slice
     }
     // the slot is free again (every lane has consumed its values): refill it with the
     // slice `stages` ahead
@@ -923,7 +914,7 @@ __global__ void scan_extras_kernel(const ExtraArgs ea) {
 
 int stages_for(uint32_t A, bool big) {
   const long table = big ? 0 : 16l * A;
-  const long avail = (long)kSmemLimit - kBarBytes - kLaBytes - table;
+  const long avail = (long)kSmemLimit - kBarBytes - kLaBytes - kPfBytes - table;
   long st = avail / ring_bytes(1);
   if (st > kMaxStages) st = kMaxStages;
   return (int)st;
@@ -941,7 +932,7 @@ template <bool kBig, bool kRows, int kPages>
 cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
   const int stages = stages_for(a.A, kBig);
   const int smem = scan_smem_bytes(a.A, kBig);
-  auto fn = scan_kernel<kBig, kRows, kPages>;
+  auto fn = a.log_ic >= 0 ? scan_kernel<kBig, kRows, kPages, true> : scan_kernel<kBig, kRows, kPages, false>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   fn<<<grid, kThreads, smem, st>>>(a, stages);
@@ -952,19 +943,24 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
 
 int scan_warps() { return kWarps; }
 
-uint32_t scan_log_chunk(uint64_t nbody, int grid) {
-  if (!kInterleave) return 0;
+int scan_schedule(uint64_t nbody, int grid, uint32_t force) {
   const uint64_t nsl = (nbody + kSlice - 1) / kSlice;
-  const uint64_t per = (uint64_t)grid * kWarps * PASTA_CHUNKS_PER_WARP;
-  uint32_t lc = 0;
-  while ((int)lc < PASTA_ICHUNK && (nsl >> (lc + 1)) >= per) ++lc;
-  return lc;
+  const uint64_t nwarp = (uint64_t)grid * kWarps;
+  if (force == PASTA_SCHED_CONTIGUOUS) return -1;
+  if (force == PASTA_SCHED_INTERLEAVED) {
+    // the largest chunk (<= PASTA_IL_LOG_CHUNK) that still gives every warp one
+    int lc = 0;
+    while (lc < PASTA_IL_LOG_CHUNK && (nsl >> (lc + 1)) >= nwarp) ++lc;
+    return lc;
+  }
+  return (PASTA_IL && (nsl >> PASTA_IL_LOG_CHUNK) >= nwarp * PASTA_IL_MIN_CHUNKS) ? PASTA_IL_LOG_CHUNK : -1;
 }
 
-size_t scan_scratch_bytes(uint64_t nbody, uint32_t log_ic) {
+size_t scan_scratch_bytes(uint64_t nbody, int log_ic) {
+  if (log_ic < 0) return 256;
   const uint64_t nsl = (nbody + kSlice - 1) / kSlice;
   const uint64_t nch = (nsl + (1ull << log_ic) - 1) >> log_ic;
-  return kInterleave ? 16 * nch + 256 : 256;
+  return 16 * nch + 256;
 }
 
 extern "C" int pasta_debug_warp_times(unsigned long long* out, int n) {
@@ -980,13 +976,13 @@ extern "C" int pasta_debug_warp_times(unsigned long long* out, int n) {
 bool scan_table_fits_smem(uint32_t A) { return stages_for(A, false) >= kMinStages; }
 
 int scan_smem_bytes(uint32_t A, bool big_table) {
-  return ring_bytes(stages_for(A, big_table)) + kBarBytes + kLaBytes + (big_table ? 0 : (int)(16ull * A));
+  return ring_bytes(stages_for(A, big_table)) + kBarBytes + kLaBytes + kPfBytes + (big_table ? 0 : (int)(16ull * A));
 }
 
 cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st, int* launches) {
   const bool big = !scan_table_fits_smem(a.A);
   const bool rows = a.kac != nullptr;  // per-kernel outputs all require kernel rows
-  if (kInterleave && rows && a.n_kernels > 1 && a.nbody > 0) {
+  if (a.log_ic >= 0 && rows && a.n_kernels > 1 && a.nbody > 0) {
     const uint64_t nsl = (a.nbody + kSlice - 1) / kSlice;
     const uint64_t nch = (nsl + (1ull << a.log_ic) - 1) >> a.log_ic;
     chunk_kernel_map<<<(unsigned)((nch + 255) / 256), 256, 0, st>>>(a, const_cast<ulonglong2*>(a.chunk_k), nch);

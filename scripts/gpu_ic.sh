@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
 {
-for c in llama uvm gpt2m rn50; do bash scripts/ab.sh $c c i6 i7 i8 i9 i8c4; done
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for c in llama uvm gpt2m rn50; do bash scripts/ab.sh $c c il nil; done
+bash scripts/scan_sizes_ab.sh "llama 1048576 8388608 33554432" c il
 } > gpurun_out/ic.log 2>&1

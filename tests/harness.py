@@ -14,12 +14,12 @@ def u64(t):
     return t.detach().cpu().numpy().view(np.uint64)
 
 
-def gpu_trace(device, va_lo, va_hi, ranges, max_ids=None, max_live=None, frees=()):
+def gpu_trace(device, va_lo, va_hi, ranges, max_ids=None, max_live=None, frees=(), schedule="auto"):
     import paper_2602_22103_b200 as pb
 
     max_ids = max_ids or max(1, len(ranges))
     max_live = max_live or max(1, len(ranges))
-    tr = pb.Trace(device, va_lo, va_hi, max_live, max_ids)
+    tr = pb.Trace(device, va_lo, va_hi, max_live, max_ids, schedule=schedule)
     for b, s in ranges:
         tr.register_alloc(b, s)
     return tr

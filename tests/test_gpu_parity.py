@@ -33,9 +33,9 @@ def _t(np_u64):
 
 
 def _case(ranges, records, va_lo, va_hi, s, ko=None, rows=True, pages=True, topk=(1, 5, 64), max_ids=None,
-          label="", misalign=False, window_kernels=0):
+          label="", misalign=False, window_kernels=0, schedule="auto"):
     rec = np.asarray(records, dtype=np.uint64)
-    tr = gpu_trace(DEV, va_lo, va_hi, ranges, max_ids=max_ids)
+    tr = gpu_trace(DEV, va_lo, va_hi, ranges, max_ids=max_ids, schedule=schedule)
     o = oracle_trace(va_lo, va_hi, ranges, max_ids=max_ids)
     if ko is None and (rows or pages):
         ko = [0, rec.size]
@@ -118,21 +118,27 @@ def test_snapshot_sequence_on_gpu():
 
 
 # ------------------------------------------------------------------ tiny config (whole oracle)
+# Both scan schedules (contiguous per-warp ranges, interleaved chunks) must give
+# identical results; "auto" picks contiguous at these sizes.
+SCHEDULES = ["contiguous", "interleaved"]
+
+
 @pytest.mark.parametrize("seed", [42, 7])
-def test_tiny_config_parity(seed):
+@pytest.mark.parametrize("schedule", SCHEDULES)
+def test_tiny_config_parity(seed, schedule):
     p = tracegen.build_plan("tiny", seed=seed)
     rec = tracegen.host_records(p)
     dp = tracegen.DevicePlan(p, DEV)
     drec = torch.empty(p.n, dtype=torch.int64, device=DEV)
     tracegen.device_records(dp, drec)
-    tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs)
+    tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs, schedule=schedule)
     o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
     ko = [int(x) for x in p.kernel_offsets]
     g = run_gpu(tr, drec, p.page_shift, ko, kernel_rows=True, kernel_pages=True, topk=(16, 1, 1000),
                 window_kernels=3)
     r = run_oracle(o, rec, p.page_shift, ko, kernel_rows=True, kernel_pages=True, topk=(16, 1, 1000),
                    window_kernels=3)
-    assert_parity(g, r, kernel_rows=True, kernel_pages=True, label=f"tiny/{seed}")
+    assert_parity(g, r, kernel_rows=True, kernel_pages=True, label=f"tiny/{seed}/{schedule}")
     assert g["hot"].shape == (3, p.n_pages) and int(g["hot"].sum()) == int(g["page_counts"].sum())
     tr.close()
 
@@ -209,7 +215,8 @@ def _adversarial(rng, n, s, nr, near_top=False, adjacent=0.5):
 
 
 @pytest.mark.parametrize("seed", range(6))
-def test_adversarial_random(seed):
+@pytest.mark.parametrize("schedule", SCHEDULES)
+def test_adversarial_random(seed, schedule):
     rng = random.Random(100 + seed)
     for trial in range(6):
         s = rng.choice([12, 21])
@@ -222,10 +229,12 @@ def test_adversarial_random(seed):
             cuts[0] = cuts[1]  # an empty kernel
         ko = [0] + cuts + [n]
         _case(ranges, rec, va_lo, va_hi, s, ko=ko, topk=(1, 7, 300), misalign=rng.random() < 0.4,
-              label=f"adv{seed}/{trial} n={n} A={len(ranges)} s={s}", window_kernels=rng.choice([0, 1, 3]))
+              label=f"adv{seed}/{trial} n={n} A={len(ranges)} s={s} {schedule}", window_kernels=rng.choice([0, 1, 3]),
+              schedule=schedule)
 
 
-def test_many_ranges_global_table():
+@pytest.mark.parametrize("schedule", SCHEDULES)
+def test_many_ranges_global_table(schedule):
     """A = 65,536 live ranges: the boundary array no longer fits shared memory."""
     rng = random.Random(9)
     va_lo = 1 << 40
@@ -243,20 +252,22 @@ def test_many_ranges_global_table():
         a = rng.randrange(va_lo, va_hi)
         rec += [a + 8 * i for i in range(64)]
     ko = [0, n // 3, n // 3, len(rec)]
-    _case(ranges, rec, va_lo, va_hi, 12, ko=ko, topk=(10,), label="A=65536")
+    _case(ranges, rec, va_lo, va_hi, 12, ko=ko, topk=(10,), label="A=65536", schedule=schedule)
 
 
-def test_contention_and_scatter():
+@pytest.mark.parametrize("schedule", SCHEDULES)
+def test_contention_and_scatter(schedule):
     MiB = 1 << 20
     va_lo, va_hi = 1 << 41, (1 << 41) + 64 * MiB
     ranges = [(va_lo + i * MiB, MiB) for i in range(64)]
     hot = [va_lo + 5 * MiB + 100] * 1_000_003  # one page, maximal contention
-    _case(ranges, hot, va_lo, va_hi, 12, ko=[0, 500_000, len(hot)], topk=(3,), label="hot page")
+    _case(ranges, hot, va_lo, va_hi, 12, ko=[0, 500_000, len(hot)], topk=(3,), label="hot page", schedule=schedule)
     # every record a distinct page (permutation over the window at 4 KiB stride)
     P = 64 * MiB >> 12
     j = np.arange(P * 3, dtype=np.uint64)
     rec = np.uint64(va_lo) + ((j * np.uint64(2654435761)) % np.uint64(P)) * np.uint64(4096)
-    _case(ranges, rec, va_lo, va_hi, 12, ko=[0, P, 2 * P, 3 * P], topk=(1, 100, 5000), label="all distinct")
+    _case(ranges, rec, va_lo, va_hi, 12, ko=[0, P, 2 * P, 3 * P], topk=(1, 100, 5000), label="all distinct",
+          schedule=schedule)
 
 
 def test_host_records_path_equals_device_path():
@@ -320,6 +331,9 @@ def test_bitmap_or_merge_kernel():
 
 
 def test_errors_are_status_codes():
+    with pytest.raises(pb.PastaError) as ei:  # unknown open flags
+        pb.pasta_trace_open(0, 0, 1 << 30, 2, 3, 0, 0, flags=3)
+    assert ei.value.status == pb.PASTA_EINVAL
     tr = pb.Trace(DEV, 0, 1 << 30, 2, 3)
     with pytest.raises(pb.PastaError) as ei:
         tr.register_alloc(0x1000, 0)
