@@ -62,12 +62,23 @@ def _ptr(a):
 class OracleTrace:
     """Oracle counterpart of a pasta_trace handle (include/pasta.h)."""
 
-    def __init__(self, va_lo: int, va_hi: int, max_live: int, max_ids: int):
+    def __init__(self, va_lo: int, va_hi: int, max_live: int, max_ids: int, max_live_tensors: int = 0,
+                 max_tensor_ids: int = 0):
         self.va_lo, self.va_hi = int(va_lo), int(va_hi)
         self.max_live, self.max_ids = int(max_live), int(max_ids)
         self.live = {}  # base -> (size, id)
         self.bases = []  # sorted live bases
         self.sizes = []  # id -> registered size (ids are never reused)
+        self.id_base = []  # id -> registered base (kept after free, for prefetch plans)
+        # tensor level (NEXT f3, DESIGN.md R18-R20): tensors inside live objects
+        self.max_live_tensors, self.max_tensor_ids = int(max_live_tensors), int(max_tensor_ids)
+        self.tlive = {}  # base -> (size, tid)
+        self.tbases = []
+        self.tsizes = []
+        self.tid_base = []
+        self.tensor_counts = np.zeros(self.max_tensor_ids, dtype=np.uint64)
+        self.untensored = 0
+        self.tensor_rows = None
         self.kernel_rows = None
         self.kun = None
         self.kernel_pages = None
@@ -94,15 +105,56 @@ class OracleTrace:
             return ECAPACITY, None
         i = len(self.sizes)
         self.sizes.append(size)
+        self.id_base.append(base)
         self.live[base] = (size, i)
         bisect.insort(self.bases, base)
         return OK, i
 
     def register_free(self, base: int):
-        if int(base) not in self.live:
+        base = int(base)
+        if base not in self.live:
             return ENOENT
-        del self.live[int(base)]
-        self.bases.pop(bisect.bisect_left(self.bases, int(base)))
+        size = self.live[base][0]
+        del self.live[base]
+        self.bases.pop(bisect.bisect_left(self.bases, base))
+        # R19: the object's live tensors end with it
+        for tb in [b for b in self.tbases if base <= b < base + size]:
+            self.register_tensor_free(tb)
+        return OK
+
+    # ---- tensor level (R18): a tensor lies inside one live object, live tensors
+    # never overlap, tensor ids are their own monotone never-reused space ----
+    def register_tensor(self, base: int, size: int):
+        base, size = int(base), int(size)
+        if self.max_tensor_ids == 0 or size <= 0 or base < 0 or base + size > U64MAX:
+            return EINVAL, None
+        # containing object: the live object with the largest base <= base
+        i = bisect.bisect_right(self.bases, base) - 1
+        if i < 0:
+            return EINVAL, None
+        ob = self.bases[i]
+        if not (base + size <= ob + self.live[ob][0]):
+            return EINVAL, None
+        i = bisect.bisect_right(self.tbases, base + size - 1) - 1
+        if i >= 0:
+            b = self.tbases[i]
+            if base < b + self.tlive[b][0] and b < base + size:
+                return EOVERLAP, None
+        if len(self.tlive) >= self.max_live_tensors or len(self.tsizes) >= self.max_tensor_ids:
+            return ECAPACITY, None
+        t = len(self.tsizes)
+        self.tsizes.append(size)
+        self.tid_base.append(base)
+        self.tlive[base] = (size, t)
+        bisect.insort(self.tbases, base)
+        return OK, t
+
+    def register_tensor_free(self, base: int):
+        base = int(base)
+        if base not in self.tlive:
+            return ENOENT
+        del self.tlive[base]
+        self.tbases.pop(bisect.bisect_left(self.tbases, base))
         return OK
 
     # ---- one analyze call, accumulating ----
@@ -145,6 +197,31 @@ class OracleTrace:
                                   _ptr(hot), window_kernels)
         if rc != 0:
             raise ValueError(f"oracle_analyze rejected its input ({rc})")
+        if self.max_tensor_ids:
+            self._analyze_tensors(addr, ko, nk, page_shift, kernel_rows)
+
+    def _analyze_tensors(self, addr, ko, nk, page_shift, kernel_rows):
+        """Tensor level (R18): the same definition over the live tensor set:
+        each record counts for the live tensor holding its address, else as untensored.
+        The page outputs of this second pass are discarded."""
+        P = (self.va_hi - self.va_lo) >> page_shift
+        scratch_pages = np.zeros(P, dtype=np.uint64)
+        tot = np.zeros(3, dtype=np.uint64)
+        ktc = kun = None
+        if kernel_rows:
+            if self.tensor_rows is None or self.tensor_rows.shape != (nk, self.max_tensor_ids):
+                self.tensor_rows = np.zeros((nk, self.max_tensor_ids), dtype=np.uint64)
+            ktc = self.tensor_rows
+            kun = np.zeros(nk, dtype=np.uint64)
+        live = (_Range * max(1, len(self.tlive)))()
+        for i, (b, (s, t)) in enumerate(sorted(self.tlive.items())):
+            live[i].base, live[i].size, live[i].id = b, s, t
+        rc = lib().oracle_analyze(ctypes.addressof(live), len(self.tlive), _ptr(addr), addr.size, _ptr(ko), nk,
+                                  self.va_lo, self.va_hi, page_shift, self.max_tensor_ids, _ptr(scratch_pages),
+                                  _ptr(self.tensor_counts), _ptr(tot), _ptr(ktc), _ptr(kun), None, None, 0)
+        if rc != 0:
+            raise ValueError(f"oracle_analyze (tensors) rejected its input ({rc})")
+        self.untensored += int(tot[1])
 
     # ---- derived results (SURVEY 8c steps 3-4) ----
     def bitmap(self):
@@ -161,6 +238,25 @@ class OracleTrace:
         ws = lib().oracle_footprint(_ptr(self.kernel_rows), nk, self.max_ids, _ptr(sizes), _ptr(fp))
         return fp, int(ws)
 
+    def tensor_footprints(self):
+        """footprint_t[k] = sum of tensor sizes with a count in kernel k; WS_tensor = max."""
+        sizes = np.zeros(self.max_tensor_ids, dtype=np.uint64)
+        sizes[: len(self.tsizes)] = self.tsizes
+        nk = self.tensor_rows.shape[0]
+        fp = np.zeros(nk, dtype=np.uint64)
+        ws = lib().oracle_footprint(_ptr(self.tensor_rows), nk, self.max_tensor_ids, _ptr(sizes), _ptr(fp))
+        return fp, int(ws)
+
+    def prefetch_plan(self, level: str):
+        """R20 (S:488-514 build_prefetch_plan): per kernel, the union of [base, base+size)
+        of every object (level "object") or tensor ("tensor") with >= 1 access in that
+        kernel, as sorted disjoint (start, end) intervals, touching ones merged."""
+        if level == "object":
+            rows, base, size = self.kernel_rows, self.id_base, self.sizes
+        else:
+            rows, base, size = self.tensor_rows, self.tid_base, self.tsizes
+        return [interval_union([(base[i], base[i] + size[i]) for i in np.nonzero(row)[0]]) for row in rows]
+
     def kernel_unique_pages(self):
         nk, W = self.kernel_pages.shape
         out = np.zeros(nk, dtype=np.uint64)
@@ -169,6 +265,17 @@ class OracleTrace:
 
     def topk(self, K: int):
         return topk(self.page_counts, K)
+
+
+def interval_union(iv):
+    """Sorted disjoint union of half-open intervals; touching intervals are merged."""
+    out = []
+    for a, b in sorted(iv):
+        if out and a <= out[-1][1]:
+            out[-1] = (out[-1][0], max(out[-1][1], b))
+        else:
+            out.append((a, b))
+    return out
 
 
 def topk(page_counts: np.ndarray, K: int):

@@ -625,8 +625,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nsl = (args.nbody + kSlice - 1) / kSlice;
-  const uint64_t gwarp = (uint64_t)blockIdx.x * kWarps + warp;
-  const uint64_t nwarp = (uint64_t)gridDim.x * kWarps;
+  const uint32_t gwarp = blockIdx.x * kWarps + warp;
+  const uint32_t nwarp = gridDim.x * kWarps;
   // the last slice of the trace may be partial
   const uint32_t tail_valid = (uint32_t)(args.nbody - (nsl - 1) * kSlice);
   // Relative slice j of this warp -> global slice gsl(j).
@@ -646,13 +646,14 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
     tail_mine = nct > 0 && (gwarp + (nct - 1) * nwarp == nch - 1);            // I own the last chunk
     nmy = (uint32_t)((nct << lc) - (tail_mine ? (nch << lc) - nsl : 0));
   } else {
-    s0 = gwarp * nsl / nwarp;
-    const uint64_t s1 = (gwarp + 1) * nsl / nwarp;
+    s0 = (uint64_t)gwarp * nsl / nwarp;
+    const uint64_t s1 = (uint64_t)(gwarp + 1) * nsl / nwarp;
     nmy = (uint32_t)(s1 - s0);
     tail_mine = s1 == nsl;
   }
   auto gsl = [&](uint32_t j) -> uint64_t {
-    if constexpr (kIL) return (((uint64_t)(j >> lc) * nwarp + gwarp) << lc) + (j & icm);
+    // chunk index < 2^32 (a launch holds < 2^32 slices)
+    if constexpr (kIL) return ((uint64_t)((j >> lc) * nwarp + gwarp) << lc) + (j & icm);
     else return s0 + j;
   };
   const uint32_t nfull = (tail_mine && nmy > 0 && tail_valid != (uint32_t)kSlice) ? nmy - 1 : nmy;
@@ -674,19 +675,11 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
 #endif
 
   const uint64_t pol = l2_evict_first_policy();
-  // TMA for relative slice j into ring slot `slot` (lane 0 only). Slices are issued in
-  // order; the interleaved schedule advances its global slice is_gs incrementally.
-  uint32_t is_gs = kIL ? (uint32_t)gsl(0) : 0u;  // < 2^32: a launch holds at most 148 * 2^31 records
+  // TMA for relative slice j into ring slot `slot` (lane 0 only)
   auto issue = [&](uint32_t j, uint32_t slot) {
     const uint32_t bytes = j < nfull ? kSliceBytes : tail_valid * 8u;
     mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, bytes);
-    if constexpr (kIL) {
-      tma_load_1d_u32(ring_u32 + slot * kSliceBytes, args.rec + (uint64_t)is_gs * kSlice, bytes,
-                      bar_u32 + 8u * slot, pol);
-      is_gs = (((j + 1) & icm) == 0) ? (uint32_t)gsl(j + 1) : is_gs + 1;
-    } else {
-      tma_load_1d_u32(ring_u32 + slot * kSliceBytes, args.rec + gsl(j) * kSlice, bytes, bar_u32 + 8u * slot, pol);
-    }
+    tma_load_1d_u32(ring_u32 + slot * kSliceBytes, args.rec + gsl(j) * kSlice, bytes, bar_u32 + 8u * slot, pol);
   };
   if (lane == 0)
     for (uint32_t j = 0; j < (uint32_t)stages && j < nmy; ++j) issue(j, j);
