@@ -59,7 +59,9 @@ enum {
   PASTA_T_OUT_OF_WINDOW = 2, /* += records outside [va_lo, va_hi) (R8)                  */
   PASTA_T_UNIQUE_PAGES = 3,  /* = popcount(bitmap) (overwritten by finalize)            */
   PASTA_T_WS_OBJ = 4,        /* = max_k footprint[k] in bytes (overwritten; R11) */
-  PASTA_TOTALS = 8           /* slots 5..7 reserved (left untouched)                    */
+  PASTA_T_UNTENSORED = 5,    /* += records in no live tensor (needs tensor_counts; R18) */
+  PASTA_T_WS_TENSOR = 6,     /* = max_k tensor footprint[k] (overwritten; needs kernel_tensor_footprint) */
+  PASTA_TOTALS = 8           /* slot 7 reserved (left untouched)                        */
 };
 
 /* Per-kernel stats row: kernel_stats[k * PASTA_KSTATS + i]. */
@@ -82,6 +84,8 @@ typedef struct {
   uint64_t va_hi;
   uintptr_t stream;   /* cudaStream_t for all device work (0 = legacy default stream)   */
   uint64_t host_chunk_bytes; /* staging chunk for PASTA_REC_HOST (0 = 256 MiB)          */
+  uint32_t max_live_tensors; /* tensor level (NEXT f3, R18): live tensors, 0 = no tensor level */
+  uint32_t max_tensor_ids;   /* tensor ids ever issued (= bins of tensor_counts)            */
 } pasta_open_params;
 
 /* Scan schedule (pasta_open_params.flags). By default a launch over few records per
@@ -126,6 +130,15 @@ typedef struct {
   uint64_t* hotness;             /* [ceil(n_kernels/window_kernels) * P] optional +=, needs
                                     kernel_alloc_counts: time-windowed page hotness, row
                                     w = kernel k / window_kernels (NEXT f1)   */
+  /* Tensor level (NEXT f3, R18; handles opened with max_tensor_ids > 0). A record
+   * counts for its object (above) and for the live tensor holding it, else in
+   * totals[UNTENSORED]. */
+  uint64_t* tensor_counts;           /* [max_tensor_ids] optional +=, indexed by tensor id  */
+  uint64_t* kernel_tensor_counts;    /* [n_kernels*max_tensor_ids] optional +=; needs
+                                        tensor_counts and kernel_alloc_counts               */
+  uint64_t* kernel_tensor_footprint; /* [n_kernels] optional, overwritten by finalize: sum
+                                        of registered tensor sizes with a count in kernel k;
+                                        totals[WS_TENSOR] = max; needs kernel_tensor_counts */
 } pasta_histograms;
 
 /* Skip the finalize step in pasta_analyze (bitmap, unique pages, footprints, WS);
@@ -147,6 +160,18 @@ int pasta_register_alloc(pasta_trace* h, uint64_t base, uint64_t size, uint32_t*
 /* Remove the live range whose base is exactly `base` (ENOENT otherwise). Its id's
  * counts stay addressable; the id is never reissued. */
 int pasta_register_free(pasta_trace* h, uint64_t base);
+
+/* Tensor level (NEXT f3; R18, R19). Register a live tensor [base, base+size)
+ * inside a live object ("[address, address+size) lies within the containing
+ * object"): size > 0, the range inside one live object, else EINVAL (also when the
+ * handle has no tensor level); intersecting a live tensor => EOVERLAP (adjacent is
+ * legal); tensor ids 0, 1, 2, ... never reused; more than max_live_tensors live or
+ * max_tensor_ids issued => ECAPACITY. Snapshot semantics as pasta_register_alloc.
+ * pasta_register_free of an object also ends every live tensor inside it (R19). */
+int pasta_register_tensor(pasta_trace* h, uint64_t base, uint64_t size, uint32_t* out_tid);
+
+/* Remove the live tensor whose base is exactly `base` (ENOENT otherwise). */
+int pasta_register_tensor_free(pasta_trace* h, uint64_t base);
 
 /* Analyze n records at page granularity 2^page_shift (12 <= page_shift <= 30;
  * va_lo and va_hi must be multiples of 2^page_shift and P < 2^32). Steps, all on the
@@ -191,6 +216,21 @@ int pasta_bitmap_or(pasta_trace* h, const uint64_t* gathered, uint32_t g, uint64
 int pasta_topk_merge(pasta_trace* h, const uint64_t* cand_page, const uint64_t* cand_count, uint32_t g, uint32_t k,
                      uint64_t shard_pages, uint64_t* out_page, uint64_t* out_count, uint64_t* out_found);
 
+/* Prefetch-plan builder (NEXT f3; S:488-514 build_prefetch_plan; R20). For
+ * each kernel row k of `rows` (device, [n_kernels * n_ids] counts: kernel_alloc_counts
+ * with level PASTA_LEVEL_OBJECT and n_ids = max_ids, or kernel_tensor_counts with
+ * PASTA_LEVEL_TENSOR and n_ids = max_tensor_ids), the ranges to stage before kernel k:
+ * the sorted disjoint union of [base, base + size) of the ids with a non-zero count
+ * (registered ranges, even if freed since), touching intervals merged. Output (device):
+ * plan_offsets[n_kernels + 1] (CSR, plan_offsets[0] = 0) and plan_ranges[2 * cap] as
+ * (start, end) pairs, row k in [plan_offsets[k], plan_offsets[k+1]). *out_total (host)
+ * = the number of intervals; if it exceeds cap nothing is written to plan_ranges and
+ * the call returns ECAPACITY (plan_offsets is valid: size the buffer and call again).
+ * Synchronizes the handle's stream (the total crosses to the host). */
+enum { PASTA_LEVEL_OBJECT = 0u, PASTA_LEVEL_TENSOR = 1u };
+int pasta_prefetch_plan(pasta_trace* h, const uint64_t* rows, uint32_t n_kernels, uint32_t level,
+                        uint64_t* plan_offsets, uint64_t* plan_ranges, uint64_t cap, uint64_t* out_total);
+
 /* Block until the handle's stream is idle; reports asynchronous faults (ECUDA). */
 int pasta_sync(pasta_trace* h);
 
@@ -207,7 +247,7 @@ const char* pasta_strerror(int status);
  * (out_ms[PASTA_PHASES]) and the number of kernels launched since open (always
  * counted). pasta_reset_timing zeroes both. */
 enum { PASTA_PH_SCAN = 0, PASTA_PH_FINALIZE = 1, PASTA_PH_TOPK = 2, PASTA_PH_MERGE = 3, PASTA_PH_COPY = 4,
-       PASTA_PHASES = 5 };
+       PASTA_PH_PLAN = 5, PASTA_PHASES = 6 };
 int pasta_set_timing(pasta_trace* h, int enable);
 int pasta_get_timing(pasta_trace* h, double* out_ms, uint64_t* out_launches);
 int pasta_reset_timing(pasta_trace* h);

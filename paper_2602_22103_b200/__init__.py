@@ -28,20 +28,23 @@ _lib = ctypes.CDLL(_LIB_PATH)
 PASTA_OK, PASTA_EINVAL, PASTA_EOVERLAP, PASTA_ENOENT, PASTA_ECAPACITY, PASTA_ECUDA, PASTA_ESTATE, PASTA_ENOMEM = (
     0, -1, -2, -3, -4, -5, -6, -7)
 T_RECORDS, T_UNATTRIBUTED, T_OUT_OF_WINDOW, T_UNIQUE_PAGES, T_WS_OBJ, TOTALS = 0, 1, 2, 3, 4, 8
+T_UNTENSORED, T_WS_TENSOR = 5, 6
+LEVEL_OBJECT, LEVEL_TENSOR = 0, 1
 K_ATTRIBUTED, K_UNATTRIBUTED, K_FOOTPRINT, K_UNIQUE_PAGES, KSTATS = 0, 1, 2, 3, 4
 PASTA_REC_HOST = 1
 PASTA_NO_FINALIZE = 1
 PASTA_SCHED_CONTIGUOUS = 1
 PASTA_SCHED_INTERLEAVED = 2
 _SCHED = {"auto": 0, "contiguous": PASTA_SCHED_CONTIGUOUS, "interleaved": PASTA_SCHED_INTERLEAVED}
-PH_SCAN, PH_FINALIZE, PH_TOPK, PH_MERGE, PH_COPY, PHASES = 0, 1, 2, 3, 4, 5
-PHASE_NAMES = ("scan", "finalize", "topk", "merge", "copy")
+PH_SCAN, PH_FINALIZE, PH_TOPK, PH_MERGE, PH_COPY, PH_PLAN, PHASES = 0, 1, 2, 3, 4, 5, 6
+PHASE_NAMES = ("scan", "finalize", "topk", "merge", "copy", "plan")
 
 
 class pasta_open_params(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("max_live", ctypes.c_uint32), ("max_ids", ctypes.c_uint32),
                 ("flags", ctypes.c_uint32), ("va_lo", ctypes.c_uint64), ("va_hi", ctypes.c_uint64),
-                ("stream", ctypes.c_void_p), ("host_chunk_bytes", ctypes.c_uint64)]
+                ("stream", ctypes.c_void_p), ("host_chunk_bytes", ctypes.c_uint64),
+                ("max_live_tensors", ctypes.c_uint32), ("max_tensor_ids", ctypes.c_uint32)]
 
 
 class pasta_records(ctypes.Structure):
@@ -53,7 +56,9 @@ class pasta_histograms(ctypes.Structure):
     _fields_ = [("page_counts", ctypes.c_void_p), ("alloc_counts", ctypes.c_void_p), ("totals", ctypes.c_void_p),
                 ("page_bitmap", ctypes.c_void_p), ("kernel_alloc_counts", ctypes.c_void_p),
                 ("kernel_stats", ctypes.c_void_p), ("kernel_page_bitmap", ctypes.c_void_p),
-                ("flags", ctypes.c_uint32), ("window_kernels", ctypes.c_uint32), ("hotness", ctypes.c_void_p)]
+                ("flags", ctypes.c_uint32), ("window_kernels", ctypes.c_uint32), ("hotness", ctypes.c_void_p),
+                ("tensor_counts", ctypes.c_void_p), ("kernel_tensor_counts", ctypes.c_void_p),
+                ("kernel_tensor_footprint", ctypes.c_void_p)]
 
 
 _vp, _u64, _u32, _int = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
@@ -61,6 +66,9 @@ _SIGS = {
     "pasta_trace_open": (_int, [ctypes.POINTER(pasta_open_params), ctypes.POINTER(_vp)]),
     "pasta_register_alloc": (_int, [_vp, _u64, _u64, ctypes.POINTER(_u32)]),
     "pasta_register_free": (_int, [_vp, _u64]),
+    "pasta_register_tensor": (_int, [_vp, _u64, _u64, ctypes.POINTER(_u32)]),
+    "pasta_register_tensor_free": (_int, [_vp, _u64]),
+    "pasta_prefetch_plan": (_int, [_vp, _vp, _u32, _u32, _vp, _vp, _u64, ctypes.POINTER(_u64)]),
     "pasta_analyze": (_int, [_vp, ctypes.POINTER(pasta_records), _u64, _u32, ctypes.POINTER(pasta_histograms)]),
     "pasta_finalize": (_int, [_vp, _u32, _u32, ctypes.POINTER(pasta_histograms)]),
     "pasta_topk": (_int, [_vp, _vp, _u64, _u32, _vp, _vp, _vp]),
@@ -108,9 +116,9 @@ def pasta_strerror(status: int) -> str:
 
 
 def pasta_trace_open(device: int, va_lo: int, va_hi: int, max_live: int, max_ids: int, stream=0,
-                     host_chunk_bytes: int = 0, flags: int = 0):
+                     host_chunk_bytes: int = 0, flags: int = 0, max_live_tensors: int = 0, max_tensor_ids: int = 0):
     p = pasta_open_params(device, max_live, max_ids, flags, va_lo, va_hi, ctypes.c_void_p(stream or 0),
-                          host_chunk_bytes)
+                          host_chunk_bytes, max_live_tensors, max_tensor_ids)
     h = ctypes.c_void_p()
     _check(_lib.pasta_trace_open(ctypes.byref(p), ctypes.byref(h)), "pasta_trace_open")
     return h
@@ -124,6 +132,26 @@ def pasta_register_alloc(h, base: int, size: int) -> int:
 
 def pasta_register_free(h, base: int):
     _check(_lib.pasta_register_free(h, base), "pasta_register_free")
+
+
+def pasta_register_tensor(h, base: int, size: int) -> int:
+    out = _u32()
+    _check(_lib.pasta_register_tensor(h, base, size, ctypes.byref(out)), "pasta_register_tensor")
+    return out.value
+
+
+def pasta_register_tensor_free(h, base: int):
+    _check(_lib.pasta_register_tensor_free(h, base), "pasta_register_tensor_free")
+
+
+def pasta_prefetch_plan(h, rows, n_kernels: int, level: int, plan_offsets, plan_ranges, cap: int) -> tuple:
+    """Returns (status, total): ECAPACITY is returned, not raised, so callers can size."""
+    total = _u64()
+    st = _lib.pasta_prefetch_plan(h, _ptr(rows), n_kernels, level, _ptr(plan_offsets), _ptr(plan_ranges), cap,
+                                  ctypes.byref(total))
+    if st not in (PASTA_OK, PASTA_ECAPACITY):
+        raise PastaError(st, "pasta_prefetch_plan")
+    return st, total.value
 
 
 def pasta_analyze(h, addr, n: int, page_shift: int, hist, kernel_offsets=None, n_kernels: int = 0, flags: int = 0):
@@ -177,30 +205,36 @@ def pasta_reset_timing(h):
 class Histograms:
     """Output arrays as int64 CUDA tensors (u64 bit patterns).
 
-    ``packed`` = [page_counts (P) | alloc_counts (max_ids) | totals (8)] is one buffer,
-    so the merge across ranks is one all_reduce(SUM). Per-kernel
-    arrays and the bitmap are separate tensors."""
+    ``packed`` = [page_counts (P) | alloc_counts (max_ids) | totals (8) | tensor_counts
+    (max_tensor_ids)] is one buffer, so the merge across ranks is one all_reduce(SUM)
+    (DESIGN.md section 5). Per-kernel arrays and the bitmap are separate tensors."""
 
     def __init__(self, P: int, max_ids: int, device, n_kernels: int = 0, kernel_rows: bool = False,
-                 kernel_pages: bool = False, bitmap: bool = True, pad_pages_to: int = 1, window_kernels: int = 0):
+                 kernel_pages: bool = False, bitmap: bool = True, pad_pages_to: int = 1, window_kernels: int = 0,
+                 max_tensor_ids: int = 0):
         import torch
 
-        self.P, self.max_ids, self.n_kernels = P, max_ids, n_kernels
+        self.P, self.max_ids, self.n_kernels, self.max_tensor_ids = P, max_ids, n_kernels, max_tensor_ids
         self.words = (P + 63) // 64
         # the page part is padded with zero pages to a multiple of `pad_pages_to` so it
         # can be reduce-scattered in equal shards (dist.ShardedMerger)
         self.P_pad = (P + pad_pages_to - 1) // pad_pages_to * pad_pages_to
-        self.packed = torch.zeros(self.P_pad + max_ids + TOTALS, dtype=torch.int64, device=device)
+        self.packed = torch.zeros(self.P_pad + max_ids + TOTALS + max_tensor_ids, dtype=torch.int64, device=device)
         self.page_counts = self.packed[:P]
         self.pages_padded = self.packed[:self.P_pad]
-        self.small = self.packed[self.P_pad:]  # [alloc_counts | totals]
+        self.small = self.packed[self.P_pad:]  # [alloc_counts | totals | tensor_counts]
         self.alloc_counts = self.packed[self.P_pad:self.P_pad + max_ids]
-        self.totals = self.packed[self.P_pad + max_ids:]
+        self.totals = self.packed[self.P_pad + max_ids:self.P_pad + max_ids + TOTALS]
+        self.tensor_counts = self.packed[self.P_pad + max_ids + TOTALS:] if max_tensor_ids else None
         self.page_bitmap = torch.zeros(self.words, dtype=torch.int64, device=device) if bitmap else None
         self.kernel_alloc_counts = self.kernel_stats = self.kernel_page_bitmap = None
+        self.kernel_tensor_counts = self.kernel_tensor_footprint = None
         if kernel_rows:
             self.kernel_alloc_counts = torch.zeros(n_kernels * max_ids, dtype=torch.int64, device=device)
             self.kernel_stats = torch.zeros(n_kernels * KSTATS, dtype=torch.int64, device=device)
+            if max_tensor_ids:
+                self.kernel_tensor_counts = torch.zeros(n_kernels * max_tensor_ids, dtype=torch.int64, device=device)
+                self.kernel_tensor_footprint = torch.zeros(n_kernels, dtype=torch.int64, device=device)
         if kernel_pages:
             self.kernel_page_bitmap = torch.zeros(n_kernels * self.words, dtype=torch.int64, device=device)
         self.window_kernels = window_kernels
@@ -211,7 +245,7 @@ class Histograms:
 
     def zero_(self):
         for t in (self.packed, self.page_bitmap, self.kernel_alloc_counts, self.kernel_stats,
-                  self.kernel_page_bitmap, self.hotness):
+                  self.kernel_page_bitmap, self.hotness, self.kernel_tensor_counts, self.kernel_tensor_footprint):
             if t is not None:
                 t.zero_()
         return self
@@ -219,14 +253,17 @@ class Histograms:
     def struct(self, flags: int = 0) -> pasta_histograms:
         return pasta_histograms(_ptr(self.page_counts), _ptr(self.alloc_counts), _ptr(self.totals),
                                 _ptr(self.page_bitmap), _ptr(self.kernel_alloc_counts), _ptr(self.kernel_stats),
-                                _ptr(self.kernel_page_bitmap), flags, self.window_kernels, _ptr(self.hotness))
+                                _ptr(self.kernel_page_bitmap), flags, self.window_kernels, _ptr(self.hotness),
+                                _ptr(self.tensor_counts), _ptr(self.kernel_tensor_counts),
+                                _ptr(self.kernel_tensor_footprint))
 
 
 class Trace:
     """A pasta_trace handle bound to one CUDA device and stream."""
 
     def __init__(self, device, va_lo: int, va_hi: int, max_live: int, max_ids: int, stream=None,
-                 host_chunk_bytes: int = 0, schedule: str = "auto"):
+                 host_chunk_bytes: int = 0, schedule: str = "auto", max_live_tensors: int = 0,
+                 max_tensor_ids: int = 0):
         import torch
 
         self.device = torch.device(device)
@@ -234,8 +271,9 @@ class Trace:
             stream = torch.cuda.current_stream(self.device)
         self.stream = stream
         self.va_lo, self.va_hi, self.max_live, self.max_ids = va_lo, va_hi, max_live, max_ids
+        self.max_tensor_ids = max_tensor_ids
         self.h = pasta_trace_open(self.device.index or 0, va_lo, va_hi, max_live, max_ids, stream.cuda_stream,
-                                  host_chunk_bytes, _SCHED[schedule])
+                                  host_chunk_bytes, _SCHED[schedule], max_live_tensors, max_tensor_ids)
 
     def n_pages(self, page_shift: int) -> int:
         return (self.va_hi - self.va_lo) >> page_shift
@@ -246,10 +284,32 @@ class Trace:
     def register_free(self, base: int):
         pasta_register_free(self.h, base)
 
+    def register_tensor(self, base: int, size: int) -> int:
+        return pasta_register_tensor(self.h, base, size)
+
+    def register_tensor_free(self, base: int):
+        pasta_register_tensor_free(self.h, base)
+
+    def prefetch_plan(self, hist: Histograms, level: str = "object"):
+        """(offsets[n_kernels + 1], ranges[total, 2]) int64 device tensors: row k's staged
+        ranges are ranges[offsets[k]:offsets[k+1]] as (start, end) (R20)."""
+        import torch
+
+        lv = LEVEL_TENSOR if level == "tensor" else LEVEL_OBJECT
+        rows = hist.kernel_tensor_counts if lv == LEVEL_TENSOR else hist.kernel_alloc_counts
+        nk = hist.n_kernels
+        offsets = torch.empty(nk + 1, dtype=torch.int64, device=self.device)
+        st, total = pasta_prefetch_plan(self.h, rows, nk, lv, offsets, None, 0)
+        ranges = torch.empty((max(total, 1), 2), dtype=torch.int64, device=self.device)
+        if total:
+            st, total = pasta_prefetch_plan(self.h, rows, nk, lv, offsets, ranges, total)
+            assert st == PASTA_OK
+        return offsets, ranges[:total]
+
     def histograms(self, page_shift: int, n_kernels: int = 0, kernel_rows=False, kernel_pages=False, bitmap=True,
                    pad_pages_to: int = 1, window_kernels: int = 0):
         return Histograms(self.n_pages(page_shift), self.max_ids, self.device, n_kernels, kernel_rows, kernel_pages,
-                          bitmap, pad_pages_to, window_kernels)
+                          bitmap, pad_pages_to, window_kernels, self.max_tensor_ids)
 
     def analyze(self, records, page_shift: int, hist: Histograms, kernel_offsets=None, n: int | None = None,
                 finalize: bool = True, host: bool = False):

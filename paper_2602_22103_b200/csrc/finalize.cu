@@ -7,7 +7,8 @@
 //    totals[UNIQUE_PAGES] (P:795 working set by pages, north star part 3; R14).
 //  * footprint: one warp per kernel row: sum of registered sizes over ids with a
 //    non-zero count; atomicMax of the rows into totals[WS_OBJ]
-//    (P:795); the row's page-bitmap popcount (per-kernel unique pages).
+//    (P:795); the row's page-bitmap popcount (per-kernel unique pages). The same kernel
+//    gives tensor footprints and totals[WS_TENSOR] from the tensor rows (NEXT f3).
 #include <cstdint>
 
 #include "common.cuh"
@@ -62,7 +63,8 @@ __global__ void __launch_bounds__(kBlock) bitmap_kernel(const uint64_t* __restri
 __global__ void __launch_bounds__(kBlock) footprint_kernel(const uint64_t* __restrict__ kac, uint32_t K,
                                                            uint64_t max_ids, const uint64_t* __restrict__ id_size,
                                                            const uint64_t* __restrict__ kpb, uint32_t words,
-                                                           uint64_t* __restrict__ kstats,
+                                                           uint64_t* __restrict__ fp_out, uint32_t fp_stride,
+                                                           uint64_t* __restrict__ up_out, uint32_t up_stride,
                                                            uint64_t* __restrict__ ws_out) {
   const unsigned lane = threadIdx.x & 31;
   const uint64_t gw = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -87,8 +89,8 @@ __global__ void __launch_bounds__(kBlock) footprint_kernel(const uint64_t* __res
       up = warp_sum_u64(up);
     }
     if (lane == 0) {
-      kstats[k * 4 + 2] = f;
-      kstats[k * 4 + 3] = up;
+      fp_out[k * fp_stride] = f;
+      if (up_out) up_out[k * up_stride] = up;
     }
     wmax = f > wmax ? f : wmax;
   }
@@ -137,12 +139,12 @@ cudaError_t launch_finalize_bitmap(const uint64_t* page_counts, uint64_t P, uint
 }
 
 cudaError_t launch_footprint(const uint64_t* kac, uint32_t n_kernels, uint64_t max_ids, const uint64_t* id_size,
-                             const uint64_t* kpb, uint32_t words, uint64_t* kstats, uint64_t* ws_out, int grid,
-                             cudaStream_t st) {
+                             const uint64_t* kpb, uint32_t words, uint64_t* fp_out, uint32_t fp_stride,
+                             uint64_t* up_out, uint32_t up_stride, uint64_t* ws_out, int grid, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(ws_out, 0, sizeof(uint64_t), st);
   if (e != cudaSuccess) return e;
-  footprint_kernel<<<grid_for(n_kernels, kBlock / 32, grid), kBlock, 0, st>>>(kac, n_kernels, max_ids, id_size, kpb,
-                                                                             words, kstats, ws_out);
+  footprint_kernel<<<grid_for(n_kernels, kBlock / 32, grid), kBlock, 0, st>>>(
+      kac, n_kernels, max_ids, id_size, kpb, words, fp_out, fp_stride, up_out, up_stride, ws_out);
   return cudaGetLastError();
 }
 

@@ -6,7 +6,9 @@
 
 namespace pasta {
 
-constexpr uint32_t kOOW = 0xFFFFFFFFu;  // page index sentinel: outside the window
+constexpr uint32_t kOOW = 0xFFFFFFFFu;       // page index sentinel: outside the window
+constexpr uint32_t kNoTensor = 0xFFFFFFFFu;  // table interval in no live tensor
+constexpr int kTotUntensored = 5;            // totals[PASTA_T_UNTENSORED]
 
 // Everything the fused scan needs.
 struct ScanArgs {
@@ -34,6 +36,11 @@ struct ScanArgs {
   uint32_t window_kernels;   // kernels per hotness window (>= 1)
   const ulonglong2* chunk_k; // [chunks] (k, koffs[k+1]) of each interleaved chunk's first record (scratch)
   int32_t log_ic;            // log2 slices per interleaved chunk, -1 = contiguous (scan_schedule)
+  // tensor level (NEXT f3): all nullptr when off
+  const uint32_t* tids;      // [A] tensor id of table interval r, kNoTensor = none
+  uint64_t* tensor_counts;   // [max_tids]
+  uint64_t* ktc;             // kernel_tensor_counts [n_kernels x max_tids] or nullptr
+  uint64_t max_tids;
 };
 
 // Extra records that are not part of the 16-byte aligned even body (<= 2).
@@ -59,9 +66,24 @@ size_t scan_scratch_bytes(uint64_t nbody, int log_ic);
 
 cudaError_t launch_finalize_bitmap(const uint64_t* page_counts, uint64_t P, uint64_t* bitmap, uint64_t* unique_out,
                                    int grid, cudaStream_t st);
+// footprint[k] = sum of id_size[i] over ids with kac[k][i] > 0 -> fp_out[k * fp_stride],
+// unique pages of row k of kpb (if non-null) -> up_out[k * up_stride] (if non-null),
+// *ws_out = max_k footprint[k].
 cudaError_t launch_footprint(const uint64_t* kac, uint32_t n_kernels, uint64_t max_ids, const uint64_t* id_size,
-                             const uint64_t* kpb, uint32_t words, uint64_t* kstats, uint64_t* ws_out, int grid,
-                             cudaStream_t st);
+                             const uint64_t* kpb, uint32_t words, uint64_t* fp_out, uint32_t fp_stride,
+                             uint64_t* up_out, uint32_t up_stride, uint64_t* ws_out, int grid, cudaStream_t st);
+
+// Prefetch plans (NEXT f3, plan.cu): for each of n_kernels rows of `rows` ([n_kernels x
+// n_ids]), the union of [base[i], base[i] + size[i]) over the ids with a non-zero
+// count, visiting ids in `order` (ids sorted by base, n_order entries). Pass 1 writes
+// per-row interval counts into offsets[1..n_kernels] and their exclusive scan (offsets[0]
+// = 0); pass 2 (ranges != nullptr) writes the (start, end) pairs.
+cudaError_t launch_plan_count(const uint64_t* rows, uint32_t n_kernels, uint64_t n_ids, const uint32_t* order,
+                              uint32_t n_order, const uint64_t* base, const uint64_t* size, uint64_t* offsets,
+                              cudaStream_t st, int* launches);
+cudaError_t launch_plan_write(const uint64_t* rows, uint32_t n_kernels, uint64_t n_ids, const uint32_t* order,
+                              uint32_t n_order, const uint64_t* base, const uint64_t* size, const uint64_t* offsets,
+                              uint64_t* ranges, cudaStream_t st);
 cudaError_t launch_bitmap_or(const uint64_t* gathered, uint32_t g, uint64_t words, uint64_t* out,
                              uint64_t* popcount, int grid, cudaStream_t st);
 

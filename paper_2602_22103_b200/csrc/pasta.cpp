@@ -39,7 +39,20 @@ struct pasta_trace {
   // host registration state
   std::map<uint64_t, std::pair<uint64_t, uint32_t>> live;  // base -> (size, id)
   std::vector<uint64_t> id_size;                           // id -> registered size
+  std::vector<uint64_t> id_base;                           // id -> registered base (plans)
   bool dirty = true;
+
+  // tensor level (NEXT f3, R18): tensors inside live objects
+  uint32_t max_live_tensors = 0, max_tids = 0;
+  std::map<uint64_t, std::pair<uint64_t, uint32_t>> tlive;  // base -> (size, tid)
+  std::vector<uint64_t> tid_size, tid_base;
+  uint32_t* d_tids = nullptr;      // [table capacity] tensor id of each table interval
+  uint64_t* d_tid_size = nullptr;  // [max_tids]
+
+  // prefetch-plan scratch: base[n], size[n], order[n]
+  unsigned char* d_plan = nullptr;
+  size_t plan_bytes = 0;
+  uint64_t* h_total = nullptr;  // pinned: the plan's interval count
 
   // device table (capacity max_live / max_ids)
   uint64_t* d_bounds = nullptr;  // [2*max_live]
@@ -71,7 +84,7 @@ struct pasta_trace {
   bool timing = false;
   std::vector<TimedLaunch> pending;
   std::vector<cudaEvent_t> free_events;
-  double ms[PASTA_PHASES] = {0, 0, 0, 0, 0};
+  double ms[PASTA_PHASES] = {};
   uint64_t launches = 0;
 };
 
@@ -122,12 +135,19 @@ struct Timed {
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? PASTA_OK : PASTA_ECUDA; }
 
-// Upload the current registration table if it changed (stream-ordered).
+// Table capacity in intervals: objects, each tensor splitting its object at most twice.
+uint64_t table_capacity(const pasta_trace* h) { return (uint64_t)h->max_live + 2ull * h->max_live_tensors; }
+
+// Upload the current registration table if it changed (stream-ordered). The device
+// table is a partition of the registered space into intervals: each live object, cut
+// at its live tensors' bounds (R18), so one lookup names the object and the tensor.
 int upload_table(pasta_trace* h) {
   if (!h->dirty) return PASTA_OK;
-  const uint32_t A = (uint32_t)h->live.size();
-  const size_t nid = h->id_size.size();
-  const size_t need = 16ull * A + 4ull * A + 8ull * nid + 64;
+  const bool tens = h->max_tids > 0;
+  uint64_t I = h->live.size();
+  if (tens) I += 2ull * h->tlive.size();  // upper bound
+  const size_t nid = h->id_size.size(), ntid = h->tid_size.size();
+  const size_t need = 16ull * I + 8ull * I + 8ull * nid + 8ull * ntid + 64;
   if (h->upload_pending) {
     // the previous upload must have left the staging buffer before we overwrite it
     if (cudaEventSynchronize(h->upload_done) != cudaSuccess) return PASTA_ECUDA;
@@ -144,24 +164,46 @@ int upload_table(pasta_trace* h) {
     h->h_stage_bytes = cap;
   }
   uint64_t* hb = reinterpret_cast<uint64_t*>(h->h_stage);
-  uint64_t* hs = hb + 2ull * A;
-  uint32_t* hi = reinterpret_cast<uint32_t*>(hs + nid);
+  uint64_t* hs = hb + 2ull * I;
+  uint64_t* hts = hs + nid;
+  uint32_t* hi = reinterpret_cast<uint32_t*>(hts + ntid);
+  uint32_t* ht = hi + I;
   uint32_t r = 0;
-  for (const auto& kv : h->live) {  // std::map iterates in ascending base order
-    hb[2 * r] = kv.first;
-    hb[2 * r + 1] = kv.first + kv.second.first;
-    hi[r] = kv.second.second;
+  auto emit = [&](uint64_t lo, uint64_t hi_, uint32_t id, uint32_t tid) {
+    hb[2 * r] = lo;
+    hb[2 * r + 1] = hi_;
+    hi[r] = id;
+    ht[r] = tid;
     ++r;
+  };
+  for (const auto& kv : h->live) {  // std::map iterates in ascending base order
+    const uint64_t ob = kv.first, oe = kv.first + kv.second.first;
+    const uint32_t id = kv.second.second;
+    if (!tens) {
+      emit(ob, oe, id, kNoTensor);
+      continue;
+    }
+    uint64_t cur = ob;
+    for (auto t = h->tlive.lower_bound(ob); t != h->tlive.end() && t->first < oe; ++t) {
+      if (t->first > cur) emit(cur, t->first, id, kNoTensor);
+      emit(t->first, t->first + t->second.first, id, t->second.second);
+      cur = t->first + t->second.first;
+    }
+    if (cur < oe) emit(cur, oe, id, kNoTensor);
   }
   for (size_t i = 0; i < nid; ++i) hs[i] = h->id_size[i];
+  for (size_t i = 0; i < ntid; ++i) hts[i] = h->tid_size[i];
   cudaError_t e = cudaSuccess;
-  if (A) e = cudaMemcpyAsync(h->d_bounds, hb, 16ull * A, cudaMemcpyHostToDevice, h->stream);
-  if (e == cudaSuccess && A) e = cudaMemcpyAsync(h->d_ids, hi, 4ull * A, cudaMemcpyHostToDevice, h->stream);
+  if (r) e = cudaMemcpyAsync(h->d_bounds, hb, 16ull * r, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess && r) e = cudaMemcpyAsync(h->d_ids, hi, 4ull * r, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess && r && tens) e = cudaMemcpyAsync(h->d_tids, ht, 4ull * r, cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess && nid) e = cudaMemcpyAsync(h->d_id_size, hs, 8ull * nid, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess && ntid)
+    e = cudaMemcpyAsync(h->d_tid_size, hts, 8ull * ntid, cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaEventRecord(h->upload_done, h->stream);
   if (e != cudaSuccess) return PASTA_ECUDA;
   h->upload_pending = true;
-  h->A_dev = A;
+  h->A_dev = r;
   h->dirty = false;
   return PASTA_OK;
 }
@@ -251,11 +293,28 @@ int finalize_impl(pasta_trace* h, uint32_t page_shift, uint32_t n_kernels, pasta
   if (out->kernel_alloc_counts && out->kernel_stats && n_kernels > 0) {
     Timed t(h, PASTA_PH_FINALIZE, h->stream);
     cudaError_t e = launch_footprint(out->kernel_alloc_counts, n_kernels, h->max_ids, h->d_id_size,
-                                     out->kernel_page_bitmap, words, out->kernel_stats,
+                                     out->kernel_page_bitmap, words, out->kernel_stats + PASTA_K_FOOTPRINT,
+                                     PASTA_KSTATS, out->kernel_stats + PASTA_K_UNIQUE_PAGES, PASTA_KSTATS,
                                      out->totals + PASTA_T_WS_OBJ, grid, h->stream);
     ++h->launches;
     if (e != cudaSuccess) return PASTA_ECUDA;
   }
+  if (out->kernel_tensor_counts && out->kernel_tensor_footprint && n_kernels > 0) {
+    Timed t(h, PASTA_PH_FINALIZE, h->stream);
+    cudaError_t e = launch_footprint(out->kernel_tensor_counts, n_kernels, h->max_tids, h->d_tid_size, nullptr, 0,
+                                     out->kernel_tensor_footprint, 1, nullptr, 0, out->totals + PASTA_T_WS_TENSOR,
+                                     grid, h->stream);
+    ++h->launches;
+    if (e != cudaSuccess) return PASTA_ECUDA;
+  }
+  return PASTA_OK;
+}
+
+// Tensor-level output requirements (R18).
+int check_tensor_outputs(const pasta_trace* h, const pasta_histograms* out) {
+  if (out->tensor_counts && h->max_tids == 0) return PASTA_EINVAL;
+  if (out->kernel_tensor_counts && (!out->tensor_counts || !out->kernel_alloc_counts)) return PASTA_EINVAL;
+  if (out->kernel_tensor_footprint && !out->kernel_tensor_counts) return PASTA_EINVAL;
   return PASTA_OK;
 }
 
@@ -314,6 +373,8 @@ int pasta_trace_open(const pasta_open_params* p, pasta_trace** out) {
   h->va_hi = p->va_hi;
   h->max_live = p->max_live;
   h->max_ids = p->max_ids;
+  h->max_live_tensors = p->max_live_tensors;
+  h->max_tids = p->max_tensor_ids;
   if (p->host_chunk_bytes) h->host_chunk_bytes = (p->host_chunk_bytes + 4095) / 4096 * 4096;
   DeviceGuard g(h->device);
   // the scan's chunk map: 4 MiB covers every launch up to ~4.3e9 records, so calls
@@ -323,12 +384,19 @@ int pasta_trace_open(const pasta_open_params* p, pasta_trace** out) {
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device) == cudaSuccess && sms > 0)
     h->sm_count = sms;
-  bool ok = cudaMalloc(&h->d_bounds, 16ull * h->max_live) == cudaSuccess &&
-            cudaMalloc(&h->d_ids, 4ull * h->max_live) == cudaSuccess &&
+  const uint64_t tcap = table_capacity(h);
+  bool ok = cudaMalloc(&h->d_bounds, 16ull * tcap) == cudaSuccess &&
+            cudaMalloc(&h->d_ids, 4ull * tcap) == cudaSuccess &&
+            cudaMallocHost(&h->h_total, sizeof(uint64_t)) == cudaSuccess &&
             cudaMalloc(&h->d_id_size, 8ull * h->max_ids) == cudaSuccess &&
             cudaMalloc(&h->d_scan, kScanScratch0) == cudaSuccess &&
             cudaEventCreateWithFlags(&h->upload_done, cudaEventDisableTiming) == cudaSuccess;
   if (ok) ok = cudaMemsetAsync(h->d_id_size, 0, 8ull * h->max_ids, h->stream) == cudaSuccess;
+  if (ok && h->max_tids) {
+    ok = cudaMalloc(&h->d_tids, 4ull * tcap) == cudaSuccess &&
+         cudaMalloc(&h->d_tid_size, 8ull * h->max_tids) == cudaSuccess &&
+         cudaMemsetAsync(h->d_tid_size, 0, 8ull * h->max_tids, h->stream) == cudaSuccess;
+  }
   if (!ok) {
     pasta_close(h);
     return PASTA_ECUDA;
@@ -351,6 +419,7 @@ int pasta_register_alloc(pasta_trace* h, uint64_t base, uint64_t size, uint32_t*
   if (h->live.size() >= h->max_live || h->id_size.size() >= h->max_ids) return PASTA_ECAPACITY;
   const uint32_t id = (uint32_t)h->id_size.size();
   h->id_size.push_back(size);
+  h->id_base.push_back(base);
   h->live.emplace(base, std::make_pair(size, id));
   h->dirty = true;
   if (out_id) *out_id = id;
@@ -361,7 +430,43 @@ int pasta_register_free(pasta_trace* h, uint64_t base) {
   if (!h) return PASTA_EINVAL;
   auto it = h->live.find(base);
   if (it == h->live.end()) return PASTA_ENOENT;
+  const uint64_t end = base + it->second.first;
   h->live.erase(it);
+  // R19: the object's live tensors end with it
+  h->tlive.erase(h->tlive.lower_bound(base), h->tlive.lower_bound(end));
+  h->dirty = true;
+  return PASTA_OK;
+}
+
+int pasta_register_tensor(pasta_trace* h, uint64_t base, uint64_t size, uint32_t* out_tid) {
+  if (!h || h->max_tids == 0) return PASTA_EINVAL;
+  if (size == 0 || base > UINT64_MAX - size) return PASTA_EINVAL;
+  const uint64_t end = base + size;
+  // containing object: the live object with the largest base <= base must hold [base, end)
+  auto ob = h->live.upper_bound(base);
+  if (ob == h->live.begin()) return PASTA_EINVAL;
+  --ob;
+  if (end > ob->first + ob->second.first) return PASTA_EINVAL;
+  auto it = h->tlive.lower_bound(end);  // first tensor base >= end
+  if (it != h->tlive.begin()) {
+    auto pr = std::prev(it);
+    if (pr->first + pr->second.first > base) return PASTA_EOVERLAP;
+  }
+  if (h->tlive.size() >= h->max_live_tensors || h->tid_size.size() >= h->max_tids) return PASTA_ECAPACITY;
+  const uint32_t tid = (uint32_t)h->tid_size.size();
+  h->tid_size.push_back(size);
+  h->tid_base.push_back(base);
+  h->tlive.emplace(base, std::make_pair(size, tid));
+  h->dirty = true;
+  if (out_tid) *out_tid = tid;
+  return PASTA_OK;
+}
+
+int pasta_register_tensor_free(pasta_trace* h, uint64_t base) {
+  if (!h) return PASTA_EINVAL;
+  auto it = h->tlive.find(base);
+  if (it == h->tlive.end()) return PASTA_ENOENT;
+  h->tlive.erase(it);
   h->dirty = true;
   return PASTA_OK;
 }
@@ -372,7 +477,9 @@ int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t 
   if ((out->kernel_stats || out->kernel_page_bitmap || out->hotness) && !out->kernel_alloc_counts) return PASTA_EINVAL;
   if (out->hotness && out->window_kernels == 0) return PASTA_EINVAL;
   if (tr->flags & ~PASTA_REC_HOST) return PASTA_EINVAL;
-  int s = check_window(h, page_shift);
+  int s = check_tensor_outputs(h, out);
+  if (s) return s;
+  s = check_window(h, page_shift);
   if (s) return s;
   if (n > 0 && (!tr->addr || !aligned8(tr->addr))) return PASTA_EINVAL;
   const uint32_t K = tr->kernel_offsets ? tr->n_kernels : 1;
@@ -408,6 +515,12 @@ int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t 
   a.hot = out->hotness;
   a.P = P;
   a.window_kernels = out->window_kernels ? out->window_kernels : 1;
+  if (out->tensor_counts) {
+    a.tids = h->d_tids;
+    a.tensor_counts = out->tensor_counts;
+    a.ktc = out->kernel_tensor_counts;
+    a.max_tids = h->max_tids;
+  }
 
   if (!host) {
     s = scan_range(h, tr->addr, n, 0, a, h->stream, n);
@@ -469,7 +582,9 @@ int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t 
 int pasta_finalize(pasta_trace* h, uint32_t page_shift, uint32_t n_kernels, pasta_histograms* out) {
   if (!h || !out || !out->page_counts || !out->totals) return PASTA_EINVAL;
   if ((out->kernel_stats || out->kernel_page_bitmap) && !out->kernel_alloc_counts) return PASTA_EINVAL;
-  int s = check_window(h, page_shift);
+  int s = check_tensor_outputs(h, out);
+  if (s) return s;
+  s = check_window(h, page_shift);
   if (s) return s;
   DeviceGuard g(h->device);
   s = upload_table(h);  // id sizes must be current for the footprints
@@ -535,6 +650,64 @@ int pasta_bitmap_or(pasta_trace* h, const uint64_t* gathered, uint32_t g, uint64
   return cuda_status(e);
 }
 
+int pasta_prefetch_plan(pasta_trace* h, const uint64_t* rows, uint32_t n_kernels, uint32_t level,
+                        uint64_t* plan_offsets, uint64_t* plan_ranges, uint64_t cap, uint64_t* out_total) {
+  if (!h || !rows || !plan_offsets || !out_total || n_kernels == 0) return PASTA_EINVAL;
+  if (level != PASTA_LEVEL_OBJECT && level != PASTA_LEVEL_TENSOR) return PASTA_EINVAL;
+  if (level == PASTA_LEVEL_TENSOR && h->max_tids == 0) return PASTA_EINVAL;
+  if (cap > 0 && !plan_ranges) return PASTA_EINVAL;
+  const std::vector<uint64_t>& base = level == PASTA_LEVEL_TENSOR ? h->tid_base : h->id_base;
+  const std::vector<uint64_t>& size = level == PASTA_LEVEL_TENSOR ? h->tid_size : h->id_size;
+  const uint64_t n_ids = level == PASTA_LEVEL_TENSOR ? h->max_tids : h->max_ids;
+  const uint32_t n = (uint32_t)base.size();  // ids issued so far (the rest have no counts)
+  DeviceGuard g(h->device);
+  // ids in base order (ties by id): the warp walk's visiting order
+  std::vector<uint32_t> order(n);
+  for (uint32_t i = 0; i < n; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
+    return base[x] != base[y] ? base[x] < base[y] : x < y;
+  });
+  const size_t need = 20ull * n + 64;
+  if (need > h->plan_bytes) {
+    if (h->d_plan) {
+      cudaStreamSynchronize(h->stream);
+      cudaFree(h->d_plan);
+    }
+    h->d_plan = nullptr;
+    h->plan_bytes = 0;
+    if (cudaMalloc(&h->d_plan, need) != cudaSuccess) return PASTA_ECUDA;
+    h->plan_bytes = need;
+  }
+  uint64_t* d_base = reinterpret_cast<uint64_t*>(h->d_plan);
+  uint64_t* d_size = d_base + n;
+  uint32_t* d_order = reinterpret_cast<uint32_t*>(d_size + n);
+  cudaStream_t st = h->stream;
+  if (n) {
+    // pageable sources: cudaMemcpyAsync stages them before returning
+    if (cudaMemcpyAsync(d_base, base.data(), 8ull * n, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(d_size, size.data(), 8ull * n, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(d_order, order.data(), 4ull * n, cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return PASTA_ECUDA;
+  }
+  {
+    Timed t(h, PASTA_PH_PLAN, st);
+    int nl = 0;
+    cudaError_t e = launch_plan_count(rows, n_kernels, n_ids, d_order, n, d_base, d_size, plan_offsets, st, &nl);
+    h->launches += (uint64_t)nl;
+    if (e != cudaSuccess) return PASTA_ECUDA;
+  }
+  if (cudaMemcpyAsync(h->h_total, plan_offsets + n_kernels, sizeof(uint64_t), cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return PASTA_ECUDA;
+  *out_total = *h->h_total;
+  if (*out_total > cap) return PASTA_ECAPACITY;
+  Timed t(h, PASTA_PH_PLAN, st);
+  cudaError_t e = launch_plan_write(rows, n_kernels, n_ids, d_order, n, d_base, d_size, plan_offsets, plan_ranges, st);
+  ++h->launches;
+  return cuda_status(e);
+}
+
 int pasta_sync(pasta_trace* h) {
   if (!h) return PASTA_EINVAL;
   DeviceGuard g(h->device);
@@ -565,6 +738,10 @@ int pasta_close(pasta_trace* h) {
   if (h->d_koffs) cudaFree(h->d_koffs);
   if (h->d_topk) cudaFree(h->d_topk);
   if (h->d_scan) cudaFree(h->d_scan);
+  if (h->d_tids) cudaFree(h->d_tids);
+  if (h->d_tid_size) cudaFree(h->d_tid_size);
+  if (h->d_plan) cudaFree(h->d_plan);
+  if (h->h_total) cudaFreeHost(h->h_total);
   if (h->d_bounds) cudaFree(h->d_bounds);
   if (h->d_ids) cudaFree(h->d_ids);
   if (h->d_id_size) cudaFree(h->d_id_size);

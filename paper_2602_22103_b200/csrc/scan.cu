@@ -203,6 +203,10 @@ struct Out {
   uint64_t* hot;    // hotness matrix [windows x P] or nullptr (NEXT f1)
   uint64_t P;
   uint32_t wk;      // kernels per hotness window
+  const uint32_t* tids;  // tensor level (NEXT f3) or nullptr
+  uint64_t* tcounts;
+  uint64_t* ktc;
+  uint64_t max_tids;
 };
 
 // Time-windowed hotness: the page run's count also goes to row k / wk.
@@ -227,6 +231,17 @@ __device__ __forceinline__ void owner_to_global(const Out& o, uint32_t own, uint
   } else {
     red_add_u64(o.totals + 1, v);
     if (kRows && o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 1, v);
+  }
+  // tensor level (R18): the table intervals refine objects by tensors, so the owner
+  // interval also names the tensor (or none)
+  if (o.tids != nullptr) {
+    const uint32_t t = own < o.A ? __ldg(o.tids + own) : kNoTensor;
+    if (t != kNoTensor) {
+      red_add_u64(o.tcounts + t, v);
+      if (kRows && o.ktc) red_add_u64(o.ktc + (uint64_t)k * o.max_tids + t, v);
+    } else {
+      red_add_u64(o.totals + kTotUntensored, v);
+    }
   }
 }
 
@@ -705,6 +720,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   o.hot = args.hot;
   o.P = args.P;
   o.wk = args.window_kernels;
+  o.tids = args.tids;
+  o.tcounts = args.tensor_counts;
+  o.ktc = args.ktc;
+  o.max_tids = args.max_tids;
 
   OwnCache oc;
   oc.olo = 1;
@@ -896,6 +915,10 @@ __global__ void scan_extras_kernel(const ExtraArgs ea) {
   o.hot = s.hot;
   o.P = s.P;
   o.wk = s.window_kernels;
+  o.tids = s.tids;
+  o.tcounts = s.tensor_counts;
+  o.ktc = s.ktc;
+  o.max_tids = s.max_tids;
   if (rows) owner_to_global<true>(o, I.own, 1, k);
   else owner_to_global<false>(o, I.own, 1, k);
   const int mode = (s.kpb ? 1 : 0) | (s.hot ? 2 : 0);

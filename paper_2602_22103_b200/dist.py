@@ -21,6 +21,10 @@ import torch
 import torch.distributed as dist
 
 
+# totals slots merged by MAX (working sets, R11; tensor level R18); the rest are sums
+_WS_SLOTS = (4, 6)  # PASTA_T_WS_OBJ, PASTA_T_WS_TENSOR
+
+
 def merge_counts(packed: torch.Tensor, group=None):
     """all_reduce(SUM) of the packed count buffer, in place."""
     dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=group)
@@ -74,19 +78,19 @@ class Merger:
         self.tr, self.hist, self.group = trace, hist, group
         self.world = dist.get_world_size(group)
         self.gathered = torch.empty(self.world * hist.words, dtype=torch.int64, device=hist.packed.device)
-        self.ws = torch.empty(1, dtype=torch.int64, device=hist.packed.device)
+        self.ws = torch.empty(len(_WS_SLOTS), dtype=torch.int64, device=hist.packed.device)
 
     def merge(self):
-        from . import T_UNIQUE_PAGES, T_WS_OBJ
+        from . import T_UNIQUE_PAGES
 
         h = self.hist
-        self.ws.copy_(h.totals[T_WS_OBJ:T_WS_OBJ + 1])
+        self.ws.copy_(h.totals[list(_WS_SLOTS)])
         merge_counts(h.packed, self.group)
         gather_bitmaps(h.page_bitmap, self.group, out=self.gathered)
         self.tr.bitmap_or(self.gathered, self.world, h.words, h.page_bitmap,
                           h.totals[T_UNIQUE_PAGES:T_UNIQUE_PAGES + 1])
         merge_max(self.ws, self.group)
-        h.totals[T_WS_OBJ:T_WS_OBJ + 1].copy_(self.ws)
+        h.totals[list(_WS_SLOTS)] = self.ws
 
 
 class ShardedMerger:
@@ -110,7 +114,7 @@ class ShardedMerger:
         self.S = hist.P_pad // self.world
         self.shard = torch.empty(self.S, dtype=torch.int64, device=dev)
         self.gathered = torch.empty(self.world * hist.words, dtype=torch.int64, device=dev)
-        self.ws = torch.empty(1, dtype=torch.int64, device=dev)
+        self.ws = torch.empty(len(_WS_SLOTS), dtype=torch.int64, device=dev)
         self.ks = tuple(ks)
         self.loc = {k: (torch.empty(k, dtype=torch.int64, device=dev), torch.empty(k, dtype=torch.int64, device=dev),
                         torch.empty(1, dtype=torch.int64, device=dev)) for k in self.ks}
@@ -120,17 +124,17 @@ class ShardedMerger:
                         torch.empty(1, dtype=torch.int64, device=dev)) for k in self.ks}
 
     def merge(self):
-        from . import T_UNIQUE_PAGES, T_WS_OBJ
+        from . import T_UNIQUE_PAGES
 
         h = self.hist
-        self.ws.copy_(h.totals[T_WS_OBJ:T_WS_OBJ + 1])
+        self.ws.copy_(h.totals[list(_WS_SLOTS)])
         dist.all_reduce(h.small, op=dist.ReduceOp.SUM, group=self.group)
         reduce_scatter_counts(h.pages_padded, self.shard, self.group)
         gather_bitmaps(h.page_bitmap, self.group, out=self.gathered)
         self.tr.bitmap_or(self.gathered, self.world, h.words, h.page_bitmap,
                           h.totals[T_UNIQUE_PAGES:T_UNIQUE_PAGES + 1])
         merge_max(self.ws, self.group)
-        h.totals[T_WS_OBJ:T_WS_OBJ + 1].copy_(self.ws)
+        h.totals[list(_WS_SLOTS)] = self.ws
         for k in self.ks:
             lp, lc, _ = self.tr.topk(self.shard, k, out=self.loc[k])
             cp, cc = self.cand[k]

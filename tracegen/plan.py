@@ -58,6 +58,9 @@ class Plan:
     want_kernel_rows: bool = True
     want_kernel_pages: bool = False
     note: str = ""
+    # the allocator's pool chunks [(base, size)]: the object level when ``allocs`` (the
+    # tensors) are registered as a second level (NEXT f3); each alloc lies in one chunk
+    objects: list = field(default_factory=list)
 
     @property
     def n_kernels(self) -> int:
@@ -287,7 +290,8 @@ def plan_tiny(seed: int = 42, n: int = 1 << 20) -> Plan:
     ko, st, cdf = b.finish(n, kernel_records=[n // 8 + (1 if i < n % 8 else 0) for i in range(8)])
     return Plan("tiny", seed, n, va_lo, va_lo + 64 * MiB, 12, allocs, ko, st, cdf, topk=[16],
                 want_kernel_rows=True, want_kernel_pages=True,
-                note="16 allocs at va_lo+i*4MiB of 64KiB*(i+1); 8 kernels")
+                note="16 allocs at va_lo+i*4MiB of 64KiB*(i+1); 8 kernels",
+                objects=[(va_lo + i * 4 * MiB, 4 * MiB) for i in range(16)])
 
 
 # ----------------------------------------------------------------------------------------
@@ -440,7 +444,8 @@ def plan_dl(name: str, seed: int, n: int, *, window: int, page_shift: int, n_lay
     ko, st, cdf = b.finish(n)
     allocs = [(t.base, t.size) for t in tensors]
     return Plan(name, seed, n, va_lo, va_lo + window, page_shift, allocs, ko, st, cdf, topk=list(topk),
-                want_kernel_rows=want_kernel_rows, want_kernel_pages=want_kernel_pages, note=note)
+                want_kernel_rows=want_kernel_rows, want_kernel_pages=want_kernel_pages, note=note,
+                objects=list(al.chunks))
 
 
 def plan_rn50(seed: int = 42, n: int = 500_000_000) -> Plan:
