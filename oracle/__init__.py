@@ -43,6 +43,9 @@ def lib():
         vp, u64, u32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32
         L.oracle_analyze.restype = ctypes.c_int
         L.oracle_analyze.argtypes = [vp, u64, vp, u64, vp, u64, u64, u64, u32, u64, vp, vp, vp, vp, vp, vp, vp, u64]
+        L.oracle_analyze_rich.restype = ctypes.c_int
+        L.oracle_analyze_rich.argtypes = [vp, u64, vp, u64, u64, u64, u64, u64, u32, u64, vp, vp, vp, vp, vp, vp, vp,
+                                          vp, vp]
         L.oracle_bitmap.restype = u64
         L.oracle_bitmap.argtypes = [vp, u64, vp]
         L.oracle_footprint.restype = u64
@@ -222,6 +225,50 @@ class OracleTrace:
         if rc != 0:
             raise ValueError(f"oracle_analyze (tensors) rejected its input ({rc})")
         self.untensored += int(tot[1])
+
+    # ---- rich 16-byte records (NEXT f4, R21-R23) ----
+    def analyze_rich(self, rec16: np.ndarray, grid_lo: int, grid_hi: int, page_shift: int = 12,
+                     kernel_rows: bool = False):
+        """rec16: uint8 [n, 16] (or any buffer of n * 16 bytes) in the layout of
+        oracle_analyze_rich. Accumulates page / alloc counts and totals like analyze, plus
+        page_writes, alloc_writes, alloc_bytes, rich_totals [filtered, shared, writes,
+        bytes]; kernel rows are indexed by grid_id - grid_lo."""
+        rec = np.ascontiguousarray(rec16).view(np.uint8).reshape(-1)
+        n = rec.size // 16
+        P = (self.va_hi - self.va_lo) >> page_shift
+        if self.page_counts is None or self.page_shift != page_shift:
+            self.page_counts = np.zeros(P, dtype=np.uint64)
+            self.page_shift = page_shift
+        if getattr(self, "page_writes", None) is None or self.page_writes.size != P:
+            self.page_writes = np.zeros(P, dtype=np.uint64)
+            self.alloc_writes = np.zeros(self.max_ids, dtype=np.uint64)
+            self.alloc_bytes = np.zeros(self.max_ids, dtype=np.uint64)
+            self.rich_totals = np.zeros(4, dtype=np.uint64)
+        nk = int(grid_hi) - int(grid_lo) + 1
+        kac = kun = None
+        if kernel_rows:
+            if self.kernel_rows is None or self.kernel_rows.shape != (nk, self.max_ids):
+                self.kernel_rows = np.zeros((nk, self.max_ids), dtype=np.uint64)
+                self.kun = np.zeros(nk, dtype=np.uint64)
+            kac, kun = self.kernel_rows, self.kun
+        live = (_Range * max(1, len(self.live)))()
+        for i, (b, (s, idx)) in enumerate(sorted(self.live.items())):
+            live[i].base, live[i].size, live[i].id = b, s, idx
+        rc = lib().oracle_analyze_rich(ctypes.addressof(live), len(self.live), _ptr(rec), n, int(grid_lo),
+                                       int(grid_hi), self.va_lo, self.va_hi, page_shift, self.max_ids,
+                                       _ptr(self.page_counts), _ptr(self.page_writes), _ptr(self.alloc_counts),
+                                       _ptr(self.alloc_writes), _ptr(self.alloc_bytes), _ptr(self.totals),
+                                       _ptr(self.rich_totals), _ptr(kac), _ptr(kun))
+        if rc != 0:
+            raise ValueError(f"oracle_analyze_rich rejected its input ({rc})")
+
+    def max_kernel(self):
+        """MAX_MEM_REFERENCED_KERNEL: the kernel with the most analyzed records
+        (attributed + unattributed), ties to the lowest index (R24); None without rows."""
+        if self.kernel_rows is None or self.kernel_rows.shape[0] == 0:
+            return None
+        per = self.kernel_rows.sum(axis=1, dtype=np.uint64) + self.kun
+        return int(np.argmax(per))
 
     # ---- derived results (SURVEY 8c steps 3-4) ----
     def bitmap(self):

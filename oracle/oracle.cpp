@@ -24,6 +24,8 @@
 //    blocks"                                     -> page histogram (s = 21; s = 12 too)
 //  * P:918-919 hot blocks are prefetch / cudaMemAdvise candidates -> top-K hot pages
 //  * P:912-920 hotness "over time" -> time-windowed page matrix (R17)
+//  * P:424 range-specific analysis (START_GRID_ID / END_GRID_ID), SPEC S:39-42 rich
+//    records                                     -> oracle_analyze_rich (R21-R23)
 // Readings where the paper is silent are DESIGN.md "Readings" R1-R14.
 //
 // Parity status: every function below is pinned by tests/test_oracle_pins.py
@@ -131,6 +133,80 @@ int oracle_analyze(const oracle_range* live, uint64_t n_live, const uint64_t* ad
   totals[0] += n;
   totals[1] += unattributed;
   totals[2] += oow;
+  return 0;
+}
+
+// Rich records (NEXT f4; R21-R23). A 16-byte record (SPEC S:39-42
+// MemAccessInfo): u64 address at byte 0, u32 grid_id at 8, u16 size_bytes at 12, u8
+// flags at 14 (bit 0 is_write, bit 1 shared space), u8 reserved at 15, little endian.
+// Per record, in this order:
+//   1. grid_id outside [grid_lo, grid_hi] -> rich_totals[0] += 1, dropped (P:424
+//      START_GRID_ID / END_GRID_ID; "grid_window keeps kernels with start <=
+//      grid_id <= end");
+//   2. shared space -> rich_totals[1] += 1, dropped (R22: the analysis is over global
+//      memory, Table II "Global Memory Access");
+//   3. otherwise analyzed exactly like an 8-byte record of kernel k = grid_id - grid_lo
+//      (R23), with write counts and byte weights (R21): totals[0..2] as oracle_analyze,
+//      alloc_counts / alloc_writes / alloc_bytes[id], kac[k][id] / kun[k], page_counts /
+//      page_writes[p], rich_totals[2] += is_write, rich_totals[3] += size_bytes.
+// Any output pointer except page_counts / alloc_counts / totals / rich_totals may be NULL.
+int oracle_analyze_rich(const oracle_range* live, uint64_t n_live, const uint8_t* rec, uint64_t n, uint64_t grid_lo,
+                        uint64_t grid_hi, uint64_t va_lo, uint64_t va_hi, uint32_t page_shift, uint64_t max_ids,
+                        uint64_t* page_counts, uint64_t* page_writes, uint64_t* alloc_counts, uint64_t* alloc_writes,
+                        uint64_t* alloc_bytes, uint64_t* totals, uint64_t* rich_totals, uint64_t* kac, uint64_t* kun) {
+  std::map<uint64_t, std::pair<uint64_t, uint32_t>> ranges;
+  for (uint64_t i = 0; i < n_live; ++i) {
+    if (live[i].id >= max_ids) return -1;
+    ranges[live[i].base] = {live[i].base + live[i].size, live[i].id};
+  }
+  if (grid_lo > grid_hi) return -1;
+  for (uint64_t j = 0; j < n; ++j) {
+    const uint8_t* r = rec + 16 * j;
+    uint64_t a = 0;
+    for (int b = 7; b >= 0; --b) a = (a << 8) | r[b];
+    const uint64_t grid = (uint64_t)r[8] | ((uint64_t)r[9] << 8) | ((uint64_t)r[10] << 16) | ((uint64_t)r[11] << 24);
+    const uint64_t size = (uint64_t)r[12] | ((uint64_t)r[13] << 8);
+    const bool is_write = (r[14] & 1) != 0;
+    const bool shared = (r[14] & 2) != 0;
+    if (grid < grid_lo || grid > grid_hi) {
+      rich_totals[0] += 1;
+      continue;
+    }
+    if (shared) {
+      rich_totals[1] += 1;
+      continue;
+    }
+    const uint64_t k = grid - grid_lo;
+    totals[0] += 1;
+    bool owned = false;
+    uint32_t owner = 0;
+    auto it = ranges.upper_bound(a);
+    if (it != ranges.begin()) {
+      auto p = std::prev(it);
+      if (a < p->second.first) {
+        owned = true;
+        owner = p->second.second;
+      }
+    }
+    if (owned) {
+      alloc_counts[owner] += 1;
+      if (alloc_writes) alloc_writes[owner] += is_write ? 1 : 0;
+      if (alloc_bytes) alloc_bytes[owner] += size;
+      if (kac) kac[k * max_ids + owner] += 1;
+    } else {
+      totals[1] += 1;
+      if (kun) kun[k] += 1;
+    }
+    if (va_lo <= a && a < va_hi) {
+      const uint64_t p = (a - va_lo) >> page_shift;
+      page_counts[p] += 1;
+      if (page_writes) page_writes[p] += is_write ? 1 : 0;
+    } else {
+      totals[2] += 1;
+    }
+    rich_totals[2] += is_write ? 1 : 0;
+    rich_totals[3] += size;
+  }
   return 0;
 }
 

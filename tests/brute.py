@@ -91,3 +91,43 @@ def topk(page, K):
             out.append((best, page[best]))
     found = sum(1 for p, c in out if c != 0)
     return out, found
+
+
+def analyze_rich(live, recs, grid_lo, grid_hi, va_lo, va_hi, s, max_ids):
+    """recs: list of (addr, grid, size, is_write, shared) tuples (R21-R23)."""
+    P = (va_hi - va_lo) >> s
+    nk = grid_hi - grid_lo + 1
+    r = dict(page=[0] * P, pw=[0] * P, alloc=[0] * max_ids, aw=[0] * max_ids, ab=[0] * max_ids,
+             kac=[[0] * max_ids for _ in range(nk)], kun=[0] * nk, records=0, unattr=0, oow=0,
+             filtered=0, shared=0, writes=0, bytes=0)
+    for a, g, size, w, sh in recs:
+        if not (grid_lo <= g <= grid_hi):
+            r["filtered"] += 1
+            continue
+        if sh:
+            r["shared"] += 1
+            continue
+        k = g - grid_lo
+        r["records"] += 1
+        o = owner_of(a, live)
+        if o is None:
+            r["unattr"] += 1
+            r["kun"][k] += 1
+        else:
+            r["alloc"][o] += 1
+            r["aw"][o] += w
+            r["ab"][o] += size
+            r["kac"][k][o] += 1
+        if va_lo <= a < va_hi:
+            p = 0
+            lo = va_lo
+            while not (lo <= a < lo + (1 << s)):
+                lo += 1 << s
+                p += 1
+            r["page"][p] += 1
+            r["pw"][p] += w
+        else:
+            r["oow"] += 1
+        r["writes"] += w
+        r["bytes"] += size
+    return r
