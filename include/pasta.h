@@ -61,7 +61,10 @@ enum {
   PASTA_T_WS_OBJ = 4,        /* = max_k footprint[k] in bytes (overwritten; R11) */
   PASTA_T_UNTENSORED = 5,    /* += records in no live tensor (needs tensor_counts; R18) */
   PASTA_T_WS_TENSOR = 6,     /* = max_k tensor footprint[k] (overwritten; needs kernel_tensor_footprint) */
-  PASTA_TOTALS = 8           /* slot 7 reserved (left untouched)                        */
+  PASTA_T_MAX_KERNEL = 7,    /* = MAX_MEM_REFERENCED_KERNEL (R24): the kernel row with
+                                the most analyzed records, ties to the lowest (overwritten by
+                                finalize when kernel_stats is given)                      */
+  PASTA_TOTALS = 8
 };
 
 /* Per-kernel stats row: kernel_stats[k * PASTA_KSTATS + i]. */
@@ -184,12 +187,52 @@ int pasta_register_tensor_free(pasta_trace* h, uint64_t base);
 int pasta_analyze(pasta_trace* h, const pasta_records* trace, uint64_t n, uint32_t page_shift,
                   pasta_histograms* out);
 
+/* Rich 16-byte records (NEXT f4; R21-R23; SPEC S:39-42 MemAccessInfo):
+ * little endian u64 address, u32 grid_id, u16 size_bytes (1..128), u8 flags
+ * (PASTA_ACC_WRITE | PASTA_ACC_SHARED), u8 zero. */
+typedef struct {
+  uint64_t addr;
+  uint32_t grid_id;
+  uint16_t size_bytes;
+  uint8_t flags;
+  uint8_t reserved;
+} pasta_rich_record;
+enum { PASTA_ACC_WRITE = 1u, PASTA_ACC_SHARED = 2u };
+
+typedef struct {
+  const pasta_rich_record* records; /* [n] DEVICE memory, 16-byte aligned, read-only     */
+  uint32_t grid_lo, grid_hi;        /* inclusive grid-id window (P:424 START_GRID_ID /
+                                       END_GRID_ID); kernel row k = grid_id - grid_lo,
+                                       n_kernels = grid_hi - grid_lo + 1               */
+} pasta_rich_records;
+
+/* Extra outputs of the rich analysis (caller-owned DEVICE memory, += like counts). */
+enum { PASTA_RT_FILTERED = 0, PASTA_RT_SHARED = 1, PASTA_RT_WRITES = 2, PASTA_RT_BYTES = 3, PASTA_RICH_TOTALS = 4 };
+typedef struct {
+  uint64_t* rich_totals;        /* [PASTA_RICH_TOTALS] required: records outside the window,
+                                   shared-space records (both dropped, R22-R23), writes and
+                                   bytes (size_bytes) of the analyzed records            */
+  uint64_t* page_write_counts;  /* [P] optional: analyzed writes per page                */
+  uint64_t* alloc_write_counts; /* [max_ids] optional: analyzed writes per alloc id      */
+  uint64_t* alloc_bytes;        /* [max_ids] optional: sum of size_bytes per alloc id (R21) */
+} pasta_rich_outputs;
+
+/* Analyze n rich records: every record whose grid_id lies in [grid_lo, grid_hi] and
+ * that is not a shared-space access is analyzed exactly as pasta_analyze analyzes an
+ * 8-byte record of kernel row grid_id - grid_lo (records of different kernels may be
+ * interleaved); totals[RECORDS] counts the analyzed records. `out` may not ask for
+ * kernel_page_bitmap, hotness or the tensor level (EINVAL). Then, unless
+ * PASTA_NO_FINALIZE, pasta_finalize with n_kernels = grid_hi - grid_lo + 1. */
+int pasta_analyze_rich(pasta_trace* h, const pasta_rich_records* trace, uint64_t n, uint32_t page_shift,
+                       pasta_histograms* out, pasta_rich_outputs* rich);
+
 /* Recompute the derived outputs from the accumulated counts in `out`:
  * page_bitmap (if non-NULL) and totals[UNIQUE_PAGES] from page_counts; for
  * n_kernels rows (if kernel_alloc_counts and kernel_stats are non-NULL)
  * footprint[k] = sum of registered sizes of ids with a non-zero count (P:797-799,
  * P:844), totals[WS_OBJ] = max_k footprint[k], and unique pages per kernel
- * from kernel_page_bitmap (if non-NULL). */
+ * from kernel_page_bitmap (if non-NULL); totals[MAX_KERNEL] from kernel_stats (R24); tensor
+ * footprints and totals[WS_TENSOR] (if kernel_tensor_footprint is non-NULL). */
 int pasta_finalize(pasta_trace* h, uint32_t page_shift, uint32_t n_kernels, pasta_histograms* out);
 
 /* Top-K hot pages: the first min(k, nnz) pages with a non-zero count,

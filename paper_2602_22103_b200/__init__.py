@@ -28,7 +28,9 @@ _lib = ctypes.CDLL(_LIB_PATH)
 PASTA_OK, PASTA_EINVAL, PASTA_EOVERLAP, PASTA_ENOENT, PASTA_ECAPACITY, PASTA_ECUDA, PASTA_ESTATE, PASTA_ENOMEM = (
     0, -1, -2, -3, -4, -5, -6, -7)
 T_RECORDS, T_UNATTRIBUTED, T_OUT_OF_WINDOW, T_UNIQUE_PAGES, T_WS_OBJ, TOTALS = 0, 1, 2, 3, 4, 8
-T_UNTENSORED, T_WS_TENSOR = 5, 6
+T_UNTENSORED, T_WS_TENSOR, T_MAX_KERNEL = 5, 6, 7
+RT_FILTERED, RT_SHARED, RT_WRITES, RT_BYTES, RICH_TOTALS = 0, 1, 2, 3, 4
+ACC_WRITE, ACC_SHARED = 1, 2
 LEVEL_OBJECT, LEVEL_TENSOR = 0, 1
 K_ATTRIBUTED, K_UNATTRIBUTED, K_FOOTPRINT, K_UNIQUE_PAGES, KSTATS = 0, 1, 2, 3, 4
 PASTA_REC_HOST = 1
@@ -61,6 +63,15 @@ class pasta_histograms(ctypes.Structure):
                 ("kernel_tensor_footprint", ctypes.c_void_p)]
 
 
+class pasta_rich_records(ctypes.Structure):
+    _fields_ = [("records", ctypes.c_void_p), ("grid_lo", ctypes.c_uint32), ("grid_hi", ctypes.c_uint32)]
+
+
+class pasta_rich_outputs(ctypes.Structure):
+    _fields_ = [("rich_totals", ctypes.c_void_p), ("page_write_counts", ctypes.c_void_p),
+                ("alloc_write_counts", ctypes.c_void_p), ("alloc_bytes", ctypes.c_void_p)]
+
+
 _vp, _u64, _u32, _int = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
 _SIGS = {
     "pasta_trace_open": (_int, [ctypes.POINTER(pasta_open_params), ctypes.POINTER(_vp)]),
@@ -71,6 +82,8 @@ _SIGS = {
     "pasta_prefetch_plan": (_int, [_vp, _vp, _u32, _u32, _vp, _vp, _u64, ctypes.POINTER(_u64)]),
     "pasta_analyze": (_int, [_vp, ctypes.POINTER(pasta_records), _u64, _u32, ctypes.POINTER(pasta_histograms)]),
     "pasta_finalize": (_int, [_vp, _u32, _u32, ctypes.POINTER(pasta_histograms)]),
+    "pasta_analyze_rich": (_int, [_vp, ctypes.POINTER(pasta_rich_records), _u64, _u32,
+                                  ctypes.POINTER(pasta_histograms), ctypes.POINTER(pasta_rich_outputs)]),
     "pasta_topk": (_int, [_vp, _vp, _u64, _u32, _vp, _vp, _vp]),
     "pasta_bitmap_or": (_int, [_vp, _vp, _u32, _u64, _vp, _vp]),
     "pasta_topk_merge": (_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp]),
@@ -157,6 +170,12 @@ def pasta_prefetch_plan(h, rows, n_kernels: int, level: int, plan_offsets, plan_
 def pasta_analyze(h, addr, n: int, page_shift: int, hist, kernel_offsets=None, n_kernels: int = 0, flags: int = 0):
     rec = pasta_records(_ptr(addr), _ptr(kernel_offsets), n_kernels, flags)
     _check(_lib.pasta_analyze(h, ctypes.byref(rec), n, page_shift, ctypes.byref(hist)), "pasta_analyze")
+
+
+def pasta_analyze_rich(h, records, n: int, grid_lo: int, grid_hi: int, page_shift: int, hist, rich):
+    tr = pasta_rich_records(_ptr(records), grid_lo, grid_hi)
+    _check(_lib.pasta_analyze_rich(h, ctypes.byref(tr), n, page_shift, ctypes.byref(hist), ctypes.byref(rich)),
+           "pasta_analyze_rich")
 
 
 def pasta_finalize(h, page_shift: int, n_kernels: int, hist):
@@ -258,6 +277,22 @@ class Histograms:
                                 _ptr(self.kernel_tensor_footprint))
 
 
+class RichOutputs:
+    """Extra outputs of the rich analysis (NEXT f4) as int64 CUDA tensors."""
+
+    def __init__(self, P: int, max_ids: int, device, writes: bool = True, bytes_: bool = True):
+        import torch
+
+        self.rich_totals = torch.zeros(RICH_TOTALS, dtype=torch.int64, device=device)
+        self.page_write_counts = torch.zeros(P, dtype=torch.int64, device=device) if writes else None
+        self.alloc_write_counts = torch.zeros(max_ids, dtype=torch.int64, device=device) if writes else None
+        self.alloc_bytes = torch.zeros(max_ids, dtype=torch.int64, device=device) if bytes_ else None
+
+    def struct(self) -> pasta_rich_outputs:
+        return pasta_rich_outputs(_ptr(self.rich_totals), _ptr(self.page_write_counts),
+                                  _ptr(self.alloc_write_counts), _ptr(self.alloc_bytes))
+
+
 class Trace:
     """A pasta_trace handle bound to one CUDA device and stream."""
 
@@ -318,6 +353,16 @@ class Trace:
         nk = 0 if kernel_offsets is None else kernel_offsets.numel() - 1
         pasta_analyze(self.h, records, n, page_shift, hist.struct(0 if finalize else PASTA_NO_FINALIZE),
                       kernel_offsets, nk, PASTA_REC_HOST if host else 0)
+
+    def rich_outputs(self, page_shift: int, writes: bool = True, bytes_: bool = True) -> RichOutputs:
+        return RichOutputs(self.n_pages(page_shift), self.max_ids, self.device, writes, bytes_)
+
+    def analyze_rich(self, records, grid_lo: int, grid_hi: int, page_shift: int, hist: Histograms,
+                     rich: RichOutputs, finalize: bool = True):
+        """records: int64 CUDA tensor [n, 2] holding pasta_rich_record bytes (tracegen.rich)."""
+        n = records.shape[0] if records.dim() == 2 else records.numel() // 2
+        pasta_analyze_rich(self.h, records, n, grid_lo, grid_hi, page_shift,
+                           hist.struct(0 if finalize else PASTA_NO_FINALIZE), rich.struct())
 
     def finalize(self, page_shift: int, hist: Histograms, n_kernels: int = 0):
         pasta_finalize(self.h, page_shift, n_kernels, hist.struct())

@@ -120,6 +120,45 @@ __global__ void __launch_bounds__(kBlock) bitmap_or_kernel(const uint64_t* gathe
   }
 }
 
+// MAX_MEM_REFERENCED_KERNEL (R24): one block, argmax of attributed +
+// unattributed records per kernel row, ties to the lowest row.
+__global__ void __launch_bounds__(1024) max_kernel_kernel(const uint64_t* __restrict__ kstats, uint32_t K,
+                                                          uint64_t* __restrict__ out) {
+  __shared__ uint64_t sv[32];
+  __shared__ uint32_t si[32];
+  uint64_t bv = 0;
+  uint32_t bi = 0xFFFFFFFFu;
+  for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) {
+    const uint64_t v = __ldg(kstats + 4ull * k) + __ldg(kstats + 4ull * k + 1);
+    if (bi == 0xFFFFFFFFu || v > bv) {  // rows visited in increasing order: the first max stays
+      bv = v;
+      bi = k;
+    }
+  }
+  // warp then block reduction of (value desc, index asc)
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t v = __shfl_xor_sync(kFull, bv, o);
+    const uint32_t i = __shfl_xor_sync(kFull, bi, o);
+    if (i != 0xFFFFFFFFu && (bi == 0xFFFFFFFFu || v > bv || (v == bv && i < bi))) {
+      bv = v;
+      bi = i;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = bv;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (si[w] != 0xFFFFFFFFu && (si[0] == 0xFFFFFFFFu || sv[w] > sv[0] || (sv[w] == sv[0] && si[w] < si[0]))) {
+        sv[0] = sv[w];
+        si[0] = si[w];
+      }
+    *out = si[0] == 0xFFFFFFFFu ? 0 : si[0];
+  }
+}
+
 int grid_for(uint64_t items, int per_block, int max_grid) {
   uint64_t b = (items + per_block - 1) / per_block;
   if (b < 1) b = 1;
@@ -145,6 +184,11 @@ cudaError_t launch_footprint(const uint64_t* kac, uint32_t n_kernels, uint64_t m
   if (e != cudaSuccess) return e;
   footprint_kernel<<<grid_for(n_kernels, kBlock / 32, grid), kBlock, 0, st>>>(
       kac, n_kernels, max_ids, id_size, kpb, words, fp_out, fp_stride, up_out, up_stride, ws_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_kernel(const uint64_t* kstats, uint32_t n_kernels, uint64_t* out, cudaStream_t st) {
+  max_kernel_kernel<<<1, 1024, 0, st>>>(kstats, n_kernels, out);
   return cudaGetLastError();
 }
 

@@ -43,6 +43,33 @@ struct ScanArgs {
   uint64_t max_tids;
 };
 
+// Rich 16-byte records (NEXT f4; R21-R24).
+struct RichArgs {
+  const uint64_t* rec;       // [2n] u64 words: record i = (rec[2i], rec[2i+1]), 16-byte aligned
+  uint64_t n;
+  uint32_t grid_lo, grid_last;  // grid-id window [grid_lo, grid_lo + grid_last] (inclusive)
+  const uint64_t* bounds;
+  const uint32_t* ids;
+  uint32_t A;
+  uint64_t va_lo, va_hi;
+  uint32_t page_shift;
+  uint64_t max_ids;
+  uint64_t* page_counts;
+  uint64_t* page_writes;     // optional
+  uint64_t* alloc_counts;
+  uint64_t* alloc_writes;    // optional
+  uint64_t* alloc_bytes;     // optional
+  uint64_t* totals;          // [0] analyzed records, [1] unattributed, [2] out of window
+  uint64_t* rich_totals;     // [4] filtered, shared, writes, bytes
+  uint64_t* kac;             // [grid_n x max_ids] or nullptr
+  uint64_t* kstats;          // [grid_n x 4] or nullptr
+};
+cudaError_t launch_rich(const RichArgs& a, int grid, cudaStream_t st);
+int rich_slice_records();
+
+// MAX_MEM_REFERENCED_KERNEL (R24): *out = argmax_k kstats[4k] + kstats[4k+1], ties low.
+cudaError_t launch_max_kernel(const uint64_t* kstats, uint32_t n_kernels, uint64_t* out, cudaStream_t st);
+
 // Extra records that are not part of the 16-byte aligned even body (<= 2).
 struct ExtraArgs {
   ScanArgs s;

@@ -299,6 +299,12 @@ int finalize_impl(pasta_trace* h, uint32_t page_shift, uint32_t n_kernels, pasta
     ++h->launches;
     if (e != cudaSuccess) return PASTA_ECUDA;
   }
+  if (out->kernel_stats && n_kernels > 0) {
+    Timed t(h, PASTA_PH_FINALIZE, h->stream);
+    cudaError_t e = launch_max_kernel(out->kernel_stats, n_kernels, out->totals + PASTA_T_MAX_KERNEL, h->stream);
+    ++h->launches;
+    if (e != cudaSuccess) return PASTA_ECUDA;
+  }
   if (out->kernel_tensor_counts && out->kernel_tensor_footprint && n_kernels > 0) {
     Timed t(h, PASTA_PH_FINALIZE, h->stream);
     cudaError_t e = launch_footprint(out->kernel_tensor_counts, n_kernels, h->max_tids, h->d_tid_size, nullptr, 0,
@@ -573,6 +579,67 @@ int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t 
     }
   }
   if (!(out->flags & PASTA_NO_FINALIZE)) {
+    s = finalize_impl(h, page_shift, K, out);
+    if (s) return s;
+  }
+  return PASTA_OK;
+}
+
+int pasta_analyze_rich(pasta_trace* h, const pasta_rich_records* tr, uint64_t n, uint32_t page_shift,
+                       pasta_histograms* out, pasta_rich_outputs* rx) {
+  if (!h || !tr || !out || !rx || !rx->rich_totals) return PASTA_EINVAL;
+  if (!out->page_counts || !out->alloc_counts || !out->totals) return PASTA_EINVAL;
+  if (out->kernel_page_bitmap || out->hotness || out->tensor_counts || out->kernel_tensor_counts ||
+      out->kernel_tensor_footprint)
+    return PASTA_EINVAL;
+  if (out->kernel_stats && !out->kernel_alloc_counts) return PASTA_EINVAL;
+  if (tr->grid_lo > tr->grid_hi) return PASTA_EINVAL;
+  if (n > 0 && (!tr->records || (reinterpret_cast<uintptr_t>(tr->records) & 15u))) return PASTA_EINVAL;
+  int s = check_window(h, page_shift);
+  if (s) return s;
+  DeviceGuard g(h->device);
+  s = upload_table(h);
+  if (s) return s;
+  const uint64_t P = (h->va_hi - h->va_lo) >> page_shift;
+  (void)P;
+  RichArgs a{};
+  a.grid_lo = tr->grid_lo;
+  a.grid_last = tr->grid_hi - tr->grid_lo;
+  const uint64_t n_rows = (uint64_t)a.grid_last + 1;
+  a.bounds = h->d_bounds;
+  a.ids = h->d_ids;
+  a.A = h->A_dev;
+  a.va_lo = h->va_lo;
+  a.va_hi = h->va_hi;
+  a.page_shift = page_shift;
+  a.max_ids = h->max_ids;
+  a.page_counts = out->page_counts;
+  a.page_writes = rx->page_write_counts;
+  a.alloc_counts = out->alloc_counts;
+  a.alloc_writes = rx->alloc_write_counts;
+  a.alloc_bytes = rx->alloc_bytes;
+  a.totals = out->totals;
+  a.rich_totals = rx->rich_totals;
+  a.kac = out->kernel_alloc_counts;
+  a.kstats = out->kernel_stats;
+  if (n_rows > 0xFFFFFFFFull && a.kac) return PASTA_EINVAL;  // 2^32 kernel rows
+  const uint64_t per_launch_max = (uint64_t)h->sm_count * (1ull << 30);
+  const uint64_t* rec = reinterpret_cast<const uint64_t*>(tr->records);
+  for (uint64_t off = 0; off < n; off += per_launch_max) {
+    const uint64_t cnt = std::min<uint64_t>(per_launch_max, n - off);
+    RichArgs b = a;
+    b.rec = rec + 2 * off;
+    b.n = cnt;
+    const uint64_t slices = (cnt + rich_slice_records() - 1) / rich_slice_records();
+    const uint64_t wpc = (uint64_t)scan_warps();
+    const int grid = (int)std::min<uint64_t>((uint64_t)h->sm_count, (slices + wpc - 1) / wpc);
+    Timed t(h, PASTA_PH_SCAN, h->stream);
+    cudaError_t e = launch_rich(b, grid, h->stream);
+    ++h->launches;
+    if (e != cudaSuccess) return PASTA_ECUDA;
+  }
+  if (!(out->flags & PASTA_NO_FINALIZE)) {
+    const uint32_t K = out->kernel_alloc_counts ? (uint32_t)n_rows : 1;
     s = finalize_impl(h, page_shift, K, out);
     if (s) return s;
   }

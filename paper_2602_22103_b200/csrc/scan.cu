@@ -955,6 +955,307 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------------------------
+// Rich 16-byte records (NEXT f4; R21-R24). Same per-warp TMA pipeline over
+// 2 KiB slices (128 records; lane l reads records l, l+32, l+64, l+96 with LDS.128).
+// A record is dropped (and counted) if its grid id is outside the window or it is a
+// shared-space access; the rest are attributed like 8-byte records of kernel row
+// grid_id - grid_lo, with write counts and byte weights. Per slice, a leader loop takes
+// one grid id at a time (usually one, two where concurrent kernels interleave); the
+// group's records inside A = interval of its first record or B = of its last are
+// counted with six warp reductions into warp-uniform run accumulators (page run:
+// count, writes; owner run: count, writes, bytes), the others go straight to L2.
+// ------------------------------------------------------------------------------------
+constexpr int kRSlice = 128;
+
+struct RichOut {
+  uint64_t* page_counts;
+  uint64_t* page_writes;
+  uint64_t* alloc_counts;
+  uint64_t* alloc_writes;
+  uint64_t* alloc_bytes;
+  uint64_t* totals;
+  uint64_t* kac;
+  uint64_t* kstats;
+  const uint32_t* ids;
+  uint64_t max_ids;
+  uint32_t A;
+};
+
+__device__ __forceinline__ void rich_page(const RichOut& o, uint32_t page, uint64_t c, uint64_t w) {
+  if (c == 0) return;
+  if (page == kOOW) {
+    red_add_u64(o.totals + 2, c);
+  } else {
+    red_add_u64(o.page_counts + page, c);
+    if (w && o.page_writes) red_add_u64(o.page_writes + page, w);
+  }
+}
+
+template <bool kRows>
+__device__ __forceinline__ void rich_owner(const RichOut& o, uint32_t own, uint64_t c, uint64_t w, uint64_t b,
+                                           uint32_t k) {
+  if (c == 0) return;
+  if (own < o.A) {
+    const uint32_t id = __ldg(o.ids + own);
+    red_add_u64(o.alloc_counts + id, c);
+    if (w && o.alloc_writes) red_add_u64(o.alloc_writes + id, w);
+    if (o.alloc_bytes) red_add_u64(o.alloc_bytes + id, b);
+    if (kRows) {
+      red_add_u64(o.kac + (uint64_t)k * o.max_ids + id, c);
+      if (o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 0, c);
+    }
+  } else {
+    red_add_u64(o.totals + 1, c);
+    if (kRows && o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 1, c);
+  }
+}
+
+struct RichAcc {  // warp-uniform run accumulators
+  uint32_t page, pcnt, pw;
+  uint32_t own, ocnt, ow;
+  uint64_t ob;
+};
+
+template <bool kRows>
+__device__ __forceinline__ void rich_flush(RichAcc& r, const RichOut& o, uint32_t k, uint32_t lane) {
+  if (lane == 0) {
+    rich_page(o, r.page, r.pcnt, r.pw);
+    rich_owner<kRows>(o, r.own, r.ocnt, r.ow, r.ob, k);
+  }
+  r.pcnt = r.pw = r.ocnt = r.ow = 0;
+  r.ob = 0;
+}
+
+template <bool kRows>
+__device__ __forceinline__ void rich_add(RichAcc& r, const RichOut& o, const Ival& I, uint32_t c, uint32_t w,
+                                         uint32_t b, uint32_t k, uint32_t lane) {
+  if (I.page != r.page) {
+    if (lane == 0) rich_page(o, r.page, r.pcnt, r.pw);
+    r.page = I.page;
+    r.pcnt = r.pw = 0;
+  }
+  r.pcnt += c;
+  r.pw += w;
+  if (I.own != r.own) {
+    if (lane == 0) rich_owner<kRows>(o, r.own, r.ocnt, r.ow, r.ob, k);
+    r.own = I.own;
+    r.ocnt = r.ow = 0;
+    r.ob = 0;
+  }
+  r.ocnt += c;
+  r.ow += w;
+  r.ob += b;
+}
+
+template <bool kBig, bool kRows>
+__global__ void __launch_bounds__(kThreads, 1) rich_kernel(const RichArgs args, const int stages) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages));
+  uint64_t* sB = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages) + kBarBytes + kLaBytes + kPfBytes);
+  const uint32_t A = args.A;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nsl = (args.n + kRSlice - 1) / kRSlice;
+  const uint32_t gwarp = blockIdx.x * kWarps + warp;
+  const uint32_t nwarp = gridDim.x * kWarps;
+  const uint64_t s0 = (uint64_t)gwarp * nsl / nwarp, s1 = (uint64_t)(gwarp + 1) * nsl / nwarp;
+  const uint32_t nmy = (uint32_t)(s1 - s0);
+  const uint32_t tail_valid = (uint32_t)(args.n - (nsl - 1) * kRSlice);
+  const uint32_t ring_u32 = smem_u32(smem) + (uint32_t)(warp * stages) * kSliceBytes;
+  const uint32_t bar_u32 = smem_u32(bars + warp * kMaxStages);
+  if (lane == 0) {
+    for (int j = 0; j < stages; ++j) mbar_init(bars + warp * kMaxStages + j, 1);
+    fence_mbar_init();
+  }
+  if (!kBig)
+    for (uint32_t i = threadIdx.x; i < 2 * A; i += kThreads) sB[i] = args.bounds[i];
+  __syncthreads();
+  const uint64_t pol = l2_evict_first_policy();
+  auto slice_valid = [&](uint32_t j) -> uint32_t { return s0 + j == nsl - 1 ? tail_valid : (uint32_t)kRSlice; };
+  auto issue = [&](uint32_t j, uint32_t slot) {
+    const uint32_t bytes = slice_valid(j) * 16u;
+    mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, bytes);
+    tma_load_1d_u32(ring_u32 + slot * kSliceBytes, args.rec + 2 * (s0 + j) * kRSlice, bytes, bar_u32 + 8u * slot,
+                    pol);
+  };
+  if (lane == 0)
+    for (uint32_t j = 0; j < (uint32_t)stages && j < nmy; ++j) issue(j, j);
+
+  Ctx c;
+  c.va_lo = args.va_lo;
+  c.va_hi = args.va_hi;
+  c.wbytes = args.va_hi - args.va_lo;
+  c.s = args.page_shift;
+  c.A = A;
+  c.B = kBig ? args.bounds : sB;
+  RichOut o;
+  o.page_counts = args.page_counts;
+  o.page_writes = args.page_writes;
+  o.alloc_counts = args.alloc_counts;
+  o.alloc_writes = args.alloc_writes;
+  o.alloc_bytes = args.alloc_bytes;
+  o.totals = args.totals;
+  o.kac = args.kac;
+  o.kstats = args.kstats;
+  o.ids = args.ids;
+  o.max_ids = args.max_ids;
+  o.A = A;
+  OwnCache oc;
+  oc.olo = 1;
+  oc.ospan = 0;
+  oc.own = A;
+  Ival cur = lookup<kBig>(oc, 0ull, c);
+  RichAcc r;
+  r.page = kOOW - 1;
+  r.own = A;
+  r.pcnt = r.pw = r.ocnt = r.ow = 0;
+  r.ob = 0;
+  uint32_t k = 0;
+  // per-lane totals: dropped by the grid window, dropped as shared, analyzed, writes, bytes
+  uint32_t n_filt = 0, n_shared = 0, n_an = 0, n_wr = 0;
+  uint64_t n_bytes = 0;
+
+  uint32_t slot = 0, phase = 0;
+  for (uint32_t j = 0; j < nmy; ++j) {
+    const uint32_t sa = ring_u32 + slot * kSliceBytes;
+    mbar_wait_u32(bar_u32 + 8u * slot, phase);
+    const uint32_t valid = slice_valid(j);
+    uint64_t a[4], m[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const ulonglong2 v = lds128(sa + 16u * (32u * i + lane));
+      a[i] = v.x;
+      m[i] = v.y;
+    }
+    __syncwarp();
+    if (lane == 0 && j + stages < nmy) issue(j + stages, slot);
+    if (++slot == (uint32_t)stages) {
+      slot = 0;
+      phase ^= 1u;
+    }
+    uint32_t pend = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (32u * i + lane < valid) {
+        const uint32_t g = (uint32_t)m[i];
+        const bool inwin = g - args.grid_lo <= args.grid_last;
+        const bool shared = (m[i] >> 49) & 1u;
+        n_filt += inwin ? 0u : 1u;
+        n_shared += (inwin && shared) ? 1u : 0u;
+        if (inwin && !shared) {
+          pend |= 1u << i;
+          ++n_an;
+          n_wr += (uint32_t)(m[i] >> 48) & 1u;
+          n_bytes += (m[i] >> 32) & 0xFFFFu;
+        }
+      }
+    }
+    for (;;) {
+      const unsigned any = __ballot_sync(kFull, pend != 0);
+      if (any == 0) break;
+      const int leader = __ffs(any) - 1;
+      const int li = pend ? __ffs(pend) - 1 : 0;
+      uint64_t al = a[0], ml = m[0];
+#pragma unroll
+      for (int i = 1; i < 4; ++i) {
+        al = (li == i) ? a[i] : al;
+        ml = (li == i) ? m[i] : ml;
+      }
+      const uint32_t g = (uint32_t)__shfl_sync(kFull, ml, leader);
+      const uint64_t a0 = __shfl_sync(kFull, al, leader);
+      uint32_t sel = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (((pend >> i) & 1u) && (uint32_t)m[i] == g) sel |= 1u << i;
+      // the group's last record (highest slice position)
+      const uint32_t mypos = sel ? 32u * (31u - __clz(sel)) + lane + 1u : 0u;
+      const uint32_t last = __reduce_max_sync(kFull, mypos) - 1u;
+      uint64_t bl = a[0];
+#pragma unroll
+      for (int i = 1; i < 4; ++i) bl = (last >> 5) == (uint32_t)i ? a[i] : bl;
+      const uint64_t b0 = __shfl_sync(kFull, bl, last & 31u);
+      const uint32_t kg = g - args.grid_lo;
+      if (kRows && kg != k) {
+        rich_flush<kRows>(r, o, k, lane);
+        k = kg;
+      }
+      Ival IA = cur;
+      if (!inside(a0, IA)) IA = lookup<kBig>(oc, a0, c);
+      Ival IB = IA;
+      if (!inside(b0, IA)) IB = lookup<kBig>(oc, b0, c);
+      cur = IB;
+      uint32_t cA = 0, wA = 0, bA = 0, cB = 0, wB = 0, bB = 0, rest = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if ((sel >> i) & 1u) {
+          const uint32_t w = (uint32_t)(m[i] >> 48) & 1u, sz = (uint32_t)(m[i] >> 32) & 0xFFFFu;
+          if (inside(a[i], IA)) {
+            ++cA;
+            wA += w;
+            bA += sz;
+          } else if (inside(a[i], IB)) {
+            ++cB;
+            wB += w;
+            bB += sz;
+          } else {
+            rest |= 1u << i;
+          }
+        }
+      }
+      cA = __reduce_add_sync(kFull, cA);
+      wA = __reduce_add_sync(kFull, wA);
+      bA = __reduce_add_sync(kFull, bA);
+      cB = __reduce_add_sync(kFull, cB);
+      wB = __reduce_add_sync(kFull, wB);
+      bB = __reduce_add_sync(kFull, bB);
+      if (cA) rich_add<kRows>(r, o, IA, cA, wA, bA, kg, lane);
+      if (cB) rich_add<kRows>(r, o, IB, cB, wB, bB, kg, lane);
+      // records outside A and B: looked up one by one, straight to L2
+#pragma unroll 1
+      while (rest) {
+        const int i = __ffs(rest) - 1;
+        rest &= rest - 1;
+        uint64_t x = a[0], mm = m[0];
+#pragma unroll
+        for (int q = 1; q < 4; ++q) {
+          x = (i == q) ? a[q] : x;
+          mm = (i == q) ? m[q] : mm;
+        }
+        const Ival I = lookup<kBig>(oc, x, c);
+        const uint64_t w = (mm >> 48) & 1u;
+        rich_page(o, I.page, 1, w);
+        rich_owner<kRows>(o, I.own, 1, w, (mm >> 32) & 0xFFFFu, kg);
+      }
+      pend &= ~sel;
+    }
+  }
+  rich_flush<kRows>(r, o, k, lane);
+  // per-warp totals
+  const uint32_t f = __reduce_add_sync(kFull, n_filt), sh = __reduce_add_sync(kFull, n_shared);
+  const uint32_t an = __reduce_add_sync(kFull, n_an), wr = __reduce_add_sync(kFull, n_wr);
+  const uint64_t by = warp_sum_u64(n_bytes);
+  if (lane == 0) {
+    if (f) red_add_u64(args.rich_totals + 0, f);
+    if (sh) red_add_u64(args.rich_totals + 1, sh);
+    if (wr) red_add_u64(args.rich_totals + 2, wr);
+    if (by) red_add_u64(args.rich_totals + 3, by);
+    if (an) red_add_u64(args.totals + 0, an);
+  }
+}
+
+template <bool kBig, bool kRows>
+cudaError_t launch_rich_variant(const RichArgs& a, int grid, cudaStream_t st) {
+  const int stages = stages_for(a.A, kBig);
+  const int smem = scan_smem_bytes(a.A, kBig);
+  auto fn = rich_kernel<kBig, kRows>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  fn<<<grid, kThreads, smem, st>>>(a, stages);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 int scan_warps() { return kWarps; }
@@ -1025,6 +1326,15 @@ cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st, int* launc
     default: return launch_variant<false, true, 3>(a, grid, st);
   }
 }
+
+cudaError_t launch_rich(const RichArgs& a, int grid, cudaStream_t st) {
+  const bool big = !scan_table_fits_smem(a.A);
+  const bool rows = a.kac != nullptr;
+  if (big) return rows ? launch_rich_variant<true, true>(a, grid, st) : launch_rich_variant<true, false>(a, grid, st);
+  return rows ? launch_rich_variant<false, true>(a, grid, st) : launch_rich_variant<false, false>(a, grid, st);
+}
+
+int rich_slice_records() { return kRSlice; }
 
 cudaError_t launch_scan_extras(const ExtraArgs& a, cudaStream_t st) {
   scan_extras_kernel<<<1, 32, 0, st>>>(a);

@@ -83,6 +83,7 @@ def run_oracle(o, records_np, page_shift, kernel_offsets=None, kernel_rows=False
         out["kun"] = o.kun.copy()
         fp, ws = o.footprints()
         out["footprint"], out["ws"] = fp, ws
+        out["max_kernel"] = o.max_kernel()
     if kernel_pages:
         out["kpb"] = o.kernel_pages.copy()
         out["kup"] = o.kernel_unique_pages()
@@ -109,6 +110,7 @@ def assert_parity(g, r, kernel_rows=False, kernel_pages=False, label=""):
         assert np.array_equal(ks[:, 1], r["kun"]), f"{label}: kstats unattributed"
         assert np.array_equal(ks[:, 2], r["footprint"]), f"{label}: footprint"
         assert int(g["totals"][4]) == r["ws"], f"{label}: ws_obj"
+        assert int(g["totals"][7]) == r["max_kernel"], f"{label}: max_mem_referenced_kernel"
     if kernel_pages:
         assert np.array_equal(g["kpb"], r["kpb"]), f"{label}: kernel_page_bitmap"
         assert np.array_equal(g["kstats"][:, 3], r["kup"]), f"{label}: kernel unique pages"
