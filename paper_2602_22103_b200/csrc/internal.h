@@ -66,6 +66,7 @@ struct RichArgs {
 };
 cudaError_t launch_rich(const RichArgs& a, int grid, cudaStream_t st);
 int rich_slice_records();
+int rich_warps();
 
 // MAX_MEM_REFERENCED_KERNEL (R24): *out = argmax_k kstats[4k] + kstats[4k+1], ties low.
 cudaError_t launch_max_kernel(const uint64_t* kstats, uint32_t n_kernels, uint64_t* out, cudaStream_t st);

@@ -631,7 +631,7 @@ int pasta_analyze_rich(pasta_trace* h, const pasta_rich_records* tr, uint64_t n,
     b.rec = rec + 2 * off;
     b.n = cnt;
     const uint64_t slices = (cnt + rich_slice_records() - 1) / rich_slice_records();
-    const uint64_t wpc = (uint64_t)scan_warps();
+    const uint64_t wpc = (uint64_t)rich_warps();
     const int grid = (int)std::min<uint64_t>((uint64_t)h->sm_count, (slices + wpc - 1) / wpc);
     Timed t(h, PASTA_PH_SCAN, h->stream);
     cudaError_t e = launch_rich(b, grid, h->stream);

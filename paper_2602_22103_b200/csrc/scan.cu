@@ -968,6 +968,18 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
 // count, writes; owner run: count, writes, bytes), the others go straight to L2.
 // ------------------------------------------------------------------------------------
 constexpr int kRSlice = 128;
+#ifndef PASTA_RICH_WARPS
+#define PASTA_RICH_WARPS 24  // warps per CTA of the rich scan (A/B: 12-24 warps, more is faster)
+#endif
+constexpr int kRWarps = PASTA_RICH_WARPS;
+constexpr int kRThreads = kRWarps * 32;
+constexpr int kRBarBytes = kRWarps * kMaxStages * 8;
+__host__ __device__ constexpr int rich_ring_bytes(int stages) { return kRWarps * stages * (int)kSliceBytes; }
+int rich_stages(uint32_t A, bool big) {
+  const long table = big ? 0 : 16l * A;
+  long st = ((long)kSmemLimit - kRBarBytes - table) / rich_ring_bytes(1);
+  return (int)(st > kMaxStages ? kMaxStages : st);
+}
 
 struct RichOut {
   uint64_t* page_counts;
@@ -1012,9 +1024,50 @@ __device__ __forceinline__ void rich_owner(const RichOut& o, uint32_t own, uint6
   }
 }
 
+// Owner run whose kernel-row share (kc of its c records, kernel k) differs from c:
+// the alloc statistics take all c records, the kernel row only kc.
+template <bool kRows>
+__device__ __forceinline__ void rich_owner_split(const RichOut& o, uint32_t own, uint64_t c, uint64_t w, uint64_t b,
+                                                 uint64_t kc, uint32_t k) {
+  if (c == 0) return;
+  if (own < o.A) {
+    const uint32_t id = __ldg(o.ids + own);
+    red_add_u64(o.alloc_counts + id, c);
+    if (w && o.alloc_writes) red_add_u64(o.alloc_writes + id, w);
+    if (o.alloc_bytes) red_add_u64(o.alloc_bytes + id, b);
+    if (kRows && kc) {
+      red_add_u64(o.kac + (uint64_t)k * o.max_ids + id, kc);
+      if (o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 0, kc);
+    }
+  } else {
+    red_add_u64(o.totals + 1, c);
+    if (kRows && kc && o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 1, kc);
+  }
+}
+
+// c records' kernel-row count only (their alloc statistics went with a run).
+__device__ __forceinline__ void rich_rows(const RichOut& o, uint32_t own, uint64_t c, uint32_t k) {
+  if (own < o.A) {
+    red_add_u64(o.kac + (uint64_t)k * o.max_ids + __ldg(o.ids + own), c);
+    if (o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 0, c);
+  } else if (o.kstats) {
+    red_add_u64(o.kstats + (uint64_t)k * 4 + 1, c);
+  }
+}
+
+// One record's kernel-row count only (its alloc statistics went with a run).
+__device__ __forceinline__ void rich_row_one(const RichOut& o, uint32_t own, uint32_t k) {
+  if (own < o.A) {
+    red_add_u64(o.kac + (uint64_t)k * o.max_ids + __ldg(o.ids + own), 1);
+    if (o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 0, 1);
+  } else if (o.kstats) {
+    red_add_u64(o.kstats + (uint64_t)k * 4 + 1, 1);
+  }
+}
+
 struct RichAcc {  // warp-uniform run accumulators
   uint32_t page, pcnt, pw;
-  uint32_t own, ocnt, ow;
+  uint32_t own, ocnt, ow, okc;  // okc: records of the run counted in kernel row k
   uint64_t ob;
 };
 
@@ -1022,15 +1075,15 @@ template <bool kRows>
 __device__ __forceinline__ void rich_flush(RichAcc& r, const RichOut& o, uint32_t k, uint32_t lane) {
   if (lane == 0) {
     rich_page(o, r.page, r.pcnt, r.pw);
-    rich_owner<kRows>(o, r.own, r.ocnt, r.ow, r.ob, k);
+    rich_owner_split<kRows>(o, r.own, r.ocnt, r.ow, r.ob, r.okc, k);
   }
-  r.pcnt = r.pw = r.ocnt = r.ow = 0;
+  r.pcnt = r.pw = r.ocnt = r.ow = r.okc = 0;
   r.ob = 0;
 }
 
 template <bool kRows>
 __device__ __forceinline__ void rich_add(RichAcc& r, const RichOut& o, const Ival& I, uint32_t c, uint32_t w,
-                                         uint32_t b, uint32_t k, uint32_t lane) {
+                                         uint32_t b, uint32_t kc, uint32_t k, uint32_t lane) {
   if (I.page != r.page) {
     if (lane == 0) rich_page(o, r.page, r.pcnt, r.pw);
     r.page = I.page;
@@ -1039,27 +1092,28 @@ __device__ __forceinline__ void rich_add(RichAcc& r, const RichOut& o, const Iva
   r.pcnt += c;
   r.pw += w;
   if (I.own != r.own) {
-    if (lane == 0) rich_owner<kRows>(o, r.own, r.ocnt, r.ow, r.ob, k);
+    if (lane == 0) rich_owner_split<kRows>(o, r.own, r.ocnt, r.ow, r.ob, r.okc, k);
     r.own = I.own;
-    r.ocnt = r.ow = 0;
+    r.ocnt = r.ow = r.okc = 0;
     r.ob = 0;
   }
   r.ocnt += c;
   r.ow += w;
   r.ob += b;
+  r.okc += kc;
 }
 
 template <bool kBig, bool kRows>
-__global__ void __launch_bounds__(kThreads, 1) rich_kernel(const RichArgs args, const int stages) {
+__global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args, const int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages));
-  uint64_t* sB = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages) + kBarBytes + kLaBytes + kPfBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + rich_ring_bytes(stages));
+  uint64_t* sB = reinterpret_cast<uint64_t*>(smem + rich_ring_bytes(stages) + kRBarBytes);
   const uint32_t A = args.A;
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nsl = (args.n + kRSlice - 1) / kRSlice;
-  const uint32_t gwarp = blockIdx.x * kWarps + warp;
-  const uint32_t nwarp = gridDim.x * kWarps;
+  const uint32_t gwarp = blockIdx.x * kRWarps + warp;
+  const uint32_t nwarp = gridDim.x * kRWarps;
   const uint64_t s0 = (uint64_t)gwarp * nsl / nwarp, s1 = (uint64_t)(gwarp + 1) * nsl / nwarp;
   const uint32_t nmy = (uint32_t)(s1 - s0);
   const uint32_t tail_valid = (uint32_t)(args.n - (nsl - 1) * kRSlice);
@@ -1070,7 +1124,7 @@ __global__ void __launch_bounds__(kThreads, 1) rich_kernel(const RichArgs args, 
     fence_mbar_init();
   }
   if (!kBig)
-    for (uint32_t i = threadIdx.x; i < 2 * A; i += kThreads) sB[i] = args.bounds[i];
+    for (uint32_t i = threadIdx.x; i < 2 * A; i += kRThreads) sB[i] = args.bounds[i];
   __syncthreads();
   const uint64_t pol = l2_evict_first_policy();
   auto slice_valid = [&](uint32_t j) -> uint32_t { return s0 + j == nsl - 1 ? tail_valid : (uint32_t)kRSlice; };
@@ -1110,12 +1164,14 @@ __global__ void __launch_bounds__(kThreads, 1) rich_kernel(const RichArgs args, 
   RichAcc r;
   r.page = kOOW - 1;
   r.own = A;
-  r.pcnt = r.pw = r.ocnt = r.ow = 0;
+  r.pcnt = r.pw = r.ocnt = r.ow = r.okc = 0;
   r.ob = 0;
   uint32_t k = 0;
   // per-lane totals: dropped by the grid window, dropped as shared, analyzed, writes, bytes
   uint32_t n_filt = 0, n_shared = 0, n_an = 0, n_wr = 0;
   uint64_t n_bytes = 0;
+  uint32_t u_an = 0, u_wr = 0;  // warp-uniform totals of fast-path slices
+  uint64_t u_bytes = 0;
 
   uint32_t slot = 0, phase = 0;
   for (uint32_t j = 0; j < nmy; ++j) {
@@ -1134,6 +1190,141 @@ __global__ void __launch_bounds__(kThreads, 1) rich_kernel(const RichArgs args, 
     if (++slot == (uint32_t)stages) {
       slot = 0;
       phase ^= 1u;
+    }
+    // Fast path (lane 0's first record analyzed): every analyzed record of the slice is
+    // classified against A = interval of the slice's first record and B = of its last;
+    // counts / writes / bytes per interval are packed into one u32 (count <= 128: bits
+    // 0-7, writes: bits 8-15, bytes <= 128 * 128: bits 16-30) and reduced warp-wide.
+    // Records of another kernel than lane 0's (concurrent kernels) share the page and
+    // alloc statistics of their interval and send their kernel-row count themselves;
+    // records outside A and B go straight to L2.
+    {
+      const uint64_t m0 = __shfl_sync(kFull, m[0], 0);
+      const uint32_t g = (uint32_t)m0;
+      const uint32_t kg = g - args.grid_lo;
+      if (kg <= args.grid_last && !((m0 >> 49) & 1u)) {
+        uint32_t an = 0, minor = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t gi = (uint32_t)m[i];
+          const bool inwin = gi - args.grid_lo <= args.grid_last;
+          const bool shared = (m[i] >> 49) & 1u;
+          const bool ok = 32u * i + lane < valid;
+          n_filt += (ok && !inwin) ? 1u : 0u;
+          n_shared += (ok && inwin && shared) ? 1u : 0u;
+          if (ok && inwin && !shared) {
+            an |= 1u << i;
+            if (gi != g) minor |= 1u << i;
+          }
+        }
+        if (kRows && kg != k) {
+          rich_flush<kRows>(r, o, k, lane);
+          k = kg;
+        }
+        const uint64_t a0 = __shfl_sync(kFull, a[0], 0);
+        const uint32_t lastpos = valid - 1u;
+        uint64_t bl = a[0];
+#pragma unroll
+        for (int i = 1; i < 4; ++i) bl = (lastpos >> 5) == (uint32_t)i ? a[i] : bl;
+        const uint64_t b0 = __shfl_sync(kFull, bl, lastpos & 31u);
+        Ival IA = cur;
+        if (!inside(a0, IA)) IA = lookup<kBig>(oc, a0, c);
+        Ival IB = IA;
+        if (!inside(b0, IA)) IB = lookup<kBig>(oc, b0, c);
+        cur = IB;
+        uint32_t pA = 0, pT = 0, pR = 0, rest = 0, mAB = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if ((an >> i) & 1u) {
+            const uint32_t v = 1u | ((uint32_t)(m[i] >> 40) & 0x100u) | (((uint32_t)(m[i] >> 32) & 0xFFFFu) << 16);
+            pT += v;
+            if (inside(a[i], IA)) {
+              pA += v;
+              mAB += (minor >> i) & 1u;
+            } else if (inside(a[i], IB)) {
+              mAB += ((minor >> i) & 1u) << 8;
+            } else {
+              rest |= 1u << i;
+              pR += v;
+            }
+          }
+        }
+        const bool any_rest = __any_sync(kFull, rest != 0);
+        const bool any_minor = kRows && __any_sync(kFull, minor != 0);
+        pA = __reduce_add_sync(kFull, pA);
+        pT = __reduce_add_sync(kFull, pT);
+        if (any_rest) pR = __reduce_add_sync(kFull, pR);
+        else pR = 0;
+        uint32_t mSum = 0;
+        if (any_minor) mSum = __reduce_add_sync(kFull, mAB);
+        const uint32_t pB = pT - pA - pR;
+        if (pA & 0xFFu)
+          rich_add<kRows>(r, o, IA, pA & 0xFFu, (pA >> 8) & 0xFFu, pA >> 16, (pA & 0xFFu) - (mSum & 0xFFu), kg, lane);
+        if (pB & 0xFFu)
+          rich_add<kRows>(r, o, IB, pB & 0xFFu, (pB >> 8) & 0xFFu, pB >> 16, (pB & 0xFFu) - ((mSum >> 8) & 0xFFu), kg,
+                          lane);
+        if (any_minor) {
+          // kernel rows of the other kernels' records in A or B: those of the first
+          // minority kernel k2 are reduced per interval, any others go one by one
+          uint32_t mm = minor & ~rest;
+          const unsigned mb = __ballot_sync(kFull, mm != 0);
+          if (mb) {
+            uint64_t ml = m[0];
+#pragma unroll
+            for (int i = 1; i < 4; ++i) ml = (mm && __ffs(mm) - 1 == i) ? m[i] : ml;
+            const uint32_t g2 = (uint32_t)__shfl_sync(kFull, ml, __ffs(mb) - 1);
+            uint32_t c2 = 0, sel2 = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (((mm >> i) & 1u) && (uint32_t)m[i] == g2) {
+                sel2 |= 1u << i;
+                c2 += inside(a[i], IA) ? 1u : 0x100u;
+              }
+            }
+            c2 = __reduce_add_sync(kFull, c2);
+            if (lane == 0) {
+              const uint32_t k2 = g2 - args.grid_lo;
+              if (c2 & 0xFFu) rich_rows(o, IA.own, c2 & 0xFFu, k2);
+              if (c2 >> 8) rich_rows(o, IB.own, c2 >> 8, k2);
+            }
+            mm &= ~sel2;
+          }
+#pragma unroll 1
+          while (mm) {
+            const int i = __ffs(mm) - 1;
+            mm &= mm - 1;
+            uint64_t x = a[0], mi = m[0];
+#pragma unroll
+            for (int q = 1; q < 4; ++q) {
+              x = (i == q) ? a[q] : x;
+              mi = (i == q) ? m[q] : mi;
+            }
+            rich_row_one(o, inside(x, IA) ? IA.own : IB.own, (uint32_t)mi - args.grid_lo);
+          }
+        }
+        if (any_rest) {
+#pragma unroll 1
+          while (rest) {
+            const int i = __ffs(rest) - 1;
+            rest &= rest - 1;
+            uint64_t x = a[0], mm = m[0];
+#pragma unroll
+            for (int q = 1; q < 4; ++q) {
+              x = (i == q) ? a[q] : x;
+              mm = (i == q) ? m[q] : mm;
+            }
+            const Ival I = lookup<kBig>(oc, x, c);
+            const uint64_t w = (mm >> 48) & 1u;
+            rich_page(o, I.page, 1, w);
+            rich_owner<kRows>(o, I.own, 1, w, (mm >> 32) & 0xFFFFu, (uint32_t)mm - args.grid_lo);
+          }
+        }
+        // warp totals (uniform values; lane 0's copy is flushed at the end)
+        u_an += pT & 0xFFu;
+        u_wr += (pT >> 8) & 0xFFu;
+        u_bytes += pT >> 16;
+        continue;
+      }
     }
     uint32_t pend = 0;
 #pragma unroll
@@ -1210,8 +1401,8 @@ __global__ void __launch_bounds__(kThreads, 1) rich_kernel(const RichArgs args, 
       cB = __reduce_add_sync(kFull, cB);
       wB = __reduce_add_sync(kFull, wB);
       bB = __reduce_add_sync(kFull, bB);
-      if (cA) rich_add<kRows>(r, o, IA, cA, wA, bA, kg, lane);
-      if (cB) rich_add<kRows>(r, o, IB, cB, wB, bB, kg, lane);
+      if (cA) rich_add<kRows>(r, o, IA, cA, wA, bA, cA, kg, lane);
+      if (cB) rich_add<kRows>(r, o, IB, cB, wB, bB, cB, kg, lane);
       // records outside A and B: looked up one by one, straight to L2
 #pragma unroll 1
       while (rest) {
@@ -1239,20 +1430,20 @@ __global__ void __launch_bounds__(kThreads, 1) rich_kernel(const RichArgs args, 
   if (lane == 0) {
     if (f) red_add_u64(args.rich_totals + 0, f);
     if (sh) red_add_u64(args.rich_totals + 1, sh);
-    if (wr) red_add_u64(args.rich_totals + 2, wr);
-    if (by) red_add_u64(args.rich_totals + 3, by);
-    if (an) red_add_u64(args.totals + 0, an);
+    if (wr + u_wr) red_add_u64(args.rich_totals + 2, (uint64_t)wr + u_wr);
+    if (by + u_bytes) red_add_u64(args.rich_totals + 3, by + u_bytes);
+    if (an + u_an) red_add_u64(args.totals + 0, (uint64_t)an + u_an);
   }
 }
 
 template <bool kBig, bool kRows>
 cudaError_t launch_rich_variant(const RichArgs& a, int grid, cudaStream_t st) {
-  const int stages = stages_for(a.A, kBig);
-  const int smem = scan_smem_bytes(a.A, kBig);
+  const int stages = rich_stages(a.A, kBig);
+  const int smem = rich_ring_bytes(stages) + kRBarBytes + (kBig ? 0 : (int)(16ull * a.A));
   auto fn = rich_kernel<kBig, kRows>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  fn<<<grid, kThreads, smem, st>>>(a, stages);
+  fn<<<grid, kRThreads, smem, st>>>(a, stages);
   return cudaGetLastError();
 }
 
@@ -1335,6 +1526,7 @@ cudaError_t launch_rich(const RichArgs& a, int grid, cudaStream_t st) {
 }
 
 int rich_slice_records() { return kRSlice; }
+int rich_warps() { return kRWarps; }
 
 cudaError_t launch_scan_extras(const ExtraArgs& a, cudaStream_t st) {
   scan_extras_kernel<<<1, 32, 0, st>>>(a);

@@ -5,9 +5,11 @@ u32 grid_id, u16 size_bytes, u8 flags (bit 0 is_write, bit 1 shared space), u8 z
 Input infrastructure only (no analysis arithmetic). Record j of kernel segment k gets,
 from h = splitmix64(seed + j):
 
-* grid_id = grid_base + k, except with probability ``mix`` (h & 0xFFFF < mix * 2^16)
-  grid_base + k - 1 when k > 0: kernels overlapping in time (concurrent streams), so
-  grid ids are not sorted within a slice;
+* grid_id = grid_base + k, except with probability ``mix`` grid_base + k - 1 when
+  k > 0: kernels overlapping in time (concurrent streams), so grid ids are not sorted
+  within a slice. The draw is made per block of 2^block_log2 records (from
+  hb = splitmix64(seed + (j >> block_log2)): hb & 0xFFFF < mix * 2^16), so 0 mixes
+  single records and 5 mixes warp-sized bursts;
 * size_bytes = 1 << ((h >> 16) & 7) (1 .. 128, S:40);
 * is_write iff ((h >> 24) & 3) == 0 (25 %);
 * shared space iff ((h >> 32) & 127) == 0 (1/128).
@@ -34,7 +36,7 @@ def _splitmix_np(x: np.ndarray) -> np.ndarray:
 
 
 def rich_host(addr: np.ndarray, kernel_offsets, seed: int, grid_base: int = 0, mix: float = 0.05,
-              j0: int = 0) -> np.ndarray:
+              j0: int = 0, block_log2: int = 0) -> np.ndarray:
     """addr: records j0 .. j0 + n - 1; kernel_offsets: global offsets."""
     addr = np.ascontiguousarray(addr, dtype=np.uint64)
     n = addr.size
@@ -43,8 +45,9 @@ def rich_host(addr: np.ndarray, kernel_offsets, seed: int, grid_base: int = 0, m
     j = jj.astype(np.uint64)
     k = np.searchsorted(ko, jj, side="right") - 1
     h = _splitmix_np(j + np.uint64(seed))
+    hb = _splitmix_np((j >> np.uint64(block_log2)) + np.uint64(seed))
     thr = np.uint64(int(mix * 65536))
-    prev = ((h & np.uint64(0xFFFF)) < thr) & (k > 0)
+    prev = ((hb & np.uint64(0xFFFF)) < thr) & (k > 0)
     out = np.zeros(n, dtype=RICH_DTYPE)
     out["addr"] = addr
     out["grid"] = (grid_base + k - prev.astype(np.int64)).astype(np.uint32)
@@ -66,7 +69,15 @@ def _wrap(c: int) -> int:
     return c - (1 << 64) if c >= 1 << 63 else c
 
 
-def rich_device(addr, kernel_offsets, seed: int, grid_base: int = 0, mix: float = 0.05, j0: int = 0):
+def _splitmix_t(x, seed: int):
+    z = x + _wrap((seed + _C1) & ((1 << 64) - 1))
+    z = (z ^ _srl(z, 30)) * _wrap(_C2)
+    z = (z ^ _srl(z, 27)) * _wrap(_C3)
+    return z ^ _srl(z, 31)
+
+
+def rich_device(addr, kernel_offsets, seed: int, grid_base: int = 0, mix: float = 0.05, j0: int = 0,
+                block_log2: int = 0):
     """addr: int64 CUDA tensor; kernel_offsets: int64 CUDA tensor (global offsets);
     records are global indices j0 .. j0 + n - 1. Returns an int64 tensor [n, 2] whose
     bytes are the RICH_DTYPE records."""
@@ -76,12 +87,10 @@ def rich_device(addr, kernel_offsets, seed: int, grid_base: int = 0, mix: float 
     dev = addr.device
     j = torch.arange(j0, j0 + n, dtype=torch.int64, device=dev)
     k = torch.searchsorted(kernel_offsets, j, right=True) - 1
-    z = j + _wrap((seed + _C1) & ((1 << 64) - 1))
-    z = (z ^ _srl(z, 30)) * _wrap(_C2)
-    z = (z ^ _srl(z, 27)) * _wrap(_C3)
-    h = z ^ _srl(z, 31)
+    h = _splitmix_t(j, seed)
+    hb = _splitmix_t(_srl(j, block_log2) if block_log2 else j, seed)
     thr = int(mix * 65536)
-    prev = ((h & 0xFFFF) < thr) & (k > 0)
+    prev = ((hb & 0xFFFF) < thr) & (k > 0)
     grid = grid_base + k - prev.to(torch.int64)
     size = torch.bitwise_left_shift(torch.ones_like(h), _srl(h, 16) & 7)
     wr = (_srl(h, 24) & 3) == 0
