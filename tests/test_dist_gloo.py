@@ -197,3 +197,74 @@ def test_gloo_sharded_topk_flow(world):
     rp, rc, rf = oracle.topk(o.page_counts, K)
     assert [pg for _, pg in cand[:K]] == [int(x) for x in rp[:rf]]
     assert [c for c, _ in cand[:K]] == [int(x) for x in rc[:rf]]
+
+
+def _worker_tensors(rank, world, port, out_q):
+    """Two-level shards (objects = pool chunks, tensors = allocations; NEXT f3): the packed
+    buffer carries the tensor counts after the totals, WS_obj and WS_tensor merge by MAX."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_22103_b200 import dist as pdist
+
+        p = tracegen.build_plan("tiny", seed=13, n=1 << 17)
+        j0, j1, k0, k1 = p.shard(rank, world)
+        o = oracle.OracleTrace(p.va_lo, p.va_hi, len(p.objects), len(p.objects), max_live_tensors=len(p.allocs),
+                               max_tensor_ids=len(p.allocs))
+        for b, s in p.objects:
+            o.register_alloc(b, s)
+        for b, s in p.allocs:
+            o.register_tensor(b, s)
+        ko = [int(x) for x in p.kernel_offsets]
+        o.analyze(tracegen.host_records(p, j0, j1), [x - j0 for x in ko[k0:k1 + 1]], p.page_shift, kernel_rows=True)
+        P, A, T = o.page_counts.size, len(p.objects), len(p.allocs)
+        packed = torch.zeros(P + A + TOTALS + T, dtype=torch.int64)
+        packed[:P] = torch.from_numpy(o.page_counts.view(np.int64))
+        packed[P:P + A] = torch.from_numpy(o.alloc_counts.view(np.int64))
+        tot = np.zeros(TOTALS, dtype=np.uint64)
+        tot[:3] = o.totals
+        tot[5] = o.untensored
+        tot[4] = o.footprints()[1]
+        tot[6] = o.tensor_footprints()[1]
+        packed[P + A:P + A + TOTALS] = torch.from_numpy(tot.view(np.int64))
+        packed[P + A + TOTALS:] = torch.from_numpy(o.tensor_counts.view(np.int64))
+        totals = packed[P + A:P + A + TOTALS]
+        ws = totals[list(pdist._WS_SLOTS)].clone()
+        pdist.merge_counts(packed)
+        pdist.merge_max(ws)
+        totals[list(pdist._WS_SLOTS)] = ws
+        if rank == 0:
+            out_q.put({"packed": packed.numpy().copy()})
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_merge_tensor_level():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_tensors, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    p = tracegen.build_plan("tiny", seed=13, n=1 << 17)
+    o = oracle.OracleTrace(p.va_lo, p.va_hi, len(p.objects), len(p.objects), max_live_tensors=len(p.allocs),
+                           max_tensor_ids=len(p.allocs))
+    for b, s in p.objects:
+        o.register_alloc(b, s)
+    for b, s in p.allocs:
+        o.register_tensor(b, s)
+    o.analyze(tracegen.host_records(p), p.kernel_offsets, p.page_shift, kernel_rows=True)
+    P, A = o.page_counts.size, len(p.objects)
+    packed = res["packed"].view(np.uint64)
+    tot = packed[P + A:P + A + TOTALS]
+    assert np.array_equal(packed[:P], o.page_counts)
+    assert np.array_equal(packed[P:P + A], o.alloc_counts)
+    assert np.array_equal(packed[P + A + TOTALS:], o.tensor_counts)
+    assert tot[:3].tolist() == o.totals.tolist() and int(tot[5]) == o.untensored
+    assert int(tot[4]) == o.footprints()[1] and int(tot[6]) == o.tensor_footprints()[1]
