@@ -38,6 +38,7 @@
 //    at kernel-segment boundaries (per warp, no CTA barrier) and at the end; the
 //    per-kernel page bit is set with atom.or at the page flush.
 #include <cstdint>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
@@ -126,6 +127,15 @@ struct OwnCache {       // last owner interval (range or gap) seen by this lane
 };
 
 __device__ __forceinline__ bool inside(uint64_t a, const Ival& I) { return a - I.lo <= I.span; }
+
+// v[i] for a runtime i, as masks: a select chain on a register array lets the compiler
+// turn it into an indexed local-memory load (and spill the whole array every slice).
+__device__ __forceinline__ uint64_t pick4(const uint64_t (&v)[4], int i) {
+  uint64_t r = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) r |= v[q] & (0ull - (uint64_t)(i == q));
+  return r;
+}
 
 // #{ i < m : B[i] <= a } by bisection.
 template <bool kGlobal>
@@ -1127,7 +1137,9 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
     for (uint32_t i = threadIdx.x; i < 2 * A; i += kRThreads) sB[i] = args.bounds[i];
   __syncthreads();
   const uint64_t pol = l2_evict_first_policy();
-  auto slice_valid = [&](uint32_t j) -> uint32_t { return s0 + j == nsl - 1 ? tail_valid : (uint32_t)kRSlice; };
+  // only the trace's last slice may be partial: the warp that owns it sees it at j = tail_j
+  const uint32_t tail_j = (s1 == nsl && nmy) ? nmy - 1u : 0xFFFFFFFFu;
+  auto slice_valid = [&](uint32_t j) -> uint32_t { return j == tail_j ? tail_valid : (uint32_t)kRSlice; };
   auto issue = [&](uint32_t j, uint32_t slot) {
     const uint32_t bytes = slice_valid(j) * 16u;
     mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, bytes);
@@ -1170,7 +1182,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
   // per-lane totals: dropped by the grid window, dropped as shared, analyzed, writes, bytes
   uint32_t n_filt = 0, n_shared = 0, n_an = 0, n_wr = 0;
   uint64_t n_bytes = 0;
-  uint32_t u_an = 0, u_wr = 0;  // warp-uniform totals of fast-path slices
+  uint32_t u_an = 0, u_wr = 0, u_sh = 0;  // warp-uniform totals of fast-path slices
   uint64_t u_bytes = 0;
 
   uint32_t slot = 0, phase = 0;
@@ -1191,28 +1203,118 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
       slot = 0;
       phase ^= 1u;
     }
-    // Fast path (lane 0's first record analyzed): every analyzed record of the slice is
-    // classified against A = interval of the slice's first record and B = of its last;
-    // counts / writes / bytes per interval are packed into one u32 (count <= 128: bits
-    // 0-7, writes: bits 8-15, bytes <= 128 * 128: bits 16-30) and reduced warp-wide.
-    // Records of another kernel than lane 0's (concurrent kernels) share the page and
-    // alloc statistics of their interval and send their kernel-row count themselves;
-    // records outside A and B go straight to L2.
+    const uint64_t m0 = __shfl_sync(kFull, m[0], 0);
+    const uint32_t g = (uint32_t)m0;
+    const uint32_t kg = g - args.grid_lo;
+    // Tier RC: all 128 records valid, of lane 0's kernel g or (concurrent kernels, with
+    // kernel rows) of one other kernel g2, both inside the grid window; shared-space
+    // records (dropped, R22) may be among them. Per analyzed record h = size_bytes |
+    // is_write << 16 | 1 << 24: a warp sum holds up to 128 * 128 bytes in bits 0-15, 128
+    // writes in bits 16-23 and 128 records in bits 24-31. Two warp reductions (interval
+    // A and all), a third when some record is in neither A nor B = the interval of the
+    // slice's last record, a fourth for g2's kernel-row counts in A (bits 0-7) and B
+    // (bits 8-15). Page and alloc statistics do not depend on the kernel.
+    auto tier_rc = [&](auto two_t, const uint32_t mis, const uint32_t k2) {
+      constexpr bool kTwo = decltype(two_t)::value;
+      if (kRows && kg != k) {
+        rich_flush<kRows>(r, o, k, lane);
+        k = kg;
+      }
+      const uint64_t a0 = __shfl_sync(kFull, a[0], 0);
+      const uint64_t b0 = __shfl_sync(kFull, a[3], 31);
+      Ival IA = cur;
+      if (!inside(a0, IA)) IA = lookup<kBig>(oc, a0, c);
+      Ival IB = IA;
+      if (!inside(b0, IA)) IB = lookup<kBig>(oc, b0, c);
+      cur = IB;
+      uint32_t hA = 0, hT = 0, hR = 0, rest = 0, mAB = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t hi = (uint32_t)(m[i] >> 32);
+        if (!(hi & 0x20000u)) {
+          const uint32_t h = (hi & 0x1FFFFu) + (1u << 24);
+          hT += h;
+          if (inside(a[i], IA)) {
+            hA += h;
+            if (kTwo && kRows) mAB += (mis >> i) & 1u;
+          } else if (!inside(a[i], IB)) {
+            rest |= 1u << i;
+            hR += h;
+          } else if (kTwo && kRows) {
+            mAB += ((mis >> i) & 1u) << 8;
+          }
+        }
+      }
+      const bool any_rest = __any_sync(kFull, rest != 0);
+      hA = __reduce_add_sync(kFull, hA);
+      hT = __reduce_add_sync(kFull, hT);
+      hR = any_rest ? __reduce_add_sync(kFull, hR) : 0u;
+      if (kTwo && kRows) mAB = __reduce_add_sync(kFull, mAB);
+      const uint32_t cA = hA >> 24, cT = hT >> 24, cB = cT - cA - (hR >> 24);
+      const uint32_t bA = hA & 0xFFFFu, wA = (hA >> 16) & 0xFFu;
+      const uint32_t bT = hT & 0xFFFFu, wT = (hT >> 16) & 0xFFu;
+      if (cA) rich_add<kRows>(r, o, IA, cA, wA, bA, cA - (mAB & 0xFFu), kg, lane);
+      if (cB)
+        rich_add<kRows>(r, o, IB, cB, wT - wA - ((hR >> 16) & 0xFFu), bT - bA - (hR & 0xFFFFu), cB - (mAB >> 8),
+                        kg, lane);
+      if (kTwo && kRows && lane == 0) {
+        if (mAB & 0xFFu) rich_rows(o, IA.own, mAB & 0xFFu, k2);
+        if (mAB >> 8) rich_rows(o, IB.own, mAB >> 8, k2);
+      }
+      if (any_rest) {
+#pragma unroll 1
+        while (rest) {
+          const int i = __ffs(rest) - 1;
+          rest &= rest - 1;
+          const uint64_t x = pick4(a, i), mm = pick4(m, i);
+          const Ival I = lookup<kBig>(oc, x, c);
+          const uint64_t w = (mm >> 48) & 1u;
+          rich_page(o, I.page, 1, w);
+          rich_owner<kRows>(o, I.own, 1, w, (mm >> 32) & 0xFFFFu, (uint32_t)mm - args.grid_lo);
+        }
+      }
+      u_an += cT;
+      u_sh += (uint32_t)kRSlice - cT;
+      u_wr += wT;
+      u_bytes += bT;
+    };
+    if (valid == (uint32_t)kRSlice && kg <= args.grid_last) {
+      uint32_t mis = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) mis |= ((uint32_t)m[i] != g ? 1u : 0u) << i;
+      const unsigned mis_lanes = __ballot_sync(kFull, mis != 0);
+      if (mis_lanes == 0) {
+        tier_rc(std::false_type{}, 0u, 0u);
+        continue;
+      }
+      const uint32_t gl = (uint32_t)pick4(m, mis ? __ffs(mis) - 1 : 0);
+      const uint32_t g2 = __shfl_sync(kFull, gl, __ffs(mis_lanes) - 1);
+      uint32_t bad = g2 - args.grid_lo > args.grid_last ? 1u : 0u;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) bad |= (((mis >> i) & 1u) && (uint32_t)m[i] != g2) ? 1u : 0u;
+      if (!__any_sync(kFull, bad != 0)) {
+        tier_rc(std::true_type{}, mis, g2 - args.grid_lo);
+        continue;
+      }
+    }
+    // Fast path (full slice, lane 0's first record analyzed): every analyzed record of
+    // the slice is classified against A = interval of the slice's first record and B =
+    // of its last; counts / writes / bytes per interval are packed into one u32 (count
+    // <= 128: bits 0-7, writes: bits 8-15, bytes <= 128 * 128: bits 16-30) and reduced
+    // warp-wide. Records of another kernel than lane 0's (concurrent kernels) share the
+    // page and alloc statistics of their interval and send their kernel-row count
+    // themselves; records outside A and B go straight to L2.
     {
-      const uint64_t m0 = __shfl_sync(kFull, m[0], 0);
-      const uint32_t g = (uint32_t)m0;
-      const uint32_t kg = g - args.grid_lo;
-      if (kg <= args.grid_last && !((m0 >> 49) & 1u)) {
+      if (valid == (uint32_t)kRSlice && kg <= args.grid_last && !((m0 >> 49) & 1u)) {
         uint32_t an = 0, minor = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const uint32_t gi = (uint32_t)m[i];
           const bool inwin = gi - args.grid_lo <= args.grid_last;
           const bool shared = (m[i] >> 49) & 1u;
-          const bool ok = 32u * i + lane < valid;
-          n_filt += (ok && !inwin) ? 1u : 0u;
-          n_shared += (ok && inwin && shared) ? 1u : 0u;
-          if (ok && inwin && !shared) {
+          n_filt += inwin ? 0u : 1u;
+          n_shared += (inwin && shared) ? 1u : 0u;
+          if (inwin && !shared) {
             an |= 1u << i;
             if (gi != g) minor |= 1u << i;
           }
@@ -1222,11 +1324,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
           k = kg;
         }
         const uint64_t a0 = __shfl_sync(kFull, a[0], 0);
-        const uint32_t lastpos = valid - 1u;
-        uint64_t bl = a[0];
-#pragma unroll
-        for (int i = 1; i < 4; ++i) bl = (lastpos >> 5) == (uint32_t)i ? a[i] : bl;
-        const uint64_t b0 = __shfl_sync(kFull, bl, lastpos & 31u);
+        const uint64_t b0 = __shfl_sync(kFull, a[3], 31);
         Ival IA = cur;
         if (!inside(a0, IA)) IA = lookup<kBig>(oc, a0, c);
         Ival IB = IA;
@@ -1269,9 +1367,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
           uint32_t mm = minor & ~rest;
           const unsigned mb = __ballot_sync(kFull, mm != 0);
           if (mb) {
-            uint64_t ml = m[0];
-#pragma unroll
-            for (int i = 1; i < 4; ++i) ml = (mm && __ffs(mm) - 1 == i) ? m[i] : ml;
+            const uint64_t ml = pick4(m, mm ? __ffs(mm) - 1 : 0);
             const uint32_t g2 = (uint32_t)__shfl_sync(kFull, ml, __ffs(mb) - 1);
             uint32_t c2 = 0, sel2 = 0;
 #pragma unroll
@@ -1293,12 +1389,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
           while (mm) {
             const int i = __ffs(mm) - 1;
             mm &= mm - 1;
-            uint64_t x = a[0], mi = m[0];
-#pragma unroll
-            for (int q = 1; q < 4; ++q) {
-              x = (i == q) ? a[q] : x;
-              mi = (i == q) ? m[q] : mi;
-            }
+            const uint64_t x = pick4(a, i), mi = pick4(m, i);
             rich_row_one(o, inside(x, IA) ? IA.own : IB.own, (uint32_t)mi - args.grid_lo);
           }
         }
@@ -1307,12 +1398,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
           while (rest) {
             const int i = __ffs(rest) - 1;
             rest &= rest - 1;
-            uint64_t x = a[0], mm = m[0];
-#pragma unroll
-            for (int q = 1; q < 4; ++q) {
-              x = (i == q) ? a[q] : x;
-              mm = (i == q) ? m[q] : mm;
-            }
+            const uint64_t x = pick4(a, i), mm = pick4(m, i);
             const Ival I = lookup<kBig>(oc, x, c);
             const uint64_t w = (mm >> 48) & 1u;
             rich_page(o, I.page, 1, w);
@@ -1348,12 +1434,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
       if (any == 0) break;
       const int leader = __ffs(any) - 1;
       const int li = pend ? __ffs(pend) - 1 : 0;
-      uint64_t al = a[0], ml = m[0];
-#pragma unroll
-      for (int i = 1; i < 4; ++i) {
-        al = (li == i) ? a[i] : al;
-        ml = (li == i) ? m[i] : ml;
-      }
+      const uint64_t al = pick4(a, li), ml = pick4(m, li);
       const uint32_t g = (uint32_t)__shfl_sync(kFull, ml, leader);
       const uint64_t a0 = __shfl_sync(kFull, al, leader);
       uint32_t sel = 0;
@@ -1363,10 +1444,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
       // the group's last record (highest slice position)
       const uint32_t mypos = sel ? 32u * (31u - __clz(sel)) + lane + 1u : 0u;
       const uint32_t last = __reduce_max_sync(kFull, mypos) - 1u;
-      uint64_t bl = a[0];
-#pragma unroll
-      for (int i = 1; i < 4; ++i) bl = (last >> 5) == (uint32_t)i ? a[i] : bl;
-      const uint64_t b0 = __shfl_sync(kFull, bl, last & 31u);
+      const uint64_t b0 = __shfl_sync(kFull, pick4(a, (int)(last >> 5)), last & 31u);
       const uint32_t kg = g - args.grid_lo;
       if (kRows && kg != k) {
         rich_flush<kRows>(r, o, k, lane);
@@ -1408,12 +1486,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
       while (rest) {
         const int i = __ffs(rest) - 1;
         rest &= rest - 1;
-        uint64_t x = a[0], mm = m[0];
-#pragma unroll
-        for (int q = 1; q < 4; ++q) {
-          x = (i == q) ? a[q] : x;
-          mm = (i == q) ? m[q] : mm;
-        }
+        const uint64_t x = pick4(a, i), mm = pick4(m, i);
         const Ival I = lookup<kBig>(oc, x, c);
         const uint64_t w = (mm >> 48) & 1u;
         rich_page(o, I.page, 1, w);
@@ -1429,7 +1502,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
   const uint64_t by = warp_sum_u64(n_bytes);
   if (lane == 0) {
     if (f) red_add_u64(args.rich_totals + 0, f);
-    if (sh) red_add_u64(args.rich_totals + 1, sh);
+    if (sh + u_sh) red_add_u64(args.rich_totals + 1, (uint64_t)sh + u_sh);
     if (wr + u_wr) red_add_u64(args.rich_totals + 2, (uint64_t)wr + u_wr);
     if (by + u_bytes) red_add_u64(args.rich_totals + 3, by + u_bytes);
     if (an + u_an) red_add_u64(args.totals + 0, (uint64_t)an + u_an);

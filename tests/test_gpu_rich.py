@@ -39,7 +39,7 @@ def _dev_rich(rec):
     return torch.from_numpy(rec.view(np.int64).reshape(-1, 2).copy()).to(DEV)
 
 
-def _run(va_lo, va_hi, live, rec, g0, g1, s=12, misalign=False):
+def _run(va_lo, va_hi, live, rec, g0, g1, s=12, misalign=False, rows=True):
     A = max(1, len(live))
     tr = pb.Trace(DEV, va_lo, va_hi, A, A)
     o = OracleTrace(va_lo, va_hi, A, A)
@@ -47,20 +47,21 @@ def _run(va_lo, va_hi, live, rec, g0, g1, s=12, misalign=False):
         tr.register_alloc(b, sz)
         o.register_alloc(b, sz)
     nk = g1 - g0 + 1
-    h = tr.histograms(s, n_kernels=nk, kernel_rows=True)
+    h = tr.histograms(s, n_kernels=nk, kernel_rows=rows)
     rx = tr.rich_outputs(s)
     tr.analyze_rich(_dev_rich(rec), g0, g1, s, h, rx)
     tr.sync()
-    o.analyze_rich(rec, g0, g1, s, kernel_rows=True)
+    o.analyze_rich(rec, g0, g1, s, kernel_rows=rows)
     g = dict(page=u64(h.page_counts), alloc=u64(h.alloc_counts), tot=u64(h.totals),
-             kac=u64(h.kernel_alloc_counts).reshape(nk, -1), kst=u64(h.kernel_stats).reshape(nk, 4),
+             kac=u64(h.kernel_alloc_counts).reshape(nk, -1) if rows else None,
+             kst=u64(h.kernel_stats).reshape(nk, 4) if rows else None,
              pw=u64(rx.page_write_counts), aw=u64(rx.alloc_write_counts), ab=u64(rx.alloc_bytes),
              rt=u64(rx.rich_totals), bm=u64(h.page_bitmap))
     tr.close()
     return g, o
 
 
-def _assert(g, o, label):
+def _assert(g, o, label, rows=True):
     assert np.array_equal(g["page"], o.page_counts), f"{label}: page_counts"
     assert np.array_equal(g["pw"], o.page_writes), f"{label}: page_write_counts"
     assert np.array_equal(g["alloc"], o.alloc_counts), f"{label}: alloc_counts"
@@ -68,10 +69,12 @@ def _assert(g, o, label):
     assert np.array_equal(g["ab"], o.alloc_bytes), f"{label}: alloc_bytes"
     assert g["tot"][:3].tolist() == o.totals.tolist(), f"{label}: totals"
     assert np.array_equal(g["rt"], o.rich_totals), f"{label}: rich_totals"
-    assert np.array_equal(g["kac"], o.kernel_rows), f"{label}: kernel rows"
-    assert np.array_equal(g["kst"][:, 1], o.kun), f"{label}: kernel unattributed"
     bm, u = o.bitmap()
     assert np.array_equal(g["bm"], bm) and int(g["tot"][3]) == u, f"{label}: bitmap"
+    if not rows:
+        return
+    assert np.array_equal(g["kac"], o.kernel_rows), f"{label}: kernel rows"
+    assert np.array_equal(g["kst"][:, 1], o.kun), f"{label}: kernel unattributed"
     fp, ws = o.footprints()
     assert np.array_equal(g["kst"][:, 2], fp) and int(g["tot"][4]) == ws, f"{label}: footprints"
     assert int(g["tot"][pb.T_MAX_KERNEL]) == o.max_kernel(), f"{label}: max kernel"
@@ -150,3 +153,23 @@ def test_rich_errors():
         pb.pasta_analyze_rich(tr.h, buf[1:], 4, 0, 1, 12, h2.struct(), rx.struct())
     assert ei.value.status == pb.PASTA_EINVAL
     tr.close()
+
+
+@pytest.mark.parametrize("mix,block_log2,rows", [(0.0, 0, True), (0.05, 5, True), (0.05, 5, False), (0.3, 0, True),
+                                                 (0.05, 0, False), (0.5, 3, True)])
+def test_llama_prefix_rich_mixes(mix, block_log2, rows):
+    """Concurrent-kernel mixes that select each scan tier: one kernel per slice (tier RC),
+    warp-sized bursts of the previous kernel (tier RC with two kernels), single records
+    of it (two-kernel tier, fast path), heavy mixing (leader loop); with and without
+    kernel rows. Partial grid window so some slices mix filtered records."""
+    p = tracegen.build_plan("llama")
+    n = (1 << 22) + 77
+    j0 = 3 << 22
+    addr = tracegen.host_records(p, j0, j0 + n)
+    rec = rich_host(addr, p.kernel_offsets, seed=5, mix=mix, j0=j0, block_log2=block_log2)
+    ko = np.asarray(p.kernel_offsets, dtype=np.int64)
+    k0 = int(np.searchsorted(ko, j0, side="right")) - 1
+    k1 = int(np.searchsorted(ko, j0 + n, side="left"))
+    for g0, g1 in ((k0 - 1, k1), (k0 + 2, k1 - 3)):
+        g, o = _run(p.va_lo, p.va_hi, p.allocs, rec, g0, g1, s=p.page_shift, rows=rows)
+        _assert(g, o, f"mix={mix} blk={block_log2} rows={rows} window=[{g0},{g1}]", rows=rows)
