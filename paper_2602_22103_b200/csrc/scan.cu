@@ -971,11 +971,14 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
 // 2 KiB slices (128 records; lane l reads records l, l+32, l+64, l+96 with LDS.128).
 // A record is dropped (and counted) if its grid id is outside the window or it is a
 // shared-space access; the rest are attributed like 8-byte records of kernel row
-// grid_id - grid_lo, with write counts and byte weights. Per slice, a leader loop takes
-// one grid id at a time (usually one, two where concurrent kernels interleave); the
-// group's records inside A = interval of its first record or B = of its last are
-// counted with six warp reductions into warp-uniform run accumulators (page run:
-// count, writes; owner run: count, writes, bytes), the others go straight to L2.
+// grid_id - grid_lo, with write counts and byte weights. Tier RC takes a full slice
+// whose records belong to at most two kernels, both in the window (one per slice in a
+// serial trace, two where a concurrent kernel's records interleave): packed per-interval
+// sums (count, writes, bytes in one u32) against A = interval of the first record and
+// B = of the last, two to four warp reductions, warp-uniform run accumulators (page
+// run: count, writes; owner run: count, writes, bytes, kernel-row share). Any other
+// slice goes to a leader loop that takes one grid id at a time with the same A / B
+// classification. Records outside A and B go straight to L2.
 // ------------------------------------------------------------------------------------
 constexpr int kRSlice = 128;
 #ifndef PASTA_RICH_WARPS
@@ -1062,16 +1065,6 @@ __device__ __forceinline__ void rich_rows(const RichOut& o, uint32_t own, uint64
     if (o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 0, c);
   } else if (o.kstats) {
     red_add_u64(o.kstats + (uint64_t)k * 4 + 1, c);
-  }
-}
-
-// One record's kernel-row count only (its alloc statistics went with a run).
-__device__ __forceinline__ void rich_row_one(const RichOut& o, uint32_t own, uint32_t k) {
-  if (own < o.A) {
-    red_add_u64(o.kac + (uint64_t)k * o.max_ids + __ldg(o.ids + own), 1);
-    if (o.kstats) red_add_u64(o.kstats + (uint64_t)k * 4 + 0, 1);
-  } else if (o.kstats) {
-    red_add_u64(o.kstats + (uint64_t)k * 4 + 1, 1);
   }
 }
 
@@ -1182,7 +1175,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
   // per-lane totals: dropped by the grid window, dropped as shared, analyzed, writes, bytes
   uint32_t n_filt = 0, n_shared = 0, n_an = 0, n_wr = 0;
   uint64_t n_bytes = 0;
-  uint32_t u_an = 0, u_wr = 0, u_sh = 0;  // warp-uniform totals of fast-path slices
+  uint32_t u_an = 0, u_wr = 0, u_sh = 0;  // warp-uniform totals of tier-RC slices
   uint64_t u_bytes = 0;
 
   uint32_t slot = 0, phase = 0;
@@ -1214,11 +1207,11 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
     // A and all), a third when some record is in neither A nor B = the interval of the
     // slice's last record, a fourth for g2's kernel-row counts in A (bits 0-7) and B
     // (bits 8-15). Page and alloc statistics do not depend on the kernel.
-    auto tier_rc = [&](auto two_t, const uint32_t mis, const uint32_t k2) {
+    auto tier_rc = [&](auto two_t, const uint32_t mis, const uint32_t km, const uint32_t k2) {
       constexpr bool kTwo = decltype(two_t)::value;
-      if (kRows && kg != k) {
+      if (kRows && km != k) {
         rich_flush<kRows>(r, o, k, lane);
-        k = kg;
+        k = km;
       }
       const uint64_t a0 = __shfl_sync(kFull, a[0], 0);
       const uint64_t b0 = __shfl_sync(kFull, a[3], 31);
@@ -1253,13 +1246,15 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
       const uint32_t cA = hA >> 24, cT = hT >> 24, cB = cT - cA - (hR >> 24);
       const uint32_t bA = hA & 0xFFFFu, wA = (hA >> 16) & 0xFFu;
       const uint32_t bT = hT & 0xFFFFu, wT = (hT >> 16) & 0xFFu;
-      if (cA) rich_add<kRows>(r, o, IA, cA, wA, bA, cA - (mAB & 0xFFu), kg, lane);
+      if (cA) rich_add<kRows>(r, o, IA, cA, wA, bA, cA - (mAB & 0xFFu), km, lane);
       if (cB)
         rich_add<kRows>(r, o, IB, cB, wT - wA - ((hR >> 16) & 0xFFu), bT - bA - (hR & 0xFFFFu), cB - (mAB >> 8),
-                        kg, lane);
-      if (kTwo && kRows && lane == 0) {
-        if (mAB & 0xFFu) rich_rows(o, IA.own, mAB & 0xFFu, k2);
-        if (mAB >> 8) rich_rows(o, IB.own, mAB >> 8, k2);
+                        km, lane);
+      if (kTwo && kRows) {
+        if (lane == 0) {
+          if (mAB & 0xFFu) rich_rows(o, IA.own, mAB & 0xFFu, k2);
+          if (mAB >> 8) rich_rows(o, IB.own, mAB >> 8, k2);
+        }
       }
       if (any_rest) {
 #pragma unroll 1
@@ -1284,7 +1279,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
       for (int i = 0; i < 4; ++i) mis |= ((uint32_t)m[i] != g ? 1u : 0u) << i;
       const unsigned mis_lanes = __ballot_sync(kFull, mis != 0);
       if (mis_lanes == 0) {
-        tier_rc(std::false_type{}, 0u, 0u);
+        tier_rc(std::false_type{}, 0u, kg, 0u);
         continue;
       }
       const uint32_t gl = (uint32_t)pick4(m, mis ? __ffs(mis) - 1 : 0);
@@ -1293,122 +1288,10 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
 #pragma unroll
       for (int i = 0; i < 4; ++i) bad |= (((mis >> i) & 1u) && (uint32_t)m[i] != g2) ? 1u : 0u;
       if (!__any_sync(kFull, bad != 0)) {
-        tier_rc(std::true_type{}, mis, g2 - args.grid_lo);
-        continue;
-      }
-    }
-    // Fast path (full slice, lane 0's first record analyzed): every analyzed record of
-    // the slice is classified against A = interval of the slice's first record and B =
-    // of its last; counts / writes / bytes per interval are packed into one u32 (count
-    // <= 128: bits 0-7, writes: bits 8-15, bytes <= 128 * 128: bits 16-30) and reduced
-    // warp-wide. Records of another kernel than lane 0's (concurrent kernels) share the
-    // page and alloc statistics of their interval and send their kernel-row count
-    // themselves; records outside A and B go straight to L2.
-    {
-      if (valid == (uint32_t)kRSlice && kg <= args.grid_last && !((m0 >> 49) & 1u)) {
-        uint32_t an = 0, minor = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t gi = (uint32_t)m[i];
-          const bool inwin = gi - args.grid_lo <= args.grid_last;
-          const bool shared = (m[i] >> 49) & 1u;
-          n_filt += inwin ? 0u : 1u;
-          n_shared += (inwin && shared) ? 1u : 0u;
-          if (inwin && !shared) {
-            an |= 1u << i;
-            if (gi != g) minor |= 1u << i;
-          }
-        }
-        if (kRows && kg != k) {
-          rich_flush<kRows>(r, o, k, lane);
-          k = kg;
-        }
-        const uint64_t a0 = __shfl_sync(kFull, a[0], 0);
-        const uint64_t b0 = __shfl_sync(kFull, a[3], 31);
-        Ival IA = cur;
-        if (!inside(a0, IA)) IA = lookup<kBig>(oc, a0, c);
-        Ival IB = IA;
-        if (!inside(b0, IA)) IB = lookup<kBig>(oc, b0, c);
-        cur = IB;
-        uint32_t pA = 0, pT = 0, pR = 0, rest = 0, mAB = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if ((an >> i) & 1u) {
-            const uint32_t v = 1u | ((uint32_t)(m[i] >> 40) & 0x100u) | (((uint32_t)(m[i] >> 32) & 0xFFFFu) << 16);
-            pT += v;
-            if (inside(a[i], IA)) {
-              pA += v;
-              mAB += (minor >> i) & 1u;
-            } else if (inside(a[i], IB)) {
-              mAB += ((minor >> i) & 1u) << 8;
-            } else {
-              rest |= 1u << i;
-              pR += v;
-            }
-          }
-        }
-        const bool any_rest = __any_sync(kFull, rest != 0);
-        const bool any_minor = kRows && __any_sync(kFull, minor != 0);
-        pA = __reduce_add_sync(kFull, pA);
-        pT = __reduce_add_sync(kFull, pT);
-        if (any_rest) pR = __reduce_add_sync(kFull, pR);
-        else pR = 0;
-        uint32_t mSum = 0;
-        if (any_minor) mSum = __reduce_add_sync(kFull, mAB);
-        const uint32_t pB = pT - pA - pR;
-        if (pA & 0xFFu)
-          rich_add<kRows>(r, o, IA, pA & 0xFFu, (pA >> 8) & 0xFFu, pA >> 16, (pA & 0xFFu) - (mSum & 0xFFu), kg, lane);
-        if (pB & 0xFFu)
-          rich_add<kRows>(r, o, IB, pB & 0xFFu, (pB >> 8) & 0xFFu, pB >> 16, (pB & 0xFFu) - ((mSum >> 8) & 0xFFu), kg,
-                          lane);
-        if (any_minor) {
-          // kernel rows of the other kernels' records in A or B: those of the first
-          // minority kernel k2 are reduced per interval, any others go one by one
-          uint32_t mm = minor & ~rest;
-          const unsigned mb = __ballot_sync(kFull, mm != 0);
-          if (mb) {
-            const uint64_t ml = pick4(m, mm ? __ffs(mm) - 1 : 0);
-            const uint32_t g2 = (uint32_t)__shfl_sync(kFull, ml, __ffs(mb) - 1);
-            uint32_t c2 = 0, sel2 = 0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              if (((mm >> i) & 1u) && (uint32_t)m[i] == g2) {
-                sel2 |= 1u << i;
-                c2 += inside(a[i], IA) ? 1u : 0x100u;
-              }
-            }
-            c2 = __reduce_add_sync(kFull, c2);
-            if (lane == 0) {
-              const uint32_t k2 = g2 - args.grid_lo;
-              if (c2 & 0xFFu) rich_rows(o, IA.own, c2 & 0xFFu, k2);
-              if (c2 >> 8) rich_rows(o, IB.own, c2 >> 8, k2);
-            }
-            mm &= ~sel2;
-          }
-#pragma unroll 1
-          while (mm) {
-            const int i = __ffs(mm) - 1;
-            mm &= mm - 1;
-            const uint64_t x = pick4(a, i), mi = pick4(m, i);
-            rich_row_one(o, inside(x, IA) ? IA.own : IB.own, (uint32_t)mi - args.grid_lo);
-          }
-        }
-        if (any_rest) {
-#pragma unroll 1
-          while (rest) {
-            const int i = __ffs(rest) - 1;
-            rest &= rest - 1;
-            const uint64_t x = pick4(a, i), mm = pick4(m, i);
-            const Ival I = lookup<kBig>(oc, x, c);
-            const uint64_t w = (mm >> 48) & 1u;
-            rich_page(o, I.page, 1, w);
-            rich_owner<kRows>(o, I.own, 1, w, (mm >> 32) & 0xFFFFu, (uint32_t)mm - args.grid_lo);
-          }
-        }
-        // warp totals (uniform values; lane 0's copy is flushed at the end)
-        u_an += pT & 0xFFu;
-        u_wr += (pT >> 8) & 0xFFu;
-        u_bytes += pT >> 16;
+        // the run accumulators keep the current kernel when it is the other one here
+        const uint32_t k2 = g2 - args.grid_lo;
+        const bool sw = kRows && kg != k && k2 == k;
+        tier_rc(std::true_type{}, sw ? ~mis & 0xFu : mis, sw ? k2 : kg, sw ? kg : k2);
         continue;
       }
     }
