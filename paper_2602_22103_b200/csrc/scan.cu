@@ -987,10 +987,11 @@ constexpr int kRSlice = 128;
 constexpr int kRWarps = PASTA_RICH_WARPS;
 constexpr int kRThreads = kRWarps * 32;
 constexpr int kRBarBytes = kRWarps * kMaxStages * 8;
+constexpr int kRSlotBytes = kRWarps * 16;  // per-warp second-kernel row run {own, k, count, -}
 __host__ __device__ constexpr int rich_ring_bytes(int stages) { return kRWarps * stages * (int)kSliceBytes; }
 int rich_stages(uint32_t A, bool big) {
   const long table = big ? 0 : 16l * A;
-  long st = ((long)kSmemLimit - kRBarBytes - table) / rich_ring_bytes(1);
+  long st = ((long)kSmemLimit - kRBarBytes - kRSlotBytes - table) / rich_ring_bytes(1);
   return (int)(st > kMaxStages ? kMaxStages : st);
 }
 
@@ -1068,6 +1069,20 @@ __device__ __forceinline__ void rich_rows(const RichOut& o, uint32_t own, uint64
   }
 }
 
+// Second-kernel row counts of tier RC (one lane): a run {own, k, count} in the warp's
+// shared-memory slot, sent to L2 when the owner or the kernel changes (registers are
+// at the 80-per-thread limit of 24 warps, so the run is not kept in registers).
+__device__ __forceinline__ void rich_rows_run(const RichOut& o, uint4* slot, uint32_t own, uint32_t k, uint32_t c) {
+  uint4 s = *slot;
+  if (s.x == own && s.y == k) {
+    s.z += c;
+  } else {
+    if (s.z) rich_rows(o, s.x, s.z, s.y);
+    s = make_uint4(own, k, c, 0u);
+  }
+  *slot = s;
+}
+
 struct RichAcc {  // warp-uniform run accumulators
   uint32_t page, pcnt, pw;
   uint32_t own, ocnt, ow, okc;  // okc: records of the run counted in kernel row k
@@ -1110,7 +1125,8 @@ template <bool kBig, bool kRows>
 __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args, const int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + rich_ring_bytes(stages));
-  uint64_t* sB = reinterpret_cast<uint64_t*>(smem + rich_ring_bytes(stages) + kRBarBytes);
+  uint4* slot2 = reinterpret_cast<uint4*>(smem + rich_ring_bytes(stages) + kRBarBytes) + (threadIdx.x >> 5);
+  uint64_t* sB = reinterpret_cast<uint64_t*>(smem + rich_ring_bytes(stages) + kRBarBytes + kRSlotBytes);
   const uint32_t A = args.A;
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -1125,6 +1141,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
   if (lane == 0) {
     for (int j = 0; j < stages; ++j) mbar_init(bars + warp * kMaxStages + j, 1);
     fence_mbar_init();
+    *slot2 = make_uint4(A, 0u, 0u, 0u);
   }
   if (!kBig)
     for (uint32_t i = threadIdx.x; i < 2 * A; i += kRThreads) sB[i] = args.bounds[i];
@@ -1252,8 +1269,8 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
                         km, lane);
       if (kTwo && kRows) {
         if (lane == 0) {
-          if (mAB & 0xFFu) rich_rows(o, IA.own, mAB & 0xFFu, k2);
-          if (mAB >> 8) rich_rows(o, IB.own, mAB >> 8, k2);
+          if (mAB & 0xFFu) rich_rows_run(o, slot2, IA.own, k2, mAB & 0xFFu);
+          if (mAB >> 8) rich_rows_run(o, slot2, IB.own, k2, mAB >> 8);
         }
       }
       if (any_rest) {
@@ -1379,6 +1396,10 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
     }
   }
   rich_flush<kRows>(r, o, k, lane);
+  if (kRows && lane == 0) {
+    const uint4 s = *slot2;
+    if (s.z) rich_rows(o, s.x, s.z, s.y);
+  }
   // per-warp totals
   const uint32_t f = __reduce_add_sync(kFull, n_filt), sh = __reduce_add_sync(kFull, n_shared);
   const uint32_t an = __reduce_add_sync(kFull, n_an), wr = __reduce_add_sync(kFull, n_wr);
@@ -1395,7 +1416,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
 template <bool kBig, bool kRows>
 cudaError_t launch_rich_variant(const RichArgs& a, int grid, cudaStream_t st) {
   const int stages = rich_stages(a.A, kBig);
-  const int smem = rich_ring_bytes(stages) + kRBarBytes + (kBig ? 0 : (int)(16ull * a.A));
+  const int smem = rich_ring_bytes(stages) + kRBarBytes + kRSlotBytes + (kBig ? 0 : (int)(16ull * a.A));
   auto fn = rich_kernel<kBig, kRows>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
