@@ -6,18 +6,19 @@
 // descending, then page ascending; only non-zero pages; K' = min(K, nnz).
 //
 // Pipeline (all on the device, no host synchronization; the host never learns nnz):
-//  1. stats: nnz and max count (block reduce + atomics);
-//  2. plan: K' = min(K, nnz); first 8-bit digit = the one holding max's MSB;
-//  3. up to 8 MSD radix passes: per-CTA shared 256-bin histogram of the current digit
-//     over the non-zero counts that match the selected prefix, global sum, then a
-//     1-CTA select picks the digit where the running count from the top reaches the
-//     remaining rank; after the last digit T = the K'-th largest count exactly and
-//     `need` = how many pages with count == T are taken;
-//  4. gather: pages with count > T go to atomically reserved slots (their order is
-//     fixed by the sort); pages with count == T are ranked in ascending page order by
-//     a per-CTA count pass + block exclusive scans (no atomics decide which are
-//     taken), and the first `need` are kept;
-//  5. bitonic sort of the K' (padded to a power of two with (0, UINT64_MAX) sentinels
+//  1. one pass: per-CTA shared histogram of a monotone 11-bit "float" key of every
+//     non-zero count (bit length + the 5 bits below the leading one); block 0 derives
+//     nnz, K' = min(K, nnz) and the bin holding the K'-th largest count;
+//  2. up to six MSD radix passes of 11 bits over the counts inside the selected bin,
+//     each followed by a 1-CTA select of the digit where the running count from the
+//     top reaches the remaining rank; they stop as soon as a bin is taken whole, so
+//     T (take every count > T) and `need` (how many pages with count == T) are fixed;
+//  3. gather: pages with count > T go to atomically reserved slots (their order is
+//     fixed by the sort) in the same pass that counts each CTA's `== T` pages; only if
+//     ties are cut, the CTAs that hold needed ties re-read their range and rank those
+//     pages in ascending page order with block exclusive scans (no atomics decide
+//     which are taken);
+//  4. bitonic sort of the K' (padded to a power of two with (0, UINT64_MAX) sentinels
 //     that sort last) by (count desc, page asc): shared-memory tiles of 2048, global
 //     compare-exchange steps for the larger strides; sentinels fill slots [K', K).
 #include <cstdint>
@@ -96,61 +97,100 @@ __device__ __forceinline__ void stream_pairs(const ulonglong2* __restrict__ pc2,
 
 // ---- selection passes (device functions of the one cooperative selection kernel) ----
 
-// Pass 1: histogram of the bit length of every non-zero count (65 bins).
-__device__ void dev_bitlen(const uint64_t* __restrict__ pc, uint64_t P, unsigned* h, unsigned* hist) {
-  for (int i = threadIdx.x; i < 65; i += kBlock) h[i] = 0;
+// Pass 1 key: a monotone 11-bit "float" of a non-zero count c with bit length L:
+// c itself for L <= 6 (exact bins 1..63), else 64 + 32 (L - 7) + the 5 bits below the
+// leading one (bins 64..1919, each covering 2^(L-6) consecutive counts). One pass
+// resolves the bit length and five more bits.
+constexpr int kFirstBins = 64 + 58 * 32;  // 1920
+static_assert(kFirstBins <= kBins, "pass-1 bins share the digit histogram buffers");
+__device__ __forceinline__ unsigned first_key(uint64_t c) {
+  const int L = 64 - __clzll((long long)c);
+  return L <= 6 ? (unsigned)c : 64u + (unsigned)(L - 7) * 32u + (unsigned)((c >> (L - 6)) & 31u);
+}
+
+// Pass 1: histogram of first_key over the non-zero counts.
+__device__ void dev_first(const uint64_t* __restrict__ pc, uint64_t P, unsigned* h, unsigned* hist) {
+  for (int i = threadIdx.x; i < kFirstBins; i += kBlock) h[i] = 0;
   __syncthreads();
   stream_pairs(reinterpret_cast<const ulonglong2*>(pc), P / 2, [&](uint64_t, const ulonglong2& v) {
-    hist_add(h, v.x != 0, 64 - __clzll((long long)v.x));
-    hist_add(h, v.y != 0, 64 - __clzll((long long)v.y));
+    hist_add(h, v.x != 0, first_key(v.x));
+    hist_add(h, v.y != 0, first_key(v.y));
   });
   if ((P & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const uint64_t c = pc[P - 1];
-    if (c) atomicAdd(&h[64 - __clzll((long long)c)], 1u);
+    if (c) atomicAdd(&h[first_key(c)], 1u);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 65; i += kBlock)
+  for (int i = threadIdx.x; i < kFirstBins; i += kBlock)
     if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
-// Pick the bit length holding the K'-th largest count (one thread).
-__device__ void dev_select_len(volatile State* st, unsigned* hist, uint64_t K) {
-  unsigned long long nnz = 0;
-  for (int b = 1; b <= 64; ++b) nnz += hist[b];
-  const unsigned long long kp = nnz < K ? nnz : K;
-  st->nnz = nnz;
-  st->kprime = kp;
-  st->gt_slots = 0;
-  st->need = 0;
-  if (kp == 0) {
-    st->done = 1;
-    st->T = ~0ull;
-  } else {
-    unsigned long long above = 0;
-    int L = 64;
-    for (; L >= 1; --L) {
-      if (above + hist[L] >= kp) break;
-      above += hist[L];
-    }
-    const unsigned long long rem = kp - above;
-    st->above = above;
-    st->remaining = rem;
-    st->lo = 1ull << (L - 1);
-    if (rem == hist[L]) {  // the whole bit-length class is taken
-      st->done = 2;
-      st->T = (1ull << (L - 1)) - 1;
-    } else if (L == 1) {  // the class is the single value 1
-      st->done = 2;
-      st->T = 1;
-      st->need = rem;
+// Pick the pass-1 bin holding the K'-th largest count (block 0, all threads): nnz and
+// K' = min(K, nnz), then chunked suffix sums from the top bin down.
+__device__ void dev_select_first(volatile State* st, unsigned* hist, uint64_t K, unsigned long long* sm) {
+  constexpr int per = (kFirstBins + kBlock - 1) / kBlock;  // bins per thread
+  const int t = threadIdx.x;
+  unsigned long long mine = 0;
+  for (int j = 0; j < per; ++j) {
+    const int d = t * per + j;
+    if (d < kFirstBins) mine += hist[d];
+  }
+  sm[t] = mine;
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long nnz = 0;
+    for (int i = 0; i < kBlock; ++i) nnz += sm[i];
+    const unsigned long long kp = nnz < K ? nnz : K;
+    st->nnz = nnz;
+    st->kprime = kp;
+    st->gt_slots = 0;
+    st->need = 0;
+    if (kp == 0) {
+      st->done = 1;
+      st->T = ~0ull;
     } else {
-      const int w = (L - 1) < kDigitBits ? (L - 1) : kDigitBits;
-      st->width = w;
-      st->shift = (L - 1) - w;
-      st->done = 0;
+      unsigned long long rem = kp, above = 0;
+      int c = kBlock - 1;
+      for (; c > 0; --c) {
+        if (sm[c] >= rem) break;
+        rem -= sm[c];
+        above += sm[c];
+      }
+      int d = c * per + per - 1;
+      if (d > kFirstBins - 1) d = kFirstBins - 1;
+      for (; d > c * per; --d) {
+        if (hist[d] >= rem) break;
+        rem -= hist[d];
+        above += hist[d];
+      }
+      const unsigned long long here = hist[d];
+      int bits = 0;  // the bin is [lo, lo + 2^bits - 1]
+      unsigned long long lo = (unsigned long long)d;
+      if (d >= 64) {
+        const int L = (d - 64) / 32 + 7;
+        bits = L - 6;
+        lo = (32ull + (unsigned)((d - 64) % 32)) << bits;
+      }
+      st->lo = lo;
+      st->above = above;
+      st->remaining = rem;
+      if (rem == here) {  // the whole bin is taken: no ties to break
+        st->done = 2;
+        st->T = lo - 1;
+      } else if (bits == 0) {  // exact value: take the first `rem` pages with this count
+        st->done = 2;
+        st->T = lo;
+        st->need = rem;
+      } else {
+        const int w = bits < kDigitBits ? bits : kDigitBits;
+        st->width = w;
+        st->shift = bits - w;
+        st->done = 0;
+      }
     }
   }
-  for (int i = 0; i <= 64; ++i) hist[i] = 0;
+  __syncthreads();
+  for (int i = t; i < kBins; i += kBlock) hist[i] = 0;
 }
 
 // One radix digit among the counts of the selected bin.
@@ -225,9 +265,13 @@ __device__ void dev_select_digit(volatile State* st, unsigned* hist, unsigned lo
   for (int i = t; i < nb; i += kBlock) hist[i] = 0;
 }
 
-// Pages with count == T in this CTA's contiguous page range.
-__device__ void dev_eq_count(const uint64_t* __restrict__ pc, uint64_t P, uint64_t T, unsigned long long* blkcnt,
-                             unsigned long long* part) {
+// Gather (one pass over this CTA's contiguous page range): every page with count > T
+// to an atomically reserved slot (the sort fixes the order), and the number of pages
+// with count == T to blkcnt[cta].
+__device__ void dev_gather_gt(const uint64_t* __restrict__ pc, uint64_t P, volatile State* st,
+                              unsigned long long* blkcnt, uint64_t* key_c, uint64_t* key_p,
+                              unsigned long long* part) {
+  const uint64_t T = st->T;
   const uint64_t b0 = (uint64_t)blockIdx.x * P / gridDim.x, b1 = (uint64_t)(blockIdx.x + 1) * P / gridDim.x;
   uint64_t n = 0;
   for (uint64_t p0 = b0 + threadIdx.x; p0 < b1; p0 += (uint64_t)kBlock * kU) {
@@ -235,10 +279,18 @@ __device__ void dev_eq_count(const uint64_t* __restrict__ pc, uint64_t P, uint64
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint64_t p = p0 + (uint64_t)u * kBlock;
-      v[u] = p < b1 ? __ldg(pc + p) : ~T;
+      v[u] = p < b1 ? __ldg(pc + p) : 0;
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) n += (v[u] == T);
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t p = p0 + (uint64_t)u * kBlock;
+      n += (p < b1 && v[u] == T) ? 1u : 0u;
+      if (v[u] > T) {
+        const unsigned long long slot = atomicAdd((unsigned long long*)&st->gt_slots, 1ull);
+        key_c[slot] = v[u];
+        key_p[slot] = p;
+      }
+    }
   }
   n = warp_sum_u64(n);
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = n;
@@ -248,63 +300,35 @@ __device__ void dev_eq_count(const uint64_t* __restrict__ pc, uint64_t P, uint64
     for (int i = 0; i < kBlock / 32; ++i) s2 += part[i];
     blkcnt[blockIdx.x] = s2;
   }
-  __syncthreads();
 }
 
-// Every page with count > T to an atomically reserved slot (the sort fixes the order);
-// pages with count == T ranked in page order, the first `need` kept; a block whose own
-// range holds no such page, or whose predecessors already supply `need`, skips ranking.
-__device__ void dev_gather(const uint64_t* __restrict__ pc, uint64_t P, volatile State* st,
-                           const unsigned long long* blkcnt, uint64_t* key_c, uint64_t* key_p,
-                           unsigned long long* part, unsigned long long* running_s) {
+// Ties (after a grid barrier): pages with count == T ranked in ascending page order
+// (block exclusive scans over the CTA ranges, no atomics decide which), the first
+// `need` kept in slots [K' - need, K'). Only CTAs whose range holds such pages and whose
+// predecessors do not already supply `need` re-read their range (at most `need` CTAs).
+__device__ void dev_gather_eq(const uint64_t* __restrict__ pc, uint64_t P, volatile State* st,
+                              const unsigned long long* blkcnt, uint64_t* key_c, uint64_t* key_p,
+                              unsigned long long* part, unsigned long long* running_s) {
   const uint64_t T = st->T, need = st->need, kp = st->kprime;
+  if (blkcnt[blockIdx.x] == 0) return;
   const uint64_t eq_base_slot = kp - need;
   const uint64_t b0 = (uint64_t)blockIdx.x * P / gridDim.x, b1 = (uint64_t)(blockIdx.x + 1) * P / gridDim.x;
-  bool ties = false;
-  if (need && blkcnt[blockIdx.x] != 0) {
-    unsigned long long pre = 0;
-    for (unsigned i = threadIdx.x; i < blockIdx.x; i += kBlock) pre += blkcnt[i];
-    pre = warp_sum_u64(pre);
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = pre;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long s2 = 0;
-      for (int i = 0; i < kBlock / 32; ++i) s2 += part[i];
-      *running_s = s2;
-    }
-    __syncthreads();
-    ties = *running_s < need;
+  unsigned long long pre = 0;
+  for (unsigned i = threadIdx.x; i < blockIdx.x; i += kBlock) pre += blkcnt[i];
+  pre = warp_sum_u64(pre);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = pre;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s2 = 0;
+    for (int i = 0; i < kBlock / 32; ++i) s2 += part[i];
+    *running_s = s2;
   }
+  __syncthreads();
+  bool ties = *running_s < need;
   const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  if (!ties) {  // only counts > T are wanted from this range: batched streaming
-    for (uint64_t p0 = b0 + threadIdx.x; p0 < b1; p0 += (uint64_t)kBlock * kU) {
-      uint64_t v[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const uint64_t p = p0 + (uint64_t)u * kBlock;
-        v[u] = p < b1 ? __ldg(pc + p) : 0;
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        if (v[u] > T) {
-          const unsigned long long slot = atomicAdd((unsigned long long*)&st->gt_slots, 1ull);
-          key_c[slot] = v[u];
-          key_p[slot] = p0 + (uint64_t)u * kBlock;
-        }
-      }
-    }
-    return;
-  }
-  for (uint64_t t0 = b0; t0 < b1; t0 += kBlock) {
+  for (uint64_t t0 = b0; ties && t0 < b1; t0 += kBlock) {
     const uint64_t p = t0 + threadIdx.x;
-    const uint64_t c = p < b1 ? __ldg(pc + p) : 0;
-    if (p < b1 && c > T) {
-      const unsigned long long slot = atomicAdd((unsigned long long*)&st->gt_slots, 1ull);
-      key_c[slot] = c;
-      key_p[slot] = p;
-    }
-    if (!ties) continue;
-    const bool eq = p < b1 && c == T;
+    const bool eq = p < b1 && __ldg(pc + p) == T;
     const unsigned bal = __ballot_sync(kFull, eq);
     const unsigned long long rank_w = __popc(bal & ((1u << lane) - 1));
     __syncthreads();
@@ -315,7 +339,7 @@ __device__ void dev_gather(const uint64_t* __restrict__ pc, uint64_t P, volatile
     if (eq) {
       const unsigned long long r = off + rank_w;
       if (r < need) {
-        key_c[eq_base_slot + r] = c;
+        key_c[eq_base_slot + r] = T;
         key_p[eq_base_slot + r] = p;
       }
     }
@@ -330,9 +354,10 @@ __device__ void dev_gather(const uint64_t* __restrict__ pc, uint64_t P, volatile
   }
 }
 
-// The whole selection in ONE cooperative launch: bit-length pass, up to six 11-bit digit
-// passes (stopping as soon as the threshold is fixed), the tie count and the gather,
-// separated by grid-wide barriers.
+// The whole selection in ONE cooperative launch: the float-key pass, up to six 11-bit
+// digit passes (stopping as soon as the threshold is fixed), the gather of counts > T
+// with per-CTA tie counts and, if ties are cut, the ordered tie gather, separated by
+// grid-wide barriers.
 __global__ void __launch_bounds__(kBlock) select_coop_kernel(const uint64_t* __restrict__ pc, uint64_t P,
                                                              uint64_t K, State* st_, unsigned* hist,
                                                              unsigned long long* blkcnt, uint64_t* key_c,
@@ -342,9 +367,9 @@ __global__ void __launch_bounds__(kBlock) select_coop_kernel(const uint64_t* __r
   __shared__ unsigned h[kBins];
   __shared__ unsigned long long sm[kBlock];
   __shared__ unsigned long long running_s;
-  dev_bitlen(pc, P, h, hist);
+  dev_first(pc, P, h, hist);
   grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) dev_select_len(st, hist, K);
+  if (blockIdx.x == 0) dev_select_first(st, hist, K, sm);
   grid.sync();
   for (int pass = 0; pass < (63 + kDigitBits - 1) / kDigitBits; ++pass) {
     if (st->done) break;  // grid-uniform: read after the barrier
@@ -354,11 +379,10 @@ __global__ void __launch_bounds__(kBlock) select_coop_kernel(const uint64_t* __r
     grid.sync();
   }
   if (st->done != 2) return;
-  if (st->need) {
-    dev_eq_count(pc, P, st->T, blkcnt, sm);
-    grid.sync();
-  }
-  dev_gather(pc, P, st, blkcnt, key_c, key_p, sm, &running_s);
+  dev_gather_gt(pc, P, st, blkcnt, key_c, key_p, sm);
+  if (st->need == 0) return;  // grid-uniform
+  grid.sync();
+  dev_gather_eq(pc, P, st, blkcnt, key_c, key_p, sm, &running_s);
 }
 
 __global__ void pad_kernel(State* st, uint64_t* key_c, uint64_t* key_p, uint64_t Kp) {

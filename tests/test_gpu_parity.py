@@ -314,6 +314,40 @@ def test_topk_direct(K):
     tr.close()
 
 
+def _topk_dists():
+    rng = np.random.default_rng(2024)
+    P = 3_000_017  # several CTAs' ranges, odd length
+    yield "all equal", np.full(P, 5, dtype=np.uint64)
+    yield "exact small bins", rng.integers(0, 64, size=P).astype(np.uint64)
+    geo = (rng.geometric(0.002, size=P) - 1).astype(np.uint64)
+    yield "geometric", geo
+    wide = (rng.integers(0, 1 << 62, size=P, dtype=np.uint64) >> rng.integers(0, 62, size=P).astype(np.uint64))
+    wide[rng.integers(0, P, 40)] = np.uint64(U64MAX)  # bit length 64, tied at the top
+    wide[rng.integers(0, P, 40)] = np.uint64(1 << 63)
+    yield "64-bit spread", wide
+    sparse = np.zeros(P, dtype=np.uint64)
+    sparse[rng.integers(0, P, 3000)] = rng.integers(1, 1 << 20, 3000).astype(np.uint64)
+    yield "sparse", sparse
+    ties = rng.integers(1000, 1010, size=P).astype(np.uint64)  # one 2^k bin, ties cut deep inside
+    yield "narrow band", ties
+
+
+@pytest.mark.parametrize("K", [1, 999, 1024, 4097, 68266])
+def test_topk_distributions(K):
+    """Threshold bins of every kind: an exact small-value bin (< 64), float-key bins
+    of every bit length up to 64, whole-bin takes, and ties spread over every CTA's
+    page range (all counts equal), checked against the oracle's full sort."""
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    for name, counts in _topk_dists():
+        p, c, f = tr.topk(_t(counts), K)
+        tr.sync()
+        rp, rc, rf = oracle.topk(counts, K)
+        assert int(u64(f)[0]) == rf, name
+        assert np.array_equal(u64(c), rc), name
+        assert np.array_equal(u64(p), rp), name
+    tr.close()
+
+
 def test_bitmap_or_merge_kernel():
     rng = np.random.default_rng(4)
     g, W = 4, 70001
