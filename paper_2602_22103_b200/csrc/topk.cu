@@ -76,7 +76,10 @@ __device__ __forceinline__ void hist_add(unsigned* h, bool valid, unsigned bin) 
 
 // Streaming helper: visit every pair index i < n2 of this grid with kU 16-byte loads in
 // flight per thread (enough memory-level parallelism to stream P x 8 bytes at HBM speed).
-constexpr int kU = 8;
+#ifndef PASTA_TOPK_U
+#define PASTA_TOPK_U 8
+#endif
+constexpr int kU = PASTA_TOPK_U;  // 16-byte loads in flight per thread in the streaming passes
 template <typename F>
 __device__ __forceinline__ void stream_pairs(const ulonglong2* __restrict__ pc2, uint64_t n2, F f) {
   const uint64_t stride = (uint64_t)gridDim.x * kBlock * kU;
@@ -125,72 +128,111 @@ __device__ void dev_first(const uint64_t* __restrict__ pc, uint64_t P, unsigned*
     if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
-// Pick the pass-1 bin holding the K'-th largest count (block 0, all threads): nnz and
-// K' = min(K, nnz), then chunked suffix sums from the top bin down.
-__device__ void dev_select_first(volatile State* st, unsigned* hist, uint64_t K, unsigned long long* sm) {
-  constexpr int per = (kFirstBins + kBlock - 1) / kBlock;  // bins per thread
-  const int t = threadIdx.x;
+// Block-wide search (block 0, all threads) for the bin d of hist[0, nb) holding rank
+// `rem` counted from the top: suffix(d + 1) < rem <= suffix(d). Thread t sums bins
+// [t * per, (t + 1) * per); a block suffix scan of those sums (warp shuffles + one
+// shared step) finds the one thread whose chunk holds d, which walks its <= per bins.
+// Returns true in that thread only, with d, the count above bin d and the rank left
+// inside it. `total` (every thread) = the sum of all bins.
+__device__ bool block_find_bin(const unsigned* hist, int nb, int per, unsigned long long rem,
+                               unsigned long long* sm, unsigned long long& total, int& d_out,
+                               unsigned long long& above_out, unsigned long long& rem_out) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   unsigned long long mine = 0;
   for (int j = 0; j < per; ++j) {
     const int d = t * per + j;
-    if (d < kFirstBins) mine += hist[d];
+    if (d < nb) mine += hist[d];
   }
-  sm[t] = mine;
+  unsigned long long v = mine;  // suffix sum within the warp (lanes >= lane)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long x = __shfl_down_sync(kFull, v, o);
+    if (lane + o < 32) v += x;
+  }
+  if (lane == 0) sm[w] = v;
   __syncthreads();
-  if (t == 0) {
-    unsigned long long nnz = 0;
-    for (int i = 0; i < kBlock; ++i) nnz += sm[i];
-    const unsigned long long kp = nnz < K ? nnz : K;
+  unsigned long long after = 0;  // warps above this one
+  total = 0;
+  for (int i = 0; i < kBlock / 32; ++i) {
+    total += sm[i];
+    if (i > w) after += sm[i];
+  }
+  __syncthreads();
+  const unsigned long long S = v + after, S_next = S - mine;  // suffix from my chunk / the next
+  if (!(S_next < rem && rem <= S)) return false;
+  rem -= S_next;
+  unsigned long long above = S_next;
+  int d = t * per + per - 1;
+  if (d > nb - 1) d = nb - 1;
+  for (; d > t * per; --d) {
+    if (hist[d] >= rem) break;
+    rem -= hist[d];
+    above += hist[d];
+  }
+  d_out = d;
+  above_out = above;
+  rem_out = rem;
+  return true;
+}
+
+// Pick the pass-1 bin holding the K'-th largest count (block 0, all threads): nnz,
+// K' = min(K, nnz) and the bin; then the threshold state.
+__device__ void dev_select_first(volatile State* st, unsigned* hist, uint64_t K, unsigned long long* sm) {
+  constexpr int per = (kFirstBins + kBlock - 1) / kBlock;  // bins per thread
+  unsigned long long nnz = 0, above = 0, rem = 0;
+  int d = 0;
+  // the rank is only known after the total: first pass for nnz, the search inside
+  unsigned long long part = 0;
+  for (int j = 0; j < per; ++j) {
+    const int b = threadIdx.x * per + j;
+    if (b < kFirstBins) part += hist[b];
+  }
+  part = warp_sum_u64(part);
+  if ((threadIdx.x & 31) == 0) sm[kBlock / 32 + (threadIdx.x >> 5)] = part;
+  __syncthreads();
+  for (int i = 0; i < kBlock / 32; ++i) nnz += sm[kBlock / 32 + i];
+  const unsigned long long kp = nnz < K ? nnz : K;
+  if (kp == 0) {
+    if (threadIdx.x == 0) {
+      st->nnz = 0;
+      st->kprime = 0;
+      st->gt_slots = 0;
+      st->need = 0;
+      st->done = 1;
+      st->T = ~0ull;
+    }
+  } else if (block_find_bin(hist, kFirstBins, per, kp, sm, nnz, d, above, rem)) {
+    const unsigned long long here = hist[d];
+    int bits = 0;  // the bin is [lo, lo + 2^bits - 1]
+    unsigned long long lo = (unsigned long long)d;
+    if (d >= 64) {
+      const int L = (d - 64) / 32 + 7;
+      bits = L - 6;
+      lo = (32ull + (unsigned)((d - 64) % 32)) << bits;
+    }
     st->nnz = nnz;
     st->kprime = kp;
     st->gt_slots = 0;
     st->need = 0;
-    if (kp == 0) {
-      st->done = 1;
-      st->T = ~0ull;
+    st->lo = lo;
+    st->above = above;
+    st->remaining = rem;
+    if (rem == here) {  // the whole bin is taken: no ties to break
+      st->done = 2;
+      st->T = lo - 1;
+    } else if (bits == 0) {  // exact value: take the first `rem` pages with this count
+      st->done = 2;
+      st->T = lo;
+      st->need = rem;
     } else {
-      unsigned long long rem = kp, above = 0;
-      int c = kBlock - 1;
-      for (; c > 0; --c) {
-        if (sm[c] >= rem) break;
-        rem -= sm[c];
-        above += sm[c];
-      }
-      int d = c * per + per - 1;
-      if (d > kFirstBins - 1) d = kFirstBins - 1;
-      for (; d > c * per; --d) {
-        if (hist[d] >= rem) break;
-        rem -= hist[d];
-        above += hist[d];
-      }
-      const unsigned long long here = hist[d];
-      int bits = 0;  // the bin is [lo, lo + 2^bits - 1]
-      unsigned long long lo = (unsigned long long)d;
-      if (d >= 64) {
-        const int L = (d - 64) / 32 + 7;
-        bits = L - 6;
-        lo = (32ull + (unsigned)((d - 64) % 32)) << bits;
-      }
-      st->lo = lo;
-      st->above = above;
-      st->remaining = rem;
-      if (rem == here) {  // the whole bin is taken: no ties to break
-        st->done = 2;
-        st->T = lo - 1;
-      } else if (bits == 0) {  // exact value: take the first `rem` pages with this count
-        st->done = 2;
-        st->T = lo;
-        st->need = rem;
-      } else {
-        const int w = bits < kDigitBits ? bits : kDigitBits;
-        st->width = w;
-        st->shift = bits - w;
-        st->done = 0;
-      }
+      const int w = bits < kDigitBits ? bits : kDigitBits;
+      st->width = w;
+      st->shift = bits - w;
+      st->done = 0;
     }
   }
   __syncthreads();
-  for (int i = t; i < kBins; i += kBlock) hist[i] = 0;
+  for (int i = threadIdx.x; i < kBins; i += kBlock) hist[i] = 0;
 }
 
 // One radix digit among the counts of the selected bin.
@@ -214,39 +256,21 @@ __device__ void dev_digit(const uint64_t* __restrict__ pc, uint64_t P, volatile 
     if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
-// Choose the digit (block 0, all threads): chunked suffix sums from the top bin down.
+// Choose the digit (block 0, all threads) where the running count from the top
+// reaches the remaining rank.
 __device__ void dev_select_digit(volatile State* st, unsigned* hist, unsigned long long* sm) {
   const int shift = (int)st->shift, width = (int)st->width;
+  const unsigned long long rem0 = st->remaining, above0 = st->above, lo0 = st->lo;
+  __syncthreads();  // every thread has read the state before the winner rewrites it
   const int nb = 1 << width;
   const int per = (nb + kBlock - 1) / kBlock;  // bins per thread (<= 8)
-  const int t = threadIdx.x;
-  unsigned long long mine = 0;
-  for (int j = 0; j < per; ++j) {
-    const int d = t * per + j;
-    if (d < nb) mine += hist[d];
-  }
-  sm[t] = mine;
-  __syncthreads();
-  if (t == 0) {
-    // thread chunks from the top: find the chunk where the running sum reaches rem
-    unsigned long long rem = st->remaining, above = st->above;
-    int c = kBlock - 1;
-    for (; c > 0; --c) {
-      if (sm[c] >= rem) break;
-      rem -= sm[c];
-      above += sm[c];
-    }
-    int d = c * per + per - 1;
-    if (d > nb - 1) d = nb - 1;
-    for (; d > c * per; --d) {
-      if (hist[d] >= rem) break;
-      rem -= hist[d];
-      above += hist[d];
-    }
+  unsigned long long total = 0, above = 0, rem = 0;
+  int d = 0;
+  if (block_find_bin(hist, nb, per, rem0, sm, total, d, above, rem)) {
     const unsigned long long here = hist[d];
-    const unsigned long long lo = st->lo + ((unsigned long long)d << shift);
+    const unsigned long long lo = lo0 + ((unsigned long long)d << shift);
     st->lo = lo;
-    st->above = above;
+    st->above = above0 + above;
     st->remaining = rem;
     if (rem == here) {  // the whole bin is taken: no ties to break
       st->done = 2;
@@ -262,7 +286,7 @@ __device__ void dev_select_digit(volatile State* st, unsigned* hist, unsigned lo
     }
   }
   __syncthreads();
-  for (int i = t; i < nb; i += kBlock) hist[i] = 0;
+  for (int i = threadIdx.x; i < nb; i += kBlock) hist[i] = 0;
 }
 
 // Gather (one pass over this CTA's contiguous page range): every page with count > T
