@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--stream-batch", type=int, default=0,
                     help="also time streaming mode: one pasta_analyze per batch of this many records "
                          "(524288 = the paper's 4 MB buffer), captured in a CUDA graph")
+    ap.add_argument("--merge", default="peer", choices=["peer", "nccl"],
+                    help="N > 1 merge: peer = pasta_peer_reduce over CUDA-IPC-mapped peer memory (dist.PeerMerger), "
+                         "nccl = reduce_scatter / all_gather + pasta_bitmap_or (dist.ShardedMerger)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -236,8 +239,17 @@ def run_ours(args):
         tr.register_alloc(b, s)
     hist = tr.histograms(plan.page_shift, n_kernels=nk_loc, kernel_rows=plan.want_kernel_rows,
                          kernel_pages=plan.want_kernel_pages, pad_pages_to=64 * world)
-    # N > 1: page counts reduce-scattered, top-K from shard candidates (dist.ShardedMerger)
-    merger = pdist.ShardedMerger(tr, hist, plan.topk, group) if world > 1 else None
+    # N > 1: each rank merges its page shard from every rank's counts over peer memory
+    # (dist.PeerMerger) or through NCCL (dist.ShardedMerger); top-K from shard candidates
+    merger, merge_kind = None, None
+    if world > 1:
+        if args.merge == "peer":
+            try:
+                merger, merge_kind = pdist.PeerMerger(tr, hist, plan.topk, group), "peer"
+            except Exception as exc:  # no peer access / IPC on this node: the NCCL merge
+                print(f"bench: peer merge unavailable ({exc!r}); using the NCCL merge", file=sys.stderr)
+        if merger is None:
+            merger, merge_kind = pdist.ShardedMerger(tr, hist, plan.topk, group), "nccl"
     K = max(plan.topk)
     top_out = (torch.empty(K, dtype=torch.int64, device=dev), torch.empty(K, dtype=torch.int64, device=dev),
                torch.empty(1, dtype=torch.int64, device=dev))
@@ -314,6 +326,7 @@ def run_ours(args):
                        "topk": plan.topk, "kernel_rows": plan.want_kernel_rows,
                        "kernel_pages": plan.want_kernel_pages,
                        "shard": "kernel-aligned contiguous, %d records on rank 0" % n_loc,
+                       "merge": merge_kind,
                        "l2": "inputs (%.1f GiB/rank) larger than L2; no flush" % (8 * n_loc / 2**30)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,

@@ -250,6 +250,27 @@ int pasta_topk(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t
 int pasta_bitmap_or(pasta_trace* h, const uint64_t* gathered, uint32_t g, uint64_t words, uint64_t* out_bitmap,
                     uint64_t* out_popcount);
 
+/* Multi-GPU merge over peer memory (every count
+ * is a pointwise sum over a partition of the records; working sets merge by MAX, R11).
+ * src[r] (a HOST array of g <= 16 pointers) are DEVICE pointers readable from this
+ * handle's device: local memory, or other ranks' buffers mapped with CUDA IPC (peer
+ * access over NVLink / NVSwitch; see pasta_enable_peer). op PASTA_PEER_SUM:
+ * out[i] = sum_r src[r][lo + i] (u64, wrapping) for i < n; if out_bitmap or
+ * out_popcount is non-NULL, lo and n must be multiples of 64 (else EINVAL) and the same
+ * pass writes out_bitmap[i / 64] bit i % 64 = (out[i] != 0) and adds the number of
+ * non-zero out[i] to *out_popcount (device u64). op PASTA_PEER_MAX: out[i] = max_r
+ * src[r][lo + i] (no bitmap). out must not overlap any source range. The sources must
+ * be complete (producers synchronized, e.g. a barrier after their analyze) and stay
+ * unchanged until this call's stream work is done. */
+enum { PASTA_PEER_SUM = 0u, PASTA_PEER_MAX = 1u };
+int pasta_peer_reduce(pasta_trace* h, const uint64_t* const* src, uint32_t g, uint64_t lo, uint64_t n, uint32_t op,
+                      uint64_t* out, uint64_t* out_bitmap, uint64_t* out_popcount);
+
+/* Enable this handle's device to access memory of CUDA device `peer_device` (for
+ * pasta_peer_reduce sources that live on another GPU). Idempotent; EINVAL for an
+ * invalid device, ECUDA if the pair has no peer access. */
+int pasta_enable_peer(pasta_trace* h, int peer_device);
+
 /* Multi-GPU top-K merge: g shard-local top-k lists, rank-major
  * (cand_page[r*k + i], cand_count[r*k + i], device pointers; pages relative to shard r,
  * empty slots have count 0), shard r covering global pages [r*shard_pages,

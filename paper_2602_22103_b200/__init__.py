@@ -87,6 +87,8 @@ _SIGS = {
     "pasta_topk": (_int, [_vp, _vp, _u64, _u32, _vp, _vp, _vp]),
     "pasta_bitmap_or": (_int, [_vp, _vp, _u32, _u64, _vp, _vp]),
     "pasta_topk_merge": (_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp]),
+    "pasta_peer_reduce": (_int, [_vp, ctypes.POINTER(_vp), _u32, _u64, _u64, _u32, _vp, _vp, _vp]),
+    "pasta_enable_peer": (_int, [_vp, _int]),
     "pasta_sync": (_int, [_vp]),
     "pasta_close": (_int, [_vp]),
     "pasta_strerror": (ctypes.c_char_p, [_int]),
@@ -195,6 +197,20 @@ def pasta_bitmap_or(h, gathered, g: int, words: int, out_bitmap, out_popcount=No
 def pasta_topk_merge(h, cand_page, cand_count, g: int, k: int, shard_pages: int, out_page, out_count, out_found):
     _check(_lib.pasta_topk_merge(h, _ptr(cand_page), _ptr(cand_count), g, k, shard_pages, _ptr(out_page),
                                  _ptr(out_count), _ptr(out_found)), "pasta_topk_merge")
+
+
+PASTA_PEER_SUM, PASTA_PEER_MAX = 0, 1
+
+
+def pasta_peer_reduce(h, srcs, lo: int, n: int, out, out_bitmap=None, out_popcount=None, op: int = PASTA_PEER_SUM):
+    """srcs: device addresses (ints) or tensors readable from h's device (local or CUDA-IPC mapped)."""
+    arr = (_vp * len(srcs))(*[_ptr(s) for s in srcs])
+    _check(_lib.pasta_peer_reduce(h, arr, len(srcs), lo, n, op, _ptr(out), _ptr(out_bitmap), _ptr(out_popcount)),
+           "pasta_peer_reduce")
+
+
+def pasta_enable_peer(h, peer_device: int):
+    _check(_lib.pasta_enable_peer(h, peer_device), "pasta_enable_peer")
 
 
 def pasta_sync(h):
@@ -383,6 +399,12 @@ class Trace:
     def topk_merge(self, cand_page, cand_count, g: int, k: int, shard_pages: int, out):
         pasta_topk_merge(self.h, cand_page, cand_count, g, k, shard_pages, out[0], out[1], out[2])
         return out
+
+    def peer_reduce(self, srcs, lo: int, n: int, out, out_bitmap=None, out_popcount=None, op: int = 0):
+        pasta_peer_reduce(self.h, srcs, lo, n, out, out_bitmap, out_popcount, op)
+
+    def enable_peer(self, peer_device: int):
+        pasta_enable_peer(self.h, peer_device)
 
     def sync(self):
         pasta_sync(self.h)

@@ -117,6 +117,10 @@ __device__ __forceinline__ void atomic_max_u64(uint64_t* p, uint64_t v) {
   atomicMax(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
 }
 
+// Streaming 8-byte load (evict-first in L1/L2: merge sources are read once).
+__device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t* p) {
+  return static_cast<uint64_t>(__ldcs(reinterpret_cast<const unsigned long long*>(p)));
+}
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);

@@ -115,6 +115,17 @@ cudaError_t launch_plan_write(const uint64_t* rows, uint32_t n_kernels, uint64_t
 cudaError_t launch_bitmap_or(const uint64_t* gathered, uint32_t g, uint64_t words, uint64_t* out,
                              uint64_t* popcount, int grid, cudaStream_t st);
 
+// Peer-memory merge (peer.cu): sources are device pointers readable from this device
+// (local, peer-enabled or CUDA-IPC-mapped allocations of other ranks).
+constexpr int kMaxPeers = 16;
+struct PeerSrc {
+  const uint64_t* p[kMaxPeers];
+};
+// op 0: out[i] = sum_r src[r][lo + i], and with out_bitmap / out_popcount (n and lo
+// multiples of 64) the bitmap words of out and their popcount (+=); op 1: MAX.
+cudaError_t launch_peer_reduce(const PeerSrc& src, uint32_t g, uint64_t lo, uint64_t n, uint32_t op, uint64_t* out,
+                               uint64_t* out_bitmap, uint64_t* out_popcount, int grid, cudaStream_t st);
+
 // Top-K scratch layout (device), sized by topk_scratch_bytes(k, grid).
 size_t topk_scratch_bytes(uint64_t k, int grid);
 // Enqueues the whole radix-select + gather + sort pipeline; `launch` is called once

@@ -717,6 +717,40 @@ int pasta_bitmap_or(pasta_trace* h, const uint64_t* gathered, uint32_t g, uint64
   return cuda_status(e);
 }
 
+int pasta_peer_reduce(pasta_trace* h, const uint64_t* const* src, uint32_t g, uint64_t lo, uint64_t n, uint32_t op,
+                      uint64_t* out, uint64_t* out_bitmap, uint64_t* out_popcount) {
+  if (!h || !src || !out || g == 0 || g > (uint32_t)kMaxPeers || n == 0) return PASTA_EINVAL;
+  if (op != PASTA_PEER_SUM && op != PASTA_PEER_MAX) return PASTA_EINVAL;
+  const bool bits = out_bitmap || out_popcount;
+  if (bits && (op != PASTA_PEER_SUM || lo % 64 || n % 64)) return PASTA_EINVAL;
+  PeerSrc s{};
+  for (uint32_t r = 0; r < g; ++r) {
+    if (!src[r]) return PASTA_EINVAL;
+    s.p[r] = src[r];
+  }
+  DeviceGuard dg(h->device);
+  Timed t(h, PASTA_PH_MERGE, h->stream);
+  cudaError_t e = launch_peer_reduce(s, g, lo, n, op, out, out_bitmap, out_popcount, h->sm_count * 8, h->stream);
+  ++h->launches;
+  return cuda_status(e);
+}
+
+int pasta_enable_peer(pasta_trace* h, int peer_device) {
+  if (!h) return PASTA_EINVAL;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || peer_device < 0 || peer_device >= count) return PASTA_EINVAL;
+  if (peer_device == h->device) return PASTA_OK;
+  DeviceGuard dg(h->device);
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, h->device, peer_device) != cudaSuccess || !can) return PASTA_ECUDA;
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // clear the sticky-free status
+    return PASTA_OK;
+  }
+  return cuda_status(e);
+}
+
 int pasta_prefetch_plan(pasta_trace* h, const uint64_t* rows, uint32_t n_kernels, uint32_t level,
                         uint64_t* plan_offsets, uint64_t* plan_ranges, uint64_t cap, uint64_t* out_total) {
   if (!h || !rows || !plan_offsets || !out_total || n_kernels == 0) return PASTA_EINVAL;

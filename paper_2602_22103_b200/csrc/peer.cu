@@ -1,0 +1,107 @@
+// peer.cu -- S5 merge over peer memory: one kernel reads every
+// rank's partial counts directly (NVLink / NVSwitch loads through CUDA IPC mappings)
+// and reduces them, fused with the bitmap and unique-page count of the reduced range.
+//
+// Every count output is a pointwise sum over any partition of the records (SPEC
+// S:291-299), so the merged page count of page p is sum_r counts_r[p]; the bitmap
+// bit p is merged_count[p] != 0 (R14); working sets merge by MAX (R11). The NCCL path
+// (reduce_scatter, then all_gather of bitmaps, then pasta_bitmap_or) needs three
+// passes and a gathered copy of every rank's bitmap; here rank r reads its shard of
+// pages from all g ranks once and emits counts, bitmap words and popcount together.
+#include <cstdint>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace pasta {
+namespace {
+
+using namespace dev;
+
+constexpr int kBlock = 256;
+
+// Words of 64 pages: warp w of the grid takes word w (grid-stride); lane l sums pages
+// 64w + l and 64w + 32 + l over the g sources (coalesced 256-byte rows per source, 2g
+// loads in flight per lane), writes them, and the two ballots are the bitmap word.
+__global__ void __launch_bounds__(kBlock) peer_sum_bitmap_kernel(PeerSrc src, uint32_t g, uint64_t lo,
+                                                                 uint64_t words, uint64_t* __restrict__ out,
+                                                                 uint64_t* __restrict__ out_bitmap,
+                                                                 uint64_t* __restrict__ out_popcount) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp0 = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * kBlock) >> 5;
+  uint64_t pop = 0;
+  for (uint64_t w = warp0; w < words; w += nwarps) {
+    const uint64_t i0 = 64 * w + lane, i1 = i0 + 32;
+    uint64_t v0[kMaxPeers], v1[kMaxPeers];
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r) {
+      if (r < (int)g) {
+        v0[r] = ld_stream_u64(src.p[r] + lo + i0);
+        v1[r] = ld_stream_u64(src.p[r] + lo + i1);
+      }
+    }
+    uint64_t c0 = 0, c1 = 0;
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r) {
+      if (r < (int)g) {
+        c0 += v0[r];
+        c1 += v1[r];
+      }
+    }
+    out[i0] = c0;
+    out[i1] = c1;
+    const uint64_t word = (uint64_t)__ballot_sync(kFull, c0 != 0) | ((uint64_t)__ballot_sync(kFull, c1 != 0) << 32);
+    if (lane == 0) {
+      if (out_bitmap) out_bitmap[w] = word;
+      pop += (uint64_t)__popcll(word);
+    }
+  }
+  if (out_popcount) {
+    __shared__ unsigned long long part[kBlock / 32];
+    if (lane == 0) part[threadIdx.x >> 5] = pop;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long s = 0;
+      for (int i = 0; i < kBlock / 32; ++i) s += part[i];
+      if (s) atomicAdd(reinterpret_cast<unsigned long long*>(out_popcount), s);
+    }
+  }
+}
+
+// Elementwise SUM or MAX of n values from g sources (small parts, WS slots).
+template <bool kMax>
+__global__ void __launch_bounds__(kBlock) peer_elementwise_kernel(PeerSrc src, uint32_t g, uint64_t lo, uint64_t n,
+                                                                   uint64_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kBlock) {
+    uint64_t acc = 0;
+    for (uint32_t r = 0; r < g; ++r) {
+      const uint64_t v = ld_stream_u64(src.p[r] + lo + i);
+      acc = kMax ? (v > acc ? v : acc) : acc + v;
+    }
+    out[i] = acc;
+  }
+}
+
+int grid_for(uint64_t items, int per_block, int cap) {
+  const uint64_t b = (items + per_block - 1) / per_block;
+  return (int)(b < 1 ? 1 : (b > (uint64_t)cap ? cap : b));
+}
+
+}  // namespace
+
+cudaError_t launch_peer_reduce(const PeerSrc& src, uint32_t g, uint64_t lo, uint64_t n, uint32_t op, uint64_t* out,
+                               uint64_t* out_bitmap, uint64_t* out_popcount, int grid, cudaStream_t st) {
+  if (op == 0 && (out_bitmap || out_popcount)) {
+    const uint64_t words = n / 64;
+    peer_sum_bitmap_kernel<<<grid_for(words, kBlock / 32, grid), kBlock, 0, st>>>(src, g, lo, words, out,
+                                                                                 out_bitmap, out_popcount);
+  } else if (op == 0) {
+    peer_elementwise_kernel<false><<<grid_for(n, kBlock, grid), kBlock, 0, st>>>(src, g, lo, n, out);
+  } else {
+    peer_elementwise_kernel<true><<<grid_for(n, kBlock, grid), kBlock, 0, st>>>(src, g, lo, n, out);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace pasta

@@ -141,3 +141,110 @@ class ShardedMerger:
             gather_candidates(lp, lc, cp, cc, self.group)
             self.tr.topk_merge(cp, cc, self.world, k, self.S, self.out[k])
         return self.out
+
+
+class PeerMerger:
+    """ShardedMerger's results through peer memory instead of NCCL data movement
+    (DESIGN.md section 5): every rank maps the other ranks' result buffers once (CUDA
+    IPC handles exchanged over the process group; NVLink / NVSwitch loads at run time)
+    and one pasta_peer_reduce kernel per merge reads its shard of every rank's page
+    counts, writing the merged counts together with the shard's bitmap words and
+    unique-page count. A second phase (after a barrier) copies the shard bitmaps,
+    unique counts and top-k candidates of the peers the same way. The process group
+    carries only the handle exchange and the barriers.
+
+    Outputs as ShardedMerger: hist.small merged (SUMs; WS slots MAX), hist.page_bitmap
+    and totals[UNIQUE_PAGES] global, the rank's merged page shard in `shard`, and the
+    global top-k lists (returned). totals[MAX_KERNEL] is not merged (an argmax needs the
+    merged kernel rows). Histograms must be allocated with pad_pages_to = world * 64."""
+
+    def __init__(self, trace, hist, ks, group=None):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        self.tr, self.hist, self.group = trace, hist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        assert hist.P_pad % (self.world * 64) == 0, "allocate Histograms with pad_pages_to = world * 64"
+        dev = hist.packed.device
+        self.S = hist.P_pad // self.world
+        self.Sw = self.S // 64
+        self.shard = torch.zeros(self.S, dtype=torch.int64, device=dev)
+        self.shard_bm = torch.zeros(self.Sw, dtype=torch.int64, device=dev)
+        self.pop = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.small_out = torch.zeros_like(hist.small)
+        self.bm_full = torch.zeros(self.world * self.Sw, dtype=torch.int64, device=dev)
+        self.ks = tuple(ks)
+        self.loc = {k: (torch.zeros(k, dtype=torch.int64, device=dev), torch.zeros(k, dtype=torch.int64, device=dev),
+                        torch.zeros(1, dtype=torch.int64, device=dev)) for k in self.ks}
+        self.cand = {k: (torch.empty(self.world * k, dtype=torch.int64, device=dev),
+                         torch.empty(self.world * k, dtype=torch.int64, device=dev)) for k in self.ks}
+        self.out = {k: (torch.empty(k, dtype=torch.int64, device=dev), torch.empty(k, dtype=torch.int64, device=dev),
+                        torch.empty(1, dtype=torch.int64, device=dev)) for k in self.ks}
+        mine = [hist.packed, self.shard_bm, self.pop]
+        for k in self.ks:
+            mine += [self.loc[k][0], self.loc[k][1]]
+        torch.cuda.synchronize(dev)
+        shared = [reduce_tensor(t) for t in mine]
+        allh = [None] * self.world
+        dist.all_gather_object(allh, (dev.index if dev.index is not None else torch.cuda.current_device(), shared),
+                               group=group)
+        self.peers, err = [], None
+        try:
+            for r, (devr, hs) in enumerate(allh):
+                if r == self.rank:
+                    self.peers.append(mine)
+                    continue
+                if devr != hist.packed.device.index:
+                    trace.enable_peer(devr)
+                self.peers.append([fn(*args) for fn, args in hs])
+        except Exception as exc:  # e.g. no peer access between these GPUs
+            err = f"rank {self.rank}: {exc!r}"
+        errs = [None] * self.world
+        dist.all_gather_object(errs, err, group=group)  # every rank takes the same decision
+        bad = [e for e in errs if e]
+        if bad:
+            self.peers = []
+            raise RuntimeError("peer mapping failed: " + "; ".join(bad))
+
+    def _addr(self, t, elem=0):
+        return t.data_ptr() + 8 * elem
+
+    def merge(self):
+        from . import PASTA_PEER_MAX, T_UNIQUE_PAGES
+
+        h, tr, W, S = self.hist, self.tr, self.world, self.S
+        P_pad = h.P_pad
+        self.pop.zero_()
+        torch.cuda.synchronize(h.packed.device)
+        tr.sync()
+        dist.barrier(group=self.group)  # every rank's local analyze is complete
+        # phase 1: my page shard of every rank -> merged counts + bitmap words + popcount
+        tr.peer_reduce([self._addr(p[0], self.rank * S) for p in self.peers], 0, S, self.shard, self.shard_bm,
+                       self.pop)
+        n_small = h.small.numel()
+        tr.peer_reduce([self._addr(p[0], P_pad) for p in self.peers], 0, n_small, self.small_out)
+        for slot in _WS_SLOTS:
+            e = h.max_ids + slot
+            tr.peer_reduce([self._addr(p[0], P_pad + e) for p in self.peers], 0, 1, self._addr(self.small_out, e),
+                           op=PASTA_PEER_MAX)
+        for k in self.ks:
+            tr.topk(self.shard, k, out=self.loc[k])
+        tr.sync()
+        dist.barrier(group=self.group)  # every shard, bitmap word, popcount and candidate list is ready
+        # phase 2: the peers' shard bitmaps, unique counts and candidates
+        for r, p in enumerate(self.peers):
+            tr.peer_reduce([p[1]], 0, self.Sw, self._addr(self.bm_full, r * self.Sw))
+        tr.peer_reduce([p[2] for p in self.peers], 0, 1, self._addr(self.small_out, h.max_ids + T_UNIQUE_PAGES))
+        for i, k in enumerate(self.ks):
+            cp, cc = self.cand[k]
+            for r, p in enumerate(self.peers):
+                tr.peer_reduce([p[3 + 2 * i]], 0, k, self._addr(cp, r * k))
+                tr.peer_reduce([p[4 + 2 * i]], 0, k, self._addr(cc, r * k))
+        tr.sync()
+        dist.barrier(group=self.group)  # nobody reads this rank's buffers any more
+        h.small.copy_(self.small_out)
+        h.page_bitmap.copy_(self.bm_full[:h.words])
+        for k in self.ks:
+            cp, cc = self.cand[k]
+            tr.topk_merge(cp, cc, W, k, S, self.out[k])
+        return self.out

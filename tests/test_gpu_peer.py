@@ -1,0 +1,167 @@
+"""GPU tests of the peer-memory merge: pasta_peer_reduce against
+plain numpy sums / maxes / bitmaps, and dist.PeerMerger with two processes on one GPU
+(CUDA IPC mappings of each other's buffers, a gloo group for the handle exchange and
+barriers) against the oracle over the whole trace (SPEC S:291-299 partition fold).
+The box has one GPU, so the peer loads stay on the device; on an NVSwitch box the
+same mappings are NVLink loads."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2602_22103_b200 as pb  # noqa: E402
+import oracle  # noqa: E402
+import tracegen  # noqa: E402
+from tests.harness import u64  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint64).view(np.int64)).to(DEV)
+
+
+@pytest.mark.parametrize("g", [1, 3, 8, 16])
+def test_peer_reduce_sum_bitmap_max(g):
+    rng = np.random.default_rng(g)
+    n_all = 64 * 1001
+    srcs = []
+    for r in range(g):
+        a = rng.integers(0, 1 << 64, size=n_all, dtype=np.uint64)
+        a[rng.random(n_all) < 0.7] = 0  # zero pages
+        srcs.append(a)
+    srcs[0][:64 * 3] = 0  # words with no set bit in any source
+    for a in srcs[1:]:
+        a[:64 * 3] = 0
+    dsrc = [_t(a) for a in srcs]
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    lo, n = 64 * 7, 64 * 990
+    out = torch.zeros(n, dtype=torch.int64, device=DEV)
+    bm = torch.zeros(n // 64, dtype=torch.int64, device=DEV)
+    pop = torch.full((1,), 5, dtype=torch.int64, device=DEV)
+    tr.peer_reduce(dsrc, lo, n, out, bm, pop)
+    mx = torch.zeros(n - 3, dtype=torch.int64, device=DEV)
+    tr.peer_reduce(dsrc, lo + 1, n - 3, mx, op=pb.PASTA_PEER_MAX)
+    tr.sync()
+    with np.errstate(over="ignore"):
+        ref = np.zeros(n, dtype=np.uint64)
+        for a in srcs:
+            ref += a[lo:lo + n]
+    assert np.array_equal(u64(out), ref)
+    bits = (ref != 0).reshape(-1, 64)
+    ref_bm = (bits.astype(np.uint64) << np.arange(64, dtype=np.uint64)).sum(axis=1, dtype=np.uint64)
+    assert np.array_equal(u64(bm), ref_bm)
+    assert int(u64(pop)[0]) == 5 + int((ref != 0).sum())
+    ref_max = np.max(np.stack([a[lo + 1:lo + 1 + n - 3] for a in srcs]), axis=0)
+    assert np.array_equal(u64(mx), ref_max)
+    # misaligned bitmap ranges, too many sources, MAX with a bitmap: EINVAL
+    for args, kw in (((dsrc, lo + 1, n, out, bm), {}), ((dsrc, lo, n - 1, out, bm), {}),
+                     ((dsrc * 17, lo, 64, out), {}), ((dsrc, lo, n, out, bm), {"op": pb.PASTA_PEER_MAX})):
+        with pytest.raises(pb.PastaError):
+            tr.peer_reduce(*args, **kw)
+    tr.close()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import traceback
+
+    try:
+        _work(rank, world, port, q)
+    except BaseException:  # report instead of leaving the parent waiting on the queue
+        q.put(("error", rank, traceback.format_exc()))
+        raise
+
+
+def _work(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_22103_b200 import dist as pdist
+
+        dev = torch.device("cuda:0")
+        torch.cuda.set_device(dev)
+        p = tracegen.build_plan("tiny", seed=17)
+        j0, j1, k0, k1 = p.shard(rank, world)
+        rec = torch.empty(j1 - j0, dtype=torch.int64, device=dev)
+        tracegen.device_records(tracegen.DevicePlan(p, dev), rec, j0, j1)
+        ko = torch.from_numpy((p.kernel_offsets[k0:k1 + 1] - np.uint64(j0)).view(np.int64).copy()).to(dev)
+        tr = pb.Trace(dev, p.va_lo, p.va_hi, len(p.allocs), len(p.allocs))
+        for b, s in p.allocs:
+            tr.register_alloc(b, s)
+        hist = tr.histograms(p.page_shift, n_kernels=k1 - k0, kernel_rows=True, pad_pages_to=64 * world)
+        merger = pdist.PeerMerger(tr, hist, (16, 3))
+        for step in range(2):  # a second merge on re-analyzed buffers (barrier discipline)
+            hist.zero_()
+            tr.analyze(rec, p.page_shift, hist, kernel_offsets=ko)
+            outs = merger.merge()
+            tr.sync()
+            torch.cuda.synchronize()
+        q.put((rank, u64(merger.shard).copy(), u64(hist.small).copy(), u64(hist.page_bitmap).copy(),
+               {k: tuple(u64(x).copy() for x in v) for k, v in outs.items()}, merger.S))
+        dist.barrier()
+        tr.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_merger_two_ranks_one_gpu():
+    import torch.multiprocessing as mp
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = {}
+    for _ in range(world):
+        r = q.get()
+        assert r[0] != "error", f"rank {r[1]} failed:\n{r[2]}"
+        res[r[0]] = r
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+
+    p = tracegen.build_plan("tiny", seed=17)
+    o = oracle.OracleTrace(p.va_lo, p.va_hi, len(p.allocs), len(p.allocs))
+    for b, s in p.allocs:
+        o.register_alloc(b, s)
+    o.analyze(tracegen.host_records(p), p.kernel_offsets, p.page_shift, kernel_rows=True)
+    bm, uniq = o.bitmap()
+    S = res[0][5]
+    pages = np.zeros(world * S, dtype=np.uint64)
+    pages[:len(o.page_counts)] = o.page_counts
+    A = len(p.allocs)
+    for r in range(world):
+        _, shard, small, pbm, outs, _ = res[r]
+        assert np.array_equal(shard, pages[r * S:(r + 1) * S]), f"rank {r}: merged page shard"
+        assert np.array_equal(small[:A], o.alloc_counts[:A]), f"rank {r}: alloc counts"
+        tot = small[len(o.alloc_counts):len(o.alloc_counts) + 8]
+        assert tot[:3].tolist() == o.totals.tolist(), f"rank {r}: totals"
+        assert int(tot[3]) == uniq, f"rank {r}: unique pages"
+        fp, ws = o.footprints()
+        assert int(tot[4]) == ws, f"rank {r}: WS_obj (MAX)"
+        assert np.array_equal(pbm, bm), f"rank {r}: bitmap"
+        for k in (16, 3):
+            rp, rc, rf = oracle.topk(o.page_counts, k)
+            assert int(outs[k][2][0]) == rf and np.array_equal(outs[k][0], rp) and np.array_equal(outs[k][1], rc), \
+                f"rank {r}: top-{k}"
