@@ -77,17 +77,17 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, two):
     import traceback
 
     try:
-        _work(rank, world, port, q)
+        _work(rank, world, port, q, two)
     except BaseException:  # report instead of leaving the parent waiting on the queue
         q.put(("error", rank, traceback.format_exc()))
         raise
 
 
-def _work(rank, world, port, q):
+def _work(rank, world, port, q, two):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -103,9 +103,14 @@ def _work(rank, world, port, q):
         rec = torch.empty(j1 - j0, dtype=torch.int64, device=dev)
         tracegen.device_records(tracegen.DevicePlan(p, dev), rec, j0, j1)
         ko = torch.from_numpy((p.kernel_offsets[k0:k1 + 1] - np.uint64(j0)).view(np.int64).copy()).to(dev)
-        tr = pb.Trace(dev, p.va_lo, p.va_hi, len(p.allocs), len(p.allocs))
-        for b, s in p.allocs:
+        objs = p.objects if two else p.allocs
+        kw = dict(max_live_tensors=len(p.allocs), max_tensor_ids=len(p.allocs)) if two else {}
+        tr = pb.Trace(dev, p.va_lo, p.va_hi, len(objs), len(objs), **kw)
+        for b, s in objs:
             tr.register_alloc(b, s)
+        if two:
+            for b, s in p.allocs:
+                tr.register_tensor(b, s)
         hist = tr.histograms(p.page_shift, n_kernels=k1 - k0, kernel_rows=True, pad_pages_to=64 * world)
         merger = pdist.PeerMerger(tr, hist, (16, 3))
         for step in range(2):  # a second merge on re-analyzed buffers (barrier discipline)
@@ -122,14 +127,16 @@ def _work(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_peer_merger_two_ranks_one_gpu():
+@pytest.mark.parametrize("world,two", [(2, False), (3, False), (2, True)])
+def test_peer_merger_ranks_on_one_gpu(world, two):
+    """two = objects (4 MiB blocks) + tensors (the allocations): tensor counts (SUM),
+    untensored total and WS_tensor (MAX) merged too."""
     import torch.multiprocessing as mp
 
-    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, two)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = {}
@@ -142,15 +149,20 @@ def test_peer_merger_two_ranks_one_gpu():
         assert pr.exitcode == 0
 
     p = tracegen.build_plan("tiny", seed=17)
-    o = oracle.OracleTrace(p.va_lo, p.va_hi, len(p.allocs), len(p.allocs))
-    for b, s in p.allocs:
+    objs = p.objects if two else p.allocs
+    kw = dict(max_live_tensors=len(p.allocs), max_tensor_ids=len(p.allocs)) if two else {}
+    o = oracle.OracleTrace(p.va_lo, p.va_hi, len(objs), len(objs), **kw)
+    for b, s in objs:
         o.register_alloc(b, s)
+    if two:
+        for b, s in p.allocs:
+            o.register_tensor(b, s)
     o.analyze(tracegen.host_records(p), p.kernel_offsets, p.page_shift, kernel_rows=True)
     bm, uniq = o.bitmap()
     S = res[0][5]
     pages = np.zeros(world * S, dtype=np.uint64)
     pages[:len(o.page_counts)] = o.page_counts
-    A = len(p.allocs)
+    A = len(objs)
     for r in range(world):
         _, shard, small, pbm, outs, _ = res[r]
         assert np.array_equal(shard, pages[r * S:(r + 1) * S]), f"rank {r}: merged page shard"
@@ -161,6 +173,11 @@ def test_peer_merger_two_ranks_one_gpu():
         fp, ws = o.footprints()
         assert int(tot[4]) == ws, f"rank {r}: WS_obj (MAX)"
         assert np.array_equal(pbm, bm), f"rank {r}: bitmap"
+        if two:
+            T = len(p.allocs)
+            assert np.array_equal(small[A + 8:A + 8 + T], o.tensor_counts), f"rank {r}: tensor counts"
+            assert int(tot[pb.T_UNTENSORED]) == o.untensored, f"rank {r}: untensored"
+            assert int(tot[pb.T_WS_TENSOR]) == o.tensor_footprints()[1], f"rank {r}: WS_tensor (MAX)"
         for k in (16, 3):
             rp, rc, rf = oracle.topk(o.page_counts, k)
             assert int(outs[k][2][0]) == rf and np.array_equal(outs[k][0], rp) and np.array_equal(outs[k][1], rc), \
