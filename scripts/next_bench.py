@@ -1,7 +1,7 @@
 """Throughput of the SURVEY §8(f) NEXT rows at full size, each against the same scan
 without the feature, on one B200 (one JSON line per variant on stdout).
 
-    python scripts/next_bench.py [--reps 5] [--warmup 2] [--only uvm,rich]
+    python scripts/next_bench.py [--reps 5] [--warmup 2] [--only uvm,rich,peer]
 
 uvm (BASELINE config 4: 4e9 8-byte records, 2 MiB blocks, 2,000 kernels, per-kernel
 rows + per-kernel page bitmaps):
@@ -10,6 +10,8 @@ rows + per-kernel page bitmaps):
   twolevel   + f3 objects (pool chunks) and tensors (allocations), tensor rows
   twolevel+hot
 gpt2m rich (f4: 2e9 16-byte records, grid window = all kernels, writes + bytes).
+peer (S5 merge kernel pasta_peer_reduce at the llama shard size, g = 8 local sources;
+134 MB of sources, so partly L2-resident across repetitions).
 
 Times: the library's own CUDA events around the scan launch on its stream
 (pasta_get_timing "scan" / "finalize"), averaged over --reps passes after --warmup.
@@ -130,11 +132,30 @@ def rich(args, pk):
         torch.cuda.empty_cache()
 
 
+def peer(args, pk):
+    """S5 merge kernel (pasta_peer_reduce) at the llama shard size for g = 8: rank 0's
+    shard of 2,097,152 pages from 8 sources, with bitmap words and popcount. The sources
+    are local here (one GPU), so this measures the kernel against HBM, not NVLink."""
+    g, S = 8, (1 << 24) // 8
+    srcs = [torch.randint(0, 1 << 20, (S,), dtype=torch.int64, device=DEV) for _ in range(g)]
+    out = torch.empty(S, dtype=torch.int64, device=DEV)
+    bm = torch.empty(S // 64, dtype=torch.int64, device=DEV)
+    pop = torch.zeros(1, dtype=torch.int64, device=DEV)
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    ph = timed(tr, lambda: tr.peer_reduce(srcs, 0, S, out, bm, pop), args.reps * 20, args.warmup)
+    ms = ph["merge"]
+    byts = 8 * S * g + 8 * S + S // 8
+    print(json.dumps({"config": "llama shard, g=8 (local sources)", "variant": "peer_reduce", "pages": S,
+                      "merge_ms": round(ms, 4), "algorithmic_GB_s": round(byts / ms / 1e6, 1), "peak_GB_s": pk,
+                      "frac": round(byts / ms / 1e6 / pk, 4)}), flush=True)
+    tr.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--only", default="uvm,rich")
+    ap.add_argument("--only", default="uvm,rich,peer")
     args = ap.parse_args()
     pk = peak()
     only = args.only.split(",")
@@ -142,6 +163,8 @@ def main():
         uvm(args, pk)
     if "rich" in only:
         rich(args, pk)
+    if "peer" in only:
+        peer(args, pk)
 
 
 if __name__ == "__main__":
