@@ -1269,8 +1269,12 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
                         km, lane);
       if (kTwo && kRows) {
         if (lane == 0) {
-          if (mAB & 0xFFu) rich_rows_run(o, slot2, IA.own, k2, mAB & 0xFFu);
-          if (mAB >> 8) rich_rows_run(o, slot2, IB.own, k2, mAB >> 8);
+          if (IA.own == IB.own) {
+            if (mAB) rich_rows_run(o, slot2, IA.own, k2, (mAB & 0xFFu) + (mAB >> 8));
+          } else {
+            if (mAB & 0xFFu) rich_rows_run(o, slot2, IA.own, k2, mAB & 0xFFu);
+            if (mAB >> 8) rich_rows_run(o, slot2, IB.own, k2, mAB >> 8);
+          }
         }
       }
       if (any_rest) {
@@ -1299,8 +1303,12 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
         tier_rc(std::false_type{}, 0u, kg, 0u);
         continue;
       }
-      const uint32_t gl = (uint32_t)pick4(m, mis ? __ffs(mis) - 1 : 0);
-      const uint32_t g2 = __shfl_sync(kFull, gl, __ffs(mis_lanes) - 1);
+      // the other kernel: the largest grid id among the records that are not g's (any
+      // third id makes `bad` below)
+      uint32_t gl = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) gl = max(gl, ((mis >> i) & 1u) ? (uint32_t)m[i] : 0u);
+      const uint32_t g2 = __reduce_max_sync(kFull, gl);
       uint32_t bad = g2 - args.grid_lo > args.grid_last ? 1u : 0u;
 #pragma unroll
       for (int i = 0; i < 4; ++i) bad |= (((mis >> i) & 1u) && (uint32_t)m[i] != g2) ? 1u : 0u;
