@@ -176,6 +176,18 @@ int pasta_register_tensor(pasta_trace* h, uint64_t base, uint64_t size, uint32_t
 /* Remove the live tensor whose base is exactly `base` (ENOENT otherwise). */
 int pasta_register_tensor_free(pasta_trace* h, uint64_t base);
 
+/* Signed-size registration in the convention of PyTorch's allocator callback
+ * c10::reportMemoryUsage ("function hooks and callbacks (e.g.
+ * c10::reportMemoryUsage ...)"; SPEC S:121-124 RawEventRMX: "a single signed size
+ * (negative = release)", normalized to positive sizes). The event goes to the
+ * tensor level if the handle has one (max_tensor_ids > 0, R18), else to the object
+ * level (R6). delta > 0: register [ptr, ptr + delta) exactly as pasta_register_tensor /
+ * pasta_register_alloc (same errors), *out_id (may be NULL) = the new id. delta < 0:
+ * release the live range whose base is ptr, which must have size -delta (EINVAL
+ * otherwise, nothing released; ENOENT if no live range starts at ptr); *out_id = its
+ * id. delta == 0 or INT64_MIN: EINVAL. */
+int pasta_report_memory_usage(pasta_trace* h, uint64_t ptr, int64_t delta, uint32_t* out_id);
+
 /* Analyze n records at page granularity 2^page_shift (12 <= page_shift <= 30;
  * va_lo and va_hi must be multiples of 2^page_shift and P < 2^32). Steps, all on the
  * device in one scan of the records (S1-S3 of DESIGN.md section 1):

@@ -160,6 +160,26 @@ class OracleTrace:
         self.tbases.pop(bisect.bisect_left(self.tbases, base))
         return OK
 
+    def report_memory_usage(self, ptr: int, delta: int):
+        """Signed-size event (P:540 c10::reportMemoryUsage; SPEC S:121-124: negative size
+        = release, normalized to a positive size) -> (status, id): to the tensor
+        level if this handle has one, else to the object level. A release must name a
+        live range starting at ptr (else ENOENT) of size -delta (else EINVAL)."""
+        ptr, delta = int(ptr), int(delta)
+        if delta == 0 or not -(1 << 63) < delta < (1 << 63):
+            return EINVAL, None
+        tensors = self.max_tensor_ids > 0
+        if delta > 0:
+            return self.register_tensor(ptr, delta) if tensors else self.register_alloc(ptr, delta)
+        table = self.tlive if tensors else self.live
+        if ptr not in table:
+            return ENOENT, None
+        size, ident = table[ptr]
+        if size != -delta:
+            return EINVAL, None
+        st = self.register_tensor_free(ptr) if tensors else self.register_free(ptr)
+        return st, ident
+
     # ---- one analyze call, accumulating ----
     def analyze(self, addr: np.ndarray, kernel_offsets=None, page_shift: int = 12, kernel_rows: bool = False,
                 kernel_pages: bool = False, window_kernels: int = 0):

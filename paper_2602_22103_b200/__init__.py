@@ -79,6 +79,7 @@ _SIGS = {
     "pasta_register_free": (_int, [_vp, _u64]),
     "pasta_register_tensor": (_int, [_vp, _u64, _u64, ctypes.POINTER(_u32)]),
     "pasta_register_tensor_free": (_int, [_vp, _u64]),
+    "pasta_report_memory_usage": (_int, [_vp, _u64, ctypes.c_int64, ctypes.POINTER(_u32)]),
     "pasta_prefetch_plan": (_int, [_vp, _vp, _u32, _u32, _vp, _vp, _u64, ctypes.POINTER(_u64)]),
     "pasta_analyze": (_int, [_vp, ctypes.POINTER(pasta_records), _u64, _u32, ctypes.POINTER(pasta_histograms)]),
     "pasta_finalize": (_int, [_vp, _u32, _u32, ctypes.POINTER(pasta_histograms)]),
@@ -157,6 +158,12 @@ def pasta_register_tensor(h, base: int, size: int) -> int:
 
 def pasta_register_tensor_free(h, base: int):
     _check(_lib.pasta_register_tensor_free(h, base), "pasta_register_tensor_free")
+
+
+def pasta_report_memory_usage(h, ptr: int, delta: int) -> int:
+    out = _u32(0)
+    _check(_lib.pasta_report_memory_usage(h, ptr, delta, ctypes.byref(out)), "pasta_report_memory_usage")
+    return out.value
 
 
 def pasta_prefetch_plan(h, rows, n_kernels: int, level: int, plan_offsets, plan_ranges, cap: int) -> tuple:
@@ -337,6 +344,10 @@ class Trace:
 
     def register_tensor(self, base: int, size: int) -> int:
         return pasta_register_tensor(self.h, base, size)
+
+    def report_memory_usage(self, ptr: int, delta: int) -> int:
+        """c10::reportMemoryUsage convention: delta > 0 allocates, < 0 releases."""
+        return pasta_report_memory_usage(self.h, ptr, delta)
 
     def register_tensor_free(self, base: int):
         pasta_register_tensor_free(self.h, base)

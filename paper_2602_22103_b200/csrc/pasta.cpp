@@ -477,6 +477,21 @@ int pasta_register_tensor_free(pasta_trace* h, uint64_t base) {
   return PASTA_OK;
 }
 
+int pasta_report_memory_usage(pasta_trace* h, uint64_t ptr, int64_t delta, uint32_t* out_id) {
+  if (!h || delta == 0 || delta == INT64_MIN) return PASTA_EINVAL;
+  const bool tensors = h->max_tids > 0;
+  if (delta > 0)
+    return tensors ? pasta_register_tensor(h, ptr, (uint64_t)delta, out_id)
+                   : pasta_register_alloc(h, ptr, (uint64_t)delta, out_id);
+  const uint64_t size = (uint64_t)(-delta);
+  auto& table = tensors ? h->tlive : h->live;
+  auto it = table.find(ptr);
+  if (it == table.end()) return PASTA_ENOENT;
+  if (it->second.first != size) return PASTA_EINVAL;
+  if (out_id) *out_id = it->second.second;
+  return tensors ? pasta_register_tensor_free(h, ptr) : pasta_register_free(h, ptr);
+}
+
 int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t page_shift, pasta_histograms* out) {
   if (!h || !tr || !out) return PASTA_EINVAL;
   if (!out->page_counts || !out->alloc_counts || !out->totals) return PASTA_EINVAL;
