@@ -182,3 +182,37 @@ def test_peer_merger_ranks_on_one_gpu(world, two):
             rp, rc, rf = oracle.topk(o.page_counts, k)
             assert int(outs[k][2][0]) == rf and np.array_equal(outs[k][0], rp) and np.array_equal(outs[k][1], rc), \
                 f"rank {r}: top-{k}"
+
+
+def test_peer_merger_world1_nccl():
+    """PeerMerger through an NCCL group (the bench's N > 1 configuration, here at world
+    size 1): the handle exchange and barriers run on NCCL, and the merged results equal
+    the single-GPU ones."""
+    import torch.distributed as dist
+
+    from paper_2602_22103_b200 import dist as pdist
+
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                            device_id=DEV)
+    try:
+        p = tracegen.build_plan("tiny", seed=19)
+        rec = torch.empty(p.n, dtype=torch.int64, device=DEV)
+        tracegen.device_records(tracegen.DevicePlan(p, DEV), rec)
+        ko = torch.from_numpy(p.kernel_offsets.view(np.int64).copy()).to(DEV)
+        tr = pb.Trace(DEV, p.va_lo, p.va_hi, len(p.allocs), len(p.allocs))
+        for b, s in p.allocs:
+            tr.register_alloc(b, s)
+        hist = tr.histograms(p.page_shift, n_kernels=p.n_kernels, kernel_rows=True, pad_pages_to=64)
+        tr.analyze(rec, p.page_shift, hist, kernel_offsets=ko)
+        ref = tuple(u64(x).copy() for x in tr.topk(hist.page_counts, 16))
+        tr.sync()
+        totals, bm = u64(hist.totals).copy(), u64(hist.page_bitmap).copy()
+        outs = pdist.PeerMerger(tr, hist, (16,)).merge()
+        tr.sync()
+        torch.cuda.synchronize()
+        assert all(np.array_equal(u64(a), b) for a, b in zip(outs[16], ref))
+        assert np.array_equal(u64(hist.totals)[:7], totals[:7])
+        assert np.array_equal(u64(hist.page_bitmap), bm)
+        tr.close()
+    finally:
+        dist.destroy_process_group()
