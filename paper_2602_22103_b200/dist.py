@@ -184,7 +184,7 @@ class PeerMerger:
         for k in self.ks:
             mine += [self.loc[k][0], self.loc[k][1]]
         torch.cuda.synchronize(dev)
-        shared = [reduce_tensor(t) for t in mine]
+        shared = [reduce_tensor(t) for t in mine] if self.world > 1 else []  # own buffers are used directly
         allh = [None] * self.world
         dist.all_gather_object(allh, (dev.index if dev.index is not None else torch.cuda.current_device(), shared),
                                group=group)
