@@ -75,9 +75,12 @@ __global__ void __launch_bounds__(kBlock) peer_elementwise_kernel(PeerSrc src, u
                                                                    uint64_t* __restrict__ out) {
   for (uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kBlock) {
     uint64_t acc = 0;
-    for (uint32_t r = 0; r < g; ++r) {
-      const uint64_t v = ld_stream_u64(src.p[r] + lo + i);
-      acc = kMax ? (v > acc ? v : acc) : acc + v;
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r) {  // static indices: the sources stay in the parameter bank
+      if (r < (int)g) {
+        const uint64_t v = ld_stream_u64(src.p[r] + lo + i);
+        acc = kMax ? (v > acc ? v : acc) : acc + v;
+      }
     }
     out[i] = acc;
   }
