@@ -111,10 +111,18 @@ typedef struct {
                                      (bad offsets mis-attribute, never write out of
                                      bounds); host offsets are checked (EINVAL).       */
   uint32_t n_kernels;
-  uint32_t flags;                 /* PASTA_REC_HOST */
+  uint32_t flags;                 /* PASTA_REC_HOST | PASTA_REC_STABLE */
 } pasta_records;
 
-enum { PASTA_REC_HOST = 1u };
+/* PASTA_REC_STABLE (device records only): the records and kernel offsets were complete
+ * before the previous kernel on the handle's stream started (that kernel does not
+ * write them), so the scan may begin loading them while that kernel is still running.
+ * Consecutive pasta_analyze scans on a stream are programmatic dependent launches:
+ * each one waits for its predecessor's completion (griddepcontrol.wait) before it
+ * writes any output, and with this flag only after issuing its first record loads —
+ * the streaming mode's per-call latency (NEXT f2). Without the flag every access to
+ * global data follows the wait. */
+enum { PASTA_REC_HOST = 1u, PASTA_REC_STABLE = 2u };
 
 /* Outputs: caller-owned DEVICE memory (e.g. torch int64 tensors viewed as u64).
  * Counts ACCUMULATE (+=) across calls, so a long trace can be analyzed in batches

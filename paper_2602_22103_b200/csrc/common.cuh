@@ -117,6 +117,14 @@ __device__ __forceinline__ void atomic_max_u64(uint64_t* p, uint64_t v) {
   atomicMax(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
 }
 
+// Programmatic dependent launch (sm_90+): let the stream's next kernel launch now, and
+// wait until the stream's previous kernel has completed and its writes are visible
+// (a no-op when this kernel was not launched as a programmatic dependent).
+__device__ __forceinline__ void grid_dep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Streaming 8-byte load (evict-first in L1/L2: merge sources are read once).
 __device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t* p) {
   return static_cast<uint64_t>(__ldcs(reinterpret_cast<const unsigned long long*>(p)));

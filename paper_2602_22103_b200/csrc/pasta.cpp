@@ -497,7 +497,8 @@ int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t 
   if (!out->page_counts || !out->alloc_counts || !out->totals) return PASTA_EINVAL;
   if ((out->kernel_stats || out->kernel_page_bitmap || out->hotness) && !out->kernel_alloc_counts) return PASTA_EINVAL;
   if (out->hotness && out->window_kernels == 0) return PASTA_EINVAL;
-  if (tr->flags & ~PASTA_REC_HOST) return PASTA_EINVAL;
+  if (tr->flags & ~(PASTA_REC_HOST | PASTA_REC_STABLE)) return PASTA_EINVAL;
+  if ((tr->flags & PASTA_REC_HOST) && (tr->flags & PASTA_REC_STABLE)) return PASTA_EINVAL;
   int s = check_tensor_outputs(h, out);
   if (s) return s;
   s = check_window(h, page_shift);
@@ -544,6 +545,7 @@ int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t 
   }
 
   if (!host) {
+    a.early = (tr->flags & PASTA_REC_STABLE) ? 1u : 0u;
     s = scan_range(h, tr->addr, n, 0, a, h->stream, n);
     if (s) return s;
   } else {

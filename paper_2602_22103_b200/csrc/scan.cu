@@ -81,6 +81,9 @@ using namespace dev;
 #define PASTA_WARPS 24
 #endif
 constexpr int kWarps = PASTA_WARPS;
+#ifndef PASTA_PDL
+#define PASTA_PDL 1  // programmatic dependent launch of consecutive scans
+#endif
 constexpr int kThreads = kWarps * 32;
 constexpr int kSlice = 256;                 // records per slice (8 per lane)
 #ifndef PASTA_TIER_S
@@ -642,6 +645,9 @@ __device__ __forceinline__ uint32_t kernel_of(const uint64_t* __restrict__ koffs
 
 template <bool kBig, bool kRows, int kPages, bool kIL>
 __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages) {
+  // Programmatic dependent launch: the next analyze call's scan may start its prologue
+  // (barrier init, range table into shared memory) on free SMs while this one runs.
+  grid_dep_launch_dependents();
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages));
   uint64_t* sB = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages) + kBarBytes + kLaBytes + kPfBytes);
@@ -689,11 +695,16 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   if (lane == 0) {
     for (int j = 0; j < stages; ++j) mbar_init(bars + warp * kMaxStages + j, 1);
     fence_mbar_init();
-    if (blockIdx.x == 0 && warp == 0 && args.add_records) red_add_u64(args.totals + 0, args.add_records);
   }
+  // the range table is only ever written by stream-ordered copies, never by a kernel
   if (!kBig)
     for (uint32_t i = threadIdx.x; i < 2 * A; i += kThreads) sB[i] = args.bounds[i];
   __syncthreads();
+  // Everything the stream's previous kernel wrote (the records, a chunk map, zeroed or
+  // partial outputs) is visible after grid_dep_wait; nothing before it touches that
+  // data, except the first record loads when the caller declared the records stable
+  // (PASTA_REC_STABLE: not written by the stream's previous kernel).
+  if (!args.early) grid_dep_wait();
 #if PASTA_TRACE_TIMING
   const uint32_t tslot = (blockIdx.x * kWarps + warp) * 4;
   if (lane == 0) g_warp_times[tslot] = gtimer();
@@ -708,6 +719,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   };
   if (lane == 0)
     for (uint32_t j = 0; j < (uint32_t)stages && j < nmy; ++j) issue(j, j);
+  if (args.early) grid_dep_wait();
+  if (lane == 0 && blockIdx.x == 0 && warp == 0 && args.add_records) red_add_u64(args.totals + 0, args.add_records);
 
   Ctx c;
   c.va_lo = args.va_lo;
@@ -961,8 +974,19 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
   auto fn = a.log_ic >= 0 ? scan_kernel<kBig, kRows, kPages, true> : scan_kernel<kBig, kRows, kPages, false>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  fn<<<grid, kThreads, smem, st>>>(a, stages);
-  return cudaGetLastError();
+  // launched as a programmatic dependent of the stream's previous kernel (the kernel
+  // waits for it with griddepcontrol.wait before touching any global data)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = PASTA_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, a, stages);
 }
 
 

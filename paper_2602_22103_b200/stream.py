@@ -35,10 +35,14 @@ def plan_batches(kernel_offsets, n: int, batch: int):
 class BatchRunner:
     """Issues the batch calls of plan_batches on a Trace's stream (all device memory)."""
 
-    def __init__(self, trace, hist, records, kernel_offsets, n: int, batch: int, page_shift: int):
+    def __init__(self, trace, hist, records, kernel_offsets, n: int, batch: int, page_shift: int,
+                 stable: bool = True):
+        """stable: the records are not written by the kernel that precedes each call on
+        the stream (true for a resident trace), so every scan may start loading its
+        batch while the previous one finishes (PASTA_REC_STABLE)."""
         import torch
 
-        from . import PASTA_NO_FINALIZE, pasta_analyze, pasta_histograms
+        from . import PASTA_NO_FINALIZE, PASTA_REC_STABLE, pasta_analyze, pasta_histograms
 
         self.tr, self.hist, self.page_shift = trace, hist, page_shift
         self.batches = plan_batches(kernel_offsets, n, batch)
@@ -60,8 +64,9 @@ class BatchRunner:
             self.calls.append((records.data_ptr() + 8 * a, b - a, self.offs.data_ptr() + 8 * pos, len(sub) - 1, hs))
             pos += len(sub)
         self._analyze = pasta_analyze
+        self.flags = PASTA_REC_STABLE if stable else 0
 
     def run(self):
         """Enqueue every batch (graph-capturable: no host synchronization)."""
         for addr, nrec, offs, nk, hs in self.calls:
-            self._analyze(self.tr.h, addr, nrec, self.page_shift, hs, offs, nk)
+            self._analyze(self.tr.h, addr, nrec, self.page_shift, hs, offs, nk, self.flags)

@@ -542,8 +542,8 @@ def test_sharded_merger_world1_nccl():
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("batch", [4096, 10_001 * 2])
-def test_streaming_batches_equal_oracle(batch):
+@pytest.mark.parametrize("batch,stable", [(4096, True), (4096, False), (10_001 * 2, True)])
+def test_streaming_batches_equal_oracle(batch, stable):
     """NEXT f2: the trace analyzed as batches (one NO_FINALIZE call each, kernels cut
     between batches accumulating into the same rows) + one finalize == the oracle."""
     from paper_2602_22103_b200.stream import BatchRunner
@@ -553,7 +553,7 @@ def test_streaming_batches_equal_oracle(batch):
     tracegen.device_records(tracegen.DevicePlan(p, DEV), drec)
     tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs)
     hist = tr.histograms(p.page_shift, n_kernels=p.n_kernels, kernel_rows=True, kernel_pages=True)
-    runner = BatchRunner(tr, hist, drec, p.kernel_offsets, p.n, batch, p.page_shift)
+    runner = BatchRunner(tr, hist, drec, p.kernel_offsets, p.n, batch, p.page_shift, stable=stable)
     runner.run()
     tr.finalize(p.page_shift, hist, n_kernels=p.n_kernels)
     tr.sync()
