@@ -1147,6 +1147,7 @@ __device__ __forceinline__ void rich_add(RichAcc& r, const RichOut& o, const Iva
 
 template <bool kBig, bool kRows>
 __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args, const int stages) {
+  grid_dep_launch_dependents();  // as scan_kernel: the next call's prologue may start now
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + rich_ring_bytes(stages));
   uint4* slot2 = reinterpret_cast<uint4*>(smem + rich_ring_bytes(stages) + kRBarBytes) + (threadIdx.x >> 5);
@@ -1170,6 +1171,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
   if (!kBig)
     for (uint32_t i = threadIdx.x; i < 2 * A; i += kRThreads) sB[i] = args.bounds[i];
   __syncthreads();
+  grid_dep_wait();  // the previous kernel's writes (records, outputs) are visible from here
   const uint64_t pol = l2_evict_first_policy();
   // only the trace's last slice may be partial: the warp that owns it sees it at j = tail_j
   const uint32_t tail_j = (s1 == nsl && nmy) ? nmy - 1u : 0xFFFFFFFFu;
@@ -1452,8 +1454,17 @@ cudaError_t launch_rich_variant(const RichArgs& a, int grid, cudaStream_t st) {
   auto fn = rich_kernel<kBig, kRows>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  fn<<<grid, kRThreads, smem, st>>>(a, stages);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kRThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = PASTA_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, a, stages);
 }
 
 }  // namespace
