@@ -1,6 +1,7 @@
-"""Scan time of llama prefixes (their own kernel offsets, kernel rows) under the
+"""Scan time of a config's prefixes (their own kernel offsets, kernel rows) under the
 contiguous and the interleaved schedule: where does interleaving start to pay?
-python scripts/sched_sizes.py [n ...]"""
+python scripts/sched_sizes.py [config] [n ...]   (config default llama; n default: 5 sizes,
+or the config's full n when a config is named without sizes)"""
 import json
 import sys
 
@@ -12,8 +13,10 @@ import paper_2602_22103_b200 as pb  # noqa: E402
 import tracegen  # noqa: E402
 
 dev = torch.device("cuda:0")
-p = tracegen.build_plan("llama")
-ns = [int(x) for x in sys.argv[1:]] or [1 << 19, 1 << 22, 1 << 25, 1 << 27, 1 << 29]
+args = sys.argv[1:]
+cfg = args.pop(0) if args and not args[0].isdigit() else None
+p = tracegen.build_plan(cfg or "llama")
+ns = [int(x) for x in args] or ([p.n] if cfg else [1 << 19, 1 << 22, 1 << 25, 1 << 27, 1 << 29])
 N = max(ns)
 rec = torch.empty(N, dtype=torch.int64, device=dev)
 tracegen.device_records(tracegen.DevicePlan(p, dev), rec, 0, N)
