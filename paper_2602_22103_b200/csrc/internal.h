@@ -34,6 +34,7 @@ struct ScanArgs {
   uint64_t* hot;             // hotness [windows x P] or nullptr
   uint64_t P;                // pages in the window
   uint32_t window_kernels;   // kernels per hotness window (>= 1)
+  uint64_t wk_magic;         // ceil(2^64 / window_kernels) for window_kernels >= 2
   const ulonglong2* chunk_k; // [chunks] (k, koffs[k+1]) of each interleaved chunk's first record (scratch)
   int32_t log_ic;            // log2 slices per interleaved chunk, -1 = contiguous (scan_schedule)
   // tensor level (NEXT f3): all nullptr when off

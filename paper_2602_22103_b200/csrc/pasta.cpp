@@ -537,6 +537,7 @@ int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t 
   a.hot = out->hotness;
   a.P = P;
   a.window_kernels = out->window_kernels ? out->window_kernels : 1;
+  a.wk_magic = a.window_kernels > 1 ? UINT64_MAX / a.window_kernels + 1 : 0;
   if (out->tensor_counts) {
     a.tids = h->d_tids;
     a.tensor_counts = out->tensor_counts;

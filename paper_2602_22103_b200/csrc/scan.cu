@@ -216,6 +216,7 @@ struct Out {
   uint64_t* hot;    // hotness matrix [windows x P] or nullptr (NEXT f1)
   uint64_t P;
   uint32_t wk;      // kernels per hotness window
+  uint64_t wk_magic;  // ceil(2^64 / wk) (wk >= 2)
   const uint32_t* tids;  // tensor level (NEXT f3) or nullptr
   uint64_t* tcounts;
   uint64_t* ktc;
@@ -227,7 +228,11 @@ struct Out {
 // bits, bit 1 = hotness.
 template <int kMode>
 __device__ __forceinline__ void hot_add(const Out& o, uint32_t page, uint64_t v, uint32_t k) {
-  if ((kMode & 2) && page != kOOW) red_add_u64(o.hot + (uint64_t)(k / o.wk) * o.P + page, v);
+  if ((kMode & 2) && page != kOOW) {
+    // window k / wk by a multiply-high: wk_magic = ceil(2^64 / wk) is exact for k, wk < 2^32
+    const uint64_t w = o.wk == 1 ? (uint64_t)k : __umul64hi((uint64_t)k, o.wk_magic);
+    red_add_u64(o.hot + w * o.P + page, v);
+  }
 }
 
 // Owner count `v` of kernel k to global (one thread).
@@ -743,6 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   o.hot = args.hot;
   o.P = args.P;
   o.wk = args.window_kernels;
+  o.wk_magic = args.wk_magic;
   o.tids = args.tids;
   o.tcounts = args.tensor_counts;
   o.ktc = args.ktc;
@@ -938,6 +944,7 @@ __global__ void scan_extras_kernel(const ExtraArgs ea) {
   o.hot = s.hot;
   o.P = s.P;
   o.wk = s.window_kernels;
+  o.wk_magic = s.wk_magic;
   o.tids = s.tids;
   o.tcounts = s.tensor_counts;
   o.ktc = s.ktc;
