@@ -177,7 +177,7 @@ __device__ bool block_find_bin(const unsigned* hist, int nb, int per, unsigned l
 
 // Pick the pass-1 bin holding the K'-th largest count (block 0, all threads): nnz,
 // K' = min(K, nnz) and the bin; then the threshold state.
-__device__ void dev_select_first(volatile State* st, unsigned* hist, uint64_t K, unsigned long long* sm) {
+__device__ void dev_select_first(volatile State* st, unsigned* hist, uint64_t K, uint64_t Kp, unsigned long long* sm) {
   constexpr int per = (kFirstBins + kBlock - 1) / kBlock;  // bins per thread
   unsigned long long nnz = 0, above = 0, rem = 0;
   int d = 0;
@@ -220,6 +220,9 @@ __device__ void dev_select_first(volatile State* st, unsigned* hist, uint64_t K,
     if (rem == here) {  // the whole bin is taken: no ties to break
       st->done = 2;
       st->T = lo - 1;
+    } else if (above + here <= Kp) {  // every count >= lo fits the sort: it picks the first K'
+      st->done = 2;
+      st->T = lo - 1;
     } else if (bits == 0) {  // exact value: take the first `rem` pages with this count
       st->done = 2;
       st->T = lo;
@@ -258,7 +261,7 @@ __device__ void dev_digit(const uint64_t* __restrict__ pc, uint64_t P, volatile 
 
 // Choose the digit (block 0, all threads) where the running count from the top
 // reaches the remaining rank.
-__device__ void dev_select_digit(volatile State* st, unsigned* hist, unsigned long long* sm) {
+__device__ void dev_select_digit(volatile State* st, unsigned* hist, uint64_t Kp, unsigned long long* sm) {
   const int shift = (int)st->shift, width = (int)st->width;
   const unsigned long long rem0 = st->remaining, above0 = st->above, lo0 = st->lo;
   __syncthreads();  // every thread has read the state before the winner rewrites it
@@ -272,7 +275,7 @@ __device__ void dev_select_digit(volatile State* st, unsigned* hist, unsigned lo
     st->lo = lo;
     st->above = above0 + above;
     st->remaining = rem;
-    if (rem == here) {  // the whole bin is taken: no ties to break
+    if (rem == here || above0 + above + here <= Kp) {  // whole bin, or all counts >= lo fit the sort
       st->done = 2;
       st->T = lo - 1;
     } else if (shift == 0) {  // exact value: take the first `rem` pages with this count
@@ -383,7 +386,7 @@ __device__ void dev_gather_eq(const uint64_t* __restrict__ pc, uint64_t P, volat
 // with per-CTA tie counts and, if ties are cut, the ordered tie gather, separated by
 // grid-wide barriers.
 __global__ void __launch_bounds__(kBlock) select_coop_kernel(const uint64_t* __restrict__ pc, uint64_t P,
-                                                             uint64_t K, State* st_, unsigned* hist,
+                                                             uint64_t K, uint64_t Kp, State* st_, unsigned* hist,
                                                              unsigned long long* blkcnt, uint64_t* key_c,
                                                              uint64_t* key_p) {
   cg::grid_group grid = cg::this_grid();
@@ -393,13 +396,13 @@ __global__ void __launch_bounds__(kBlock) select_coop_kernel(const uint64_t* __r
   __shared__ unsigned long long running_s;
   dev_first(pc, P, h, hist);
   grid.sync();
-  if (blockIdx.x == 0) dev_select_first(st, hist, K, sm);
+  if (blockIdx.x == 0) dev_select_first(st, hist, K, Kp, sm);
   grid.sync();
   for (int pass = 0; pass < (63 + kDigitBits - 1) / kDigitBits; ++pass) {
     if (st->done) break;  // grid-uniform: read after the barrier
     dev_digit(pc, P, st, h, hist);
     grid.sync();
-    if (blockIdx.x == 0) dev_select_digit(st, hist, sm);
+    if (blockIdx.x == 0) dev_select_digit(st, hist, Kp, sm);
     grid.sync();
   }
   if (st->done != 2) return;
@@ -410,7 +413,8 @@ __global__ void __launch_bounds__(kBlock) select_coop_kernel(const uint64_t* __r
 }
 
 __global__ void pad_kernel(State* st, uint64_t* key_c, uint64_t* key_p, uint64_t Kp) {
-  const uint64_t kp = st->kprime;
+  // filled slots: K' (threshold + ties) or every candidate >= the bin (need = 0)
+  const uint64_t kp = st->need ? st->kprime : st->gt_slots;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Kp; i += (uint64_t)gridDim.x * blockDim.x) {
     if (i >= kp) {
       key_c[i] = 0;
@@ -591,9 +595,9 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
     const uint64_t need_blocks = (P + kBlock - 1) / kBlock;
     if ((uint64_t)g > need_blocks) g = (int)(need_blocks < 1 ? 1 : need_blocks);
     if (g > grid) g = grid;
-    uint64_t K64 = k;
-    void* args[] = {(void*)&pc, (void*)&P, (void*)&K64, (void*)&s.st, (void*)&s.hist, (void*)&s.blkcnt,
-                    (void*)&s.key_c, (void*)&s.key_p};
+    uint64_t K64 = k, Kp64 = Kp;
+    void* args[] = {(void*)&pc, (void*)&P, (void*)&K64, (void*)&Kp64, (void*)&s.st, (void*)&s.hist,
+                    (void*)&s.blkcnt, (void*)&s.key_c, (void*)&s.key_p};
     PASTA_TRY(cudaLaunchCooperativeKernel((void*)select_coop_kernel, dim3(g), dim3(kBlock), args, 0, st));
   }
   const int pg = (int)((Kp + 1023) / 1024 < 1024 ? (Kp + 1023) / 1024 : 1024);
