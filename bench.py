@@ -199,6 +199,31 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our leg
+# Test-only: PASTA_BENCH_GLOO=1 runs the N > 1 path with a gloo group and every rank on
+# cuda:0 (one GPU, several processes), so the multi-rank code is exercised on a one-GPU
+# box (tests/test_bench_contract.py). The peer merge works there through CUDA IPC; the
+# NCCL merge needs the nccl backend.
+_GLOO = os.environ.get("PASTA_BENCH_GLOO") == "1"
+
+
+def _dist_barrier(local):
+    import torch.distributed as dist
+
+    if _GLOO:
+        dist.barrier()
+    else:
+        dist.barrier(device_ids=[local])
+
+
+def _max_over_ranks(x: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if _GLOO else dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args):
     import torch
 
@@ -209,13 +234,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if _GLOO:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if _GLOO:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
 
     plan = tracegen.build_plan(args.config, args.seed, args.n)
@@ -265,7 +295,7 @@ def run_ours(args):
 
     def barrier():
         if world > 1:
-            torch.distributed.barrier(device_ids=[local])
+            _dist_barrier(local)
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
@@ -285,10 +315,7 @@ def run_ours(args):
     ms = ev0.elapsed_time(ev1)
     tr.set_timing(False)
     phases, launches = tr.timing()
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max = _max_over_ranks(ms, dev) if world > 1 else ms
 
     # ---- correctness guard (cheap invariants on the merged result) ----
     tot = hist.totals.cpu().numpy().view(np.uint64)
@@ -343,7 +370,7 @@ def run_ours(args):
             line["stream"] = stream_res
         print(json.dumps(line), flush=True)
     if world > 1:
-        torch.distributed.barrier(device_ids=[local])
+        _dist_barrier(local)
         torch.distributed.destroy_process_group()
 
 
@@ -433,7 +460,15 @@ def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, d
                         kernel_pages=plan.want_kernel_pages, pad_pages_to=64 * world)
     from paper_2602_22103_b200 import dist as pdist
 
-    merger = pdist.ShardedMerger(tr, h_e, plan.topk, group) if world > 1 else None
+    merger = None
+    if world > 1:  # the same merge as the device-resident step
+        if args.merge == "peer":
+            try:
+                merger = pdist.PeerMerger(tr, h_e, plan.topk, group)
+            except Exception as exc:
+                print(f"bench: e2e peer merge unavailable ({exc!r}); using the NCCL merge", file=sys.stderr)
+        if merger is None:
+            merger = pdist.ShardedMerger(tr, h_e, plan.topk, group)
     res_host = torch.empty(8 + 2 * top_out[0].numel() + 1, dtype=torch.int64, pin_memory=True)
     K = top_out[0].numel()
 
@@ -457,7 +492,7 @@ def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, d
         step()
     torch.cuda.synchronize()
     if world > 1:
-        torch.distributed.barrier(device_ids=[local])
+        _dist_barrier(local)
     s = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
@@ -466,10 +501,8 @@ def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, d
     e1.record(s)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
-        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
-    ms = float(ms_t.item())
+        ms = _max_over_ranks(ms, dev)
     n_tot = n_e * world
     out = {"value": n_tot * steps / (ms / 1e3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * n_e + ko_h.numel() * 8,
            "d2h_bytes_per_step": res_host.numel() * 8, "records_per_rank": n_e, "steps": steps,

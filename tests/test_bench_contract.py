@@ -44,3 +44,27 @@ def test_our_arm_line_tiny():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+def test_two_rank_bench_on_one_gpu():
+    """The N > 1 bench path (kernel-aligned shards, dist.PeerMerger through CUDA IPC,
+    max-over-ranks timing, e2e with the same merge) as two processes on one GPU with a
+    gloo group (PASTA_BENCH_GLOO=1; the driver's multi-GPU runs use NCCL)."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, PASTA_BENCH_GLOO="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "gpt2m",
+           "--steps", "3", "--warmup", "3", "--no-cpu", "--e2e-records", "4194304"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["merge"] == "peer" and d["value"] > 0
+    assert d["phases_ms_per_step"]["merge"] > 0 and d["e2e"]["value"] > 0
