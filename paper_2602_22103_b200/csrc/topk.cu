@@ -79,7 +79,10 @@ __device__ __forceinline__ void hist_add(unsigned* h, bool valid, unsigned bin) 
 #ifndef PASTA_TOPK_U
 #define PASTA_TOPK_U 8
 #endif
-constexpr int kU = PASTA_TOPK_U;  // 16-byte loads in flight per thread in the streaming passes
+constexpr int kU = PASTA_TOPK_U;
+#ifndef PASTA_TOPK_CTAS_PER_SM
+#define PASTA_TOPK_CTAS_PER_SM 4  // co-resident CTAs per SM of the cooperative selection kernel
+#endif  // 16-byte loads in flight per thread in the streaming passes
 template <typename F>
 __device__ __forceinline__ void stream_pairs(const ulonglong2* __restrict__ pc2, uint64_t n2, F f) {
   const uint64_t stride = (uint64_t)gridDim.x * kBlock * kU;
@@ -591,7 +594,7 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int g = sms * (coop_blocks < 4 ? coop_blocks : 4);
+    int g = sms * (coop_blocks < PASTA_TOPK_CTAS_PER_SM ? coop_blocks : PASTA_TOPK_CTAS_PER_SM);
     const uint64_t need_blocks = (P + kBlock - 1) / kBlock;
     if ((uint64_t)g > need_blocks) g = (int)(need_blocks < 1 ? 1 : need_blocks);
     if (g > grid) g = grid;
