@@ -128,11 +128,21 @@ __global__ void __launch_bounds__(1024) max_kernel_kernel(const uint64_t* __rest
   __shared__ uint32_t si[32];
   uint64_t bv = 0;
   uint32_t bi = 0xFFFFFFFFu;
-  for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) {
-    const uint64_t v = __ldg(kstats + 4ull * k) + __ldg(kstats + 4ull * k + 1);
-    if (bi == 0xFFFFFFFFu || v > bv) {  // rows visited in increasing order: the first max stays
-      bv = v;
-      bi = k;
+  // 8 rows per thread in flight at once (one block: the loads' latency is the cost)
+  for (uint32_t k0 = threadIdx.x; k0 < K; k0 += 8u * blockDim.x) {
+    uint64_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t k = k0 + (uint32_t)u * blockDim.x;
+      v[u] = k < K ? __ldg(kstats + 4ull * k) + __ldg(kstats + 4ull * k + 1) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t k = k0 + (uint32_t)u * blockDim.x;
+      if (k < K && (bi == 0xFFFFFFFFu || v[u] > bv)) {  // rows visited in increasing order: the first max stays
+        bv = v[u];
+        bi = k;
+      }
     }
   }
   // warp then block reduction of (value desc, index asc)
