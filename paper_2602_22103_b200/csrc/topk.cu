@@ -469,6 +469,42 @@ __global__ void __launch_bounds__(1024) bitonic_tile_kernel(uint64_t* key_c, uin
   }
 }
 
+// Whole bitonic sort of Kp <= 1024 keys in one CTA, one key per thread: strides below
+// 32 exchange through warp shuffles (no shared memory, no barrier), larger strides
+// through shared memory. Same network and order as bitonic_tile_kernel.
+__global__ void __launch_bounds__(1024) bitonic_small_kernel(uint64_t* key_c, uint64_t* key_p, uint32_t Kp) {
+  __shared__ uint64_t sc[1024], sp[1024];
+  const uint32_t i = threadIdx.x;
+  const unsigned mask = Kp >= 32 ? kFull : (1u << Kp) - 1u;  // the one partial warp when Kp < 32
+  uint64_t c = key_c[i], p = key_p[i];
+  for (uint32_t size = 2; size <= Kp; size <<= 1) {
+    const bool asc = (i & size) == 0;
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      uint64_t oc, op;
+      if (stride >= 32) {
+        sc[i] = c;
+        sp[i] = p;
+        __syncthreads();
+        oc = sc[i ^ stride];
+        op = sp[i ^ stride];
+        __syncthreads();
+      } else {
+        oc = __shfl_xor_sync(mask, c, stride);
+        op = __shfl_xor_sync(mask, p, stride);
+      }
+      // the lower index of the pair keeps the element that comes first (asc) or last
+      const bool other_first = before(oc, op, c, p);
+      const bool lower = (i & stride) == 0;
+      if (lower == asc ? other_first : !other_first) {
+        c = oc;
+        p = op;
+      }
+    }
+  }
+  key_c[i] = c;
+  key_p[i] = p;
+}
+
 __global__ void __launch_bounds__(kBlock) bitonic_global_kernel(uint64_t* key_c, uint64_t* key_p, uint64_t Kp,
                                                                 uint64_t size, uint64_t stride) {
   for (uint64_t q = (uint64_t)blockIdx.x * kBlock + threadIdx.x; q < Kp / 2; q += (uint64_t)gridDim.x * kBlock) {
@@ -560,6 +596,11 @@ size_t topk_scratch_bytes(uint64_t k, int grid) {
 
 // Bitonic sort of Kp (power of two) keys by (count desc, page asc).
 cudaError_t sort_keys(uint64_t* key_c, uint64_t* key_p, uint64_t Kp, int grid, cudaStream_t st, int* n_launches) {
+  if (Kp <= 1024) {
+    bitonic_small_kernel<<<1, (unsigned)Kp, 0, st>>>(key_c, key_p, (uint32_t)Kp);
+    PASTA_TRY(cudaGetLastError());
+    return cudaSuccess;
+  }
   const uint64_t tile = Kp < (uint64_t)kTile ? Kp : (uint64_t)kTile;
   const int tiles = (int)((Kp + kTile - 1) / kTile);
   bitonic_tile_kernel<<<tiles, 1024, 0, st>>>(key_c, key_p, Kp, 2, tile, ~0ull);
