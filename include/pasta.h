@@ -121,7 +121,10 @@ typedef struct {
  * each one waits for its predecessor's completion (griddepcontrol.wait) before it
  * writes any output, and with this flag only after issuing its first record loads —
  * the streaming mode's per-call latency (NEXT f2). Without the flag every access to
- * global data follows the wait. */
+ * global data follows the wait. The scan triggers its dependents on entry, so a
+ * caller's own kernel launched as a programmatic dependent right after it must
+ * griddepcontrol.wait (cudaGridDependencySynchronize) before reading the outputs;
+ * ordinary launches, copies and events after the call are ordered as usual. */
 enum { PASTA_REC_HOST = 1u, PASTA_REC_STABLE = 2u };
 
 /* Outputs: caller-owned DEVICE memory (e.g. torch int64 tensors viewed as u64).
