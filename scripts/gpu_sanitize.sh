@@ -1,10 +1,12 @@
 # compute-sanitizer runs over the small GPU parity tests (memcheck, racecheck, synccheck, initcheck)
 mkdir -p gpurun_out
-K='hand_worked or snapshot or tiny_config or adversarial_random or contention or host_records or topk_direct or topk_distributions or bitmap_or or topk_merge'
+K='hand_worked or snapshot or tiny_config or adversarial_random or contention or host_records or topk_direct or topk_distributions or bitmap_or or topk_merge or streaming'
 KR='spec_range_filter or random_rich or tiny_rich'
 for tool in memcheck racecheck synccheck initcheck; do
   timeout 1500 compute-sanitizer --tool $tool --error-exitcode 99 --print-limit 20 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "$K" -p no:cacheprovider > gpurun_out/san_$tool.log 2>&1
   echo $tool parity rc=$?; grep -E "ERROR SUMMARY|passed|failed" gpurun_out/san_$tool.log | tail -3
   timeout 1500 compute-sanitizer --tool $tool --error-exitcode 99 --print-limit 20 python -m pytest tests/test_gpu_rich.py -m gpu -x -q -k "$KR" -p no:cacheprovider > gpurun_out/san_rich_$tool.log 2>&1
   echo $tool rich rc=$?; grep -E "ERROR SUMMARY|passed|failed" gpurun_out/san_rich_$tool.log | tail -3
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 99 --print-limit 20 python -m pytest tests/test_gpu_peer.py tests/test_gpu_report_usage.py -m gpu -x -q -k "sum_bitmap or world1 or streams" -p no:cacheprovider > gpurun_out/san_peer_$tool.log 2>&1
+  echo $tool peer rc=$?; grep -E "ERROR SUMMARY|passed|failed" gpurun_out/san_peer_$tool.log | tail -3
 done
