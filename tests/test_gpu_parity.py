@@ -566,3 +566,44 @@ def test_streaming_batches_equal_oracle(batch, stable):
          "kpb": u64(hist.kernel_page_bitmap).reshape(p.n_kernels, -1), "topk": {}}
     assert_parity(g, r, kernel_rows=True, kernel_pages=True, label=f"stream/{batch}")
     tr.close()
+
+
+def test_pdl_ordering_after_producer_kernels():
+    """Programmatic dependent launch must not read stale data: each analyze follows, on
+    the same stream, a torch kernel that rewrites the records (and one that zeroes the
+    outputs), alternating between two traces; without PASTA_REC_STABLE the scan may only
+    touch the records after griddepcontrol.wait. Back-to-back analyze calls into the same
+    outputs (the streaming pattern) must also add up exactly."""
+    p = tracegen.build_plan("tiny", seed=23)
+    r0 = torch.empty(p.n, dtype=torch.int64, device=DEV)
+    tracegen.device_records(tracegen.DevicePlan(p, DEV), r0)
+    r1 = torch.flip(r0, [0]).contiguous()
+    live = torch.empty_like(r0)
+    s = torch.cuda.Stream(DEV)
+    tr = pb.Trace(DEV, p.va_lo, p.va_hi, len(p.allocs), len(p.allocs), stream=s)
+    for b, sz in p.allocs:
+        tr.register_alloc(b, sz)
+    h = tr.histograms(p.page_shift)
+    refs = []
+    for rec in (r0, r1):
+        o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
+        o.analyze(u64(rec), None, p.page_shift)
+        refs.append(o.page_counts.copy())
+    with torch.cuda.stream(s):
+        for it in range(40):
+            src = (r0, r1)[it % 2]
+            live.copy_(src)  # producer kernel right before the scan
+            h.zero_()
+            tr.analyze(live, p.page_shift, h)
+            got = h.page_counts.clone()  # consumer on the same stream
+            s.synchronize()
+            assert np.array_equal(u64(got), refs[it % 2]), f"iteration {it}"
+        # chained calls into the same outputs: 4 x the same records
+        h.zero_()
+        for _ in range(4):
+            tr.analyze(live, p.page_shift, h, finalize=False, stable=True)
+        got = h.page_counts.clone()
+        s.synchronize()
+    with np.errstate(over="ignore"):
+        assert np.array_equal(u64(got), refs[1] * np.uint64(4))
+    tr.close()
