@@ -216,3 +216,13 @@ def test_peer_merger_world1_nccl():
         tr.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_enable_peer_status_codes():
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    tr.enable_peer(DEV.index or 0)  # own device: nothing to enable
+    for bad in (-1, torch.cuda.device_count()):
+        with pytest.raises(pb.PastaError) as ei:
+            tr.enable_peer(bad)
+        assert ei.value.status == pb.PASTA_EINVAL
+    tr.close()
