@@ -31,6 +31,16 @@
  *     torch CUDA tensors; pinned host memory also qualifies). The caller owns
  *     records and outputs; the handle owns its range table and scratch.
  *   - a handle is not thread-safe; several handles per device are fine.
+ *
+ * Entry points (in this file's order): handle (pasta_trace_open / pasta_close /
+ * pasta_strerror / pasta_sync), registration (pasta_register_alloc / _free,
+ * pasta_register_tensor / _free, pasta_report_memory_usage), analysis (pasta_analyze
+ * for 8-byte records, pasta_analyze_rich for 16-byte records, pasta_finalize,
+ * pasta_topk), multi-GPU merge (pasta_peer_reduce + pasta_enable_peer over peer
+ * memory; pasta_bitmap_or + pasta_topk_merge after NCCL collectives), prefetch plans
+ * (pasta_prefetch_plan) and timing (pasta_set_timing / pasta_get_timing /
+ * pasta_reset_timing). Readings R15-R25 (tensor level, rich records, grid-id window,
+ * signed sizes) are in DESIGN.md as well.
  */
 #ifndef PASTA_H
 #define PASTA_H
