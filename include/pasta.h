@@ -135,7 +135,14 @@ typedef struct {
  * caller's own kernel launched as a programmatic dependent right after it must
  * griddepcontrol.wait (cudaGridDependencySynchronize) before reading the outputs;
  * ordinary launches, copies and events after the call are ordered as usual. */
-enum { PASTA_REC_HOST = 1u, PASTA_REC_STABLE = 2u };
+/* PASTA_REC_CHAINED (device records; implies PASTA_REC_STABLE): in addition, the
+ * previous kernel on the handle's stream is a pasta_analyze scan of this handle into
+ * the same outputs, with no other work in between. Its REDs commute with this call's,
+ * so this scan does not wait for it at all before working; it waits only before it
+ * exits, which keeps completion in stream order (a reader enqueued after the last call
+ * of a chain sees every call's counts). The first call of a chain (e.g. after zeroing
+ * the outputs) must not carry the flag. */
+enum { PASTA_REC_HOST = 1u, PASTA_REC_STABLE = 2u, PASTA_REC_CHAINED = 4u };
 
 /* Outputs: caller-owned DEVICE memory (e.g. torch int64 tensors viewed as u64).
  * Counts ACCUMULATE (+=) across calls, so a long trace can be analyzed in batches

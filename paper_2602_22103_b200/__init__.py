@@ -35,6 +35,7 @@ LEVEL_OBJECT, LEVEL_TENSOR = 0, 1
 K_ATTRIBUTED, K_UNATTRIBUTED, K_FOOTPRINT, K_UNIQUE_PAGES, KSTATS = 0, 1, 2, 3, 4
 PASTA_REC_HOST = 1
 PASTA_REC_STABLE = 2
+PASTA_REC_CHAINED = 4
 PASTA_NO_FINALIZE = 1
 PASTA_SCHED_CONTIGUOUS = 1
 PASTA_SCHED_INTERLEAVED = 2
@@ -375,12 +376,13 @@ class Trace:
                           bitmap, pad_pages_to, window_kernels, self.max_tensor_ids)
 
     def analyze(self, records, page_shift: int, hist: Histograms, kernel_offsets=None, n: int | None = None,
-                finalize: bool = True, host: bool = False, stable: bool = False):
+                finalize: bool = True, host: bool = False, stable: bool = False, chained: bool = False):
         if n is None:
             n = records.numel()
         nk = 0 if kernel_offsets is None else kernel_offsets.numel() - 1
         pasta_analyze(self.h, records, n, page_shift, hist.struct(0 if finalize else PASTA_NO_FINALIZE),
-                      kernel_offsets, nk, (PASTA_REC_HOST if host else 0) | (PASTA_REC_STABLE if stable else 0))
+                      kernel_offsets, nk, (PASTA_REC_HOST if host else 0) | (PASTA_REC_STABLE if stable else 0)
+                      | (PASTA_REC_CHAINED if chained else 0))
 
     def rich_outputs(self, page_shift: int, writes: bool = True, bytes_: bool = True) -> RichOutputs:
         return RichOutputs(self.n_pages(page_shift), self.max_ids, self.device, writes, bytes_)

@@ -42,7 +42,7 @@ struct ScanArgs {
   uint64_t* tensor_counts;   // [max_tids]
   uint64_t* ktc;             // kernel_tensor_counts [n_kernels x max_tids] or nullptr
   uint64_t max_tids;
-  uint32_t early;            // PASTA_REC_STABLE: first record loads before the grid-dependency wait
+  uint32_t early;            // 1 PASTA_REC_STABLE: first loads before the grid-dependency wait; 2 CHAINED: wait at the end
 };
 
 // Rich 16-byte records (NEXT f4; R21-R24).

@@ -249,6 +249,7 @@ int scan_range(pasta_trace* h, const uint64_t* rec, uint64_t n, uint64_t g0, Sca
     const uint64_t wpc = (uint64_t)scan_warps();
     const int grid = (int)std::min<uint64_t>((uint64_t)h->sm_count, (slices + wpc - 1) / wpc);
     a.log_ic = scan_schedule(cnt, grid, h->sched);
+    if (a.log_ic >= 0 && a.early == 2) a.early = 1;  // the chunk-map pre-pass is this scan's predecessor
     const size_t sneed = scan_scratch_bytes(cnt, a.log_ic);
     if (sneed > h->scan_bytes) {
       if (h->d_scan) {
@@ -497,8 +498,8 @@ int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t 
   if (!out->page_counts || !out->alloc_counts || !out->totals) return PASTA_EINVAL;
   if ((out->kernel_stats || out->kernel_page_bitmap || out->hotness) && !out->kernel_alloc_counts) return PASTA_EINVAL;
   if (out->hotness && out->window_kernels == 0) return PASTA_EINVAL;
-  if (tr->flags & ~(PASTA_REC_HOST | PASTA_REC_STABLE)) return PASTA_EINVAL;
-  if ((tr->flags & PASTA_REC_HOST) && (tr->flags & PASTA_REC_STABLE)) return PASTA_EINVAL;
+  if (tr->flags & ~(PASTA_REC_HOST | PASTA_REC_STABLE | PASTA_REC_CHAINED)) return PASTA_EINVAL;
+  if ((tr->flags & PASTA_REC_HOST) && (tr->flags & (PASTA_REC_STABLE | PASTA_REC_CHAINED))) return PASTA_EINVAL;
   int s = check_tensor_outputs(h, out);
   if (s) return s;
   s = check_window(h, page_shift);
@@ -546,7 +547,7 @@ int pasta_analyze(pasta_trace* h, const pasta_records* tr, uint64_t n, uint32_t 
   }
 
   if (!host) {
-    a.early = (tr->flags & PASTA_REC_STABLE) ? 1u : 0u;
+    a.early = (tr->flags & PASTA_REC_CHAINED) ? 2u : (tr->flags & PASTA_REC_STABLE) ? 1u : 0u;
     s = scan_range(h, tr->addr, n, 0, a, h->stream, n);
     if (s) return s;
   } else {

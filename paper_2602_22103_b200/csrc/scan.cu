@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   };
   if (lane == 0)
     for (uint32_t j = 0; j < (uint32_t)stages && j < nmy; ++j) issue(j, j);
-  if (args.early) grid_dep_wait();
+  if (args.early == 1) grid_dep_wait();
   if (lane == 0 && blockIdx.x == 0 && warp == 0 && args.add_records) red_add_u64(args.totals + 0, args.add_records);
 
   Ctx c;
@@ -901,6 +901,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
     }
   }
   warp_flush<kRows, kPages>(w, la, o, k, lane);
+  // PASTA_REC_CHAINED: the predecessor is a scan into the same outputs (its REDs commute
+  // with ours), so the work above never waited for it; this grid still completes only
+  // after it, which keeps completion in stream order for every later reader.
+  if (args.early == 2) grid_dep_wait();
 #if PASTA_TRACE_TIMING
   if (lane == 0) g_warp_times[tslot + 3] = gtimer();
 #endif

@@ -42,7 +42,7 @@ class BatchRunner:
         batch while the previous one finishes (PASTA_REC_STABLE)."""
         import torch
 
-        from . import PASTA_NO_FINALIZE, PASTA_REC_STABLE, pasta_analyze, pasta_histograms
+        from . import PASTA_NO_FINALIZE, PASTA_REC_CHAINED, PASTA_REC_STABLE, pasta_analyze, pasta_histograms
 
         self.tr, self.hist, self.page_shift = trace, hist, page_shift
         self.batches = plan_batches(kernel_offsets, n, batch)
@@ -65,8 +65,12 @@ class BatchRunner:
             pos += len(sub)
         self._analyze = pasta_analyze
         self.flags = PASTA_REC_STABLE if stable else 0
+        # after the first batch every call follows a scan of this handle into the same
+        # outputs: chained (no wait before working, completion still in order)
+        self.chain_flags = (PASTA_REC_STABLE | PASTA_REC_CHAINED) if stable else 0
 
     def run(self):
-        """Enqueue every batch (graph-capturable: no host synchronization)."""
-        for addr, nrec, offs, nk, hs in self.calls:
-            self._analyze(self.tr.h, addr, nrec, self.page_shift, hs, offs, nk, self.flags)
+        """Enqueue every batch (graph-capturable: no host synchronization). Nothing else
+        may be enqueued on the trace's stream between the calls."""
+        for i, (addr, nrec, offs, nk, hs) in enumerate(self.calls):
+            self._analyze(self.tr.h, addr, nrec, self.page_shift, hs, offs, nk, self.chain_flags if i else self.flags)

@@ -600,8 +600,8 @@ def test_pdl_ordering_after_producer_kernels():
             assert np.array_equal(u64(got), refs[it % 2]), f"iteration {it}"
         # chained calls into the same outputs: 4 x the same records
         h.zero_()
-        for _ in range(4):
-            tr.analyze(live, p.page_shift, h, finalize=False, stable=True)
+        for i in range(4):  # the first call waits for the zeroing, the rest are chained
+            tr.analyze(live, p.page_shift, h, finalize=False, stable=True, chained=i > 0)
         got = h.page_counts.clone()
         s.synchronize()
     with np.errstate(over="ignore"):
