@@ -35,7 +35,7 @@
  * Entry points (in this file's order): handle (pasta_trace_open / pasta_close /
  * pasta_strerror / pasta_sync), registration (pasta_register_alloc / _free,
  * pasta_register_tensor / _free, pasta_report_memory_usage), analysis (pasta_analyze
- * for 8-byte records, pasta_analyze_rich for 16-byte records, pasta_finalize,
+ * and pasta_analyze_batches for 8-byte records, pasta_analyze_rich for 16-byte records, pasta_finalize,
  * pasta_topk), multi-GPU merge (pasta_peer_reduce + pasta_enable_peer over peer
  * memory; pasta_bitmap_or + pasta_topk_merge after NCCL collectives), prefetch plans
  * (pasta_prefetch_plan) and timing (pasta_set_timing / pasta_get_timing /
@@ -226,6 +226,21 @@ int pasta_report_memory_usage(pasta_trace* h, uint64_t ptr, int64_t delta, uint3
  * then, unless PASTA_NO_FINALIZE, pasta_finalize. n = 0 is legal (finalize only). */
 int pasta_analyze(pasta_trace* h, const pasta_records* trace, uint64_t n, uint32_t page_shift,
                   pasta_histograms* out);
+
+/* Streaming submission (NEXT f2; "a device buffer"): `count` batches, each
+ * analyzed exactly as pasta_analyze(h, &b[i].trace, b[i].n, page_shift, &b[i].out), in
+ * order, with the host-side per-call overhead of one C loop instead of one foreign call
+ * per batch. A batch's outputs usually point into one shared set of histograms (per-
+ * kernel rows offset to the batch's first kernel, PASTA_NO_FINALIZE), with
+ * PASTA_REC_STABLE on the first batch and PASTA_REC_STABLE | PASTA_REC_CHAINED on the
+ * rest. Stops at the first failing batch and returns its status; batches before it
+ * stay enqueued. */
+typedef struct {
+  pasta_records trace;
+  uint64_t n;
+  pasta_histograms out;
+} pasta_batch;
+int pasta_analyze_batches(pasta_trace* h, const pasta_batch* batches, uint32_t count, uint32_t page_shift);
 
 /* Rich 16-byte records (NEXT f4; R21-R23; SPEC S:39-42 MemAccessInfo):
  * little endian u64 address, u32 grid_id, u16 size_bytes (1..128), u8 flags

@@ -65,6 +65,10 @@ class pasta_histograms(ctypes.Structure):
                 ("kernel_tensor_footprint", ctypes.c_void_p)]
 
 
+class pasta_batch(ctypes.Structure):
+    _fields_ = [("trace", pasta_records), ("n", ctypes.c_uint64), ("out", pasta_histograms)]
+
+
 class pasta_rich_records(ctypes.Structure):
     _fields_ = [("records", ctypes.c_void_p), ("grid_lo", ctypes.c_uint32), ("grid_hi", ctypes.c_uint32)]
 
@@ -84,6 +88,7 @@ _SIGS = {
     "pasta_report_memory_usage": (_int, [_vp, _u64, ctypes.c_int64, ctypes.POINTER(_u32)]),
     "pasta_prefetch_plan": (_int, [_vp, _vp, _u32, _u32, _vp, _vp, _u64, ctypes.POINTER(_u64)]),
     "pasta_analyze": (_int, [_vp, ctypes.POINTER(pasta_records), _u64, _u32, ctypes.POINTER(pasta_histograms)]),
+    "pasta_analyze_batches": (_int, [_vp, ctypes.POINTER(pasta_batch), _u32, _u32]),
     "pasta_finalize": (_int, [_vp, _u32, _u32, ctypes.POINTER(pasta_histograms)]),
     "pasta_analyze_rich": (_int, [_vp, ctypes.POINTER(pasta_rich_records), _u64, _u32,
                                   ctypes.POINTER(pasta_histograms), ctypes.POINTER(pasta_rich_outputs)]),
@@ -181,6 +186,11 @@ def pasta_prefetch_plan(h, rows, n_kernels: int, level: int, plan_offsets, plan_
 def pasta_analyze(h, addr, n: int, page_shift: int, hist, kernel_offsets=None, n_kernels: int = 0, flags: int = 0):
     rec = pasta_records(_ptr(addr), _ptr(kernel_offsets), n_kernels, flags)
     _check(_lib.pasta_analyze(h, ctypes.byref(rec), n, page_shift, ctypes.byref(hist)), "pasta_analyze")
+
+
+def pasta_analyze_batches(h, batches, page_shift: int):
+    """batches: a ctypes array of pasta_batch (kept alive by the caller)."""
+    _check(_lib.pasta_analyze_batches(h, batches, len(batches), page_shift), "pasta_analyze_batches")
 
 
 def pasta_analyze_rich(h, records, n: int, grid_lo: int, grid_hi: int, page_shift: int, hist, rich):

@@ -484,6 +484,16 @@ int pasta_register_tensor_free(pasta_trace* h, uint64_t base) {
   return PASTA_OK;
 }
 
+int pasta_analyze_batches(pasta_trace* h, const pasta_batch* batches, uint32_t count, uint32_t page_shift) {
+  if (!h || (count > 0 && !batches)) return PASTA_EINVAL;
+  for (uint32_t i = 0; i < count; ++i) {
+    pasta_histograms out = batches[i].out;
+    const int s = pasta_analyze(h, &batches[i].trace, batches[i].n, page_shift, &out);
+    if (s != PASTA_OK) return s;
+  }
+  return PASTA_OK;
+}
+
 int pasta_report_memory_usage(pasta_trace* h, uint64_t ptr, int64_t delta, uint32_t* out_id) {
   if (!h || delta == 0 || delta == INT64_MIN) return PASTA_EINVAL;
   const bool tensors = h->max_tids > 0;

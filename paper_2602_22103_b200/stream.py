@@ -42,7 +42,8 @@ class BatchRunner:
         batch while the previous one finishes (PASTA_REC_STABLE)."""
         import torch
 
-        from . import PASTA_NO_FINALIZE, PASTA_REC_CHAINED, PASTA_REC_STABLE, pasta_analyze, pasta_histograms
+        from . import (PASTA_NO_FINALIZE, PASTA_REC_CHAINED, PASTA_REC_STABLE, pasta_analyze_batches, pasta_batch,
+                       pasta_histograms, pasta_records)
 
         self.tr, self.hist, self.page_shift = trace, hist, page_shift
         self.batches = plan_batches(kernel_offsets, n, batch)
@@ -63,14 +64,17 @@ class BatchRunner:
                 PASTA_NO_FINALIZE, 0, None)
             self.calls.append((records.data_ptr() + 8 * a, b - a, self.offs.data_ptr() + 8 * pos, len(sub) - 1, hs))
             pos += len(sub)
-        self._analyze = pasta_analyze
-        self.flags = PASTA_REC_STABLE if stable else 0
         # after the first batch every call follows a scan of this handle into the same
         # outputs: chained (no wait before working, completion still in order)
-        self.chain_flags = (PASTA_REC_STABLE | PASTA_REC_CHAINED) if stable else 0
+        flags = PASTA_REC_STABLE if stable else 0
+        chain_flags = (PASTA_REC_STABLE | PASTA_REC_CHAINED) if stable else 0
+        self.array = (pasta_batch * len(self.calls))()
+        for i, (addr, nrec, offs, nk, hs) in enumerate(self.calls):
+            self.array[i] = pasta_batch(pasta_records(addr, offs, nk, chain_flags if i else flags), nrec, hs)
+        self._submit = pasta_analyze_batches
 
     def run(self):
-        """Enqueue every batch (graph-capturable: no host synchronization). Nothing else
-        may be enqueued on the trace's stream between the calls."""
-        for i, (addr, nrec, offs, nk, hs) in enumerate(self.calls):
-            self._analyze(self.tr.h, addr, nrec, self.page_shift, hs, offs, nk, self.chain_flags if i else self.flags)
+        """Enqueue every batch with one pasta_analyze_batches call (graph-capturable: no
+        host synchronization). Nothing else may be enqueued on the trace's stream
+        between the batches."""
+        self._submit(self.tr.h, self.array, self.page_shift)
