@@ -1,6 +1,8 @@
 """Randomized GPU-vs-oracle stress beyond the pytest suite (same helpers, other seeds):
-scan adversarial cases under both schedules, rich traces, top-K distributions.
-python scripts/stress_gpu.py [n_scan] [n_rich] [n_topk] [seed]"""
+scan adversarial cases under both schedules, rich traces, top-K distributions, and
+streaming batches (chained launches, odd batch sizes so misaligned heads and odd tails
+put the extras kernel inside chains).
+python scripts/stress_gpu.py [n_scan] [n_rich] [n_topk] [seed] [n_stream]"""
 import random
 import sys
 import time
@@ -15,7 +17,7 @@ from tests.test_oracle_rich import _pack, _random_rich  # noqa: E402
 import oracle  # noqa: E402
 import paper_2602_22103_b200 as pb  # noqa: E402
 
-n_scan, n_rich, n_topk, seed = [int(x) for x in sys.argv[1:5]] + [200, 200, 100, 7][len(sys.argv) - 1:]
+n_scan, n_rich, n_topk, seed, n_stream = ([int(x) for x in sys.argv[1:6]] + [200, 200, 100, 7, 50][len(sys.argv) - 1:])[:5]
 t0 = time.time()
 rng = random.Random(seed)
 for i in range(n_scan):
@@ -63,3 +65,31 @@ for i in range(n_topk):
         f"stress topk {i}: P={P} kind={kind} K={K}"
 tr.close()
 print(f"topk: {n_topk} cases ok ({time.time() - t0:.0f} s)", flush=True)
+
+from paper_2602_22103_b200.stream import BatchRunner  # noqa: E402
+
+for i in range(n_stream):
+    s = rng.choice([12, 21])
+    n = rng.choice([1, 3, 4097, 60001, 250_000, 700_001])
+    ranges, rec, va_lo, va_hi = tp._adversarial(rng, n, s, rng.choice([0, 5, 40, 300]), near_top=rng.random() < 0.3)
+    nk = rng.choice([1, 2, 7, 50])
+    ko = [0] + sorted(rng.randint(0, n) for _ in range(nk - 1)) + [n]
+    batch = rng.choice([1, 2, 255, 256, 257, 4095, 4096, 65537])
+    tr = tp.gpu_trace(tp.DEV, va_lo, va_hi, ranges)
+    h = tr.histograms(s, n_kernels=nk, kernel_rows=True, kernel_pages=True)
+    drec = tp._t(np.asarray(rec, dtype=np.uint64))
+    runner = BatchRunner(tr, h, drec, np.asarray(ko, dtype=np.int64), n, batch, s, stable=rng.random() < 0.8)
+    for _ in range(rng.choice([1, 2])):  # a second pass accumulates on top
+        runner.run()
+    reps = _ + 1
+    tr.finalize(s, h, n_kernels=nk)
+    tr.sync()
+    o = tp.oracle_trace(va_lo, va_hi, ranges)
+    for _ in range(reps):
+        o.analyze(np.asarray(rec, dtype=np.uint64), ko, s, kernel_rows=True, kernel_pages=True)
+    assert np.array_equal(tp.u64(h.page_counts), o.page_counts), f"stress stream {i}: pages"
+    assert np.array_equal(tp.u64(h.alloc_counts), o.alloc_counts), f"stress stream {i}: allocs"
+    assert np.array_equal(tp.u64(h.kernel_alloc_counts).reshape(nk, -1), o.kernel_rows), f"stress stream {i}: rows"
+    assert tp.u64(h.totals)[:3].tolist() == o.totals.tolist(), f"stress stream {i}: totals"
+    tr.close()
+print(f"stream: {n_stream} cases ok ({time.time() - t0:.0f} s)", flush=True)
