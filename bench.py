@@ -46,8 +46,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=None, help="override the record count (testing only)")
     ap.add_argument("--e2e-records", type=int, default=1 << 31, help="cap of the pinned host trace for e2e")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 28, help="records in the oracle's bounded sample")
-    ap.add_argument("--ref-sample", type=int, default=1 << 24, help="records per --impl reference step")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 28,
+                    help="records in the single-thread oracle's bounded sample")
+    ap.add_argument("--cpu-sample-all", type=int, default=1 << 31,
+                    help="records in the all-core oracle's bounded sample")
+    ap.add_argument("--ref-sample", type=int, default=1 << 28, help="records per --impl reference step (all cores)")
     ap.add_argument("--stream-batch", type=int, default=0,
                     help="also time streaming mode: one pasta_analyze per batch of this many records "
                          "(524288 = the paper's 4 MB buffer), captured in a CUDA graph")
@@ -134,13 +137,38 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle leg
-def oracle_prepare(plan, n_sample):
-    """The first n_sample records of the workload (host generator) and their kernel
-    segments (whole kernel prefix + the cut kernel's head). Not timed."""
+def host_cpu():
+    """(logical CPUs this process may use, CPU model name from /proc/cpuinfo)."""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except Exception:
+        n = os.cpu_count() or 1
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return n, model
+
+
+def oracle_prepare(plan, n_sample, threads=1):
+    """The first n_sample records of the workload (host generator, on `threads` threads)
+    and their kernel segments (whole kernel prefix + the cut kernel's head). Not timed."""
     import tracegen
 
     n_sample = min(n_sample, plan.n)
-    rec = tracegen.host_records(plan, 0, n_sample)
+    rec = np.empty(n_sample, dtype=np.uint64)
+    step = max(1 << 20, -(-n_sample // max(1, threads)))
+    parts = [(j, min(n_sample, j + step)) for j in range(0, n_sample, step)]
+    ths = [threading.Thread(target=tracegen.host_records, args=(plan, j0, j1, rec[j0:j1])) for j0, j1 in parts]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
     ko = plan.kernel_offsets.astype(np.int64)
     k1 = int(np.searchsorted(ko, n_sample, side="right")) - 1
     sub = [int(x) for x in ko[: k1 + 1]]
@@ -149,16 +177,22 @@ def oracle_prepare(plan, n_sample):
     return rec, sub
 
 
-def oracle_run(plan, rec, sub):
-    """Time the oracle (as it stands, single thread) over the prepared sample: the whole
-    path (lookup, histograms, per-kernel rows, bitmap, footprints, top-K)."""
+def oracle_run(plan, rec, sub, threads=1):
+    """Time the oracle (as it stands) over the prepared sample: the whole path (lookup,
+    histograms, per-kernel rows, bitmap, footprints, top-K). threads == 1: the single-
+    thread oracle_analyze; threads > 1: OracleTrace.analyze_parallel (the same C
+    definition on kernel-aligned slabs, per-thread arrays summed)."""
     import oracle
 
     o = oracle.OracleTrace(plan.va_lo, plan.va_hi, len(plan.allocs), len(plan.allocs))
     for b, s in plan.allocs:
         o.register_alloc(b, s)
     t0 = time.perf_counter()
-    o.analyze(rec, sub, plan.page_shift, kernel_rows=True, kernel_pages=plan.want_kernel_pages)
+    if threads > 1:
+        o.analyze_parallel(rec, sub, plan.page_shift, kernel_rows=True, kernel_pages=plan.want_kernel_pages,
+                           threads=threads)
+    else:
+        o.analyze(rec, sub, plan.page_shift, kernel_rows=True, kernel_pages=plan.want_kernel_pages)
     o.bitmap()
     o.footprints()
     for K in plan.topk:
@@ -166,9 +200,24 @@ def oracle_run(plan, rec, sub):
     return time.perf_counter() - t0
 
 
-def oracle_sample(plan, n_sample):
-    rec, sub = oracle_prepare(plan, n_sample)
-    return rec.size, oracle_run(plan, rec, sub), len(sub) - 1
+def cpu_baseline(plan, args):
+    """The oracle timed on this host's cores (rank 0, N = 1 leg): all cores on a bounded
+    sample (the headline `value`) and one thread on a smaller one (the paper's CPU tools
+    are "typically single" threaded). Generation excluded."""
+    nproc, model = host_cpu()
+    rec, sub = oracle_prepare(plan, args.cpu_sample_all, threads=nproc)
+    dt_all = oracle_run(plan, rec, sub, threads=nproc)
+    n_all, nk_all = rec.size, len(sub) - 1
+    del rec
+    rec, sub = oracle_prepare(plan, args.cpu_sample, threads=nproc)
+    dt_one = oracle_run(plan, rec, sub, threads=1)
+    n_one, nk_one = rec.size, len(sub) - 1
+    return {"value": n_all / dt_all / 1e9, "unit": UNIT, "cores": nproc, "kind": "oracle",
+            "sample": f"first {n_all} records ({nk_all} kernel segments) of the {args.config} plan, {nproc} threads "
+                      f"(OracleTrace.analyze_parallel), generation excluded",
+            "nproc": nproc, "cpu_model": model,
+            "single_thread": {"value": n_one / dt_one / 1e9, "unit": UNIT, "cores": 1,
+                              "sample": f"first {n_one} records ({nk_one} kernel segments), 1 thread"}}
 
 
 def run_reference(args):
@@ -178,22 +227,24 @@ def run_reference(args):
     if rank != 0:
         return
     plan = tracegen.build_plan(args.config, args.seed, args.n)
-    rec, sub = oracle_prepare(plan, args.ref_sample)
+    nproc, model = host_cpu()
+    rec, sub = oracle_prepare(plan, args.ref_sample, threads=nproc)
     n_s = rec.size
     times = []
     for i in range(args.warmup + args.steps):
-        dt = oracle_run(plan, rec, sub)
+        dt = oracle_run(plan, rec, sub, threads=nproc)
         if i >= args.warmup:
             times.append(dt)
     tot = sum(times)
     value = n_s * len(times) / tot / 1e9
     sample = (f"first {n_s} records ({len(sub) - 1} kernel segments) of the {args.config} plan per step, "
-              f"1 thread, generation excluded")
+              f"{nproc} threads (OracleTrace.analyze_parallel), generation excluded")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(times) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": args.config, "n_records": n_s, "sample_of": plan.n},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nproc, "kind": "oracle", "sample": sample,
+                             "nproc": nproc, "cpu_model": model},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -268,7 +319,7 @@ def run_ours(args):
     for b, s in plan.allocs:
         tr.register_alloc(b, s)
     hist = tr.histograms(plan.page_shift, n_kernels=nk_loc, kernel_rows=plan.want_kernel_rows,
-                         kernel_pages=plan.want_kernel_pages, pad_pages_to=64 * world)
+                         kernel_pages=plan.want_kernel_pages, pad_pages_to=64 * world, kernel_row0=k0)
     # N > 1: each rank merges its page shard from every rank's counts over peer memory
     # (dist.PeerMerger) or through NCCL (dist.ShardedMerger); top-K from shard candidates
     merger, merge_kind = None, None
@@ -333,14 +384,11 @@ def run_ours(args):
         stream_res = run_stream(args, plan, rec, n_loc, ko_loc, nk_loc, dev, int(hist.totals[0].item()))
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, dev, top_out)
+        e2e = run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, k0, world, group, local, dev, top_out)
     del rec
     cpu = None
-    if rank == 0 and not args.no_cpu:
-        n_s, dt, nk = oracle_sample(plan, args.cpu_sample)
-        cpu = {"value": n_s / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"first {n_s} records ({nk} kernel segments) of the {args.config} plan, 1 thread, "
-                         f"generation excluded"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(plan, args)
     if rank == 0:
         traffic = ncu_traffic(args.config)
         line = {
@@ -430,11 +478,13 @@ def run_stream(args, plan, rec, n_loc, ko_loc, nk_loc, dev, expect_records):
             "graph_us_per_call": graph_ms * 1e3 / calls}
 
 
-def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, dev, top_out):
+def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, k0, world, group, local, dev, top_out):
     """End to end through the public API: every step copies its records from pinned
     host memory (inside pasta_analyze, chunked and overlapped with the scan), runs the
     whole path, and reads the results (totals + top-K) back to the host."""
     import torch
+
+    import paper_2602_22103_b200 as pb
 
     try:
         import psutil
@@ -457,7 +507,7 @@ def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, d
     host.copy_(rec[:n_e])
     ko_h = torch.from_numpy(ko_e.astype(np.int64)).pin_memory()
     h_e = tr.histograms(plan.page_shift, n_kernels=len(ko_e) - 1, kernel_rows=plan.want_kernel_rows,
-                        kernel_pages=plan.want_kernel_pages, pad_pages_to=64 * world)
+                        kernel_pages=plan.want_kernel_pages, pad_pages_to=64 * world, kernel_row0=k0)
     from paper_2602_22103_b200 import dist as pdist
 
     merger = None
@@ -469,7 +519,7 @@ def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, d
                 print(f"bench: e2e peer merge unavailable ({exc!r}); using the NCCL merge", file=sys.stderr)
         if merger is None:
             merger = pdist.ShardedMerger(tr, h_e, plan.topk, group)
-    res_host = torch.empty(8 + 2 * top_out[0].numel() + 1, dtype=torch.int64, pin_memory=True)
+    res_host = torch.empty(pb.TOTALS + 2 * top_out[0].numel() + 1, dtype=torch.int64, pin_memory=True)
     K = top_out[0].numel()
 
     def step():
@@ -482,10 +532,11 @@ def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, world, group, local, d
             for k in plan.topk:
                 tr.topk(h_e.page_counts, k, out=top_out)
             res = top_out
-        res_host[:8].copy_(h_e.totals, non_blocking=True)
-        res_host[8:8 + K].copy_(res[0], non_blocking=True)
-        res_host[8 + K:8 + 2 * K].copy_(res[1], non_blocking=True)
-        res_host[8 + 2 * K:].copy_(res[2], non_blocking=True)
+        T = pb.TOTALS
+        res_host[:T].copy_(h_e.totals, non_blocking=True)
+        res_host[T:T + K].copy_(res[0], non_blocking=True)
+        res_host[T + K:T + 2 * K].copy_(res[1], non_blocking=True)
+        res_host[T + 2 * K:].copy_(res[2], non_blocking=True)
 
     steps = max(2, min(args.steps, 5))
     for _ in range(2):

@@ -71,10 +71,13 @@ enum {
   PASTA_T_WS_OBJ = 4,        /* = max_k footprint[k] in bytes (overwritten; R11) */
   PASTA_T_UNTENSORED = 5,    /* += records in no live tensor (needs tensor_counts; R18) */
   PASTA_T_WS_TENSOR = 6,     /* = max_k tensor footprint[k] (overwritten; needs kernel_tensor_footprint) */
-  PASTA_T_MAX_KERNEL = 7,    /* = MAX_MEM_REFERENCED_KERNEL (R24): the kernel row with
-                                the most analyzed records, ties to the lowest (overwritten by
-                                finalize when kernel_stats is given)                      */
-  PASTA_TOTALS = 8
+  PASTA_T_MAX_KERNEL = 7,    /* = MAX_MEM_REFERENCED_KERNEL (R24): kernel_row0 + the
+                                kernel row with the most analyzed records, ties to the lowest
+                                (overwritten by finalize when kernel_stats is given)      */
+  PASTA_T_MAX_KERNEL_RECORDS = 8, /* = the analyzed records of that kernel (overwritten with
+                                it). Slots 7-8 form one (index, records) pair: shards merge
+                                it with pasta_peer_reduce(PASTA_PEER_ARGMAX), not by sum */
+  PASTA_TOTALS = 9
 };
 
 /* Per-kernel stats row: kernel_stats[k * PASTA_KSTATS + i]. */
@@ -131,17 +134,19 @@ typedef struct {
  * each one waits for its predecessor's completion (griddepcontrol.wait) before it
  * writes any output, and with this flag only after issuing its first record loads —
  * the streaming mode's per-call latency (NEXT f2). Without the flag every access to
- * global data follows the wait. The scan triggers its dependents on entry, so a
- * caller's own kernel launched as a programmatic dependent right after it must
- * griddepcontrol.wait (cudaGridDependencySynchronize) before reading the outputs;
- * ordinary launches, copies and events after the call are ordered as usual. */
+ * global data follows the wait. The scan triggers its dependents right after that wait
+ * (a chained scan, below, at entry), so a caller's own kernel launched as a
+ * programmatic dependent right after it must griddepcontrol.wait
+ * (cudaGridDependencySynchronize) before reading the outputs; ordinary launches, copies
+ * and events after the call are ordered as usual. */
 /* PASTA_REC_CHAINED (device records; implies PASTA_REC_STABLE): in addition, the
  * previous kernel on the handle's stream is a pasta_analyze scan of this handle into
  * the same outputs, with no other work in between. Its REDs commute with this call's,
  * so this scan does not wait for it at all before working; it waits only before it
  * exits, which keeps completion in stream order (a reader enqueued after the last call
  * of a chain sees every call's counts). The first call of a chain (e.g. after zeroing
- * the outputs) must not carry the flag. */
+ * the outputs) must not carry the flag: it waits for the zeroing before it lets any
+ * chained successor launch. */
 enum { PASTA_REC_HOST = 1u, PASTA_REC_STABLE = 2u, PASTA_REC_CHAINED = 4u };
 
 /* Outputs: caller-owned DEVICE memory (e.g. torch int64 tensors viewed as u64).
@@ -170,6 +175,10 @@ typedef struct {
   uint64_t* kernel_tensor_footprint; /* [n_kernels] optional, overwritten by finalize: sum
                                         of registered tensor sizes with a count in kernel k;
                                         totals[WS_TENSOR] = max; needs kernel_tensor_counts */
+  uint64_t kernel_row0;              /* global index of kernel row 0 of these outputs (a
+                                        shard's first kernel; 0 for a whole trace): finalize
+                                        reports totals[MAX_KERNEL] as kernel_row0 + row, so
+                                        shards' (index, records) pairs merge by ARGMAX    */
 } pasta_histograms;
 
 /* Skip the finalize step in pasta_analyze (bitmap, unique pages, footprints, WS);
@@ -314,10 +323,14 @@ int pasta_bitmap_or(pasta_trace* h, const uint64_t* gathered, uint32_t g, uint64
  * out_popcount is non-NULL, lo and n must be multiples of 64 (else EINVAL) and the same
  * pass writes out_bitmap[i / 64] bit i % 64 = (out[i] != 0) and adds the number of
  * non-zero out[i] to *out_popcount (device u64). op PASTA_PEER_MAX: out[i] = max_r
- * src[r][lo + i] (no bitmap). out must not overlap any source range. The sources must
+ * src[r][lo + i] (no bitmap). op PASTA_PEER_ARGMAX (n must be 2): each source holds an
+ * (index, value) pair at src[r][lo], src[r][lo + 1] -- the totals[MAX_KERNEL,
+ * MAX_KERNEL_RECORDS] pair of kernel-aligned shards (R24); out[0..1] = the pair with the
+ * largest value, ties to the smallest index ("the kernel with the most memory
+ * references"). out must not overlap any source range. The sources must
  * be complete (producers synchronized, e.g. a barrier after their analyze) and stay
  * unchanged until this call's stream work is done. */
-enum { PASTA_PEER_SUM = 0u, PASTA_PEER_MAX = 1u };
+enum { PASTA_PEER_SUM = 0u, PASTA_PEER_MAX = 1u, PASTA_PEER_ARGMAX = 2u };
 int pasta_peer_reduce(pasta_trace* h, const uint64_t* const* src, uint32_t g, uint64_t lo, uint64_t n, uint32_t op,
                       uint64_t* out, uint64_t* out_bitmap, uint64_t* out_popcount);
 

@@ -246,6 +246,104 @@ class OracleTrace:
             raise ValueError(f"oracle_analyze (tensors) rejected its input ({rc})")
         self.untensored += int(tot[1])
 
+    def analyze_parallel(self, records, kernel_offsets, page_shift: int = 12, kernel_rows: bool = False,
+                         kernel_pages: bool = False, threads: int | None = None, slab: int = 1 << 24):
+        """The same definition as ``analyze`` over a whole trace, run chunk-parallel on
+        the host's cores (the full-size parity tests and the all-core cpu_baseline).
+
+        The trace is cut at kernel boundaries into slabs of about ``slab`` records; each
+        worker thread runs the unchanged single-thread oracle_analyze on one slab after
+        another into its OWN page / alloc / totals arrays (kernel rows, per-kernel
+        unattributed and per-kernel page rows are disjoint between kernel-aligned slabs,
+        so they are written in place), and the per-thread arrays are summed at the end.
+        That fold is SPEC S:291-299 (every count is a pointwise sum over any partition
+        of the records), pinned in tests/test_oracle_pins.py against the serial call.
+
+        records: a numpy uint64 array [n], or a callable (j0, j1) -> numpy records of
+        [j0, j1) (e.g. tracegen.host_records, so a 10^10-record trace never has to be
+        held in host memory at once). ctypes releases the GIL around every C call, so
+        the threads run concurrently. No hotness, no tensor level (use ``analyze``)."""
+        import threading
+
+        assert not self.max_tensor_ids, "analyze_parallel: one level only"
+        ko = np.ascontiguousarray(kernel_offsets, dtype=np.uint64)
+        nk = ko.size - 1
+        n = int(ko[-1])
+        if callable(records):
+            get = records
+        else:
+            arr = np.ascontiguousarray(records, dtype=np.uint64)
+            assert arr.size == n
+            get = lambda j0, j1: arr[j0:j1]  # noqa: E731
+        P = (self.va_hi - self.va_lo) >> page_shift
+        W = (P + 63) // 64
+        if self.page_counts is None or self.page_shift != page_shift:
+            self.page_counts = np.zeros(P, dtype=np.uint64)
+            self.page_shift = page_shift
+        kac = kun = kp = None
+        if kernel_rows:
+            if self.kernel_rows is None or self.kernel_rows.shape != (nk, self.max_ids):
+                self.kernel_rows = np.zeros((nk, self.max_ids), dtype=np.uint64)
+                self.kun = np.zeros(nk, dtype=np.uint64)
+            kac, kun = self.kernel_rows, self.kun
+        if kernel_pages:
+            if self.kernel_pages is None or self.kernel_pages.shape != (nk, W):
+                self.kernel_pages = np.zeros((nk, W), dtype=np.uint64)
+            kp = self.kernel_pages
+        # kernel-aligned slabs [k_a, k_b) of about `slab` records (a kernel is never cut)
+        slabs, k = [], 0
+        while k < nk:
+            kb = int(np.searchsorted(ko, int(ko[k]) + slab, side="right")) - 1
+            kb = min(nk, max(kb, k + 1))
+            slabs.append((k, kb))
+            k = kb
+        live = (_Range * max(1, len(self.live)))()
+        for i, (b, (s, idx)) in enumerate(sorted(self.live.items())):
+            live[i].base, live[i].size, live[i].id = b, s, idx
+        n_live = len(self.live)
+        T = max(1, min(threads or os.cpu_count() or 1, len(slabs)))
+        acc = [(np.zeros(P, dtype=np.uint64), np.zeros(self.max_ids, dtype=np.uint64), np.zeros(3, dtype=np.uint64))
+               for _ in range(T)]
+        nxt = [0]
+        lock = threading.Lock()
+        errors = []
+
+        def row(a, k0, width):
+            return None if a is None else a.ctypes.data + 8 * k0 * width
+
+        def worker(t):
+            pages, allocs, tot = acc[t]
+            while not errors:
+                with lock:
+                    i = nxt[0]
+                    nxt[0] += 1
+                if i >= len(slabs):
+                    return
+                ka, kb = slabs[i]
+                j0, j1 = int(ko[ka]), int(ko[kb])
+                rec = np.ascontiguousarray(get(j0, j1), dtype=np.uint64)
+                offs = np.ascontiguousarray(ko[ka:kb + 1] - np.uint64(j0))
+                rc = lib().oracle_analyze(ctypes.addressof(live), n_live, _ptr(rec), j1 - j0, _ptr(offs), kb - ka,
+                                          self.va_lo, self.va_hi, page_shift, self.max_ids, _ptr(pages),
+                                          _ptr(allocs), _ptr(tot), row(kac, ka, self.max_ids), row(kun, ka, 1),
+                                          row(kp, ka, W), None, 0)
+                if rc != 0:
+                    errors.append(f"oracle_analyze rejected slab {ka}..{kb} ({rc})")
+
+        ths = [threading.Thread(target=worker, args=(t,)) for t in range(T)]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        if errors:
+            raise ValueError(errors[0])
+        with np.errstate(over="ignore"):
+            for pages, allocs, tot in acc:  # the partition fold (S:291-299)
+                self.page_counts += pages
+                self.alloc_counts += allocs
+                self.totals += tot
+        return T
+
     # ---- rich 16-byte records (NEXT f4, R21-R23) ----
     def analyze_rich(self, rec16: np.ndarray, grid_lo: int, grid_hi: int, page_shift: int = 12,
                      kernel_rows: bool = False):

@@ -27,8 +27,8 @@ _lib = ctypes.CDLL(_LIB_PATH)
 
 PASTA_OK, PASTA_EINVAL, PASTA_EOVERLAP, PASTA_ENOENT, PASTA_ECAPACITY, PASTA_ECUDA, PASTA_ESTATE, PASTA_ENOMEM = (
     0, -1, -2, -3, -4, -5, -6, -7)
-T_RECORDS, T_UNATTRIBUTED, T_OUT_OF_WINDOW, T_UNIQUE_PAGES, T_WS_OBJ, TOTALS = 0, 1, 2, 3, 4, 8
-T_UNTENSORED, T_WS_TENSOR, T_MAX_KERNEL = 5, 6, 7
+T_RECORDS, T_UNATTRIBUTED, T_OUT_OF_WINDOW, T_UNIQUE_PAGES, T_WS_OBJ, TOTALS = 0, 1, 2, 3, 4, 9
+T_UNTENSORED, T_WS_TENSOR, T_MAX_KERNEL, T_MAX_KERNEL_RECORDS = 5, 6, 7, 8
 RT_FILTERED, RT_SHARED, RT_WRITES, RT_BYTES, RICH_TOTALS = 0, 1, 2, 3, 4
 ACC_WRITE, ACC_SHARED = 1, 2
 LEVEL_OBJECT, LEVEL_TENSOR = 0, 1
@@ -62,7 +62,7 @@ class pasta_histograms(ctypes.Structure):
                 ("kernel_stats", ctypes.c_void_p), ("kernel_page_bitmap", ctypes.c_void_p),
                 ("flags", ctypes.c_uint32), ("window_kernels", ctypes.c_uint32), ("hotness", ctypes.c_void_p),
                 ("tensor_counts", ctypes.c_void_p), ("kernel_tensor_counts", ctypes.c_void_p),
-                ("kernel_tensor_footprint", ctypes.c_void_p)]
+                ("kernel_tensor_footprint", ctypes.c_void_p), ("kernel_row0", ctypes.c_uint64)]
 
 
 class pasta_batch(ctypes.Structure):
@@ -218,7 +218,7 @@ def pasta_topk_merge(h, cand_page, cand_count, g: int, k: int, shard_pages: int,
                                  _ptr(out_count), _ptr(out_found)), "pasta_topk_merge")
 
 
-PASTA_PEER_SUM, PASTA_PEER_MAX = 0, 1
+PASTA_PEER_SUM, PASTA_PEER_MAX, PASTA_PEER_ARGMAX = 0, 1, 2
 
 
 def pasta_peer_reduce(h, srcs, lo: int, n: int, out, out_bitmap=None, out_popcount=None, op: int = PASTA_PEER_SUM):
@@ -259,16 +259,17 @@ def pasta_reset_timing(h):
 class Histograms:
     """Output arrays as int64 CUDA tensors (u64 bit patterns).
 
-    ``packed`` = [page_counts (P) | alloc_counts (max_ids) | totals (8) | tensor_counts
+    ``packed`` = [page_counts (P) | alloc_counts (max_ids) | totals (9) | tensor_counts
     (max_tensor_ids)] is one buffer, so the merge across ranks is one all_reduce(SUM)
     (DESIGN.md section 5). Per-kernel arrays and the bitmap are separate tensors."""
 
     def __init__(self, P: int, max_ids: int, device, n_kernels: int = 0, kernel_rows: bool = False,
                  kernel_pages: bool = False, bitmap: bool = True, pad_pages_to: int = 1, window_kernels: int = 0,
-                 max_tensor_ids: int = 0):
+                 max_tensor_ids: int = 0, kernel_row0: int = 0):
         import torch
 
         self.P, self.max_ids, self.n_kernels, self.max_tensor_ids = P, max_ids, n_kernels, max_tensor_ids
+        self.kernel_row0 = kernel_row0  # global index of kernel row 0 (a shard's first kernel)
         self.words = (P + 63) // 64
         # the page part is padded with zero pages to a multiple of `pad_pages_to` so it
         # can be reduce-scattered in equal shards (dist.ShardedMerger)
@@ -309,7 +310,7 @@ class Histograms:
                                 _ptr(self.page_bitmap), _ptr(self.kernel_alloc_counts), _ptr(self.kernel_stats),
                                 _ptr(self.kernel_page_bitmap), flags, self.window_kernels, _ptr(self.hotness),
                                 _ptr(self.tensor_counts), _ptr(self.kernel_tensor_counts),
-                                _ptr(self.kernel_tensor_footprint))
+                                _ptr(self.kernel_tensor_footprint), self.kernel_row0)
 
 
 class RichOutputs:
@@ -381,9 +382,9 @@ class Trace:
         return offsets, ranges[:total]
 
     def histograms(self, page_shift: int, n_kernels: int = 0, kernel_rows=False, kernel_pages=False, bitmap=True,
-                   pad_pages_to: int = 1, window_kernels: int = 0):
+                   pad_pages_to: int = 1, window_kernels: int = 0, kernel_row0: int = 0):
         return Histograms(self.n_pages(page_shift), self.max_ids, self.device, n_kernels, kernel_rows, kernel_pages,
-                          bitmap, pad_pages_to, window_kernels, self.max_tensor_ids)
+                          bitmap, pad_pages_to, window_kernels, self.max_tensor_ids, kernel_row0)
 
     def analyze(self, records, page_shift: int, hist: Histograms, kernel_offsets=None, n: int | None = None,
                 finalize: bool = True, host: bool = False, stable: bool = False, chained: bool = False):

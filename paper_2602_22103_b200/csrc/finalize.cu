@@ -122,8 +122,10 @@ __global__ void __launch_bounds__(kBlock) bitmap_or_kernel(const uint64_t* gathe
 
 // MAX_MEM_REFERENCED_KERNEL (R24): one block, argmax of attributed +
 // unattributed records per kernel row, ties to the lowest row.
+// out[0] = row0 + argmax, out[1] = that row's records (the (index, records) pair that
+// kernel-aligned shards merge with pasta_peer_reduce(PASTA_PEER_ARGMAX)).
 __global__ void __launch_bounds__(1024) max_kernel_kernel(const uint64_t* __restrict__ kstats, uint32_t K,
-                                                          uint64_t* __restrict__ out) {
+                                                          uint64_t row0, uint64_t* __restrict__ out) {
   __shared__ uint64_t sv[32];
   __shared__ uint32_t si[32];
   uint64_t bv = 0;
@@ -165,7 +167,8 @@ __global__ void __launch_bounds__(1024) max_kernel_kernel(const uint64_t* __rest
         sv[0] = sv[w];
         si[0] = si[w];
       }
-    *out = si[0] == 0xFFFFFFFFu ? 0 : si[0];
+    out[0] = row0 + (si[0] == 0xFFFFFFFFu ? 0 : si[0]);
+    out[1] = si[0] == 0xFFFFFFFFu ? 0 : sv[0];
   }
 }
 
@@ -197,8 +200,9 @@ cudaError_t launch_footprint(const uint64_t* kac, uint32_t n_kernels, uint64_t m
   return cudaGetLastError();
 }
 
-cudaError_t launch_max_kernel(const uint64_t* kstats, uint32_t n_kernels, uint64_t* out, cudaStream_t st) {
-  max_kernel_kernel<<<1, 1024, 0, st>>>(kstats, n_kernels, out);
+cudaError_t launch_max_kernel(const uint64_t* kstats, uint32_t n_kernels, uint64_t row0, uint64_t* out,
+                              cudaStream_t st) {
+  max_kernel_kernel<<<1, 1024, 0, st>>>(kstats, n_kernels, row0, out);
   return cudaGetLastError();
 }
 

@@ -71,7 +71,8 @@ int rich_slice_records();
 int rich_warps();
 
 // MAX_MEM_REFERENCED_KERNEL (R24): *out = argmax_k kstats[4k] + kstats[4k+1], ties low.
-cudaError_t launch_max_kernel(const uint64_t* kstats, uint32_t n_kernels, uint64_t* out, cudaStream_t st);
+cudaError_t launch_max_kernel(const uint64_t* kstats, uint32_t n_kernels, uint64_t row0, uint64_t* out,
+                              cudaStream_t st);
 
 // Extra records that are not part of the 16-byte aligned even body (<= 2).
 struct ExtraArgs {

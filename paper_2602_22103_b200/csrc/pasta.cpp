@@ -308,7 +308,8 @@ int finalize_impl(pasta_trace* h, uint32_t page_shift, uint32_t n_kernels, pasta
   }
   if (out->kernel_stats && n_kernels > 0) {
     Timed t(h, PASTA_PH_FINALIZE, h->stream);
-    cudaError_t e = launch_max_kernel(out->kernel_stats, n_kernels, out->totals + PASTA_T_MAX_KERNEL, h->stream);
+    cudaError_t e = launch_max_kernel(out->kernel_stats, n_kernels, out->kernel_row0,
+                                      out->totals + PASTA_T_MAX_KERNEL, h->stream);
     ++h->launches;
     if (e != cudaSuccess) return PASTA_ECUDA;
   }
@@ -755,7 +756,8 @@ int pasta_bitmap_or(pasta_trace* h, const uint64_t* gathered, uint32_t g, uint64
 int pasta_peer_reduce(pasta_trace* h, const uint64_t* const* src, uint32_t g, uint64_t lo, uint64_t n, uint32_t op,
                       uint64_t* out, uint64_t* out_bitmap, uint64_t* out_popcount) {
   if (!h || !src || !out || g == 0 || g > (uint32_t)kMaxPeers || n == 0) return PASTA_EINVAL;
-  if (op != PASTA_PEER_SUM && op != PASTA_PEER_MAX) return PASTA_EINVAL;
+  if (op != PASTA_PEER_SUM && op != PASTA_PEER_MAX && op != PASTA_PEER_ARGMAX) return PASTA_EINVAL;
+  if (op == PASTA_PEER_ARGMAX && n != 2) return PASTA_EINVAL;
   const bool bits = out_bitmap || out_popcount;
   if (bits && (op != PASTA_PEER_SUM || lo % 64 || n % 64)) return PASTA_EINVAL;
   PeerSrc s{};

@@ -86,6 +86,26 @@ __global__ void __launch_bounds__(kBlock) peer_elementwise_kernel(PeerSrc src, u
   }
 }
 
+// (index, value) pairs of g sources -> the pair with the largest value, ties to the
+// smallest index (the merged MAX_MEM_REFERENCED_KERNEL of kernel-aligned shards, R24).
+__global__ void peer_argmax_kernel(PeerSrc src, uint32_t g, uint64_t lo, uint64_t* __restrict__ out) {
+  uint64_t bi = 0, bv = 0;
+  bool any = false;
+#pragma unroll
+  for (int r = 0; r < kMaxPeers; ++r) {
+    if (r < (int)g) {
+      const uint64_t i = ld_stream_u64(src.p[r] + lo), v = ld_stream_u64(src.p[r] + lo + 1);
+      if (!any || v > bv || (v == bv && i < bi)) {
+        bi = i;
+        bv = v;
+        any = true;
+      }
+    }
+  }
+  out[0] = bi;
+  out[1] = bv;
+}
+
 int grid_for(uint64_t items, int per_block, int cap) {
   const uint64_t b = (items + per_block - 1) / per_block;
   return (int)(b < 1 ? 1 : (b > (uint64_t)cap ? cap : b));
@@ -95,7 +115,9 @@ int grid_for(uint64_t items, int per_block, int cap) {
 
 cudaError_t launch_peer_reduce(const PeerSrc& src, uint32_t g, uint64_t lo, uint64_t n, uint32_t op, uint64_t* out,
                                uint64_t* out_bitmap, uint64_t* out_popcount, int grid, cudaStream_t st) {
-  if (op == 0 && (out_bitmap || out_popcount)) {
+  if (op == 2) {
+    peer_argmax_kernel<<<1, 1, 0, st>>>(src, g, lo, out);
+  } else if (op == 0 && (out_bitmap || out_popcount)) {
     const uint64_t words = n / 64;
     peer_sum_bitmap_kernel<<<grid_for(words, kBlock / 32, grid), kBlock, 0, st>>>(src, g, lo, words, out,
                                                                                  out_bitmap, out_popcount);

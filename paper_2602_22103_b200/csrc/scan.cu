@@ -651,8 +651,12 @@ __device__ __forceinline__ uint32_t kernel_of(const uint64_t* __restrict__ koffs
 template <bool kBig, bool kRows, int kPages, bool kIL>
 __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages) {
   // Programmatic dependent launch: the next analyze call's scan may start its prologue
-  // (barrier init, range table into shared memory) on free SMs while this one runs.
-  grid_dep_launch_dependents();
+  // (barrier init, range table into shared memory) on free SMs while this one runs. A
+  // chained scan (early == 2) triggers at entry: its predecessor is a scan that already
+  // passed its own grid-dependency wait. Any other scan triggers only after its wait, so
+  // a chained successor (which never waits before its REDs) cannot start before the
+  // chain's first call has seen every earlier kernel (e.g. the outputs' zeroing) complete.
+  if (args.early == 2) grid_dep_launch_dependents();
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages));
   uint64_t* sB = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages) + kBarBytes + kLaBytes + kPfBytes);
@@ -709,7 +713,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   // partial outputs) is visible after grid_dep_wait; nothing before it touches that
   // data, except the first record loads when the caller declared the records stable
   // (PASTA_REC_STABLE: not written by the stream's previous kernel).
-  if (!args.early) grid_dep_wait();
+  if (!args.early) {
+    grid_dep_wait();
+    grid_dep_launch_dependents();
+  }
 #if PASTA_TRACE_TIMING
   const uint32_t tslot = (blockIdx.x * kWarps + warp) * 4;
   if (lane == 0) g_warp_times[tslot] = gtimer();
@@ -724,7 +731,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   };
   if (lane == 0)
     for (uint32_t j = 0; j < (uint32_t)stages && j < nmy; ++j) issue(j, j);
-  if (args.early == 1) grid_dep_wait();
+  if (args.early == 1) {
+    grid_dep_wait();
+    grid_dep_launch_dependents();
+  }
   if (lane == 0 && blockIdx.x == 0 && warp == 0 && args.add_records) red_add_u64(args.totals + 0, args.add_records);
 
   Ctx c;
@@ -1158,7 +1168,6 @@ __device__ __forceinline__ void rich_add(RichAcc& r, const RichOut& o, const Iva
 
 template <bool kBig, bool kRows>
 __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args, const int stages) {
-  grid_dep_launch_dependents();  // as scan_kernel: the next call's prologue may start now
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + rich_ring_bytes(stages));
   uint4* slot2 = reinterpret_cast<uint4*>(smem + rich_ring_bytes(stages) + kRBarBytes) + (threadIdx.x >> 5);
@@ -1183,6 +1192,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
     for (uint32_t i = threadIdx.x; i < 2 * A; i += kRThreads) sB[i] = args.bounds[i];
   __syncthreads();
   grid_dep_wait();  // the previous kernel's writes (records, outputs) are visible from here
+  grid_dep_launch_dependents();  // as scan_kernel (after the wait): the next call's prologue may start
   const uint64_t pol = l2_evict_first_policy();
   // only the trace's last slice may be partial: the warp that owns it sees it at j = tail_j
   const uint32_t tail_j = (s1 == nsl && nmy) ? nmy - 1u : 0xFFFFFFFFu;

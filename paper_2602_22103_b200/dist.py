@@ -11,6 +11,12 @@ any partition of the records, so:
   ReduceOp.BOR on NCCL), so ranks all_gather their bitmaps and the pasta_bitmap_or
   kernel ORs them and recounts unique pages;
 * WS_obj (a max over kernels) merges with all_reduce(MAX);
+* MAX_MEM_REFERENCED_KERNEL (totals slots 7-8, an (index, records) pair per rank with
+  the index global through Histograms.kernel_row0) merges by ARGMAX: the pairs are
+  gathered and pasta_peer_reduce(PASTA_PEER_ARGMAX) keeps the one with the most records,
+  ties to the lowest kernel (R24). Exact for kernel-aligned shards, whose kernel
+  rows are disjoint; for arbitrary cuts merge_kernel_rows + pasta_finalize on the merged
+  rows recompute it;
 * per-kernel rows are disjoint across ranks for kernel-aligned shards; for arbitrary
   cuts merge_kernel_rows sums the straddling rows.
 Compute stays in the CUDA kernels; these helpers only move data.
@@ -21,8 +27,10 @@ import torch
 import torch.distributed as dist
 
 
-# totals slots merged by MAX (working sets, R11; tensor level R18); the rest are sums
+# totals slots merged by MAX (working sets, R11; tensor level R18), the (index, records)
+# pair of MAX_MEM_REFERENCED_KERNEL merged by ARGMAX (R24); the rest are sums
 _WS_SLOTS = (4, 6)  # PASTA_T_WS_OBJ, PASTA_T_WS_TENSOR
+_MK = 7  # PASTA_T_MAX_KERNEL, PASTA_T_MAX_KERNEL + 1 = PASTA_T_MAX_KERNEL_RECORDS
 
 
 def merge_counts(packed: torch.Tensor, group=None):
@@ -43,6 +51,26 @@ def gather_bitmaps(bitmap: torch.Tensor, group=None, out: torch.Tensor | None = 
 def merge_max(x: torch.Tensor, group=None):
     dist.all_reduce(x, op=dist.ReduceOp.MAX, group=group)
     return x
+
+
+def gather_pairs(pair: torch.Tensor, group=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """[world * 2] rank-major concatenation of every rank's (index, records) pair."""
+    world = dist.get_world_size(group)
+    if out is None:
+        out = torch.empty(world * 2, dtype=pair.dtype, device=pair.device)
+    dist.all_gather_into_tensor(out, pair.contiguous(), group=group)
+    return out
+
+
+def merge_max_kernel(trace, totals: torch.Tensor, saved_pair: torch.Tensor, gathered: torch.Tensor, group=None):
+    """totals[7:9] = the ARGMAX over ranks of the saved (index, records) pairs (one
+    pasta_peer_reduce over the gathered rows, local memory)."""
+    from . import PASTA_PEER_ARGMAX
+
+    world = dist.get_world_size(group)
+    gather_pairs(saved_pair, group, out=gathered)
+    trace.peer_reduce([gathered.data_ptr() + 16 * r for r in range(world)], 0, 2,
+                      totals.data_ptr() + 8 * _MK, op=PASTA_PEER_ARGMAX)
 
 
 def merge_kernel_rows(rows_local: torch.Tensor, k0: int, n_kernels_total: int, group=None) -> torch.Tensor:
@@ -79,13 +107,17 @@ class Merger:
         self.world = dist.get_world_size(group)
         self.gathered = torch.empty(self.world * hist.words, dtype=torch.int64, device=hist.packed.device)
         self.ws = torch.empty(len(_WS_SLOTS), dtype=torch.int64, device=hist.packed.device)
+        self.mk = torch.empty(2, dtype=torch.int64, device=hist.packed.device)
+        self.mk_all = torch.empty(2 * self.world, dtype=torch.int64, device=hist.packed.device)
 
     def merge(self):
         from . import T_UNIQUE_PAGES
 
         h = self.hist
         self.ws.copy_(h.totals[list(_WS_SLOTS)])
+        self.mk.copy_(h.totals[_MK:_MK + 2])
         merge_counts(h.packed, self.group)
+        merge_max_kernel(self.tr, h.totals, self.mk, self.mk_all, self.group)
         gather_bitmaps(h.page_bitmap, self.group, out=self.gathered)
         self.tr.bitmap_or(self.gathered, self.world, h.words, h.page_bitmap,
                           h.totals[T_UNIQUE_PAGES:T_UNIQUE_PAGES + 1])
@@ -115,6 +147,8 @@ class ShardedMerger:
         self.shard = torch.empty(self.S, dtype=torch.int64, device=dev)
         self.gathered = torch.empty(self.world * hist.words, dtype=torch.int64, device=dev)
         self.ws = torch.empty(len(_WS_SLOTS), dtype=torch.int64, device=dev)
+        self.mk = torch.empty(2, dtype=torch.int64, device=dev)
+        self.mk_all = torch.empty(2 * self.world, dtype=torch.int64, device=dev)
         self.ks = tuple(ks)
         self.loc = {k: (torch.empty(k, dtype=torch.int64, device=dev), torch.empty(k, dtype=torch.int64, device=dev),
                         torch.empty(1, dtype=torch.int64, device=dev)) for k in self.ks}
@@ -128,7 +162,9 @@ class ShardedMerger:
 
         h = self.hist
         self.ws.copy_(h.totals[list(_WS_SLOTS)])
+        self.mk.copy_(h.totals[_MK:_MK + 2])
         dist.all_reduce(h.small, op=dist.ReduceOp.SUM, group=self.group)
+        merge_max_kernel(self.tr, h.totals, self.mk, self.mk_all, self.group)
         reduce_scatter_counts(h.pages_padded, self.shard, self.group)
         gather_bitmaps(h.page_bitmap, self.group, out=self.gathered)
         self.tr.bitmap_or(self.gathered, self.world, h.words, h.page_bitmap,
@@ -155,8 +191,9 @@ class PeerMerger:
 
     Outputs as ShardedMerger: hist.small merged (SUMs; WS slots MAX), hist.page_bitmap
     and totals[UNIQUE_PAGES] global, the rank's merged page shard in `shard`, and the
-    global top-k lists (returned). totals[MAX_KERNEL] is not merged (an argmax needs the
-    merged kernel rows). Histograms must be allocated with pad_pages_to = world * 64."""
+    global top-k lists (returned), totals[MAX_KERNEL, MAX_KERNEL_RECORDS] by ARGMAX (exact
+    for kernel-aligned shards with Histograms.kernel_row0 = the shard's first kernel).
+    Histograms must be allocated with pad_pages_to = world * 64."""
 
     def __init__(self, trace, hist, ks, group=None):
         from torch.multiprocessing.reductions import reduce_tensor
@@ -210,7 +247,7 @@ class PeerMerger:
         return t.data_ptr() + 8 * elem
 
     def merge(self):
-        from . import PASTA_PEER_MAX, T_UNIQUE_PAGES
+        from . import PASTA_PEER_ARGMAX, PASTA_PEER_MAX, T_UNIQUE_PAGES
 
         h, tr, W, S = self.hist, self.tr, self.world, self.S
         P_pad = h.P_pad
@@ -227,6 +264,9 @@ class PeerMerger:
             e = h.max_ids + slot
             tr.peer_reduce([self._addr(p[0], P_pad + e) for p in self.peers], 0, 1, self._addr(self.small_out, e),
                            op=PASTA_PEER_MAX)
+        e = h.max_ids + _MK
+        tr.peer_reduce([self._addr(p[0], P_pad + e) for p in self.peers], 0, 2, self._addr(self.small_out, e),
+                       op=PASTA_PEER_ARGMAX)
         for k in self.ks:
             tr.topk(self.shard, k, out=self.loc[k])
         tr.sync()

@@ -45,6 +45,11 @@ class BatchRunner:
         from . import (PASTA_NO_FINALIZE, PASTA_REC_CHAINED, PASTA_REC_STABLE, pasta_analyze_batches, pasta_batch,
                        pasta_histograms, pasta_records)
 
+        if hist.hotness is not None or hist.tensor_counts is not None:
+            # hotness rows are windows of kernels and tensor outputs are per-level rows that
+            # the batch structs below do not carry: refuse instead of leaving them zero
+            raise ValueError("BatchRunner: streaming supports page / alloc / kernel outputs only "
+                             "(no hotness, no tensor level)")
         self.tr, self.hist, self.page_shift = trace, hist, page_shift
         self.batches = plan_batches(kernel_offsets, n, batch)
         dev = records.device

@@ -75,6 +75,12 @@ def run_oracle(o, records_np, page_shift, kernel_offsets=None, kernel_rows=False
                window_kernels=0):
     o.analyze(records_np, kernel_offsets, page_shift, kernel_rows=kernel_rows, kernel_pages=kernel_pages,
               window_kernels=window_kernels)
+    return oracle_results(o, kernel_rows=kernel_rows, kernel_pages=kernel_pages, topk=topk,
+                          window_kernels=window_kernels)
+
+
+def oracle_results(o, kernel_rows=False, kernel_pages=False, topk=(), window_kernels=0):
+    """Every output of an OracleTrace after its analyze calls, in assert_parity's form."""
     out = {"page_counts": o.page_counts.copy(), "alloc_counts": o.alloc_counts.copy(), "totals3": o.totals.copy()}
     bm, u = o.bitmap()
     out["bitmap"], out["unique"] = bm, u
@@ -84,6 +90,8 @@ def run_oracle(o, records_np, page_shift, kernel_offsets=None, kernel_rows=False
         fp, ws = o.footprints()
         out["footprint"], out["ws"] = fp, ws
         out["max_kernel"] = o.max_kernel()
+        per = o.kernel_rows.sum(axis=1, dtype=np.uint64) + o.kun
+        out["max_kernel_records"] = int(per[out["max_kernel"]]) if per.size else 0
     if kernel_pages:
         out["kpb"] = o.kernel_pages.copy()
         out["kup"] = o.kernel_unique_pages()
@@ -111,6 +119,7 @@ def assert_parity(g, r, kernel_rows=False, kernel_pages=False, label=""):
         assert np.array_equal(ks[:, 2], r["footprint"]), f"{label}: footprint"
         assert int(g["totals"][4]) == r["ws"], f"{label}: ws_obj"
         assert int(g["totals"][7]) == r["max_kernel"], f"{label}: max_mem_referenced_kernel"
+        assert int(g["totals"][8]) == r["max_kernel_records"], f"{label}: max_mem_referenced_kernel records"
     if kernel_pages:
         assert np.array_equal(g["kpb"], r["kpb"]), f"{label}: kernel_page_bitmap"
         assert np.array_equal(g["kstats"][:, 3], r["kup"]), f"{label}: kernel unique pages"

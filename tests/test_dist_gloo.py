@@ -21,7 +21,7 @@ import torch.multiprocessing as mp
 import oracle
 import tracegen
 
-TOTALS = 8
+TOTALS = 9  # include/pasta.h PASTA_TOTALS
 
 
 def _free_port():
@@ -76,9 +76,15 @@ def _worker(rank, world, port, aligned, out_q):
         pdist.merge_max(wst)
         rows = torch.from_numpy(o.kernel_rows.view(np.int64).copy())
         full_rows = pdist.merge_kernel_rows(rows, k0, p.n_kernels)
+        # MAX_MEM_REFERENCED_KERNEL: the shard's (global index, records) pair, as finalize
+        # writes it into totals[7:9] with kernel_row0 = k0; gathered for the ARGMAX merge
+        per = o.kernel_rows.sum(axis=1, dtype=np.uint64) + o.kun
+        i = int(np.argmax(per))
+        pairs = pdist.gather_pairs(torch.tensor([k0 + i, int(per[i])], dtype=torch.int64))
         if rank == 0:
             out_q.put({"packed": packed.numpy().copy(), "gathered": gathered.numpy().copy(), "ws": int(wst[0]),
-                       "rows": full_rows.numpy().copy(), "shard": (j0, j1, k0, k1)})
+                       "rows": full_rows.numpy().copy(), "shard": (j0, j1, k0, k1),
+                       "pairs": pairs.numpy().copy()})
     finally:
         dist.destroy_process_group()
 
@@ -122,6 +128,12 @@ def test_gloo_merge_equals_whole_trace(world, aligned):
     fp, ws = o.footprints()
     if aligned:  # kernel-aligned shards: per-kernel rows are disjoint, so WS = max of shard WS
         assert res["ws"] == ws
+        # ... and the ARGMAX of the shards' (index, records) pairs (most records, ties to
+        # the lowest index: the rule of pasta_peer_reduce(PASTA_PEER_ARGMAX), tested on the
+        # GPU) is the whole trace's MAX_MEM_REFERENCED_KERNEL (R24)
+        pairs = res["pairs"].reshape(world, 2)
+        best = min(range(world), key=lambda r: (-int(pairs[r, 1]), int(pairs[r, 0])))
+        assert int(pairs[best, 0]) == o.max_kernel()
     assert np.array_equal(res["rows"].view(np.uint64), o.kernel_rows)
 
 

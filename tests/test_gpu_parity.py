@@ -21,7 +21,8 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_2602_22103_b200 as pb  # noqa: E402
 import oracle  # noqa: E402
 import tracegen  # noqa: E402
-from tests.harness import assert_parity, gpu_trace, oracle_trace, run_gpu, run_oracle, u64  # noqa: E402
+from tests.harness import (assert_parity, gpu_trace, oracle_results, oracle_trace, run_gpu, run_oracle,  # noqa: E402
+                           u64)  # noqa: E402
 
 DEV = torch.device("cuda:0")
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -394,14 +395,18 @@ FULL = ["rn50", "gpt2m", "uvm", "llama"]
 
 
 @pytest.mark.parametrize("name", FULL)
-def test_full_config_sampled(name):
-    """Full-size config in the bench launch configuration: device-generated records,
-    one analyze; oracle recomputes sampled kernel segments one by one (kernel rows,
-    per-kernel unattributed, per-kernel page bits) from host-generated records; global
-    outputs checked by conservation and bitmap/count invariants."""
+def test_full_config_bit_exact(name):
+    """Every output of a full BASELINE config (rn50 5e8, gpt2m 2e9, uvm 4e9 at 2 MiB pages
+    with per-kernel page bitmaps and top-68,266, llama 10.7e9) in the bench's launch
+    configuration (device-generated records, one analyze + finalize, top-K per plan),
+    compared element by element with the WHOLE-trace oracle: page counts (P up to
+    16.8 M), alloc counts, totals, bitmap, unique pages, kernel rows and stats,
+    footprints, WS_obj, MAX_MEM_REFERENCED_KERNEL, per-kernel page bitmaps, top-K lists.
+    The oracle runs chunk-parallel on the host's cores (OracleTrace.analyze_parallel:
+    kernel-aligned slabs, host-generated records, per-thread arrays summed)."""
     p = tracegen.build_plan(name)
     free = torch.cuda.mem_get_info(DEV)[0]
-    if p.n * 8 + (2 << 30) > free:
+    if p.n * 8 + (4 << 30) > free:
         pytest.skip(f"{name} needs {p.n * 8 / 2**30:.1f} GiB")
     dp = tracegen.DevicePlan(p, DEV)
     drec = torch.empty(p.n, dtype=torch.int64, device=DEV)
@@ -410,37 +415,50 @@ def test_full_config_sampled(name):
     ko = [int(x) for x in p.kernel_offsets]
     g = run_gpu(tr, drec, p.page_shift, ko, kernel_rows=True, kernel_pages=p.want_kernel_pages,
                 topk=tuple(p.topk))
-    del drec
-    torch.cuda.empty_cache()
-    n = p.n
-    tot = g["totals"]
-    assert int(tot[0]) == n
-    assert int(g["page_counts"].sum()) + int(tot[2]) == n
-    assert int(g["alloc_counts"].sum()) + int(tot[1]) == n
-    assert np.array_equal(g["kac"].sum(axis=0), g["alloc_counts"])
-    assert int(g["kstats"][:, 1].sum()) == int(tot[1])
-    bm, u = oracle.bitmap(g["page_counts"])  # bitmap/unique recomputed from the GPU's counts
-    assert np.array_equal(g["bitmap"], bm) and int(tot[3]) == u
-    for K in p.topk:  # top-K exactly as the oracle selects from the GPU's counts
-        rp, rc, rf = oracle.topk(g["page_counts"], K)
-        gp, gc, gf = g["topk"][K]
-        assert gf == rf and np.array_equal(gp, rp) and np.array_equal(gc, rc)
-    rng = random.Random(1)
-    ks = sorted(set([0, p.n_kernels - 1] + [rng.randrange(p.n_kernels) for _ in range(6)]))
-    sizes = np.array([s for _, s in p.allocs], dtype=np.uint64)
-    for k in ks:
-        j0, j1 = ko[k], ko[k + 1]
-        if j1 - j0 > 60_000_000:
-            continue
-        rec = tracegen.host_records(p, j0, j1)
-        o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
-        o.analyze(rec, [0, j1 - j0], p.page_shift, kernel_rows=True, kernel_pages=p.want_kernel_pages)
-        assert np.array_equal(g["kac"][k], o.kernel_rows[0]), (name, k)
-        assert int(g["kstats"][k, 1]) == int(o.kun[0]), (name, k)
-        assert int(g["kstats"][k, 2]) == int(sizes[o.kernel_rows[0] > 0].sum()), (name, k)
-        if p.want_kernel_pages:
-            assert np.array_equal(g["kpb"][k], o.kernel_pages[0]), (name, k)
     tr.close()
+    del drec, g["hist"]
+    torch.cuda.empty_cache()
+    o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
+    o.analyze_parallel(lambda j0, j1: tracegen.host_records(p, j0, j1), p.kernel_offsets, p.page_shift,
+                       kernel_rows=True, kernel_pages=p.want_kernel_pages)
+    r = oracle_results(o, kernel_rows=True, kernel_pages=p.want_kernel_pages, topk=tuple(p.topk))
+    assert int(r["totals3"][0]) == p.n
+    assert_parity(g, r, kernel_rows=True, kernel_pages=p.want_kernel_pages, label=name)
+
+
+def _table(rng, A, va_lo, page_shift):
+    """A live ranges packed upward from va_lo: sizes 1 B .. 6 pages, half of them adjacent
+    to their predecessor, the rest after a gap of up to 2 pages."""
+    ranges, b = [], va_lo + rng.randrange(0, 4096)
+    for _ in range(A):
+        if ranges and rng.random() >= 0.5:
+            b += rng.randrange(1, 2 << page_shift)
+        sz = rng.randrange(1, 6 << page_shift)
+        ranges.append((b, sz))
+        b += sz
+    return ranges, b
+
+
+@pytest.mark.parametrize("A", [1544, 1545, 4616, 4617])
+@pytest.mark.parametrize("schedule", SCHEDULES)
+def test_table_size_transitions(A, schedule):
+    """The scan's shared-memory budget changes shape at these table sizes (24 warps: 4 ring
+    stages up to 1,544 ranges, 3 up to 4,616, the global-memory table above): the whole
+    oracle on 3 M records over each, every output."""
+    rng = random.Random(A)
+    va_lo = 1 << 40
+    ranges, end = _table(rng, A, va_lo, 12)
+    va_hi = ((end >> 21) + 1) << 21
+    npr = np.random.default_rng(A)
+    n = 3_000_001
+    starts = npr.integers(va_lo - 8192, va_hi + 8192, size=n // 256 + 1, dtype=np.uint64)
+    elem = npr.choice(np.array([4, 8, 64, 4096], dtype=np.uint64), size=starts.size)
+    rec = (starts[:, None] + elem[:, None] * np.arange(256, dtype=np.uint64)[None, :]).reshape(-1)[:n]
+    scatter = npr.random(n) < 0.05
+    rec[scatter] = npr.integers(va_lo - 8192, va_hi + 8192, size=int(scatter.sum()), dtype=np.uint64)
+    nk = 37
+    ko = [0] + sorted(int(x) for x in npr.integers(0, n, nk - 1)) + [n]
+    _case(ranges, rec, va_lo, va_hi, 12, ko=ko, topk=(1, 1024), label=f"A={A} {schedule}", schedule=schedule)
 
 
 def test_merger_world1_nccl():
@@ -475,6 +493,11 @@ def test_merger_world1_nccl():
         assert np.array_equal(u64(hist.page_bitmap), before[1])
         bm, uq = oracle.bitmap(u64(hist.page_counts))
         assert np.array_equal(u64(hist.page_bitmap), bm) and int(u64(hist.totals)[3]) == uq
+        o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
+        r = run_oracle(o, tracegen.host_records(p), p.page_shift, [int(x) for x in p.kernel_offsets],
+                       kernel_rows=True)
+        assert int(after[-pb.TOTALS:][pb.T_MAX_KERNEL]) == r["max_kernel"]  # the ARGMAX merge of the pair
+        assert int(after[-pb.TOTALS:][pb.T_MAX_KERNEL_RECORDS]) == r["max_kernel_records"]
         tr.close()
     finally:
         dist.destroy_process_group()

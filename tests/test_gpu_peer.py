@@ -111,7 +111,8 @@ def _work(rank, world, port, q, two):
         if two:
             for b, s in p.allocs:
                 tr.register_tensor(b, s)
-        hist = tr.histograms(p.page_shift, n_kernels=k1 - k0, kernel_rows=True, pad_pages_to=64 * world)
+        hist = tr.histograms(p.page_shift, n_kernels=k1 - k0, kernel_rows=True, pad_pages_to=64 * world,
+                             kernel_row0=k0)
         merger = pdist.PeerMerger(tr, hist, (16, 3))
         for step in range(2):  # a second merge on re-analyzed buffers (barrier discipline)
             hist.zero_()
@@ -167,15 +168,19 @@ def test_peer_merger_ranks_on_one_gpu(world, two):
         _, shard, small, pbm, outs, _ = res[r]
         assert np.array_equal(shard, pages[r * S:(r + 1) * S]), f"rank {r}: merged page shard"
         assert np.array_equal(small[:A], o.alloc_counts[:A]), f"rank {r}: alloc counts"
-        tot = small[len(o.alloc_counts):len(o.alloc_counts) + 8]
+        tot = small[len(o.alloc_counts):len(o.alloc_counts) + pb.TOTALS]
         assert tot[:3].tolist() == o.totals.tolist(), f"rank {r}: totals"
         assert int(tot[3]) == uniq, f"rank {r}: unique pages"
         fp, ws = o.footprints()
         assert int(tot[4]) == ws, f"rank {r}: WS_obj (MAX)"
+        mk = o.max_kernel()
+        assert int(tot[pb.T_MAX_KERNEL]) == mk, f"rank {r}: MAX_MEM_REFERENCED_KERNEL (ARGMAX)"
+        per = o.kernel_rows.sum(axis=1, dtype=np.uint64) + o.kun
+        assert int(tot[pb.T_MAX_KERNEL_RECORDS]) == int(per[mk]), f"rank {r}: its records"
         assert np.array_equal(pbm, bm), f"rank {r}: bitmap"
         if two:
             T = len(p.allocs)
-            assert np.array_equal(small[A + 8:A + 8 + T], o.tensor_counts), f"rank {r}: tensor counts"
+            assert np.array_equal(small[A + pb.TOTALS:A + pb.TOTALS + T], o.tensor_counts), f"rank {r}: tensor counts"
             assert int(tot[pb.T_UNTENSORED]) == o.untensored, f"rank {r}: untensored"
             assert int(tot[pb.T_WS_TENSOR]) == o.tensor_footprints()[1], f"rank {r}: WS_tensor (MAX)"
         for k in (16, 3):
@@ -211,11 +216,40 @@ def test_peer_merger_world1_nccl():
         tr.sync()
         torch.cuda.synchronize()
         assert all(np.array_equal(u64(a), b) for a, b in zip(outs[16], ref))
-        assert np.array_equal(u64(hist.totals)[:7], totals[:7])
+        assert np.array_equal(u64(hist.totals), totals)  # every slot, the ARGMAX pair included
+        o = oracle.OracleTrace(p.va_lo, p.va_hi, len(p.allocs), len(p.allocs))
+        for b, s in p.allocs:
+            o.register_alloc(b, s)
+        o.analyze(tracegen.host_records(p), p.kernel_offsets, p.page_shift, kernel_rows=True)
+        assert int(totals[pb.T_MAX_KERNEL]) == o.max_kernel()
         assert np.array_equal(u64(hist.page_bitmap), bm)
         tr.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_peer_argmax_pairs():
+    """PASTA_PEER_ARGMAX: the (index, records) pair with the most records, ties to the
+    lowest index (the MAX_MEM_REFERENCED_KERNEL merge, R24), over 1-16 sources; n != 2
+    is EINVAL."""
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    rng = np.random.default_rng(5)
+    for g in (1, 2, 3, 8, 16):
+        for trial in range(20):
+            vals = rng.integers(0, 4, size=g).astype(np.uint64)  # many ties
+            if trial % 5 == 0:
+                vals[rng.integers(0, g)] = np.uint64((1 << 64) - 1)
+            idx = rng.permutation(10 * g)[:g].astype(np.uint64)
+            buf = torch.from_numpy(np.stack([idx, vals], axis=1).reshape(-1).view(np.int64).copy()).to(DEV)
+            out = torch.zeros(2, dtype=torch.int64, device=DEV)
+            tr.peer_reduce([buf.data_ptr() + 16 * r for r in range(g)], 0, 2, out, op=pb.PASTA_PEER_ARGMAX)
+            tr.sync()
+            best = max(range(g), key=lambda r: (int(vals[r]), -int(idx[r])))
+            assert u64(out).tolist() == [int(idx[best]), int(vals[best])], (g, trial)
+    with pytest.raises(pb.PastaError) as ei:
+        tr.peer_reduce([buf], 0, 3, out, op=pb.PASTA_PEER_ARGMAX)
+    assert ei.value.status == pb.PASTA_EINVAL
+    tr.close()
 
 
 def test_enable_peer_status_codes():

@@ -401,3 +401,51 @@ def test_spec_hotness_matrix_examples():
     assert o3.hotness.shape == (4, 32)
     for w in range(4):
         assert np.array_equal(o3.hotness[w], h[3 * w:3 * w + 3].sum(axis=0))
+
+
+# ---------------- chunk-parallel oracle (full-size parity, all-core cpu_baseline) ----------------
+def test_parallel_oracle_brute_force():
+    """analyze_parallel (kernel-aligned slabs on worker threads, per-thread arrays summed:
+    the S:291-299 partition fold) against the dumb brute force, slab = 1 record so every
+    kernel is its own slab and several threads share each trace."""
+    rng = random.Random(77)
+    for case in range(300):
+        live, recs, ko, va_lo, va_hi, s = _random_case(rng)
+        nk = rng.randint(1, 9)
+        n = len(recs)
+        ko = [0] + sorted(rng.randint(0, n) for _ in range(nk - 1)) + [n]
+        max_ids = max(1, len(live))
+        o = OracleTrace(va_lo, va_hi, 16, max_ids)
+        for b, sz, _ in live:
+            o.register_alloc(b, sz)
+        o.analyze_parallel(np.array(recs, dtype=np.uint64), ko, s, kernel_rows=True, kernel_pages=True,
+                           threads=rng.randint(1, 4), slab=1)
+        bf = brute.analyze(live, recs, ko, va_lo, va_hi, s, max_ids)
+        assert o.page_counts.tolist() == bf["page"], case
+        assert o.alloc_counts.tolist() == bf["alloc"], case
+        assert o.kernel_rows.tolist() == bf["kac"], case
+        assert o.kun.tolist() == bf["kun"], case
+        assert int(o.totals[0]) == n and int(o.totals[1]) == bf["unattr"] and int(o.totals[2]) == bf["oow"], case
+        assert o.kernel_unique_pages().tolist() == [sum(r) for r in bf["kpages"]], case
+
+
+@pytest.mark.parametrize("threads,slab", [(1, 1 << 24), (3, 50_000), (8, 1)])
+def test_parallel_oracle_equals_serial_tiny(threads, slab):
+    """The tiny BASELINE config: analyze_parallel with records given by a generator
+    callback equals the single-thread analyze on the whole array, every output; and two
+    calls accumulate like the serial oracle."""
+    import tracegen
+
+    p = tracegen.build_plan("tiny", seed=5)
+    rec = tracegen.host_records(p)
+    ser = OracleTrace(p.va_lo, p.va_hi, len(p.allocs), len(p.allocs))
+    par = OracleTrace(p.va_lo, p.va_hi, len(p.allocs), len(p.allocs))
+    for b, sz in p.allocs:
+        ser.register_alloc(b, sz)
+        par.register_alloc(b, sz)
+    for _ in range(2):
+        ser.analyze(rec, p.kernel_offsets, p.page_shift, kernel_rows=True, kernel_pages=True)
+        par.analyze_parallel(lambda j0, j1: tracegen.host_records(p, j0, j1), p.kernel_offsets, p.page_shift,
+                             kernel_rows=True, kernel_pages=True, threads=threads, slab=slab)
+    for a in ("page_counts", "alloc_counts", "totals", "kernel_rows", "kun", "kernel_pages"):
+        assert np.array_equal(getattr(par, a), getattr(ser, a)), a
