@@ -41,7 +41,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="llama", choices=["tiny", "rn50", "gpt2m", "uvm", "llama"])
+    ap.add_argument("--config", default="llama",
+                    choices=["tiny", "rn50", "gpt2m", "uvm", "llama", "s_perm", "s_hot", "s_manyranges"],
+                    help="BASELINE config (default: llama, the headline) or a SURVEY section 8d stress row")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=None, help="override the record count (testing only)")

@@ -129,8 +129,10 @@ struct PeerSrc {
 cudaError_t launch_peer_reduce(const PeerSrc& src, uint32_t g, uint64_t lo, uint64_t n, uint32_t op, uint64_t* out,
                                uint64_t* out_bitmap, uint64_t* out_popcount, int grid, cudaStream_t st);
 
-// Top-K scratch layout (device), sized by topk_scratch_bytes(k, grid).
-size_t topk_scratch_bytes(uint64_t k, int grid);
+// Top-K scratch (device): run_topk needs topk_scratch_bytes(k, P), run_topk_merge
+// topk_merge_scratch_bytes(g * k, grid).
+size_t topk_scratch_bytes(uint64_t k, uint64_t P);
+size_t topk_merge_scratch_bytes(uint64_t n, int grid);
 // Enqueues the whole radix-select + gather + sort pipeline; `launch` is called once
 // per kernel launch with the phase's cudaError_t (for counting / timing hooks).
 typedef void (*launch_hook)(void* ctx, int begin);

@@ -700,7 +700,7 @@ int pasta_topk(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t
   if (!h || !page_counts || !out_page || !out_count || !out_found || k == 0 || P == 0) return PASTA_EINVAL;
   DeviceGuard g(h->device);
   const int grid = h->sm_count * 4;
-  const size_t need = topk_scratch_bytes(k, grid);
+  const size_t need = topk_scratch_bytes(k, P);
   if (need > h->topk_bytes) {
     if (h->d_topk) {
       cudaStreamSynchronize(h->stream);
@@ -724,7 +724,7 @@ int pasta_topk_merge(pasta_trace* h, const uint64_t* cand_page, const uint64_t* 
     return PASTA_EINVAL;
   DeviceGuard dg(h->device);
   const int grid = h->sm_count * 4;
-  const size_t need = topk_scratch_bytes((uint64_t)g * k, grid);
+  const size_t need = topk_merge_scratch_bytes((uint64_t)g * k, grid);
   if (need > h->topk_bytes) {
     if (h->d_topk) {
       cudaStreamSynchronize(h->stream);

@@ -5,22 +5,11 @@
 // cudaMemAdvise") but gives no algorithm. Result order (R10): count
 // descending, then page ascending; only non-zero pages; K' = min(K, nnz).
 //
-// Pipeline (all on the device, no host synchronization; the host never learns nnz):
-//  1. one pass: per-CTA shared histogram of a monotone 11-bit "float" key of every
-//     non-zero count (bit length + the 5 bits below the leading one); block 0 derives
-//     nnz, K' = min(K, nnz) and the bin holding the K'-th largest count;
-//  2. up to six MSD radix passes of 11 bits over the counts inside the selected bin,
-//     each followed by a 1-CTA select of the digit where the running count from the
-//     top reaches the remaining rank; they stop as soon as a bin is taken whole, so
-//     T (take every count > T) and `need` (how many pages with count == T) are fixed;
-//  3. gather: pages with count > T go to atomically reserved slots (their order is
-//     fixed by the sort) in the same pass that counts each CTA's `== T` pages; only if
-//     ties are cut, the CTAs that hold needed ties re-read their range and rank those
-//     pages in ascending page order with block exclusive scans (no atomics decide
-//     which are taken);
-//  4. bitonic sort of the K' (padded to a power of two with (0, UINT64_MAX) sentinels
-//     that sort last) by (count desc, page asc): shared-memory tiles of 2048, global
-//     compare-exchange steps for the larger strides; sentinels fill slots [K', K).
+// pasta_topk is ONE cooperative kernel (selection by unique composite keys, see
+// topk_kernel below): at most two passes over the P counts in the common case, the
+// remaining radix digits resolved over a compacted candidate buffer, and the sort of the
+// K' results in the same launch. pasta_topk_merge (g shard lists, multi-GPU) sorts the
+// g * K candidates with the bitonic kernels at the end of this file.
 #include <cstdint>
 
 #include <cooperative_groups.h>
@@ -66,85 +55,177 @@ __device__ __forceinline__ bool before(uint64_t c1, uint64_t p1, uint64_t c2, ui
   return c1 > c2 || (c1 == c2 && p1 < p2);
 }
 
-// Warp-aggregated shared-memory histogram increment: lanes with equal bins are grouped
-// with __match_any_sync and the group leader adds the group size (counts are heavily
-// tied, so plain per-lane atomics would serialize on one bin).
-// Shared-memory histogram increment.
-__device__ __forceinline__ void hist_add(unsigned* h, bool valid, unsigned bin) {
-  if (valid) atomicAdd(&h[bin], 1u);
-}
+// ---- selection by unique composite keys (one cooperative kernel) ----
+//
+// key(p) = (count << pbits) | (pmask - p), pbits = bit length of P - 1: a 128-bit
+// integer, unique per page, whose descending order is exactly (count desc, page asc)
+// (R10). The top-K' list is then the K' largest keys: there are no ties to break, and the
+// selection is an MSD radix select over keys:
+//  A. one pass over the counts: per-CTA shared histogram of a monotone 11-bit "float"
+//     key of every non-zero count (bit length + the 5 bits below the leading one); every
+//     CTA derives nnz, K' = min(K, nnz) and the bin holding the K'-th largest count,
+//     i.e. a key range [rlo, rlo + 2^w - 1] and the rank left inside it;
+//  B. one pass over the counts: keys above the range go to the output slots, keys inside
+//     it are appended to a candidate buffer (capacity C) and counted into the histogram
+//     of the range's next 11-bit digit; the digit holding the rank narrows the range;
+//  C. while the range still has more keys than C (heavy ties over > C pages), more passes
+//     like B; once the buffer holds the whole range, the remaining digits are resolved
+//     over the buffer alone (C keys, not P counts);
+//  D. as soon as the rank covers a whole digit bucket, every key >= its lower bound is
+//     taken (from the buffer, or by one last pass);
+//  E. the K' gathered keys are sorted descending (bitonic: one CTA in shared memory for
+//     K' <= 2048, else grid-wide steps between grid barriers) and decoded into the
+//     outputs; slots [K', K) get (UINT64_MAX, 0).
+// Every CTA computes each digit choice itself from the same global histogram (read after
+// the grid barrier), so one barrier per pass suffices. Nothing depends on the order of
+// the atomics that reserve buffer / output slots: keys are unique and sorted at the end.
+using u128 = unsigned __int128;
 
-// Streaming helper: visit every pair index i < n2 of this grid with kU 16-byte loads in
-// flight per thread (enough memory-level parallelism to stream P x 8 bytes at HBM speed).
-#ifndef PASTA_TOPK_U
-#define PASTA_TOPK_U 8
-#endif
-constexpr int kU = PASTA_TOPK_U;
-#ifndef PASTA_TOPK_CTAS_PER_SM
-#define PASTA_TOPK_CTAS_PER_SM 4  // co-resident CTAs per SM of the cooperative selection kernel
-#endif  // 16-byte loads in flight per thread in the streaming passes
-template <typename F>
-__device__ __forceinline__ void stream_pairs(const ulonglong2* __restrict__ pc2, uint64_t n2, F f) {
-  const uint64_t stride = (uint64_t)gridDim.x * kBlock * kU;
-  for (uint64_t base = (uint64_t)blockIdx.x * kBlock * kU + threadIdx.x; base < n2; base += stride) {
-    ulonglong2 v[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint64_t i = base + (uint64_t)u * kBlock;
-      v[u] = i < n2 ? __ldg(pc2 + i) : make_ulonglong2(0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint64_t i = base + (uint64_t)u * kBlock;
-      if (i < n2) f(i, v[u]);
-    }
-  }
-}
+constexpr int kTB = 512;        // threads per block
+constexpr int kTU = 4;          // 16-byte count loads in flight per thread
+constexpr int kMaxPass = 11;    // pass 0 (float key) + <= ceil(96 / 11) digit passes
+constexpr int kSortTile = 2048; // keys per shared-memory bitonic tile
+constexpr uint64_t kBufMax = 1ull << 20;
 
-// ---- selection passes (device functions of the one cooperative selection kernel) ----
+struct TkHead {  // zeroed before every call
+  unsigned hist[kMaxPass][kBins];
+  unsigned long long fill[kMaxPass];  // keys that fell in the range during full pass i
+  unsigned long long slots;           // keys gathered into the output list
+};
 
-// Pass 1 key: a monotone 11-bit "float" of a non-zero count c with bit length L:
+struct TkArgs {
+  const uint64_t* pc;
+  uint64_t P, K;
+  TkHead* head;
+  u128* buf;
+  uint64_t cap;  // buffer capacity (keys)
+  u128* keys;    // gathered keys [kcap]
+  uint64_t kcap;
+  uint64_t* out_page;
+  uint64_t* out_count;
+  uint64_t* out_found;
+  int pbits;
+};
+
+// Pass-1 key: a monotone 11-bit "float" of a non-zero count c with bit length L:
 // c itself for L <= 6 (exact bins 1..63), else 64 + 32 (L - 7) + the 5 bits below the
-// leading one (bins 64..1919, each covering 2^(L-6) consecutive counts). One pass
-// resolves the bit length and five more bits.
+// leading one (bins 64..1919, each covering 2^(L-6) consecutive counts).
 constexpr int kFirstBins = 64 + 58 * 32;  // 1920
-static_assert(kFirstBins <= kBins, "pass-1 bins share the digit histogram buffers");
+static_assert(kFirstBins <= kBins, "pass-1 bins fit the digit histogram");
 __device__ __forceinline__ unsigned first_key(uint64_t c) {
   const int L = 64 - __clzll((long long)c);
   return L <= 6 ? (unsigned)c : 64u + (unsigned)(L - 7) * 32u + (unsigned)((c >> (L - 6)) & 31u);
 }
 
-// Pass 1: histogram of first_key over the non-zero counts.
-__device__ void dev_first(const uint64_t* __restrict__ pc, uint64_t P, unsigned* h, unsigned* hist) {
-  for (int i = threadIdx.x; i < kFirstBins; i += kBlock) h[i] = 0;
-  __syncthreads();
-  stream_pairs(reinterpret_cast<const ulonglong2*>(pc), P / 2, [&](uint64_t, const ulonglong2& v) {
-    hist_add(h, v.x != 0, first_key(v.x));
-    hist_add(h, v.y != 0, first_key(v.y));
-  });
-  if ((P & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-    const uint64_t c = pc[P - 1];
-    if (c) atomicAdd(&h[first_key(c)], 1u);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kFirstBins; i += kBlock)
-    if (h[i]) atomicAdd(&hist[i], h[i]);
+__device__ __forceinline__ u128 make_key(uint64_t c, uint64_t p, int pbits, uint64_t pmask) {
+  return ((u128)c << pbits) | (u128)(pmask - p);
 }
 
-// Block-wide search (block 0, all threads) for the bin d of hist[0, nb) holding rank
-// `rem` counted from the top: suffix(d + 1) < rem <= suffix(d). Thread t sums bins
-// [t * per, (t + 1) * per); a block suffix scan of those sums (warp shuffles + one
-// shared step) finds the one thread whose chunk holds d, which walks its <= per bins.
-// Returns true in that thread only, with d, the count above bin d and the rank left
-// inside it. `total` (every thread) = the sum of all bins.
-__device__ bool block_find_bin(const unsigned* hist, int nb, int per, unsigned long long rem,
-                               unsigned long long* sm, unsigned long long& total, int& d_out,
-                               unsigned long long& above_out, unsigned long long& rem_out) {
+// Streams the counts: f(p, c) for every page, called by every lane of every warp in step
+// (zero counts for lanes past the end), so f may use warp collectives. 16-byte loads,
+// kTU in flight per thread; an unaligned head element and an odd tail element are
+// visited by warp 0 of block 0 at the end.
+template <typename F>
+__device__ __forceinline__ void tk_stream(const uint64_t* __restrict__ pc, uint64_t P, F&& f) {
+  const uint64_t h = ((reinterpret_cast<uintptr_t>(pc) & 15u) != 0 && P > 0) ? 1 : 0;
+  const ulonglong2* v2 = reinterpret_cast<const ulonglong2*>(pc + h);
+  const uint64_t n2 = (P - h) / 2;
+  const uint64_t step = (uint64_t)gridDim.x * kTB * kTU;
+  for (uint64_t b0 = (uint64_t)blockIdx.x * kTB * kTU; b0 < n2; b0 += step) {
+    ulonglong2 v[kTU];
+#pragma unroll
+    for (int u = 0; u < kTU; ++u) {
+      const uint64_t i = b0 + (uint64_t)u * kTB + threadIdx.x;
+      v[u] = i < n2 ? __ldg(v2 + i) : make_ulonglong2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kTU; ++u) {
+      const uint64_t i = b0 + (uint64_t)u * kTB + threadIdx.x;
+      f(h + 2 * i, v[u].x);
+      f(h + 2 * i + 1, v[u].y);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const bool tail = ((P - h) & 1) != 0;
+    uint64_t p = 0, c = 0;
+    if (threadIdx.x == 0 && h) c = __ldg(pc);
+    if (threadIdx.x == 1 && tail) {
+      p = P - 1;
+      c = __ldg(pc + P - 1);
+    }
+    f(p, c);
+  }
+}
+
+// Warp-aggregated append of `key` (lanes with want) to dst[*ctr ...], slots >= cap
+// dropped (the counter still counts them). Every lane of the warp calls it.
+__device__ __forceinline__ void warp_append(bool want, u128 key, u128* dst, unsigned long long* ctr, uint64_t cap) {
+  const unsigned m = __ballot_sync(kFull, want);
+  if (m == 0) return;
+  const unsigned lane = threadIdx.x & 31u;
+  const int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if ((int)lane == leader) base = atomicAdd(ctr, (unsigned long long)__popc(m));
+  base = __shfl_sync(kFull, base, leader);
+  if (want) {
+    const uint64_t slot = base + __popc(m & ((1u << lane) - 1u));
+    if (slot < cap) dst[slot] = key;
+  }
+}
+
+// Run-length shared-histogram increments: equal consecutive bins (tied counts) cost
+// one shared atomic per run.
+struct RunHist {
+  unsigned bin = 0xFFFFFFFFu, n = 0;
+  __device__ __forceinline__ void add(unsigned* sh, unsigned b) {
+    if (b != bin) {
+      if (n) atomicAdd(&sh[bin], n);
+      bin = b;
+      n = 0;
+    }
+    ++n;
+  }
+  __device__ __forceinline__ void flush(unsigned* sh) {
+    if (n) atomicAdd(&sh[bin], n);
+    n = 0;
+  }
+};
+
+// Shared histogram -> global histogram gh (nb bins), shared bins re-zeroed.
+__device__ __forceinline__ void hist_publish(unsigned* sh, unsigned* gh, int nb) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb; i += kTB) {
+    const unsigned v = sh[i];
+    if (v) {
+      atomicAdd(&gh[i], v);
+      sh[i] = 0;
+    }
+  }
+  __syncthreads();
+}
+
+struct Pick {
+  unsigned long long above;  // keys in bins above d
+  unsigned long long rem;    // rank left inside bin d
+  unsigned long long here;   // keys in bin d
+  unsigned long long total;  // all keys in the histogram
+  int d;
+};
+
+// Every thread of the block: the bin d of the global histogram gh[0, nb) holding rank
+// `rank` counted from the top (suffix(d + 1) < rank <= suffix(d)); with clamp, rank is
+// first replaced by min(rank, total). Thread t sums bins [4t, 4t + 4); a block suffix
+// scan finds the one thread whose chunk holds d; the result is broadcast via `out`.
+__device__ Pick block_pick(const unsigned* gh, int nb, unsigned long long rank, bool clamp,
+                           unsigned long long* sw, Pick* out) {
+  constexpr int per = kBins / kTB;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  unsigned long long mine = 0;
+  unsigned long long b[per], mine = 0;
+#pragma unroll
   for (int j = 0; j < per; ++j) {
     const int d = t * per + j;
-    if (d < nb) mine += hist[d];
+    b[j] = d < nb ? __ldcg(gh + d) : 0u;
+    mine += b[j];
   }
   unsigned long long v = mine;  // suffix sum within the warp (lanes >= lane)
 #pragma unroll
@@ -152,278 +233,255 @@ __device__ bool block_find_bin(const unsigned* hist, int nb, int per, unsigned l
     const unsigned long long x = __shfl_down_sync(kFull, v, o);
     if (lane + o < 32) v += x;
   }
-  if (lane == 0) sm[w] = v;
+  if (lane == 0) sw[w] = v;
   __syncthreads();
-  unsigned long long after = 0;  // warps above this one
-  total = 0;
-  for (int i = 0; i < kBlock / 32; ++i) {
-    total += sm[i];
-    if (i > w) after += sm[i];
+  unsigned long long after = 0, total = 0;
+  for (int i = 0; i < kTB / 32; ++i) {
+    total += sw[i];
+    if (i > w) after += sw[i];
+  }
+  if (clamp && rank > total) rank = total;
+  const unsigned long long S = v + after, Sn = S - mine;
+  if (t == 0) {
+    out->total = total;
+    out->d = -1;
+    out->above = out->rem = out->here = 0;
   }
   __syncthreads();
-  const unsigned long long S = v + after, S_next = S - mine;  // suffix from my chunk / the next
-  if (!(S_next < rem && rem <= S)) return false;
-  rem -= S_next;
-  unsigned long long above = S_next;
-  int d = t * per + per - 1;
-  if (d > nb - 1) d = nb - 1;
-  for (; d > t * per; --d) {
-    if (hist[d] >= rem) break;
-    rem -= hist[d];
-    above += hist[d];
+  if (rank > 0 && Sn < rank && rank <= S) {
+    unsigned long long r = rank - Sn, above = Sn;
+    int j = per - 1;
+    for (; j > 0; --j) {
+      if (b[j] >= r) break;
+      r -= b[j];
+      above += b[j];
+    }
+    out->d = t * per + j;
+    out->above = above;
+    out->rem = r;
+    out->here = b[j];
   }
-  d_out = d;
-  above_out = above;
-  rem_out = rem;
-  return true;
+  __syncthreads();
+  const Pick p = *out;
+  __syncthreads();
+  return p;
 }
 
-// Pick the pass-1 bin holding the K'-th largest count (block 0, all threads): nnz,
-// K' = min(K, nnz) and the bin; then the threshold state.
-__device__ void dev_select_first(volatile State* st, unsigned* hist, uint64_t K, uint64_t Kp, unsigned long long* sm) {
-  constexpr int per = (kFirstBins + kBlock - 1) / kBlock;  // bins per thread
-  unsigned long long nnz = 0, above = 0, rem = 0;
-  int d = 0;
-  // the rank is only known after the total: first pass for nnz, the search inside
-  unsigned long long part = 0;
-  for (int j = 0; j < per; ++j) {
-    const int b = threadIdx.x * per + j;
-    if (b < kFirstBins) part += hist[b];
-  }
-  part = warp_sum_u64(part);
-  if ((threadIdx.x & 31) == 0) sm[kBlock / 32 + (threadIdx.x >> 5)] = part;
-  __syncthreads();
-  for (int i = 0; i < kBlock / 32; ++i) nnz += sm[kBlock / 32 + i];
-  const unsigned long long kp = nnz < K ? nnz : K;
-  if (kp == 0) {
-    if (threadIdx.x == 0) {
-      st->nnz = 0;
-      st->kprime = 0;
-      st->gt_slots = 0;
-      st->need = 0;
-      st->done = 1;
-      st->T = ~0ull;
-    }
-  } else if (block_find_bin(hist, kFirstBins, per, kp, sm, nnz, d, above, rem)) {
-    const unsigned long long here = hist[d];
-    int bits = 0;  // the bin is [lo, lo + 2^bits - 1]
-    unsigned long long lo = (unsigned long long)d;
-    if (d >= 64) {
-      const int L = (d - 64) / 32 + 7;
-      bits = L - 6;
-      lo = (32ull + (unsigned)((d - 64) % 32)) << bits;
-    }
-    st->nnz = nnz;
-    st->kprime = kp;
-    st->gt_slots = 0;
-    st->need = 0;
-    st->lo = lo;
-    st->above = above;
-    st->remaining = rem;
-    if (rem == here) {  // the whole bin is taken: no ties to break
-      st->done = 2;
-      st->T = lo - 1;
-    } else if (above + here <= Kp) {  // every count >= lo fits the sort: it picks the first K'
-      st->done = 2;
-      st->T = lo - 1;
-    } else if (bits == 0) {  // exact value: take the first `rem` pages with this count
-      st->done = 2;
-      st->T = lo;
-      st->need = rem;
-    } else {
-      const int w = bits < kDigitBits ? bits : kDigitBits;
-      st->width = w;
-      st->shift = bits - w;
-      st->done = 0;
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kBins; i += kBlock) hist[i] = 0;
-}
+struct Sel {
+  u128 rlo;    // current key range [rlo, rlo + 2^w - 1]
+  u128 ghi;    // every key above ghi is already in the output list
+  unsigned long long rem;  // how many keys of the range to take (from the top)
+  int w;
+  bool done;   // take every key >= rlo
+};
 
-// One radix digit among the counts of the selected bin.
-__device__ void dev_digit(const uint64_t* __restrict__ pc, uint64_t P, volatile State* st, unsigned* h,
-                          unsigned* hist) {
-  const uint64_t lo = st->lo;
-  const int shift = (int)st->shift, width = (int)st->width;
-  for (int i = threadIdx.x; i < (1 << width); i += kBlock) h[i] = 0;
-  __syncthreads();
-  const uint64_t span = (1ull << (shift + width)) - 1;  // bin = [lo, lo + span]
-  stream_pairs(reinterpret_cast<const ulonglong2*>(pc), P / 2, [&](uint64_t, const ulonglong2& v) {
-    hist_add(h, v.x - lo <= span, (unsigned)((v.x - lo) >> shift));
-    hist_add(h, v.y - lo <= span, (unsigned)((v.y - lo) >> shift));
+__device__ __forceinline__ u128 range_hi(const Sel& s) { return s.rlo + (((u128)1 << s.w) - 1); }
+
+// A full pass over the counts: keys in (range_hi, ghi] (or [rlo, ghi] once done) to the
+// output list; keys inside the range appended to the buffer and counted by next digit.
+__device__ void tk_full_pass(const TkArgs& a, const Sel& s, int ps, unsigned* sh) {
+  const uint64_t pmask = a.pbits ? ((~0ull) >> (64 - a.pbits)) : 0ull;
+  const u128 rlo = s.rlo, rhi = range_hi(s), ghi = s.ghi;
+  const u128 glo = s.done ? rlo : rhi + 1;
+  const bool rng = !s.done;
+  const int dw = s.w < kDigitBits ? s.w : kDigitBits;
+  const int dsh = s.w - dw;
+  RunHist rh;
+  TkHead* hd = a.head;
+  tk_stream(a.pc, a.P, [&](uint64_t p, uint64_t c) {
+    const u128 k = make_key(c, p, a.pbits, pmask);
+    const bool g = c != 0 && k >= glo && k <= ghi;
+    const bool r = rng && c != 0 && k >= rlo && k <= rhi;
+    if (r) rh.add(sh, (unsigned)((k - rlo) >> dsh));
+    warp_append(g, k, a.keys, &hd->slots, a.kcap);
+    if (rng) warp_append(r, k, a.buf, &hd->fill[ps], a.cap);
   });
-  if ((P & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-    const uint64_t c = pc[P - 1];
-    if (c - lo <= span) atomicAdd(&h[(c - lo) >> shift], 1u);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < (1 << width); i += kBlock)
-    if (h[i]) atomicAdd(&hist[i], h[i]);
+  rh.flush(sh);
+  if (rng) hist_publish(sh, hd->hist[ps], 1 << dw);
 }
 
-// Choose the digit (block 0, all threads) where the running count from the top
-// reaches the remaining rank.
-__device__ void dev_select_digit(volatile State* st, unsigned* hist, uint64_t Kp, unsigned long long* sm) {
-  const int shift = (int)st->shift, width = (int)st->width;
-  const unsigned long long rem0 = st->remaining, above0 = st->above, lo0 = st->lo;
-  __syncthreads();  // every thread has read the state before the winner rewrites it
-  const int nb = 1 << width;
-  const int per = (nb + kBlock - 1) / kBlock;  // bins per thread (<= 8)
-  unsigned long long total = 0, above = 0, rem = 0;
-  int d = 0;
-  if (block_find_bin(hist, nb, per, rem0, sm, total, d, above, rem)) {
-    const unsigned long long here = hist[d];
-    const unsigned long long lo = lo0 + ((unsigned long long)d << shift);
-    st->lo = lo;
-    st->above = above0 + above;
-    st->remaining = rem;
-    if (rem == here || above0 + above + here <= Kp) {  // whole bin, or all counts >= lo fit the sort
-      st->done = 2;
-      st->T = lo - 1;
-    } else if (shift == 0) {  // exact value: take the first `rem` pages with this count
-      st->done = 2;
-      st->T = lo;
-      st->need = rem;
-    } else {
-      const int w = shift < kDigitBits ? shift : kDigitBits;
-      st->width = w;
-      st->shift = shift - w;
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < nb; i += kBlock) hist[i] = 0;
-}
-
-// Gather (one pass over this CTA's contiguous page range): every page with count > T
-// to an atomically reserved slot (the sort fixes the order), and the number of pages
-// with count == T to blkcnt[cta].
-__device__ void dev_gather_gt(const uint64_t* __restrict__ pc, uint64_t P, volatile State* st,
-                              unsigned long long* blkcnt, uint64_t* key_c, uint64_t* key_p,
-                              unsigned long long* part) {
-  const uint64_t T = st->T;
-  const uint64_t b0 = (uint64_t)blockIdx.x * P / gridDim.x, b1 = (uint64_t)(blockIdx.x + 1) * P / gridDim.x;
-  uint64_t n = 0;
-  for (uint64_t p0 = b0 + threadIdx.x; p0 < b1; p0 += (uint64_t)kBlock * kU) {
-    uint64_t v[kU];
+// A pass over the buffer's n keys (the whole range of the last full pass): histogram of
+// the current range's next digit, or (done) every key >= rlo to the output list.
+__device__ void tk_buf_pass(const TkArgs& a, const Sel& s, int ps, uint64_t n, unsigned* sh) {
+  const u128 rlo = s.rlo, rhi = range_hi(s);
+  const int dw = s.w < kDigitBits ? s.w : kDigitBits;
+  const int dsh = s.w - dw;
+  RunHist rh;
+  const uint64_t step = (uint64_t)gridDim.x * kTB * kTU;
+  for (uint64_t b0 = (uint64_t)blockIdx.x * kTB * kTU; b0 < n; b0 += step) {
+    u128 v[kTU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint64_t p = p0 + (uint64_t)u * kBlock;
-      v[u] = p < b1 ? __ldg(pc + p) : 0;
+    for (int u = 0; u < kTU; ++u) {
+      const uint64_t i = b0 + (uint64_t)u * kTB + threadIdx.x;
+      v[u] = 0;
+      if (i < n) {
+        const ulonglong2 x = __ldcg(reinterpret_cast<const ulonglong2*>(a.buf + i));
+        v[u] = ((u128)x.y << 64) | x.x;
+      }
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint64_t p = p0 + (uint64_t)u * kBlock;
-      n += (p < b1 && v[u] == T) ? 1u : 0u;
-      if (v[u] > T) {
-        const unsigned long long slot = atomicAdd((unsigned long long*)&st->gt_slots, 1ull);
-        key_c[slot] = v[u];
-        key_p[slot] = p;
+    for (int u = 0; u < kTU; ++u) {
+      const u128 k = v[u];  // 0 is never a key (counts >= 1)
+      if (s.done) {
+        warp_append(k != 0 && k >= rlo, k, a.keys, &a.head->slots, a.kcap);
+      } else if (k >= rlo && k <= rhi && k != 0) {
+        rh.add(sh, (unsigned)((k - rlo) >> dsh));
       }
     }
   }
-  n = warp_sum_u64(n);
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = n;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long s2 = 0;
-    for (int i = 0; i < kBlock / 32; ++i) s2 += part[i];
-    blkcnt[blockIdx.x] = s2;
-  }
+  rh.flush(sh);
+  if (!s.done) hist_publish(sh, a.head->hist[ps], 1 << dw);
 }
 
-// Ties (after a grid barrier): pages with count == T ranked in ascending page order
-// (block exclusive scans over the CTA ranges, no atomics decide which), the first
-// `need` kept in slots [K' - need, K'). Only CTAs whose range holds such pages and whose
-// predecessors do not already supply `need` re-read their range (at most `need` CTAs).
-__device__ void dev_gather_eq(const uint64_t* __restrict__ pc, uint64_t P, volatile State* st,
-                              const unsigned long long* blkcnt, uint64_t* key_c, uint64_t* key_p,
-                              unsigned long long* part, unsigned long long* running_s) {
-  const uint64_t T = st->T, need = st->need, kp = st->kprime;
-  if (blkcnt[blockIdx.x] == 0) return;
-  const uint64_t eq_base_slot = kp - need;
-  const uint64_t b0 = (uint64_t)blockIdx.x * P / gridDim.x, b1 = (uint64_t)(blockIdx.x + 1) * P / gridDim.x;
-  unsigned long long pre = 0;
-  for (unsigned i = threadIdx.x; i < blockIdx.x; i += kBlock) pre += blkcnt[i];
-  pre = warp_sum_u64(pre);
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = pre;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long s2 = 0;
-    for (int i = 0; i < kBlock / 32; ++i) s2 += part[i];
-    *running_s = s2;
-  }
-  __syncthreads();
-  bool ties = *running_s < need;
-  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  for (uint64_t t0 = b0; ties && t0 < b1; t0 += kBlock) {
-    const uint64_t p = t0 + threadIdx.x;
-    const bool eq = p < b1 && __ldg(pc + p) == T;
-    const unsigned bal = __ballot_sync(kFull, eq);
-    const unsigned long long rank_w = __popc(bal & ((1u << lane) - 1));
-    __syncthreads();
-    if (lane == 0) part[wib] = __popc(bal);
-    __syncthreads();
-    unsigned long long off = *running_s;
-    for (unsigned i = 0; i < wib; ++i) off += part[i];
-    if (eq) {
-      const unsigned long long r = off + rank_w;
-      if (r < need) {
-        key_c[eq_base_slot + r] = T;
-        key_p[eq_base_slot + r] = p;
+__device__ __forceinline__ u128 ld_key(const u128* p) {
+  const ulonglong2 x = __ldcg(reinterpret_cast<const ulonglong2*>(p));
+  return ((u128)x.y << 64) | x.x;
+}
+
+// Bitonic steps on n keys of a shared tile whose first key has global index gbase, for
+// sizes [size_lo, size_hi] and strides from min(size / 2, stride_cap) down to 1;
+// descending overall (pairs with (gbase + i) & size == 0 put the larger key first).
+__device__ void tile_bitonic(u128* t, uint32_t n, uint64_t gbase, uint64_t size_lo, uint64_t size_hi,
+                             uint64_t stride_cap) {
+  for (uint64_t size = size_lo; size <= size_hi; size <<= 1) {
+    uint64_t s0 = size >> 1;
+    if (s0 > stride_cap) s0 = stride_cap;
+    for (uint64_t stride = s0; stride > 0; stride >>= 1) {
+      for (uint32_t q = threadIdx.x; q < n / 2; q += kTB) {
+        const uint32_t lo = q & (uint32_t)(stride - 1);
+        const uint32_t i = ((q - lo) << 1) | lo, j = i | (uint32_t)stride;
+        const bool desc = ((gbase + i) & size) == 0;
+        const u128 x = t[i], y = t[j];
+        if (desc ? x < y : x > y) {
+          t[i] = y;
+          t[j] = x;
+        }
       }
+      __syncthreads();
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long s2 = 0;
-      for (int i = 0; i < kBlock / 32; ++i) s2 += part[i];
-      *running_s += s2;
-    }
-    __syncthreads();
-    ties = *running_s < need;
   }
 }
 
-// The whole selection in ONE cooperative launch: the float-key pass, up to six 11-bit
-// digit passes (stopping as soon as the threshold is fixed), the gather of counts > T
-// with per-CTA tie counts and, if ties are cut, the ordered tie gather, separated by
-// grid-wide barriers.
-__global__ void __launch_bounds__(kBlock) select_coop_kernel(const uint64_t* __restrict__ pc, uint64_t P,
-                                                             uint64_t K, uint64_t Kp, State* st_, unsigned* hist,
-                                                             unsigned long long* blkcnt, uint64_t* key_c,
-                                                             uint64_t* key_p) {
+__device__ __forceinline__ void put_key(const TkArgs& a, uint64_t i, u128 k, uint64_t pmask) {
+  a.out_count[i] = (uint64_t)(k >> a.pbits);
+  a.out_page[i] = pmask - (uint64_t)(k & (u128)pmask);
+}
+
+__global__ void __launch_bounds__(kTB, 2) topk_kernel(const TkArgs a) {
   cg::grid_group grid = cg::this_grid();
-  volatile State* st = st_;
-  __shared__ unsigned h[kBins];
-  __shared__ unsigned long long sm[kBlock];
-  __shared__ unsigned long long running_s;
-  dev_first(pc, P, h, hist);
-  grid.sync();
-  if (blockIdx.x == 0) dev_select_first(st, hist, K, Kp, sm);
-  grid.sync();
-  for (int pass = 0; pass < (63 + kDigitBits - 1) / kDigitBits; ++pass) {
-    if (st->done) break;  // grid-uniform: read after the barrier
-    dev_digit(pc, P, st, h, hist);
-    grid.sync();
-    if (blockIdx.x == 0) dev_select_digit(st, hist, Kp, sm);
-    grid.sync();
-  }
-  if (st->done != 2) return;
-  dev_gather_gt(pc, P, st, blkcnt, key_c, key_p, sm);
-  if (st->need == 0) return;  // grid-uniform
-  grid.sync();
-  dev_gather_eq(pc, P, st, blkcnt, key_c, key_p, sm, &running_s);
-}
+  __shared__ unsigned sh[kBins];
+  __shared__ unsigned long long sw[kTB / 32];
+  __shared__ Pick pk;
+  __shared__ u128 tile[kSortTile];
+  for (int i = threadIdx.x; i < kBins; i += kTB) sh[i] = 0;
+  __syncthreads();
+  TkHead* hd = a.head;
+  const uint64_t pmask = a.pbits ? ((~0ull) >> (64 - a.pbits)) : 0ull;
 
-__global__ void pad_kernel(State* st, uint64_t* key_c, uint64_t* key_p, uint64_t Kp) {
-  // filled slots: K' (threshold + ties) or every candidate >= the bin (need = 0)
-  const uint64_t kp = st->need ? st->kprime : st->gt_slots;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Kp; i += (uint64_t)gridDim.x * blockDim.x) {
-    if (i >= kp) {
-      key_c[i] = 0;
-      key_p[i] = ~0ull;
+  // A: float-key histogram of the non-zero counts
+  {
+    RunHist rh;
+    tk_stream(a.pc, a.P, [&](uint64_t, uint64_t c) {
+      if (c) rh.add(sh, first_key(c));
+    });
+    rh.flush(sh);
+    hist_publish(sh, hd->hist[0], kFirstBins);
+  }
+  grid.sync();
+  const Pick p0 = block_pick(hd->hist[0], kFirstBins, a.K, true, sw, &pk);
+  const uint64_t kprime = a.K < p0.total ? a.K : p0.total;
+  if (kprime > 0) {
+    Sel s;
+    uint64_t lo = (uint64_t)p0.d;
+    int bits = 0;
+    if (p0.d >= 64) {
+      const int L = (p0.d - 64) / 32 + 7;
+      bits = L - 6;
+      lo = (32ull + (uint64_t)((p0.d - 64) % 32)) << bits;
+    }
+    s.rlo = (u128)lo << a.pbits;
+    s.w = bits + a.pbits;
+    s.rem = p0.rem;
+    s.done = p0.here == p0.rem;
+    s.ghi = ~(u128)0;
+    bool buf_ok = false;
+    uint64_t nbuf = 0;
+    // B / C / D
+    for (int ps = 1; ps < kMaxPass; ++ps) {
+      if (!buf_ok) {
+        tk_full_pass(a, s, ps, sh);
+        grid.sync();
+        if (s.done) break;
+        const unsigned long long f = __ldcg(&hd->fill[ps]);
+        s.ghi = range_hi(s);
+        if (f <= a.cap) {
+          buf_ok = true;
+          nbuf = f;
+        }
+      } else {
+        tk_buf_pass(a, s, ps, nbuf, sh);
+        grid.sync();
+        if (s.done) break;
+      }
+      const int dw = s.w < kDigitBits ? s.w : kDigitBits;
+      const Pick q = block_pick(hd->hist[ps], 1 << dw, s.rem, false, sw, &pk);
+      s.rlo += (u128)(uint64_t)q.d << (s.w - dw);
+      s.w -= dw;
+      s.rem = q.rem;
+      s.done = q.here == q.rem || s.w == 0;
     }
   }
+  // E: sort the K' gathered keys descending and write the outputs
+  uint64_t kp2 = 2;
+  while (kp2 < kprime) kp2 <<= 1;
+  if (kp2 <= (uint64_t)kSortTile) {
+    if (blockIdx.x == 0) {
+      for (uint32_t i = threadIdx.x; i < (uint32_t)kp2; i += kTB) tile[i] = i < kprime ? ld_key(a.keys + i) : (u128)0;
+      __syncthreads();
+      tile_bitonic(tile, (uint32_t)kp2, 0, 2, kp2, kp2);
+      for (uint32_t i = threadIdx.x; i < (uint32_t)kprime; i += kTB) put_key(a, i, tile[i], pmask);
+    }
+  } else {
+    const uint64_t nthreads = (uint64_t)gridDim.x * kTB, tid = (uint64_t)blockIdx.x * kTB + threadIdx.x;
+    for (uint64_t i = kprime + tid; i < kp2; i += nthreads) a.keys[i] = 0;
+    grid.sync();
+    const uint64_t ntiles = kp2 / kSortTile;
+    auto tile_pass = [&](uint64_t size_lo, uint64_t size_hi, uint64_t cap) {
+      for (uint64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+        u128* g = a.keys + tl * kSortTile;
+        for (int i = threadIdx.x; i < kSortTile; i += kTB) tile[i] = ld_key(g + i);
+        __syncthreads();
+        tile_bitonic(tile, kSortTile, tl * kSortTile, size_lo, size_hi, cap);
+        for (int i = threadIdx.x; i < kSortTile; i += kTB) g[i] = tile[i];
+        __syncthreads();
+      }
+      grid.sync();
+    };
+    tile_pass(2, kSortTile, kSortTile);
+    for (uint64_t size = 2 * (uint64_t)kSortTile; size <= kp2; size <<= 1) {
+      for (uint64_t stride = size >> 1; stride >= (uint64_t)kSortTile; stride >>= 1) {
+        for (uint64_t q = tid; q < kp2 / 2; q += nthreads) {
+          const uint64_t lo = q & (stride - 1);
+          const uint64_t i = ((q - lo) << 1) | lo, j = i | stride;
+          const bool desc = (i & size) == 0;
+          const u128 x = ld_key(a.keys + i), y = ld_key(a.keys + j);
+          if (desc ? x < y : x > y) {
+            a.keys[i] = y;
+            a.keys[j] = x;
+          }
+        }
+        grid.sync();
+      }
+      tile_pass(size, size, kSortTile / 2);
+    }
+    for (uint64_t i = tid; i < kprime; i += nthreads) put_key(a, i, ld_key(a.keys + i), pmask);
+  }
+  // slots [K', K): sentinels; found = K'
+  for (uint64_t i = kprime + (uint64_t)blockIdx.x * kTB + threadIdx.x; i < a.K; i += (uint64_t)gridDim.x * kTB) {
+    a.out_page[i] = ~0ull;
+    a.out_count[i] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.out_found = kprime;
 }
 
 // Bitonic network restricted to one tile in shared memory: for sizes in
@@ -582,8 +640,15 @@ Scratch carve(void* base, uint64_t Kp, int grid) {
 
 }  // namespace
 
-size_t topk_scratch_bytes(uint64_t k, int grid) {
-  const uint64_t Kp = pow2_ceil(k < 2 ? 2 : k);
+size_t topk_scratch_bytes(uint64_t k, uint64_t P) {
+  const uint64_t m = k < P ? k : P;
+  const uint64_t Kp = pow2_ceil(m < 2 ? 2 : m);
+  const uint64_t cap = pow2_ceil(P) < kBufMax ? pow2_ceil(P) : kBufMax;
+  return (sizeof(TkHead) + 255) / 256 * 256 + 16 * cap + 16 * Kp;
+}
+
+size_t topk_merge_scratch_bytes(uint64_t n, int grid) {
+  const uint64_t Kp = pow2_ceil(n < 2 ? 2 : n);
   return 256 + kBins * sizeof(unsigned) + ((size_t)grid * 8 + 255) / 256 * 256 + 2 * Kp * 8;
 }
 
@@ -620,39 +685,44 @@ cudaError_t sort_keys(uint64_t* key_c, uint64_t* key_p, uint64_t Kp, int grid, c
 
 cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_page, uint64_t* out_count,
                      uint64_t* out_found, void* scratch, int grid, cudaStream_t st, int* n_launches) {
-  const uint64_t Kp = pow2_ceil(k < 2 ? 2 : k);
-  Scratch s = carve(scratch, Kp, grid);
-  cudaError_t e = cudaMemsetAsync(scratch, 0, 256 + kBins * sizeof(unsigned), st);
+  const uint64_t m = (uint64_t)k < P ? (uint64_t)k : P;
+  TkArgs a;
+  a.pc = pc;
+  a.P = P;
+  a.K = k;
+  char* b = static_cast<char*>(scratch);
+  a.head = reinterpret_cast<TkHead*>(b);
+  b += (sizeof(TkHead) + 255) / 256 * 256;
+  a.cap = pow2_ceil(P) < kBufMax ? pow2_ceil(P) : kBufMax;
+  a.buf = reinterpret_cast<u128*>(b);
+  b += 16 * a.cap;
+  a.kcap = pow2_ceil(m < 2 ? 2 : m);
+  a.keys = reinterpret_cast<u128*>(b);
+  a.out_page = out_page;
+  a.out_count = out_count;
+  a.out_found = out_found;
+  a.pbits = P > 1 ? 64 - __builtin_clzll(P - 1) : 0;
+  cudaError_t e = cudaMemsetAsync(a.head, 0, sizeof(TkHead), st);
   if (e != cudaSuccess) return e;
-  {
-    static int coop_blocks = 0;  // co-resident blocks per SM for the cooperative launch
-    if (coop_blocks == 0) {
-      int nb = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, select_coop_kernel, kBlock, 0) != cudaSuccess || nb < 1)
-        nb = 1;
-      coop_blocks = nb;
-    }
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int g = sms * (coop_blocks < PASTA_TOPK_CTAS_PER_SM ? coop_blocks : PASTA_TOPK_CTAS_PER_SM);
-    const uint64_t need_blocks = (P + kBlock - 1) / kBlock;
-    if ((uint64_t)g > need_blocks) g = (int)(need_blocks < 1 ? 1 : need_blocks);
-    if (g > grid) g = grid;
-    uint64_t K64 = k, Kp64 = Kp;
-    void* args[] = {(void*)&pc, (void*)&P, (void*)&K64, (void*)&Kp64, (void*)&s.st, (void*)&s.hist,
-                    (void*)&s.blkcnt, (void*)&s.key_c, (void*)&s.key_p};
-    PASTA_TRY(cudaLaunchCooperativeKernel((void*)select_coop_kernel, dim3(g), dim3(kBlock), args, 0, st));
+  static int coop_blocks = 0;  // co-resident blocks per SM for the cooperative launch
+  if (coop_blocks == 0) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, topk_kernel, kTB, 0) != cudaSuccess || nb < 1) nb = 1;
+    coop_blocks = nb;
   }
-  const int pg = (int)((Kp + 1023) / 1024 < 1024 ? (Kp + 1023) / 1024 : 1024);
-  pad_kernel<<<pg, 1024, 0, st>>>(s.st, s.key_c, s.key_p, Kp);
-  PASTA_TRY(cudaGetLastError());
-  e = sort_keys(s.key_c, s.key_p, Kp, grid, st, n_launches);
-  if (e != cudaSuccess) return e;
-  int wg = (int)((k + 255) / 256);
-  if (wg > grid) wg = grid;
-  write_kernel<<<wg, 256, 0, st>>>(s.st, s.key_c, s.key_p, k, out_page, out_count, out_found, 0);
-  PASTA_TRY(cudaGetLastError());
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int g = sms * (coop_blocks < 2 ? coop_blocks : 2);
+  // no more CTAs than the counts (or the sort) give work to
+  const uint64_t want = (P + 2ull * kTB * kTU - 1) / (2ull * kTB * kTU);
+  const uint64_t want_sort = a.kcap / kSortTile;
+  uint64_t w = want > want_sort ? want : want_sort;
+  if (w < 1) w = 1;
+  if ((uint64_t)g > w) g = (int)w;
+  if (g > grid) g = grid;
+  void* args[] = {(void*)&a};
+  PASTA_TRY(cudaLaunchCooperativeKernel((void*)topk_kernel, dim3(g), dim3(kTB), args, 0, st));
   return cudaSuccess;
 }
 

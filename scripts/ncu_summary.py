@@ -14,7 +14,13 @@ for r in det[1:]:
 raw = list(csv.reader(io.StringIO(run(["--page", "raw", "--csv"]))))
 if raw:
     hh = raw[0]; vals = raw[2] if len(raw) > 2 else raw[1]
-    for key in ["dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_requests_op_red.sum", "lts__t_requests_op_atom.sum",
+    for key in ["dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_requests_srcunit_tex_op_red.sum",
+                "lts__t_requests_srcunit_tex_op_atom_dot_alu.sum", "lts__t_requests_srcunit_tex_op_atom_dot_cas.sum",
+                "lts__t_sectors_srcunit_tex_op_red.sum.pct_of_peak_sustained_elapsed",
+                "lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed",
+                "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+                "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                "smsp__issue_active.avg.pct_of_peak_sustained_active", "lts__t_requests_srcunit_tex_op_read.sum",
                 "smsp__inst_executed.sum", "gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
                 "smsp__average_warp_latency_issue_stalled_barrier", "smsp__pcsamp_warps_issue_stalled_long_scoreboard"]:
         for i, name in enumerate(hh):

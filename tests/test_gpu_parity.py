@@ -315,6 +315,24 @@ def test_topk_direct(K):
     tr.close()
 
 
+def test_topk_unaligned_tiny_and_k_above_p():
+    """The count array may start at an 8-byte (not 16-byte) boundary (a slice of a
+    larger buffer), hold 1 or 2 pages, or be shorter than K (scratch sized by min(K, P);
+    slots [found, K) are sentinels)."""
+    rng = np.random.default_rng(5)
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    big = rng.integers(0, 9, size=200_001).astype(np.uint64)
+    dbig = _t(big)
+    for off, P, K in [(1, 200_000, 1000), (1, 1, 5), (3, 2, 1), (0, 1, 68266), (1, 77, 68266), (0, 2, 2)]:
+        sub = big[off:off + P]
+        p, c, f = tr.topk(dbig[off:off + P], K)
+        tr.sync()
+        rp, rc, rf = oracle.topk(sub, K)
+        assert int(u64(f)[0]) == rf, (off, P, K)
+        assert np.array_equal(u64(p), rp) and np.array_equal(u64(c), rc), (off, P, K)
+    tr.close()
+
+
 def _topk_dists():
     rng = np.random.default_rng(2024)
     P = 3_000_017  # several CTAs' ranges, odd length
@@ -392,9 +410,12 @@ def test_errors_are_status_codes():
 
 # ------------------------------------------------------------------ full BASELINE sizes
 FULL = ["rn50", "gpt2m", "uvm", "llama"]
+# SURVEY.md section 8d stress rows at their full sizes: s_perm (gpt2m with every stream a
+# permutation), s_hot (2^31 records on one page), s_manyranges (A = 65,536: global table)
+STRESS = list(tracegen.plan.STRESS)
 
 
-@pytest.mark.parametrize("name", FULL)
+@pytest.mark.parametrize("name", FULL + STRESS)
 def test_full_config_bit_exact(name):
     """Every output of a full BASELINE config (rn50 5e8, gpt2m 2e9, uvm 4e9 at 2 MiB pages
     with per-kernel page bitmaps and top-68,266, llama 10.7e9) in the bench's launch

@@ -122,3 +122,29 @@ def test_pattern_closed_forms():
             assert all(x == p0 or x == p0 - S for x in d)
         if kind == STRIDED:
             assert all((int(a) - base) % (1 << p0) == 0 for a in seg[:1000])
+
+
+def test_stress_plans_structure():
+    """SURVEY.md section 8d stress rows: s_perm keeps gpt2m's kernels / allocations /
+    record counts with every non-stray stream a permutation; s_hot puts every record on
+    one 4 KiB page; s_manyranges registers 65,536 disjoint ranges inside its window and
+    sends ~30 % of its records to the small ones."""
+    g, sp = build_plan("gpt2m"), build_plan("s_perm")
+    assert sp.n == g.n and sp.allocs == g.allocs and np.array_equal(sp.kernel_offsets, g.kernel_offsets)
+    assert np.array_equal(sp.streams[:, 0], g.streams[:, 0])
+    kinds = set(int(k) for k in sp.streams[:, 1])
+    assert kinds <= {PERM, STRAY} and PERM in kinds
+    for row in sp.streams[:50]:
+        if int(row[1]) == PERM:
+            S, e = int(row[3]), int(row[4])
+            assert S & (S - 1) == 0 and S % e == 0 and int(row[5]) & 1
+    h = build_plan("s_hot")
+    (pb, psz), = h.allocs
+    assert psz == 4096 and pb % 4096 == 0 and h.n == 1 << 31
+    r = host_records(h, h.n - (1 << 16), h.n)
+    assert int(r.min()) >= pb and int(r.max()) < pb + 4096
+    m = build_plan("s_manyranges")
+    assert len(m.allocs) == 65536
+    iv = sorted(m.allocs)
+    assert all(b0 + s0 <= b1 for (b0, s0), (b1, _) in zip(iv, iv[1:]))
+    assert iv[0][0] >= m.va_lo and iv[-1][0] + iv[-1][1] <= m.va_hi

@@ -485,13 +485,94 @@ def plan_llama(seed: int = 42, n: int = 10 * (1 << 30)) -> Plan:
                    topk=(1024,), want_kernel_rows=True, note="Llama-7B-shaped bf16 train step, s4096")
 
 
+# ----------------------------------------------------------------------------------------
+# stress rows (SURVEY.md section 8d "Stress rows"; reported separately, never the headline)
+# ----------------------------------------------------------------------------------------
+def plan_s_perm(seed: int = 42, n: int = 2_000_000_000) -> Plan:
+    """S-perm: the gpt2m plan with every stream replaced by the permutation pattern over
+    the same allocation (its largest power-of-two prefix), element size 4: worst-case
+    locality -- consecutive records of a stream land on unrelated pages of the tensor.
+    Stray streams stay strays (they are already scattered). Same allocations, kernels and
+    record counts as gpt2m."""
+    p = plan_gpt2m(seed, n)
+    rng = random.Random(seed ^ 0x9E7A)
+    st = p.streams.copy()
+    for r in range(st.shape[0]):
+        if int(st[r, 1]) == STRAY:
+            continue
+        base, S = int(st[r, 2]), int(st[r, 3])
+        S2 = _pow2_floor(S)
+        e = 4 if S2 >= 4 else 1
+        M = S2 // e
+        st[r, 1:7] = [PERM, base, S2, e, (rng.getrandbits(40) << 1) | 1, rng.randrange(M)]
+    p.streams = st
+    p.name = "s_perm"
+    p.note = "gpt2m with every stream a permutation (scattered pages inside each tensor)"
+    return p
+
+
+def plan_s_hot(seed: int = 42, n: int = 1 << 31) -> Plan:
+    """S-hot: 2^31 records all on one 4 KiB page (one 4 KiB allocation), 1,000 kernels
+    alternating a sweep (e = 8, every lane a different word) and a permutation (e = 4) of
+    the page: maximum same-address contention on one page counter and one alloc bin."""
+    va_lo = 0x7D0000000000
+    b = _Builder(seed)
+    page = va_lo + 0x1000 * 37
+    allocs = [(page, 4096)]
+    for k in range(1000):
+        b.add_kernel([(1, b.sweep(page, 4096, 8) if k % 2 == 0 else b.perm(page, 4096, 4))])
+    ko, st, cdf = b.finish(n)
+    return Plan("s_hot", seed, n, va_lo, va_lo + 2 * MiB, 12, allocs, ko, st, cdf, topk=[16],
+                want_kernel_rows=True, want_kernel_pages=False,
+                note="2^31 records on one 4 KiB page, 1000 kernels", objects=[(va_lo, 2 * MiB)])
+
+
+def plan_s_manyranges(seed: int = 42, n: int = 500_000_000, A: int = 65_536) -> Plan:
+    """S-manyranges: the rn50 kernel sequence with A = 65,536 live ranges (the range table
+    no longer fits shared memory: the scan's global-memory table). The rn50 tensors plus
+    small tensors (512 B .. 32 KiB, 512 B steps) up to A; every kernel also sweeps 24 of
+    the small tensors in turn (all of them over the 3,000 kernels; ~30 % of the records), so
+    interval changes and table searches are frequent. 8 GiB window at 4 KiB pages."""
+    window = 8 * GiB
+    va_lo = 0x7E0000000000
+    tensors = _transformer_tensors(8, 512, 2048, 1000, 8192, 4, True)
+    rng = random.Random(seed ^ 0xA11C)
+    rng2 = random.Random(seed ^ 0x5EED)
+    base_count = len(tensors)
+    for i in range(A - base_count):
+        tensors.append(_Tensor(f"small{i}", 512 * rng.randrange(1, 65), role="workspace"))
+    small = tensors[base_count:]
+    al = _place(tensors, va_lo, 2 * MiB)
+    assert al.next <= va_lo + window
+    b = _Builder(seed)
+    gaps = list(al.holes)
+    _dl_kernels(b, tensors[:base_count], 3000, rng2, gap_regions=gaps[:64], oow_base=va_lo + window + 2 * MiB)
+    per = 24
+    w_base = sum(int(w) for parts in b.kernels for w, _ in parts)
+    w_small = sum(small[i % len(small)].size // 8 for i in range(len(b.kernels) * per))
+    rep = max(1, -(-3 * w_base // (7 * w_small)))  # small tensors get ~30 % of the records
+    for k, parts in enumerate(b.kernels):
+        for q in range(per):
+            t = small[(k * per + q) % len(small)]
+            parts.append((rep * (t.size // 8), b.sweep(t.base, t.size, 8)))
+    ko, st, cdf = b.finish(n)
+    allocs = [(t.base, t.size) for t in tensors]
+    return Plan("s_manyranges", seed, n, va_lo, va_lo + window, 12, allocs, ko, st, cdf, topk=[16, 1024],
+                want_kernel_rows=True, want_kernel_pages=False,
+                note=f"rn50 kernels + {A - base_count} small tensors (A = {A})", objects=list(al.chunks))
+
+
 CONFIGS = {
     "tiny": plan_tiny,
     "rn50": plan_rn50,
     "gpt2m": plan_gpt2m,
     "uvm": plan_uvm,
     "llama": plan_llama,
+    "s_perm": plan_s_perm,
+    "s_hot": plan_s_hot,
+    "s_manyranges": plan_s_manyranges,
 }
+STRESS = ("s_perm", "s_hot", "s_manyranges")
 
 
 def build_plan(name: str, seed: int = 42, n: int | None = None) -> Plan:
