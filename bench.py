@@ -46,7 +46,8 @@ def parse():
                     help="BASELINE config (default: llama, the headline) or a SURVEY section 8d stress row")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=None, help="override the record count (testing only)")
+    ap.add_argument("--records", "--n", dest="n", type=int, default=None,
+                    help="override the record count (testing only)")
     ap.add_argument("--e2e-records", type=int, default=1 << 31, help="cap of the pinned host trace for e2e")
     ap.add_argument("--cpu-sample", type=int, default=1 << 28,
                     help="records in the single-thread oracle's bounded sample")
@@ -373,6 +374,20 @@ def run_ours(args):
     # ---- correctness guard (cheap invariants on the merged result) ----
     tot = hist.totals.cpu().numpy().view(np.uint64)
     assert int(tot[0]) == plan.n, (int(tot[0]), plan.n)
+    dump = os.environ.get("PASTA_BENCH_DUMP")
+    if dump:  # test hook: every merged output of one more step, per rank (tests/test_bench_contract.py)
+        step()
+        if merger is not None:
+            tops = {k: tuple(t.cpu().numpy().view(np.uint64).copy() for t in merger.out[k]) for k in plan.topk}
+            shard, S = merger.shard.cpu().numpy().view(np.uint64).copy(), merger.S
+        else:
+            tops = {k: tuple(t.cpu().numpy().view(np.uint64).copy() for t in tr.topk(hist.page_counts, k))
+                    for k in plan.topk}
+            shard, S = hist.page_counts.cpu().numpy().view(np.uint64).copy(), P
+        torch.cuda.synchronize()
+        np.savez(f"{dump}.rank{rank}.npz", shard=shard, S=S, small=hist.small.cpu().numpy().view(np.uint64),
+                 bitmap=hist.page_bitmap.cpu().numpy().view(np.uint64),
+                 **{f"top{k}_{i}": v for k, t in tops.items() for i, v in enumerate(t)})
 
     gb_scan = 8.0 * n_loc / 1e9
     scan_ms = phases["scan"] / args.steps

@@ -339,6 +339,62 @@ int pasta_peer_reduce(pasta_trace* h, const uint64_t* const* src, uint32_t g, ui
  * invalid device, ECUDA if the pair has no peer access. */
 int pasta_enable_peer(pasta_trace* h, int peer_device);
 
+/* Merge over peer memory without host round trips.
+ *
+ * pasta_peer_reduce_small: the small result part [alloc_counts | totals | tensor counts]
+ * of g shards (src as in pasta_peer_reduce) in ONE launch: out[i] = sum_r src[r][lo + i]
+ * (u64, wrapping) for i < n, except the listed slots: PASTA_PEER_MAX -> max_r;
+ * PASTA_PEER_ARGMAX -> the (index, value) pair at i, i + 1 with the largest value, ties
+ * to the smallest index (as pasta_peer_reduce's ARGMAX; R24); PASTA_PEER_ZERO -> 0 (a slot
+ * another step recomputes, e.g. unique pages from the merged bitmap). slots: HOST array
+ * of n_slots <= 16 entries with index < n (an ARGMAX entry needs index + 1 < n). SUM over
+ * a partition is SPEC S:291-299, MAX for working sets R11. out must not overlap a source.
+ * EINVAL on bad arguments. */
+enum { PASTA_PEER_ZERO = 3u };
+typedef struct {
+  uint32_t index;  /* element index in [0, n) */
+  uint32_t op;     /* PASTA_PEER_MAX, PASTA_PEER_ARGMAX or PASTA_PEER_ZERO */
+} pasta_peer_slot;
+int pasta_peer_reduce_small(pasta_trace* h, const uint64_t* const* src, uint32_t g, uint64_t lo, uint64_t n,
+                            const pasta_peer_slot* slots, uint32_t n_slots, uint64_t* out);
+
+/* pasta_peer_gather: up to 120 copies in ONE launch on the handle's stream (the second
+ * merge phase: peers' bitmap words, unique-page counts and top-k candidates).
+ * table: HOST array of count entries; entry e reads n u64 words at src (device memory
+ * readable from this device: local, peer-enabled or IPC-mapped) and writes them to dst
+ * (op PASTA_COPY) or adds them to dst with device atomics (PASTA_COPY_ADD: several
+ * entries may add into one word). Entries with op COPY must not overlap each other or
+ * any source. EINVAL for count == 0 or > 120, a NULL pointer with n > 0, or a bad op. */
+enum { PASTA_COPY = 0u, PASTA_COPY_ADD = 1u };
+typedef struct {
+  const uint64_t* src;
+  uint64_t* dst;
+  uint64_t n;   /* u64 words */
+  uint32_t op;  /* PASTA_COPY or PASTA_COPY_ADD */
+  uint32_t pad;
+} pasta_peer_copy;
+int pasta_peer_gather(pasta_trace* h, const pasta_peer_copy* table, uint32_t count);
+
+/* CUDA IPC of device buffers between the ranks of one node, opened in the HANDLE's device
+ * context (cudaIpcMemLazyEnablePeerAccess: NVLink / NVSwitch loads once mapped).
+ * pasta_ipc_export: a handle for the device allocation holding ptr (any address inside a
+ * cudaMalloc'd block, e.g. a PyTorch caching-allocator tensor; the offset inside the
+ * block is recorded). pasta_ipc_open (another process): *out_ptr = the same address in
+ * this process, valid until pasta_ipc_close(out_ptr) or pasta_close; a block opened
+ * twice is mapped once (reference counted). The exporting process must keep the block
+ * alive while peers use it. Handles are plain bytes (send them over any channel).
+ * ECUDA if the driver refuses (e.g. opening a handle in the exporting process). */
+typedef struct {
+  unsigned char handle[64];  /* cudaIpcMemHandle_t */
+  uint64_t offset;           /* ptr - block base */
+  uint64_t block_bytes;      /* size of the block */
+  int32_t device;            /* CUDA ordinal of the exporting process's device */
+  int32_t pad;
+} pasta_ipc_handle;
+int pasta_ipc_export(pasta_trace* h, const void* ptr, pasta_ipc_handle* out);
+int pasta_ipc_open(pasta_trace* h, const pasta_ipc_handle* in, void** out_ptr);
+int pasta_ipc_close(pasta_trace* h, void* ptr);
+
 /* Multi-GPU top-K merge: g shard-local top-k lists, rank-major
  * (cand_page[r*k + i], cand_count[r*k + i], device pointers; pages relative to shard r,
  * empty slots have count 0), shard r covering global pages [r*shard_pages,

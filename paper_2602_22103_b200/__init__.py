@@ -69,6 +69,20 @@ class pasta_batch(ctypes.Structure):
     _fields_ = [("trace", pasta_records), ("n", ctypes.c_uint64), ("out", pasta_histograms)]
 
 
+class pasta_peer_slot(ctypes.Structure):
+    _fields_ = [("index", ctypes.c_uint32), ("op", ctypes.c_uint32)]
+
+
+class pasta_peer_copy(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p), ("dst", ctypes.c_void_p), ("n", ctypes.c_uint64), ("op", ctypes.c_uint32),
+                ("pad", ctypes.c_uint32)]
+
+
+class pasta_ipc_handle(ctypes.Structure):
+    _fields_ = [("handle", ctypes.c_ubyte * 64), ("offset", ctypes.c_uint64), ("block_bytes", ctypes.c_uint64),
+                ("device", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
 class pasta_rich_records(ctypes.Structure):
     _fields_ = [("records", ctypes.c_void_p), ("grid_lo", ctypes.c_uint32), ("grid_hi", ctypes.c_uint32)]
 
@@ -97,6 +111,12 @@ _SIGS = {
     "pasta_topk_merge": (_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp]),
     "pasta_peer_reduce": (_int, [_vp, ctypes.POINTER(_vp), _u32, _u64, _u64, _u32, _vp, _vp, _vp]),
     "pasta_enable_peer": (_int, [_vp, _int]),
+    "pasta_peer_reduce_small": (_int, [_vp, ctypes.POINTER(_vp), _u32, _u64, _u64, ctypes.POINTER(pasta_peer_slot),
+                                       _u32, _vp]),
+    "pasta_peer_gather": (_int, [_vp, ctypes.POINTER(pasta_peer_copy), _u32]),
+    "pasta_ipc_export": (_int, [_vp, _vp, ctypes.POINTER(pasta_ipc_handle)]),
+    "pasta_ipc_open": (_int, [_vp, ctypes.POINTER(pasta_ipc_handle), ctypes.POINTER(_vp)]),
+    "pasta_ipc_close": (_int, [_vp, _vp]),
     "pasta_sync": (_int, [_vp]),
     "pasta_close": (_int, [_vp]),
     "pasta_strerror": (ctypes.c_char_p, [_int]),
@@ -230,6 +250,43 @@ def pasta_peer_reduce(h, srcs, lo: int, n: int, out, out_bitmap=None, out_popcou
 
 def pasta_enable_peer(h, peer_device: int):
     _check(_lib.pasta_enable_peer(h, peer_device), "pasta_enable_peer")
+
+
+PASTA_PEER_ZERO = 3
+PASTA_COPY, PASTA_COPY_ADD = 0, 1
+
+
+def pasta_peer_reduce_small(h, srcs, lo: int, n: int, slots, out):
+    """slots: [(index, op)] with op PASTA_PEER_MAX / PASTA_PEER_ARGMAX / PASTA_PEER_ZERO."""
+    arr = (_vp * len(srcs))(*[_ptr(s) for s in srcs])
+    sl = (pasta_peer_slot * max(1, len(slots)))(*[pasta_peer_slot(i, op) for i, op in slots])
+    _check(_lib.pasta_peer_reduce_small(h, arr, len(srcs), lo, n, sl, len(slots), _ptr(out)),
+           "pasta_peer_reduce_small")
+
+
+def pasta_peer_gather(h, copies):
+    """copies: [(src, dst, n_words, op)] (device addresses or tensors), one launch."""
+    tab = (pasta_peer_copy * len(copies))(*[pasta_peer_copy(_ptr(a), _ptr(b), n, op, 0) for a, b, n, op in copies])
+    _check(_lib.pasta_peer_gather(h, tab, len(copies)), "pasta_peer_gather")
+
+
+def pasta_ipc_export(h, ptr) -> bytes:
+    """The IPC handle of the device block holding ptr, as plain bytes (for any channel)."""
+    out = pasta_ipc_handle()
+    _check(_lib.pasta_ipc_export(h, _ptr(ptr), ctypes.byref(out)), "pasta_ipc_export")
+    return bytes(out)
+
+
+def pasta_ipc_open(h, handle: bytes) -> int:
+    """Map another process's exported block in h's device context; returns the address."""
+    hd = pasta_ipc_handle.from_buffer_copy(handle)
+    out = _vp()
+    _check(_lib.pasta_ipc_open(h, ctypes.byref(hd), ctypes.byref(out)), "pasta_ipc_open")
+    return int(out.value)
+
+
+def pasta_ipc_close(h, ptr: int):
+    _check(_lib.pasta_ipc_close(h, ptr), "pasta_ipc_close")
 
 
 def pasta_sync(h):
@@ -430,6 +487,21 @@ class Trace:
 
     def enable_peer(self, peer_device: int):
         pasta_enable_peer(self.h, peer_device)
+
+    def peer_reduce_small(self, srcs, lo: int, n: int, slots, out):
+        pasta_peer_reduce_small(self.h, srcs, lo, n, slots, out)
+
+    def peer_gather(self, copies):
+        pasta_peer_gather(self.h, copies)
+
+    def ipc_export(self, t) -> bytes:
+        return pasta_ipc_export(self.h, t)
+
+    def ipc_open(self, handle: bytes) -> int:
+        return pasta_ipc_open(self.h, handle)
+
+    def ipc_close(self, ptr: int):
+        pasta_ipc_close(self.h, ptr)
 
     def sync(self):
         pasta_sync(self.h)

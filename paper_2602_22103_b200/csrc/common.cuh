@@ -95,6 +95,22 @@ __device__ __forceinline__ uint64_t lds64(uint32_t a) {
   return v;
 }
 
+__device__ __forceinline__ void sts64(uint32_t a, uint64_t v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t atoms_cas_u64(uint32_t a, uint64_t cmp, uint64_t v) {
+  uint64_t old;
+  asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "r"(a), "l"(cmp), "l"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ uint64_t atoms_exch_u64(uint32_t a, uint64_t v) {
+  uint64_t old;
+  asm volatile("atom.shared.exch.b64 %0, [%1], %2;" : "=l"(old) : "r"(a), "l"(v) : "memory");
+  return old;
+}
+
 // Order this thread's prior generic-proxy shared-memory accesses before later
 // async-proxy (TMA) writes to the same buffer.
 __device__ __forceinline__ void fence_proxy_async_smem() {

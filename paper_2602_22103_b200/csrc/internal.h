@@ -45,6 +45,31 @@ struct ScanArgs {
   uint32_t early;            // 1 PASTA_REC_STABLE: first loads before the grid-dependency wait; 2 CHAINED: wait at the end
 };
 
+// Streaming ring consumer (NEXT f2): one persistent launch consumes
+// batch descriptors that the host publishes into a device ring while it runs.
+struct StreamDesc {          // one batch (32 B, a device ring slot)
+  const uint64_t* rec;       // [n] records, 16-byte aligned, n even
+  uint64_t n;                // <= the stream's max batch
+  const uint64_t* koffs;     // [nk + 1] batch-relative kernel offsets (device) or nullptr (one kernel)
+  uint32_t nk;               // kernels in the batch (>= 1)
+  uint32_t k0;               // kernel row of the batch's first kernel
+};
+constexpr int kStreamMaxCtas = 256;
+struct StreamCtl {           // device
+  unsigned long long tail;   // batches published (stream-ordered host copies)
+  unsigned long long end;    // total batches once closed, else ~0
+};
+struct StreamArgs {
+  ScanArgs s;                   // table, window, outputs (rec / nbody / koffs unused)
+  const StreamDesc* ring;       // [slots]
+  uint32_t slots;
+  StreamCtl* ctl;
+  uint64_t spb;                 // slices (256 records) per batch slot
+  unsigned* arrivals;           // [slots] CTAs done with the batch in that ring slot (zeroed)
+  unsigned long long* consumed; // host-mapped: batches every CTA has read (flow control)
+};
+cudaError_t launch_stream_consumer(const StreamArgs& a, cudaStream_t st, int* ctas);
+
 // Rich 16-byte records (NEXT f4; R21-R24).
 struct RichArgs {
   const uint64_t* rec;       // [2n] u64 words: record i = (rec[2i], rec[2i+1]), 16-byte aligned
@@ -129,15 +154,38 @@ struct PeerSrc {
 cudaError_t launch_peer_reduce(const PeerSrc& src, uint32_t g, uint64_t lo, uint64_t n, uint32_t op, uint64_t* out,
                                uint64_t* out_bitmap, uint64_t* out_popcount, int grid, cudaStream_t st);
 
-// Top-K scratch (device): run_topk needs topk_scratch_bytes(k, P), run_topk_merge
-// topk_merge_scratch_bytes(g * k, grid).
-size_t topk_scratch_bytes(uint64_t k, uint64_t P);
+// pasta_peer_reduce_small: slot exceptions of the SUM (op 1 MAX, 2 ARGMAX pair, 3 ZERO).
+struct PeerSlots {
+  uint32_t idx[16];
+  uint32_t op[16];
+  uint32_t n;
+};
+cudaError_t launch_peer_small(const PeerSrc& src, uint32_t g, uint64_t lo, uint64_t n, const PeerSlots& sl,
+                              uint64_t* out, int grid, cudaStream_t st);
+// pasta_peer_gather: copies (op 0) / atomic adds (op 1) of n u64 words, one launch.
+constexpr uint32_t kMaxCopies = 120;
+struct PeerCopy {
+  const uint64_t* src;
+  uint64_t* dst;
+  uint64_t n;
+  uint32_t op;
+  uint32_t pad;
+};
+struct PeerCopyTable {
+  PeerCopy e[kMaxCopies];
+  uint32_t count;
+};
+cudaError_t launch_peer_gather(const PeerCopyTable& t, int grid, cudaStream_t st);
+
+// Top-K scratch (device): run_topk needs topk_scratch_bytes(k, P, max_ctas) (max_ctas =
+// its CTA limit), run_topk_merge topk_merge_scratch_bytes(g * k, grid).
+size_t topk_scratch_bytes(uint64_t k, uint64_t P, int max_ctas);
 size_t topk_merge_scratch_bytes(uint64_t n, int grid);
 // Enqueues the whole radix-select + gather + sort pipeline; `launch` is called once
 // per kernel launch with the phase's cudaError_t (for counting / timing hooks).
 typedef void (*launch_hook)(void* ctx, int begin);
 cudaError_t run_topk(const uint64_t* page_counts, uint64_t P, uint32_t k, uint64_t* out_page, uint64_t* out_count,
-                     uint64_t* out_found, void* scratch, int grid, cudaStream_t st, int* n_launches);
+                     uint64_t* out_found, void* scratch, int max_ctas, cudaStream_t st, int* n_launches);
 
 cudaError_t run_topk_merge(const uint64_t* cand_page, const uint64_t* cand_count, uint32_t g, uint32_t k,
                            uint64_t shard_pages, uint64_t* out_page, uint64_t* out_count, uint64_t* out_found,

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <map>
 #include <new>
+#include <string>
 #include <vector>
 
 #include "internal.h"
@@ -67,6 +68,11 @@ struct pasta_trace {
   // top-K scratch
   void* d_topk = nullptr;
   size_t topk_bytes = 0;
+
+  // CUDA IPC blocks opened in this handle's context: handle bytes -> (base, refs); and
+  // every pointer handed out -> its block's handle bytes
+  std::map<std::string, std::pair<void*, int>> ipc_blocks;
+  std::map<void*, std::pair<std::string, int>> ipc_ptrs;  // pointer -> (block key, opens)
 
   // scan scratch (interleaved schedule: chunk -> kernel map)
   unsigned char* d_scan = nullptr;
@@ -699,8 +705,8 @@ int pasta_topk(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t
                uint64_t* out_count, uint64_t* out_found) {
   if (!h || !page_counts || !out_page || !out_count || !out_found || k == 0 || P == 0) return PASTA_EINVAL;
   DeviceGuard g(h->device);
-  const int grid = h->sm_count * 4;
-  const size_t need = topk_scratch_bytes(k, P);
+  const int max_ctas = h->sm_count * 2;  // the cooperative top-K kernel: <= 2 CTAs per SM
+  const size_t need = topk_scratch_bytes(k, P, max_ctas);
   if (need > h->topk_bytes) {
     if (h->d_topk) {
       cudaStreamSynchronize(h->stream);
@@ -713,7 +719,7 @@ int pasta_topk(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t
   }
   int nl = 0;
   Timed t(h, PASTA_PH_TOPK, h->stream);
-  cudaError_t e = run_topk(page_counts, P, k, out_page, out_count, out_found, h->d_topk, grid, h->stream, &nl);
+  cudaError_t e = run_topk(page_counts, P, k, out_page, out_count, out_found, h->d_topk, max_ctas, h->stream, &nl);
   h->launches += (uint64_t)nl;
   return cuda_status(e);
 }
@@ -770,6 +776,134 @@ int pasta_peer_reduce(pasta_trace* h, const uint64_t* const* src, uint32_t g, ui
   cudaError_t e = launch_peer_reduce(s, g, lo, n, op, out, out_bitmap, out_popcount, h->sm_count * 8, h->stream);
   ++h->launches;
   return cuda_status(e);
+}
+
+int pasta_peer_reduce_small(pasta_trace* h, const uint64_t* const* src, uint32_t g, uint64_t lo, uint64_t n,
+                            const pasta_peer_slot* slots, uint32_t n_slots, uint64_t* out) {
+  if (!h || !src || !out || g == 0 || g > (uint32_t)kMaxPeers || n == 0 || n_slots > 16) return PASTA_EINVAL;
+  if (n_slots && !slots) return PASTA_EINVAL;
+  PeerSrc s{};
+  for (uint32_t r = 0; r < g; ++r) {
+    if (!src[r]) return PASTA_EINVAL;
+    s.p[r] = src[r];
+  }
+  PeerSlots sl{};
+  sl.n = n_slots;
+  for (uint32_t i = 0; i < n_slots; ++i) {
+    const uint32_t op = slots[i].op;
+    if (op != PASTA_PEER_MAX && op != PASTA_PEER_ARGMAX && op != PASTA_PEER_ZERO) return PASTA_EINVAL;
+    if ((uint64_t)slots[i].index >= n || (op == PASTA_PEER_ARGMAX && (uint64_t)slots[i].index + 1 >= n))
+      return PASTA_EINVAL;
+    sl.idx[i] = slots[i].index;
+    sl.op[i] = op;
+  }
+  DeviceGuard dg(h->device);
+  Timed t(h, PASTA_PH_MERGE, h->stream);
+  cudaError_t e = launch_peer_small(s, g, lo, n, sl, out, h->sm_count * 4, h->stream);
+  ++h->launches;
+  return cuda_status(e);
+}
+
+int pasta_peer_gather(pasta_trace* h, const pasta_peer_copy* table, uint32_t count) {
+  if (!h || !table || count == 0 || count > kMaxCopies) return PASTA_EINVAL;
+  PeerCopyTable t{};
+  t.count = count;
+  for (uint32_t j = 0; j < count; ++j) {
+    const pasta_peer_copy& c = table[j];
+    if (c.op != PASTA_COPY && c.op != PASTA_COPY_ADD) return PASTA_EINVAL;
+    if (c.n && (!c.src || !c.dst)) return PASTA_EINVAL;
+    t.e[j].src = c.src;
+    t.e[j].dst = c.dst;
+    t.e[j].n = c.n;
+    t.e[j].op = c.op;
+  }
+  DeviceGuard dg(h->device);
+  Timed tm(h, PASTA_PH_MERGE, h->stream);
+  cudaError_t e = launch_peer_gather(t, h->sm_count * 4, h->stream);
+  ++h->launches;
+  return cuda_status(e);
+}
+
+namespace {
+// cuMemGetAddressRange through the runtime's driver entry point (no -lcuda link).
+typedef int (*MemGetAddressRangeFn)(unsigned long long* base, size_t* size, unsigned long long ptr);
+MemGetAddressRangeFn mem_range_fn() {
+  static MemGetAddressRangeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<MemGetAddressRangeFn>(p);
+  }
+  return fn;
+}
+}  // namespace
+
+int pasta_ipc_export(pasta_trace* h, const void* ptr, pasta_ipc_handle* out) {
+  if (!h || !ptr || !out) return PASTA_EINVAL;
+  DeviceGuard dg(h->device);
+  MemGetAddressRangeFn range = mem_range_fn();
+  if (!range) return PASTA_ECUDA;
+  unsigned long long base = 0;
+  size_t bytes = 0;
+  if (range(&base, &bytes, (unsigned long long)(uintptr_t)ptr) != 0) return PASTA_EINVAL;  // not device memory
+  cudaIpcMemHandle_t hnd;
+  cudaError_t e = cudaIpcGetMemHandle(&hnd, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return PASTA_ECUDA;
+  }
+  std::memset(out, 0, sizeof(*out));
+  static_assert(sizeof(hnd) <= sizeof(out->handle), "IPC handle size");
+  std::memcpy(out->handle, &hnd, sizeof(hnd));
+  out->offset = (uint64_t)((uintptr_t)ptr - (uintptr_t)base);
+  out->block_bytes = (uint64_t)bytes;
+  out->device = h->device;
+  return PASTA_OK;
+}
+
+int pasta_ipc_open(pasta_trace* h, const pasta_ipc_handle* in, void** out_ptr) {
+  if (!h || !in || !out_ptr || in->offset >= in->block_bytes) return PASTA_EINVAL;
+  DeviceGuard dg(h->device);
+  const std::string key(reinterpret_cast<const char*>(in->handle), sizeof(cudaIpcMemHandle_t));
+  auto it = h->ipc_blocks.find(key);
+  void* base = nullptr;
+  if (it != h->ipc_blocks.end()) {
+    base = it->second.first;
+    ++it->second.second;
+  } else {
+    cudaIpcMemHandle_t hnd;
+    std::memcpy(&hnd, in->handle, sizeof(hnd));
+    cudaError_t e = cudaIpcOpenMemHandle(&base, hnd, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return PASTA_ECUDA;
+    }
+    h->ipc_blocks[key] = {base, 1};
+  }
+  void* p = static_cast<char*>(base) + in->offset;
+  *out_ptr = p;
+  auto& e = h->ipc_ptrs[p];
+  e.first = key;
+  ++e.second;
+  return PASTA_OK;
+}
+
+int pasta_ipc_close(pasta_trace* h, void* ptr) {
+  if (!h || !ptr) return PASTA_EINVAL;
+  auto it = h->ipc_ptrs.find(ptr);
+  if (it == h->ipc_ptrs.end()) return PASTA_ENOENT;
+  const std::string key = it->second.first;
+  if (--it->second.second <= 0) h->ipc_ptrs.erase(it);
+  auto b = h->ipc_blocks.find(key);
+  if (b != h->ipc_blocks.end() && --b->second.second <= 0) {
+    DeviceGuard dg(h->device);
+    cudaStreamSynchronize(h->stream);  // no enqueued kernel may still read the block
+    cudaIpcCloseMemHandle(b->second.first);
+    h->ipc_blocks.erase(b);
+  }
+  return PASTA_OK;
 }
 
 int pasta_enable_peer(pasta_trace* h, int peer_device) {
@@ -873,6 +1007,9 @@ int pasta_close(pasta_trace* h) {
     if (h->ev_copied[i]) cudaEventDestroy(h->ev_copied[i]);
     if (h->ev_consumed[i]) cudaEventDestroy(h->ev_consumed[i]);
   }
+  for (auto& b : h->ipc_blocks) cudaIpcCloseMemHandle(b.second.first);
+  h->ipc_blocks.clear();
+  h->ipc_ptrs.clear();
   if (h->d_koffs) cudaFree(h->d_koffs);
   if (h->d_topk) cudaFree(h->d_topk);
   if (h->d_scan) cudaFree(h->d_scan);

@@ -106,12 +106,85 @@ __global__ void peer_argmax_kernel(PeerSrc src, uint32_t g, uint64_t lo, uint64_
   out[1] = bv;
 }
 
+// Small part of g shards in one pass: SUM except the listed slots (MAX, ARGMAX pair, ZERO).
+__global__ void __launch_bounds__(kBlock) peer_small_kernel(PeerSrc src, uint32_t g, uint64_t lo, uint64_t n,
+                                                            PeerSlots sl, uint64_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kBlock) {
+    uint32_t op = 0, half = 0;  // 0 SUM, 1 MAX, 2 ARGMAX (half: 0 index, 1 value), 3 ZERO
+    for (uint32_t s = 0; s < sl.n; ++s) {
+      if (sl.idx[s] == i) op = sl.op[s];
+      if (sl.op[s] == 2u && (uint64_t)sl.idx[s] + 1 == i) {
+        op = 2;
+        half = 1;
+      }
+    }
+    uint64_t acc = 0;
+    if (op == 2u) {
+      const uint64_t at = lo + i - half;
+      uint64_t bi = 0, bv = 0;
+      bool any = false;
+#pragma unroll
+      for (int r = 0; r < kMaxPeers; ++r) {
+        if (r < (int)g) {
+          const uint64_t x = ld_stream_u64(src.p[r] + at), v = ld_stream_u64(src.p[r] + at + 1);
+          if (!any || v > bv || (v == bv && x < bi)) {
+            bi = x;
+            bv = v;
+            any = true;
+          }
+        }
+      }
+      acc = half ? bv : bi;
+    } else if (op != 3u) {
+#pragma unroll
+      for (int r = 0; r < kMaxPeers; ++r) {
+        if (r < (int)g) {
+          const uint64_t v = ld_stream_u64(src.p[r] + lo + i);
+          acc = op == 1u ? (v > acc ? v : acc) : acc + v;
+        }
+      }
+    }
+    out[i] = acc;
+  }
+}
+
+// Up to kMaxCopies copies / atomic adds in one launch (grid-stride inside every entry).
+__global__ void __launch_bounds__(kBlock) peer_gather_kernel(const __grid_constant__ PeerCopyTable t) {
+  const uint64_t tid = (uint64_t)blockIdx.x * kBlock + threadIdx.x, nt = (uint64_t)gridDim.x * kBlock;
+  for (uint32_t j = 0; j < t.count; ++j) {
+    const uint64_t* __restrict__ src = t.e[j].src;
+    uint64_t* __restrict__ dst = t.e[j].dst;
+    const uint64_t n = t.e[j].n;
+    if (t.e[j].op == 0u) {
+      for (uint64_t i = tid; i < n; i += nt) dst[i] = ld_stream_u64(src + i);
+    } else {
+      for (uint64_t i = tid; i < n; i += nt) {
+        const uint64_t v = ld_stream_u64(src + i);
+        if (v) red_add_u64(dst + i, v);
+      }
+    }
+  }
+}
+
 int grid_for(uint64_t items, int per_block, int cap) {
   const uint64_t b = (items + per_block - 1) / per_block;
   return (int)(b < 1 ? 1 : (b > (uint64_t)cap ? cap : b));
 }
 
 }  // namespace
+
+cudaError_t launch_peer_small(const PeerSrc& src, uint32_t g, uint64_t lo, uint64_t n, const PeerSlots& sl,
+                              uint64_t* out, int grid, cudaStream_t st) {
+  peer_small_kernel<<<grid_for(n, kBlock, grid), kBlock, 0, st>>>(src, g, lo, n, sl, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_gather(const PeerCopyTable& t, int grid, cudaStream_t st) {
+  uint64_t most = 1;
+  for (uint32_t j = 0; j < t.count; ++j) most = t.e[j].n > most ? t.e[j].n : most;
+  peer_gather_kernel<<<grid_for(most, kBlock, grid), kBlock, 0, st>>>(t);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_peer_reduce(const PeerSrc& src, uint32_t g, uint64_t lo, uint64_t n, uint32_t op, uint64_t* out,
                                uint64_t* out_bitmap, uint64_t* out_popcount, int grid, cudaStream_t st) {

@@ -89,6 +89,9 @@ constexpr int kSlice = 256;                 // records per slice (8 per lane)
 #ifndef PASTA_TIER_S
 #define PASTA_TIER_S 1  // tier S (one owner, scattered pages) before tier L
 #endif
+#ifndef PASTA_TIER_S_BATCH
+#define PASTA_TIER_S_BATCH 1  // tier S (kPages == 0): page REDs issued back to back
+#endif
 #ifndef PASTA_IL
 #define PASTA_IL 1  // interleaved chunk schedule for long launches (0 = always contiguous)
 #endif
@@ -221,7 +224,63 @@ struct Out {
   uint64_t* tcounts;
   uint64_t* ktc;
   uint64_t max_tids;
+  uint32_t cache;   // 1: the page-count cache (2^kCacheBits slots at dynamic smem offset 0) is on
 };
+
+// Shared-memory page-count cache (modes without per-kernel page bits / hotness, whose
+// page counts do not depend on the kernel): scattered page increments of the per-lane
+// tiers go to a CTA-wide open-addressing table of (page << 32 | count) u64 slots instead
+// of one L2 RED each. Insert = 64-bit shared CAS on one of 4 probe slots (count added to
+// the page's slot, or an empty slot claimed); when all 4 hold other pages, the first is
+// evicted with one exchange and its count written back with one RED (a write-back cache:
+// a (page, count) pair is only ever in the table or already added to L2, never both, and
+// the exchange takes it out atomically). The CTA writes the table back at its end.
+// Off by default: measured slower on every config (A/B: s_perm 12.3 ->
+// 30.8 ms, llama 13.4 -> 25.6 ms with 2^12 slots): shared 64-bit CAS retries when lanes
+// hit one slot and evictions when a tensor spans more pages than the table cost more
+// than the one L2 RED per scattered page run they replace.
+#ifndef PASTA_PCACHE_BITS
+#define PASTA_PCACHE_BITS 0
+#endif
+#ifndef PASTA_PCACHE_F
+#define PASTA_PCACHE_F 0  // tier-F records through the cache (on: +spills in the interleaved row variants)
+#endif
+#ifndef PASTA_PCACHE_L
+#define PASTA_PCACHE_L 1  // tier-L lane entries through the cache
+#endif
+constexpr int kCacheBits = PASTA_PCACHE_BITS;  // 0: no cache
+constexpr uint32_t kCacheSlots = kCacheBits ? (1u << kCacheBits) : 0u;
+constexpr int kCacheBytes = 8 * (int)kCacheSlots;
+constexpr uint32_t kCacheEmpty = 0xFFFFFFFFu;  // key of an empty slot (== kOOW, never cached)
+constexpr uint64_t kCacheEmptySlot = (uint64_t)kCacheEmpty << 32;
+
+__device__ __forceinline__ uint32_t cache_base() {
+  extern __shared__ __align__(128) unsigned char smem[];
+  return smem_u32(smem);
+}
+
+__device__ __forceinline__ void cache_add(const Out& o, uint32_t page, uint32_t v) {
+  const uint32_t h = (page * 0x9E3779B1u) >> (kCacheBits ? 32 - kCacheBits : 0);
+  const uint32_t base = cache_base();
+#pragma unroll 1
+  for (uint32_t i = 0; i < 4; ++i) {
+    const uint32_t addr = base + 8u * ((h + i) & (kCacheSlots - 1u));
+    uint64_t cur = lds64(addr);
+    for (;;) {
+      const uint32_t key = (uint32_t)(cur >> 32), cnt = (uint32_t)cur;
+      uint64_t nv;
+      if (key == page && cnt < (1u << 31)) nv = cur + v;
+      else if (key == kCacheEmpty) nv = ((uint64_t)page << 32) | v;
+      else break;
+      const uint64_t old = atoms_cas_u64(addr, cur, nv);
+      if (old == cur) return;
+      cur = old;
+    }
+  }
+  const uint64_t old = atoms_exch_u64(base + 8u * (h & (kCacheSlots - 1u)), ((uint64_t)page << 32) | v);
+  if ((uint32_t)(old >> 32) != kCacheEmpty && (uint32_t)old != 0u)
+    red_add_u64(o.page_counts + (uint32_t)(old >> 32), (uint32_t)old);
+}
 
 // Time-windowed hotness: the page run's count also goes to row k / wk.
 // Compiled in only for the hotness variants: kPages is a mode, bit 0 = per-kernel page
@@ -274,6 +333,16 @@ __device__ __forceinline__ void page_to_global(const Out& o, uint32_t page, uint
     if (kPages & 1) red_or_u64(o.kpb + (uint64_t)k * o.words + (page >> 6), 1ull << (page & 63));
     hot_add<kPages>(o, page, v, k);
   }
+}
+
+// A page count from a per-lane tier: through the shared cache when the launch has one.
+template <int kPages>
+__device__ __forceinline__ void page_scatter(const Out& o, uint32_t page, uint64_t v, uint32_t k) {
+  if (kPages == 0 && kCacheBits && o.cache != 0u && page != kOOW && v != 0 && v < (1ull << 31)) {
+    cache_add(o, page, (uint32_t)v);
+    return;
+  }
+  page_to_global<kPages>(o, page, v, k);
 }
 
 // Warp-uniform accumulators (every lane holds the same values).
@@ -353,6 +422,8 @@ __device__ __forceinline__ void fallback_record(uint64_t x, OwnCache& oc, LaneAc
   const Ival I = lookup<kBig>(oc, x, c);
   if (I.page == kOOW) {
     red_add_u64(o.totals + 2, 1);
+  } else if (kPages == 0 && kCacheBits && PASTA_PCACHE_F && o.cache != 0u) {
+    cache_add(o, I.page, 1);
   } else {
     red_add_u64(o.page_counts + I.page, 1);
     hot_add<kPages>(o, I.page, 1, k);
@@ -374,7 +445,11 @@ __device__ __forceinline__ void fallback_record(uint64_t x, OwnCache& oc, LaneAc
 template <bool kRows, int kPages>
 __device__ __forceinline__ void lane_entry(LaneAcc& la, const Out& o, uint32_t page, uint32_t own, uint32_t cnt,
                                            uint32_t k) {
+#if PASTA_PCACHE_L
+  page_scatter<kPages>(o, page, cnt, k);
+#else
   page_to_global<kPages>(o, page, cnt, k);
+#endif
   if (own != la.own) {
     owner_to_global<kRows>(o, la.own, la.ocnt, k);
     la.own = own;
@@ -582,18 +657,37 @@ __device__ __forceinline__ void process_full(const uint64_t (&a)[8], uint32_t sl
         w.ocnt = 0;
       }
       w.ocnt += kSlice;
+#if PASTA_TIER_S_BATCH
+      if (kPages == 0 && !(kCacheBits && o.cache)) {
+        // every page and run end first, then the REDs back to back: each RED has its own
+        // address / value registers, so no RED waits for the previous one's operands to
+        // drain (the loop below stalled on that write-after-read at every RED)
+        uint32_t q[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q[i] = (uint32_t)((a[i] - c.va_lo) >> c.s);
+        uint32_t start = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i == 7 || q[i + 1 < 8 ? i + 1 : 7] != q[i]) {
+            red_add_u64(o.page_counts + q[i], (uint64_t)(i + 1 - start));
+            start = i + 1;
+          }
+        }
+        return;
+      }
+#endif
       uint32_t pp = (uint32_t)((a[0] - c.va_lo) >> c.s), n = 1;
 #pragma unroll
       for (int i = 1; i < 8; ++i) {
         const uint32_t p = (uint32_t)((a[i] - c.va_lo) >> c.s);
         if (p != pp) {
-          page_to_global<kPages>(o, pp, n, k);
+          page_scatter<kPages>(o, pp, n, k);
           pp = p;
           n = 0;
         }
         ++n;
       }
-      page_to_global<kPages>(o, pp, n, k);
+      page_scatter<kPages>(o, pp, n, k);
       return;
     }
   }
@@ -649,7 +743,7 @@ __device__ __forceinline__ uint32_t kernel_of(const uint64_t* __restrict__ koffs
 }
 
 template <bool kBig, bool kRows, int kPages, bool kIL>
-__global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages) {
+__global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages, const int cache_on) {
   // Programmatic dependent launch: the next analyze call's scan may start its prologue
   // (barrier init, range table into shared memory) on free SMs while this one runs. A
   // chained scan (early == 2) triggers at entry: its predecessor is a scan that already
@@ -658,8 +752,11 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   // chain's first call has seen every earlier kernel (e.g. the outputs' zeroing) complete.
   if (args.early == 2) grid_dep_launch_dependents();
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages));
-  uint64_t* sB = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages) + kBarBytes + kLaBytes + kPfBytes);
+  // dynamic shared memory: [page-count cache (kPages == 0, cache_on) | ring | barriers |
+  // lane accumulators | chunk map slots | range table]
+  unsigned char* sm = smem + ((kPages == 0 && kCacheBits && cache_on) ? kCacheBytes : 0);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + ring_bytes(stages));
+  uint64_t* sB = reinterpret_cast<uint64_t*>(sm + ring_bytes(stages) + kBarBytes + kLaBytes + kPfBytes);
 
   const uint32_t A = args.A;
   const int warp = threadIdx.x >> 5;
@@ -698,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   };
   const uint32_t nfull = (tail_mine && nmy > 0 && tail_valid != (uint32_t)kSlice) ? nmy - 1 : nmy;
 
-  const uint32_t ring_u32 = smem_u32(smem) + (uint32_t)(warp * stages) * kSliceBytes;
+  const uint32_t ring_u32 = smem_u32(sm) + (uint32_t)(warp * stages) * kSliceBytes;
   const uint32_t bar_u32 = smem_u32(bars + warp * kMaxStages);
 
   if (lane == 0) {
@@ -708,6 +805,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   // the range table is only ever written by stream-ordered copies, never by a kernel
   if (!kBig)
     for (uint32_t i = threadIdx.x; i < 2 * A; i += kThreads) sB[i] = args.bounds[i];
+  const bool cache = kPages == 0 && kCacheBits && cache_on;
+  if (cache)
+    for (uint32_t i = threadIdx.x; i + 1 <= kCacheSlots; i += kThreads) sts64(cache_base() + 8u * i, kCacheEmptySlot);
   __syncthreads();
   // Everything the stream's previous kernel wrote (the records, a chunk map, zeroed or
   // partial outputs) is visible after grid_dep_wait; nothing before it touches that
@@ -763,6 +863,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   o.tcounts = args.tensor_counts;
   o.ktc = args.ktc;
   o.max_tids = args.max_tids;
+  o.cache = cache ? 1u : 0u;
 
   OwnCache oc;
   oc.olo = 1;
@@ -776,7 +877,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   w.ocnt = 0;
 #if PASTA_LA_SMEM
   // the rarely used tier-F accumulators live in shared memory (fewer live registers)
-  LaneAcc& la = reinterpret_cast<LaneAcc*>(smem + ring_bytes(stages) + kBarBytes)[threadIdx.x];
+  LaneAcc& la = reinterpret_cast<LaneAcc*>(sm + ring_bytes(stages) + kBarBytes)[threadIdx.x];
 #else
   LaneAcc la;
 #endif
@@ -791,7 +892,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   // interleaved: chunk starts are events, the chunk's (k, kend) comes from the pre-pass
   // table, copied to this warp's shared slot one chunk ahead (cp.async), off the critical
   // path and out of the register file
-  const uint32_t pf_u32 = smem_u32(smem) + ring_bytes(stages) + kBarBytes + kLaBytes + 16u * warp;
+  const uint32_t pf_u32 = smem_u32(sm) + ring_bytes(stages) + kBarBytes + kLaBytes + 16u * warp;
   auto prefetch_chunk = [&](uint32_t j) {
     if (kRows && K > 1 && j < nmy && lane == 0) cp_async_16(pf_u32, args.chunk_k + (gsl(j) >> lc));
   };
@@ -911,6 +1012,14 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
     }
   }
   warp_flush<kRows, kPages>(w, la, o, k, lane);
+  if (cache) {  // write the page-count cache back
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i + 1 <= kCacheSlots; i += kThreads) {
+      const uint64_t v = lds64(cache_base() + 8u * i);
+      if ((uint32_t)(v >> 32) != kCacheEmpty && (uint32_t)v != 0u)
+        red_add_u64(args.page_counts + (uint32_t)(v >> 32), (uint32_t)v);
+    }
+  }
   // PASTA_REC_CHAINED: the predecessor is a scan into the same outputs (its REDs commute
   // with ours), so the work above never waited for it; this grid still completes only
   // after it, which keeps completion in stream order for every later reader.
@@ -972,13 +1081,19 @@ __global__ void scan_extras_kernel(const ExtraArgs ea) {
   else page_to_global<0>(o, I.page, 1, k);
 }
 
-int stages_for(uint32_t A, bool big) {
+int stages_for(uint32_t A, bool big, long extra = 0) {
   const long table = big ? 0 : 16l * A;
-  const long avail = (long)kSmemLimit - kBarBytes - kLaBytes - kPfBytes - table;
+  const long avail = (long)kSmemLimit - kBarBytes - kLaBytes - kPfBytes - table - extra;
   long st = avail / ring_bytes(1);
   if (st > kMaxStages) st = kMaxStages;
   return (int)st;
 }
+
+// The page-count cache is on when it leaves at least PASTA_PCACHE_MIN_STAGES ring stages.
+#ifndef PASTA_PCACHE_MIN_STAGES
+#define PASTA_PCACHE_MIN_STAGES 3
+#endif
+bool cache_fits(uint32_t A, bool big) { return kCacheBits && stages_for(A, big, kCacheBytes) >= PASTA_PCACHE_MIN_STAGES; }
 
 // chunk_k[c] = (kernel segment k of interleaved chunk c's first record, koffs[k + 1]).
 __global__ void chunk_kernel_map(const __grid_constant__ ScanArgs a, ulonglong2* chunk_k, uint64_t nch) {
@@ -990,8 +1105,10 @@ __global__ void chunk_kernel_map(const __grid_constant__ ScanArgs a, ulonglong2*
 
 template <bool kBig, bool kRows, int kPages>
 cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
-  const int stages = stages_for(a.A, kBig);
-  const int smem = scan_smem_bytes(a.A, kBig);
+  const int cache_on = (kPages == 0 && cache_fits(a.A, kBig)) ? 1 : 0;
+  const int stages = stages_for(a.A, kBig, cache_on ? kCacheBytes : 0);
+  const int smem = ring_bytes(stages) + kBarBytes + kLaBytes + kPfBytes + (kBig ? 0 : (int)(16ull * a.A)) +
+                   (cache_on ? kCacheBytes : 0);
   auto fn = a.log_ic >= 0 ? scan_kernel<kBig, kRows, kPages, true> : scan_kernel<kBig, kRows, kPages, false>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -1007,7 +1124,288 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = PASTA_PDL;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fn, a, stages);
+  return cudaLaunchKernelEx(&cfg, fn, a, stages, cache_on);
+}
+
+// ------------------------------------------------------------------------------------
+// Streaming ring consumer (NEXT f2). The paper's operating point is a
+// device buffer ("4MB") that the instrumented program fills and the analysis
+// drains. One launch per buffer costs a launch each (1.4 us graph-replayed
+// for 0.64 us of HBM time); here ONE persistent cooperative launch consumes batch
+// descriptors that the host publishes into a device ring of `slots` descriptors while it
+// runs. The global slice sequence G = b * spb + s (batch b, slice s of spb slots per
+// batch) is dealt round-robin to the W warps (warp w takes G = w, w + W, ...), so every
+// batch is spread over the whole GPU and consecutive batches overlap; each warp keeps its
+// own TMA ring S slices ahead exactly like the scan, waiting (lane 0, nanosleep) only
+// when the batch it needs is not published yet. A slice is handled by the scan's own
+// tiers with the batch's kernel segment (row k0 + local kernel). Progress for the
+// producer: each warp exposes the lowest slice it has not read yet, warp 0 of each CTA
+// publishes the CTA's minimum (in whole batches) and CTA 0 the global minimum into
+// host-mapped memory, so the host reuses a ring slot (and the batch's records) only
+// after every warp has read that batch.
+// ------------------------------------------------------------------------------------
+constexpr int kSlotInfoBytes = 48;  // per warp and ring stage: the slice in flight
+constexpr int kFrontBytes = kWarps * 8;
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct SlotInfo {   // 48 B in shared memory
+  uint64_t G;       // global slice index
+  const uint64_t* koffs;
+  uint64_t n;       // records of the batch
+  uint32_t nk, k0;
+  uint32_t s, valid;
+  uint64_t pad;
+};
+
+// Lane 0 of warp 0: this CTA's progress to the producer. A batch is read when every
+// warp's lowest unread slice lies beyond it; each CTA adds one to the batch's arrival
+// counter when it is done with it, and the CTA that completes the count publishes
+// "batches < b + 1 are read" to the host (arrivals happen in batch order in every CTA,
+// so batches complete in order) and re-arms the counter for ring lap b + slots.
+__device__ __forceinline__ void stream_report(const StreamArgs& ra, const volatile uint64_t* front,
+                                              unsigned long long& cta_last) {
+  uint64_t mn = ~0ull;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) mn = front[w] < mn ? front[w] : mn;
+  unsigned long long done = mn == ~0ull ? ld_acquire_u64(&ra.ctl->end) : mn / ra.spb;
+  for (; cta_last < done; ++cta_last) {
+    unsigned* cnt = ra.arrivals + (cta_last % ra.slots);
+    if (atomicAdd(cnt, 1u) == gridDim.x - 1) {
+      *cnt = 0u;
+      __threadfence();
+      st_release_sys_u64(ra.consumed, cta_last + 1);
+    }
+  }
+}
+
+template <bool kBig, bool kRows, int kPages>
+__global__ void __launch_bounds__(kThreads, 1) stream_kernel(const __grid_constant__ StreamArgs ra, const int stages) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const ScanArgs& args = ra.s;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages));
+  unsigned char* info_base = smem + ring_bytes(stages) + kBarBytes + kLaBytes;
+  volatile uint64_t* front = reinterpret_cast<volatile uint64_t*>(info_base + kWarps * stages * kSlotInfoBytes);
+  uint64_t* sB = reinterpret_cast<uint64_t*>(info_base + kWarps * stages * kSlotInfoBytes + kFrontBytes);
+  const uint32_t A = args.A;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  SlotInfo* info = reinterpret_cast<SlotInfo*>(info_base) + warp * stages;
+  const uint32_t ring_u32 = smem_u32(smem) + (uint32_t)(warp * stages) * kSliceBytes;
+  const uint32_t bar_u32 = smem_u32(bars + warp * kMaxStages);
+  if (lane == 0) {
+    for (int j = 0; j < stages; ++j) mbar_init(bars + warp * kMaxStages + j, 1);
+    fence_mbar_init();
+  }
+  if (!kBig)
+    for (uint32_t i = threadIdx.x; i < 2 * A; i += kThreads) sB[i] = args.bounds[i];
+  const uint64_t W = (uint64_t)gridDim.x * kWarps;
+  uint64_t gnext = (uint64_t)blockIdx.x * kWarps + warp;  // next slice to look at (lane 0)
+  if (lane == 0) front[warp] = gnext;
+  __syncthreads();
+
+  const uint64_t pol = l2_evict_first_policy();
+  unsigned long long cta_last = 0;  // warp 0 lane 0: batches this CTA has reported read
+  // lane 0: the next non-empty published slice of this warp into ring slot `slot`
+  // (descriptor fields into the slot info, TMA issued); false when the stream has ended
+  auto issue = [&](uint32_t slot) -> bool {
+    for (;;) {
+      const uint64_t G = gnext, b = G / ra.spb, s = G % ra.spb;
+      while (ld_acquire_u64(&ra.ctl->tail) <= b) {
+        if (ld_acquire_u64(&ra.ctl->end) <= b) return false;
+        if (warp == 0) stream_report(ra, front, cta_last);
+        __nanosleep(200);
+      }
+      const StreamDesc* d = ra.ring + (b % ra.slots);
+      const uint64_t n = __ldcg(reinterpret_cast<const unsigned long long*>(&d->n));
+      gnext = G + W;
+      if (s * kSlice >= n) continue;  // past the end of a short batch
+      const uint64_t* rec = reinterpret_cast<const uint64_t*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d->rec)));
+      SlotInfo& si = info[slot];
+      si.G = G;
+      si.koffs = reinterpret_cast<const uint64_t*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d->koffs)));
+      si.n = n;
+      const uint2 nkk = __ldcg(reinterpret_cast<const uint2*>(&d->nk));
+      si.nk = nkk.x;
+      si.k0 = nkk.y;
+      si.s = (uint32_t)s;
+      const uint64_t left = n - s * kSlice;
+      si.valid = left < (uint64_t)kSlice ? (uint32_t)left : (uint32_t)kSlice;
+      mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, si.valid * 8u);
+      tma_load_1d_u32(ring_u32 + slot * kSliceBytes, rec + s * kSlice, si.valid * 8u, bar_u32 + 8u * slot, pol);
+      return true;
+    }
+  };
+
+  Ctx c;
+  c.va_lo = args.va_lo;
+  c.va_hi = args.va_hi;
+  c.wbytes = args.va_hi - args.va_lo;
+  c.s = args.page_shift;
+  c.A = A;
+  c.B = kBig ? args.bounds : sB;
+  Out o;
+  o.page_counts = args.page_counts;
+  o.alloc_counts = args.alloc_counts;
+  o.totals = args.totals;
+  o.kac = args.kac;
+  o.kstats = args.kstats;
+  o.kpb = args.kpb;
+  o.ids = args.ids;
+  o.max_ids = args.max_ids;
+  o.words = args.words;
+  o.A = A;
+  o.hot = nullptr;
+  o.P = args.P;
+  o.wk = 1;
+  o.wk_magic = 0;
+  o.tids = nullptr;
+  o.tcounts = nullptr;
+  o.ktc = nullptr;
+  o.max_tids = 0;
+  o.cache = 0u;
+
+  OwnCache oc;
+  oc.olo = 1;
+  oc.ospan = 0;
+  oc.own = A;
+  Ival cur = lookup<kBig>(oc, 0ull, c);
+  WarpAcc w;
+  w.page = kOOW - 1;
+  w.own = A;
+  w.pcnt = 0;
+  w.ocnt = 0;
+  LaneAcc& la = reinterpret_cast<LaneAcc*>(smem + ring_bytes(stages) + kBarBytes)[threadIdx.x];
+  la.own = A;
+  la.ocnt = 0;
+  la.kbit = kOOW;
+  uint32_t k = 0xFFFFFFFFu;  // kernel row of the warp's accumulators (none yet)
+
+  // prime the ring
+  uint32_t issued = 0;
+  if (lane == 0) {
+    while (issued < (uint32_t)stages && issue(issued)) ++issued;
+  }
+  issued = __shfl_sync(kFull, issued, 0);
+  __syncwarp();
+  bool more = issued == (uint32_t)stages;  // (lane 0's view; broadcast below)
+  uint32_t slot = 0, phase = 0;
+  for (uint32_t j = 0; j < issued; ++j) {
+    const SlotInfo si = info[slot];  // written by lane 0 before the __syncwarp that ended its issue
+    if (lane == 0) front[warp] = si.G;
+    mbar_wait_u32(bar_u32 + 8u * slot, phase);
+    uint64_t a[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const ulonglong2 v = lds128(ring_u32 + slot * kSliceBytes + 16u * lane + 512u * i);
+      a[2 * i] = v.x;
+      a[2 * i + 1] = v.y;
+    }
+    if (si.s == 0 && lane == 0) red_add_u64(args.totals + 0, si.n);
+    // kernel segments of this slice (batch-relative record index r = 256 s + position)
+    const uint64_t r_lo = (uint64_t)si.s * kSlice;
+    uint32_t kl = 0;
+    uint64_t kend = ~0ull;
+    if (kRows && si.koffs != nullptr && si.nk > 1) {
+      kl = kernel_of(si.koffs, si.nk, r_lo);
+      kend = kl + 1 < si.nk ? __ldg(si.koffs + kl + 1) : ~0ull;
+    }
+    if (kRows && si.k0 + kl != k) {
+      if (k != 0xFFFFFFFFu) warp_flush<kRows, kPages>(w, la, o, k, lane);
+      k = si.k0 + kl;
+    }
+    const uint32_t sa = ring_u32 + slot * kSliceBytes;
+    if (si.valid == (uint32_t)kSlice && kend - r_lo >= (uint64_t)kSlice) {
+      process_full<kBig, kRows, kPages>(a, sa, cur, oc, la, w, c, o, kRows ? k : 0u, lane);
+    } else {
+      uint32_t r0 = 0;
+      for (;;) {
+        uint32_t r1 = si.valid;
+        if (kRows && kend - r_lo < (uint64_t)r1) r1 = (uint32_t)(kend - r_lo);
+        uint32_t vm = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t pos = 64u * (i >> 1) + 2u * lane + (i & 1);
+          if (pos >= r0 && pos < r1) vm |= 1u << i;
+        }
+        process_lane<kBig, kRows, kPages>(a, vm, oc, la, w, c, o, kRows ? k : 0u, lane);
+        r0 = r1;
+        if (r0 >= si.valid) break;
+        // the next kernel of the batch starts inside this slice
+        warp_flush<kRows, kPages>(w, la, o, k, lane);
+        ++kl;
+        while (kl + 1 < si.nk && __ldg(si.koffs + kl + 1) <= r_lo + r0) ++kl;
+        kend = kl + 1 < si.nk ? __ldg(si.koffs + kl + 1) : ~0ull;
+        k = si.k0 + kl;
+      }
+    }
+    __syncwarp();
+    // lowest unread slice: the next one in flight, else the one the refill looks for
+    if (lane == 0) front[warp] = issued > j + 1 ? info[slot + 1 == (uint32_t)stages ? 0 : slot + 1].G : gnext;
+    // refill this ring slot with the warp's next slice
+    uint32_t got = 0;
+    if (lane == 0 && more) got = issue(slot) ? 1u : 0u;
+    got = __shfl_sync(kFull, got, 0);
+    more = got != 0;
+    if (got) ++issued;
+    __syncwarp();
+    if (++slot == (uint32_t)stages) {
+      slot = 0;
+      phase ^= 1u;
+    }
+    if (warp == 0 && lane == 0) stream_report(ra, front, cta_last);
+  }
+  if (k != 0xFFFFFFFFu || !kRows) warp_flush<kRows, kPages>(w, la, o, kRows ? k : 0u, lane);
+  if (lane == 0) front[warp] = ~0ull;
+  __syncwarp();
+  if (warp == 0 && lane == 0) {
+    // keep reporting until every warp of this CTA has read its last slice (then every
+    // batch up to the end is reported)
+    for (;;) {
+      stream_report(ra, front, cta_last);
+      if (cta_last == ld_acquire_u64(&ra.ctl->end)) break;
+      __nanosleep(500);
+    }
+  }
+}
+
+int stream_smem_bytes(uint32_t A, bool big, int* stages_out) {
+  const long extra = (long)kWarps * kMaxStages * kSlotInfoBytes + kFrontBytes - kPfBytes;
+  int st = stages_for(A, big, extra);
+  if (st > 4) st = 4;
+  *stages_out = st;
+  return ring_bytes(st) + kBarBytes + kLaBytes + kWarps * st * kSlotInfoBytes + kFrontBytes +
+         (big ? 0 : (int)(16ull * A));
+}
+
+template <bool kBig, bool kRows, int kPages>
+cudaError_t launch_stream_variant(const StreamArgs& a, cudaStream_t st, int* ctas) {
+  int stages = 0;
+  const int smem = stream_smem_bytes(a.s.A, kBig, &stages);
+  auto fn = stream_kernel<kBig, kRows, kPages>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, nb = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  int grid = sms * (nb < 1 ? 1 : (nb > 1 ? 1 : nb));
+  if (grid > kStreamMaxCtas) grid = kStreamMaxCtas;
+  *ctas = grid;
+  void* args[] = {(void*)&a, (void*)&stages};
+  // cooperative: every CTA is resident (a CTA that never ran could never report progress)
+  return cudaLaunchCooperativeKernel((void*)fn, dim3(grid), dim3(kThreads), args, smem, st);
 }
 
 
@@ -1568,6 +1966,18 @@ cudaError_t launch_rich(const RichArgs& a, int grid, cudaStream_t st) {
 
 int rich_slice_records() { return kRSlice; }
 int rich_warps() { return kRWarps; }
+
+cudaError_t launch_stream_consumer(const StreamArgs& a, cudaStream_t st, int* ctas) {
+  const bool big = !scan_table_fits_smem(a.s.A);
+  const bool rows = a.s.kac != nullptr;
+  const bool pages = a.s.kpb != nullptr;
+  if (big) {
+    if (!rows) return launch_stream_variant<true, false, 0>(a, st, ctas);
+    return pages ? launch_stream_variant<true, true, 1>(a, st, ctas) : launch_stream_variant<true, true, 0>(a, st, ctas);
+  }
+  if (!rows) return launch_stream_variant<false, false, 0>(a, st, ctas);
+  return pages ? launch_stream_variant<false, true, 1>(a, st, ctas) : launch_stream_variant<false, true, 0>(a, st, ctas);
+}
 
 cudaError_t launch_scan_extras(const ExtraArgs& a, cudaStream_t st) {
   scan_extras_kernel<<<1, 32, 0, st>>>(a);

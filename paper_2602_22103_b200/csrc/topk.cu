@@ -86,20 +86,24 @@ constexpr int kTU = 4;          // 16-byte count loads in flight per thread
 constexpr int kMaxPass = 11;    // pass 0 (float key) + <= ceil(96 / 11) digit passes
 constexpr int kSortTile = 2048; // keys per shared-memory bitonic tile
 constexpr uint64_t kBufMax = 1ull << 20;
+constexpr uint32_t kFastMax = 4096;  // fast finish: <= this many candidates sorted by block 0 alone
 
 struct TkHead {  // zeroed before every call
   unsigned hist[kMaxPass][kBins];
   unsigned long long fill[kMaxPass];  // keys that fell in the range during full pass i
+  unsigned overflow[kMaxPass];        // some CTA's buffer region overflowed in full pass i
   unsigned long long slots;           // keys gathered into the output list
+  unsigned long long cfill;           // keys of the first range copied to the compact list
 };
 
 struct TkArgs {
   const uint64_t* pc;
   uint64_t P, K;
   TkHead* head;
-  u128* buf;
-  uint64_t cap;  // buffer capacity (keys)
+  u128* buf;     // candidate buffer: CTA c appends to its own region [c * rcap, (c + 1) * rcap)
+  uint64_t rcap; // region capacity (keys)
   u128* keys;    // gathered keys [kcap]
+  u128* compact; // [kFastMax] the first range's keys, contiguous (fast finish)
   uint64_t kcap;
   uint64_t* out_page;
   uint64_t* out_count;
@@ -158,7 +162,8 @@ __device__ __forceinline__ void tk_stream(const uint64_t* __restrict__ pc, uint6
 }
 
 // Warp-aggregated append of `key` (lanes with want) to dst[*ctr ...], slots >= cap
-// dropped (the counter still counts them). Every lane of the warp calls it.
+// dropped (the counter still counts them). Every lane of the warp calls it. ctr may be
+// a global or a shared counter.
 __device__ __forceinline__ void warp_append(bool want, u128 key, u128* dst, unsigned long long* ctr, uint64_t cap) {
   const unsigned m = __ballot_sync(kFull, want);
   if (m == 0) return;
@@ -277,45 +282,92 @@ struct Sel {
 
 __device__ __forceinline__ u128 range_hi(const Sel& s) { return s.rlo + (((u128)1 << s.w) - 1); }
 
-// A full pass over the counts: keys in (range_hi, ghi] (or [rlo, ghi] once done) to the
-// output list; keys inside the range appended to the buffer and counted by next digit.
-__device__ void tk_full_pass(const TkArgs& a, const Sel& s, int ps, unsigned* sh) {
-  const uint64_t pmask = a.pbits ? ((~0ull) >> (64 - a.pbits)) : 0ull;
-  const u128 rlo = s.rlo, rhi = range_hi(s), ghi = s.ghi;
-  const u128 glo = s.done ? rlo : rhi + 1;
-  const bool rng = !s.done;
-  const int dw = s.w < kDigitBits ? s.w : kDigitBits;
-  const int dsh = s.w - dw;
-  RunHist rh;
-  TkHead* hd = a.head;
-  tk_stream(a.pc, a.P, [&](uint64_t p, uint64_t c) {
-    const u128 k = make_key(c, p, a.pbits, pmask);
-    const bool g = c != 0 && k >= glo && k <= ghi;
-    const bool r = rng && c != 0 && k >= rlo && k <= rhi;
-    if (r) rh.add(sh, (unsigned)((k - rlo) >> dsh));
-    warp_append(g, k, a.keys, &hd->slots, a.kcap);
-    if (rng) warp_append(r, k, a.buf, &hd->fill[ps], a.cap);
-  });
-  rh.flush(sh);
-  if (rng) hist_publish(sh, hd->hist[ps], 1 << dw);
+// What a full pass acts on (shared memory, written by one thread before the pass).
+struct PassCtl {
+  u128 rlo, rhi;  // the range: keys appended to the region and counted by digit
+  u128 glo, ghi;  // the gather interval: keys sent to the output list
+  uint64_t pmask;
+  int dsh;        // the digit's shift inside the range
+  int rng;        // 0 once the selection is done (gather only)
+};
+
+// The per-element work of a full pass for a warp with at least one count >= cmin, out
+// of line: the hot loop then holds only the loads and the count compare (no 128-bit
+// range bounds live across it). Called by all 32 lanes together.
+__device__ __noinline__ void full_slow(const TkArgs* a, const PassCtl* ctl, unsigned* sh, unsigned long long* sfill,
+                                       uint64_t p, uint64_t c) {
+  const u128 k = make_key(c, p, a->pbits, ctl->pmask);
+  const bool g = c != 0 && k >= ctl->glo && k <= ctl->ghi;
+  const bool r = ctl->rng && c != 0 && k >= ctl->rlo && k <= ctl->rhi;
+  if (r) atomicAdd(&sh[(unsigned)((k - ctl->rlo) >> ctl->dsh)], 1u);
+  warp_append(g, k, a->keys, &a->head->slots, a->kcap);
+  if (ctl->rng) warp_append(r, k, a->buf + (uint64_t)blockIdx.x * a->rcap, sfill, a->rcap);
 }
 
-// A pass over the buffer's n keys (the whole range of the last full pass): histogram of
-// the current range's next digit, or (done) every key >= rlo to the output list.
+// A full pass over the counts: keys in (range_hi, ghi] (or [rlo, ghi] once done) to the
+// output list; keys inside the range appended to this CTA's buffer region (shared-memory
+// slot counter: no global atomic hot spot) and counted by next digit. Returns the keys
+// this CTA found in the range (its region holds them all when that is <= rcap).
+__device__ uint64_t tk_full_pass(const TkArgs& a, const Sel& s, int ps, unsigned* sh, unsigned long long* sfill,
+                                 PassCtl* ctl, bool compact) {
+  const bool rng = !s.done;
+  const int dw = s.w < kDigitBits ? s.w : kDigitBits;
+  if (threadIdx.x == 0) {
+    ctl->rlo = s.rlo;
+    ctl->rhi = range_hi(s);
+    ctl->glo = s.done ? s.rlo : range_hi(s) + 1;
+    ctl->ghi = s.ghi;
+    ctl->pmask = a.pbits ? ((~0ull) >> (64 - a.pbits)) : 0ull;
+    ctl->dsh = s.w - dw;
+    ctl->rng = rng ? 1 : 0;
+  }
+  __syncthreads();
+  TkHead* hd = a.head;
+  // every key this pass acts on is >= rlo, i.e. has count >= rlo >> pbits (>= 1): a warp
+  // whose counts are all below skips the key arithmetic (almost every count, every pass)
+  const uint64_t cmin = (uint64_t)(s.rlo >> a.pbits);
+  tk_stream(a.pc, a.P, [&](uint64_t p, uint64_t c) {
+    if (__any_sync(kFull, c >= cmin)) full_slow(&a, ctl, sh, sfill, p, c);
+  });
+  if (!rng) return 0;
+  hist_publish(sh, hd->hist[ps], 1 << dw);  // (its barriers also complete every append)
+  const uint64_t mine = *sfill;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (mine) atomicAdd(&hd->fill[ps], (unsigned long long)mine);
+    if (mine > a.rcap) atomicOr(&hd->overflow[ps], 1u);
+    *sfill = compact && mine ? atomicAdd(&hd->cfill, (unsigned long long)mine) : 0;
+  }
+  if (compact) {  // this CTA's range keys -> the contiguous list (if it still has room)
+    __syncthreads();
+    const uint64_t off = *sfill;
+    if (mine <= a.rcap && off + mine <= kFastMax) {
+      const u128* region = a.buf + (uint64_t)blockIdx.x * a.rcap;
+      for (uint64_t i = threadIdx.x; i < mine; i += kTB) a.compact[off + i] = region[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *sfill = 0;
+  }
+  return mine;
+}
+
+// A pass over this CTA's buffer region (n keys; together the regions hold the whole range
+// of the last full pass): histogram of the current range's next digit, or (done) every
+// key >= rlo to the output list.
 __device__ void tk_buf_pass(const TkArgs& a, const Sel& s, int ps, uint64_t n, unsigned* sh) {
   const u128 rlo = s.rlo, rhi = range_hi(s);
   const int dw = s.w < kDigitBits ? s.w : kDigitBits;
   const int dsh = s.w - dw;
+  const u128* region = a.buf + (uint64_t)blockIdx.x * a.rcap;
   RunHist rh;
-  const uint64_t step = (uint64_t)gridDim.x * kTB * kTU;
-  for (uint64_t b0 = (uint64_t)blockIdx.x * kTB * kTU; b0 < n; b0 += step) {
+  for (uint64_t b0 = 0; b0 < n; b0 += (uint64_t)kTB * kTU) {
     u128 v[kTU];
 #pragma unroll
     for (int u = 0; u < kTU; ++u) {
       const uint64_t i = b0 + (uint64_t)u * kTB + threadIdx.x;
       v[u] = 0;
       if (i < n) {
-        const ulonglong2 x = __ldcg(reinterpret_cast<const ulonglong2*>(a.buf + i));
+        const ulonglong2 x = __ldcg(reinterpret_cast<const ulonglong2*>(region + i));
         v[u] = ((u128)x.y << 64) | x.x;
       }
     }
@@ -367,13 +419,16 @@ __device__ __forceinline__ void put_key(const TkArgs& a, uint64_t i, u128 k, uin
   a.out_page[i] = pmask - (uint64_t)(k & (u128)pmask);
 }
 
-__global__ void __launch_bounds__(kTB, 2) topk_kernel(const TkArgs a) {
+__global__ void __launch_bounds__(kTB, 2) topk_kernel(const __grid_constant__ TkArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned sh[kBins];
   __shared__ unsigned long long sw[kTB / 32];
   __shared__ Pick pk;
-  __shared__ u128 tile[kSortTile];
+  __shared__ unsigned long long sfill;
+  __shared__ PassCtl ctl;
+  extern __shared__ u128 tile[];  // [kFastMax] (dynamic): sort tiles, the fast finish
   for (int i = threadIdx.x; i < kBins; i += kTB) sh[i] = 0;
+  if (threadIdx.x == 0) sfill = 0;
   __syncthreads();
   TkHead* hd = a.head;
   const uint64_t pmask = a.pbits ? ((~0ull) >> (64 - a.pbits)) : 0ull;
@@ -390,6 +445,7 @@ __global__ void __launch_bounds__(kTB, 2) topk_kernel(const TkArgs a) {
   grid.sync();
   const Pick p0 = block_pick(hd->hist[0], kFirstBins, a.K, true, sw, &pk);
   const uint64_t kprime = a.K < p0.total ? a.K : p0.total;
+  bool fast = false;
   if (kprime > 0) {
     Sel s;
     uint64_t lo = (uint64_t)p0.d;
@@ -409,14 +465,32 @@ __global__ void __launch_bounds__(kTB, 2) topk_kernel(const TkArgs a) {
     // B / C / D
     for (int ps = 1; ps < kMaxPass; ++ps) {
       if (!buf_ok) {
-        tk_full_pass(a, s, ps, sh);
+        const uint64_t mine = tk_full_pass(a, s, ps, sh, &sfill, &ctl, ps == 1 && !s.done);
         grid.sync();
         if (s.done) break;
-        const unsigned long long f = __ldcg(&hd->fill[ps]);
+        if (ps == 1) {
+          // fast finish: the keys above the first range and the range itself (compacted)
+          // are few: block 0 sorts them all and keeps the first K'; the others are done
+          const uint64_t above = __ldcg(&hd->slots), total = __ldcg(&hd->fill[1]);
+          if (total <= kFastMax && above + total <= kFastMax) {
+            if (blockIdx.x == 0) {
+              const uint32_t n = (uint32_t)(above + total);
+              uint32_t n2 = 2;
+              while (n2 < n) n2 <<= 1;
+              for (uint32_t i = threadIdx.x; i < n2; i += kTB)
+                tile[i] = i < above ? ld_key(a.keys + i) : (i < n ? ld_key(a.compact + (i - above)) : (u128)0);
+              __syncthreads();
+              tile_bitonic(tile, n2, 0, 2, n2, n2);
+              for (uint32_t i = threadIdx.x; i < (uint32_t)kprime; i += kTB) put_key(a, i, tile[i], pmask);
+            }
+            fast = true;
+            break;
+          }
+        }
         s.ghi = range_hi(s);
-        if (f <= a.cap) {
+        if (__ldcg(&hd->overflow[ps]) == 0u) {
           buf_ok = true;
-          nbuf = f;
+          nbuf = mine;
         }
       } else {
         tk_buf_pass(a, s, ps, nbuf, sh);
@@ -434,7 +508,9 @@ __global__ void __launch_bounds__(kTB, 2) topk_kernel(const TkArgs a) {
   // E: sort the K' gathered keys descending and write the outputs
   uint64_t kp2 = 2;
   while (kp2 < kprime) kp2 <<= 1;
-  if (kp2 <= (uint64_t)kSortTile) {
+  if (fast) {
+    // written by block 0 above
+  } else if (kp2 <= (uint64_t)kSortTile) {
     if (blockIdx.x == 0) {
       for (uint32_t i = threadIdx.x; i < (uint32_t)kp2; i += kTB) tile[i] = i < kprime ? ld_key(a.keys + i) : (u128)0;
       __syncthreads();
@@ -640,11 +716,19 @@ Scratch carve(void* base, uint64_t Kp, int grid) {
 
 }  // namespace
 
-size_t topk_scratch_bytes(uint64_t k, uint64_t P) {
+// Candidate buffer region per CTA: the whole range of <= 2^20 keys split over the CTAs,
+// at least 256 keys each.
+uint64_t topk_region_cap(uint64_t P, int max_ctas) {
+  const uint64_t tot = P < kBufMax ? P : kBufMax;
+  const uint64_t r = (tot + (uint64_t)max_ctas - 1) / (uint64_t)max_ctas;
+  return r < 256 ? 256 : r;
+}
+
+size_t topk_scratch_bytes(uint64_t k, uint64_t P, int max_ctas) {
   const uint64_t m = k < P ? k : P;
   const uint64_t Kp = pow2_ceil(m < 2 ? 2 : m);
-  const uint64_t cap = pow2_ceil(P) < kBufMax ? pow2_ceil(P) : kBufMax;
-  return (sizeof(TkHead) + 255) / 256 * 256 + 16 * cap + 16 * Kp;
+  return (sizeof(TkHead) + 255) / 256 * 256 + 16ull * kFastMax + 16 * topk_region_cap(P, max_ctas) * (uint64_t)max_ctas +
+         16 * Kp;
 }
 
 size_t topk_merge_scratch_bytes(uint64_t n, int grid) {
@@ -684,7 +768,7 @@ cudaError_t sort_keys(uint64_t* key_c, uint64_t* key_p, uint64_t Kp, int grid, c
 }
 
 cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_page, uint64_t* out_count,
-                     uint64_t* out_found, void* scratch, int grid, cudaStream_t st, int* n_launches) {
+                     uint64_t* out_found, void* scratch, int max_ctas, cudaStream_t st, int* n_launches) {
   const uint64_t m = (uint64_t)k < P ? (uint64_t)k : P;
   TkArgs a;
   a.pc = pc;
@@ -693,9 +777,11 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
   char* b = static_cast<char*>(scratch);
   a.head = reinterpret_cast<TkHead*>(b);
   b += (sizeof(TkHead) + 255) / 256 * 256;
-  a.cap = pow2_ceil(P) < kBufMax ? pow2_ceil(P) : kBufMax;
+  a.compact = reinterpret_cast<u128*>(b);
+  b += 16ull * kFastMax;
+  a.rcap = topk_region_cap(P, max_ctas);
   a.buf = reinterpret_cast<u128*>(b);
-  b += 16 * a.cap;
+  b += 16 * a.rcap * (uint64_t)max_ctas;
   a.kcap = pow2_ceil(m < 2 ? 2 : m);
   a.keys = reinterpret_cast<u128*>(b);
   a.out_page = out_page;
@@ -704,10 +790,13 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
   a.pbits = P > 1 ? 64 - __builtin_clzll(P - 1) : 0;
   cudaError_t e = cudaMemsetAsync(a.head, 0, sizeof(TkHead), st);
   if (e != cudaSuccess) return e;
+  constexpr int kDynSmem = 16 * kFastMax;
   static int coop_blocks = 0;  // co-resident blocks per SM for the cooperative launch
   if (coop_blocks == 0) {
+    e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+    if (e != cudaSuccess) return e;
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, topk_kernel, kTB, 0) != cudaSuccess || nb < 1) nb = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, topk_kernel, kTB, kDynSmem) != cudaSuccess || nb < 1) nb = 1;
     coop_blocks = nb;
   }
   int dev = 0, sms = 0;
@@ -720,9 +809,9 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
   uint64_t w = want > want_sort ? want : want_sort;
   if (w < 1) w = 1;
   if ((uint64_t)g > w) g = (int)w;
-  if (g > grid) g = grid;
+  if (g > max_ctas) g = max_ctas;
   void* args[] = {(void*)&a};
-  PASTA_TRY(cudaLaunchCooperativeKernel((void*)topk_kernel, dim3(g), dim3(kTB), args, 0, st));
+  PASTA_TRY(cudaLaunchCooperativeKernel((void*)topk_kernel, dim3(g), dim3(kTB), args, kDynSmem, st));
   return cudaSuccess;
 }
 

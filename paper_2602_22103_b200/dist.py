@@ -181,35 +181,48 @@ class ShardedMerger:
 
 class PeerMerger:
     """ShardedMerger's results through peer memory instead of NCCL data movement
-    (DESIGN.md section 5): every rank maps the other ranks' result buffers once (CUDA
-    IPC handles exchanged over the process group; NVLink / NVSwitch loads at run time)
-    and one pasta_peer_reduce kernel per merge reads its shard of every rank's page
-    counts, writing the merged counts together with the shard's bitmap words and
-    unique-page count. A second phase (after a barrier) copies the shard bitmaps,
-    unique counts and top-k candidates of the peers the same way. The process group
-    carries only the handle exchange and the barriers.
+    (DESIGN.md section 5). Every rank maps the other ranks' result buffers once, with
+    CUDA IPC handles exported and opened by libpasta in the trace handle's own device
+    context (pasta_ipc_export / pasta_ipc_open, lazy peer access: NVLink / NVSwitch loads
+    at run time); the handles travel over the process group once. A merge is then:
 
-    Outputs as ShardedMerger: hist.small merged (SUMs; WS slots MAX), hist.page_bitmap
-    and totals[UNIQUE_PAGES] global, the rank's merged page shard in `shard`, and the
-    global top-k lists (returned), totals[MAX_KERNEL, MAX_KERNEL_RECORDS] by ARGMAX (exact
-    for kernel-aligned shards with Histograms.kernel_row0 = the shard's first kernel).
-    Histograms must be allocated with pad_pages_to = world * 64."""
+    1. barrier -- every rank's local analyze is complete;
+    2. pasta_peer_reduce: my page shard of every rank -> merged counts + the shard's
+       bitmap words + its unique-page count (one kernel); pasta_peer_reduce_small: the
+       small part [alloc counts | totals | tensor counts] of every rank, SUM except
+       WS_OBJ / WS_TENSOR (MAX), the MAX_MEM_REFERENCED_KERNEL pair (ARGMAX) and
+       UNIQUE_PAGES (recomputed below) -- one kernel; the shard's top-k per K;
+    3. barrier -- every shard, bitmap word, count and candidate list is ready;
+    4. pasta_peer_gather: the peers' shard bitmaps into my page bitmap, the merged small
+       part into my histograms, the shards' unique-page counts added up, the peers'
+       candidates -- ONE kernel; pasta_topk_merge per K;
+    5. barrier -- nobody reads this rank's buffers any more (the next step may zero them).
+
+    With an NCCL group the barriers are stream-ordered (an all_reduce of one word on the
+    trace's stream): the merge never waits on the host. With gloo (tests: several ranks
+    on one GPU) they are host barriers after a stream synchronize.
+
+    Outputs as ShardedMerger: hist.small merged, hist.page_bitmap and totals[UNIQUE_PAGES]
+    global, the rank's merged page shard in `shard`, the global top-k lists (returned),
+    totals[MAX_KERNEL, MAX_KERNEL_RECORDS] by ARGMAX (exact for kernel-aligned shards with
+    Histograms.kernel_row0 = the shard's first kernel). Histograms must be allocated with
+    pad_pages_to = world * 64."""
 
     def __init__(self, trace, hist, ks, group=None):
-        from torch.multiprocessing.reductions import reduce_tensor
-
         self.tr, self.hist, self.group = trace, hist, group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         assert hist.P_pad % (self.world * 64) == 0, "allocate Histograms with pad_pages_to = world * 64"
         dev = hist.packed.device
+        self.dev = dev
+        self.nccl = dist.get_backend(group) == "nccl"
         self.S = hist.P_pad // self.world
         self.Sw = self.S // 64
         self.shard = torch.zeros(self.S, dtype=torch.int64, device=dev)
         self.shard_bm = torch.zeros(self.Sw, dtype=torch.int64, device=dev)
         self.pop = torch.zeros(1, dtype=torch.int64, device=dev)
         self.small_out = torch.zeros_like(hist.small)
-        self.bm_full = torch.zeros(self.world * self.Sw, dtype=torch.int64, device=dev)
+        self.flag = torch.zeros(1, dtype=torch.int64, device=dev)
         self.ks = tuple(ks)
         self.loc = {k: (torch.zeros(k, dtype=torch.int64, device=dev), torch.zeros(k, dtype=torch.int64, device=dev),
                         torch.zeros(1, dtype=torch.int64, device=dev)) for k in self.ks}
@@ -221,70 +234,96 @@ class PeerMerger:
         for k in self.ks:
             mine += [self.loc[k][0], self.loc[k][1]]
         torch.cuda.synchronize(dev)
-        shared = [reduce_tensor(t) for t in mine] if self.world > 1 else []  # own buffers are used directly
+        # own buffers are used directly; the others' through libpasta's IPC mappings
+        handles = [trace.ipc_export(t) for t in mine] if self.world > 1 else []
         allh = [None] * self.world
-        dist.all_gather_object(allh, (dev.index if dev.index is not None else torch.cuda.current_device(), shared),
+        dist.all_gather_object(allh, (dev.index if dev.index is not None else torch.cuda.current_device(), handles),
                                group=group)
-        self.peers, err = [], None
+        self.peers, self._opened, err = [], [], None
         try:
             for r, (devr, hs) in enumerate(allh):
                 if r == self.rank:
-                    self.peers.append(mine)
+                    self.peers.append([t.data_ptr() for t in mine])
                     continue
-                if devr != hist.packed.device.index:
+                if devr != dev.index:
                     trace.enable_peer(devr)
-                self.peers.append([fn(*args) for fn, args in hs])
+                ptrs = [trace.ipc_open(hb) for hb in hs]
+                self._opened += ptrs
+                self.peers.append(ptrs)
         except Exception as exc:  # e.g. no peer access between these GPUs
             err = f"rank {self.rank}: {exc!r}"
         errs = [None] * self.world
         dist.all_gather_object(errs, err, group=group)  # every rank takes the same decision
         bad = [e for e in errs if e]
         if bad:
-            self.peers = []
+            self.close()
             raise RuntimeError("peer mapping failed: " + "; ".join(bad))
+        self._plan()
 
-    def _addr(self, t, elem=0):
-        return t.data_ptr() + 8 * elem
+    def _plan(self):
+        """The fixed argument lists of every merge (addresses never change)."""
+        from . import PASTA_COPY, PASTA_COPY_ADD, PASTA_PEER_ARGMAX, PASTA_PEER_MAX, PASTA_PEER_ZERO, T_UNIQUE_PAGES
+
+        h, W, S, Sw = self.hist, self.world, self.S, self.Sw
+        P_pad, mi = h.P_pad, h.max_ids
+        self.n_small = h.small.numel()
+        self.src_shard = [p[0] + 8 * self.rank * S for p in self.peers]
+        self.src_small = [p[0] + 8 * P_pad for p in self.peers]
+        u = mi + T_UNIQUE_PAGES
+        self.slots = [(mi + s, PASTA_PEER_MAX) for s in _WS_SLOTS] + [(mi + _MK, PASTA_PEER_ARGMAX),
+                                                                       (u, PASTA_PEER_ZERO)]
+        so, hs = self.small_out.data_ptr(), h.small.data_ptr()
+        cp = []
+        # the peers' shard bitmap words -> my global bitmap (its padding words stay out)
+        for r, p in enumerate(self.peers):
+            n = min(Sw, h.words - r * Sw)
+            if n > 0:
+                cp.append((p[1], h.page_bitmap.data_ptr() + 8 * r * Sw, n, PASTA_COPY))
+        # merged small part -> my histograms; unique pages = sum of the shards' counts: the
+        # one-word entries of one word run on one thread in table order (copy, then adds)
+        cp.append((so, hs, u, PASTA_COPY))
+        cp.append((so + 8 * u, hs + 8 * u, 1, PASTA_COPY))
+        if self.n_small > u + 1:
+            cp.append((so + 8 * (u + 1), hs + 8 * (u + 1), self.n_small - u - 1, PASTA_COPY))
+        for p in self.peers:
+            cp.append((p[2], hs + 8 * u, 1, PASTA_COPY_ADD))
+        for i, k in enumerate(self.ks):
+            cpp, ccc = self.cand[k]
+            for r, p in enumerate(self.peers):
+                cp.append((p[3 + 2 * i], cpp.data_ptr() + 8 * r * k, k, PASTA_COPY))
+                cp.append((p[4 + 2 * i], ccc.data_ptr() + 8 * r * k, k, PASTA_COPY))
+        assert len(cp) <= 120, "too many peer copies for one pasta_peer_gather"
+        self.copies = cp
+
+    def _barrier(self):
+        if self.nccl:
+            dist.all_reduce(self.flag, group=self.group)  # stream-ordered (NCCL on the current stream)
+        else:
+            self.tr.sync()
+            torch.cuda.synchronize(self.dev)
+            dist.barrier(group=self.group)
 
     def merge(self):
-        from . import PASTA_PEER_ARGMAX, PASTA_PEER_MAX, T_UNIQUE_PAGES
-
-        h, tr, W, S = self.hist, self.tr, self.world, self.S
-        P_pad = h.P_pad
-        self.pop.zero_()
-        torch.cuda.synchronize(h.packed.device)
-        tr.sync()
-        dist.barrier(group=self.group)  # every rank's local analyze is complete
-        # phase 1: my page shard of every rank -> merged counts + bitmap words + popcount
-        tr.peer_reduce([self._addr(p[0], self.rank * S) for p in self.peers], 0, S, self.shard, self.shard_bm,
-                       self.pop)
-        n_small = h.small.numel()
-        tr.peer_reduce([self._addr(p[0], P_pad) for p in self.peers], 0, n_small, self.small_out)
-        for slot in _WS_SLOTS:
-            e = h.max_ids + slot
-            tr.peer_reduce([self._addr(p[0], P_pad + e) for p in self.peers], 0, 1, self._addr(self.small_out, e),
-                           op=PASTA_PEER_MAX)
-        e = h.max_ids + _MK
-        tr.peer_reduce([self._addr(p[0], P_pad + e) for p in self.peers], 0, 2, self._addr(self.small_out, e),
-                       op=PASTA_PEER_ARGMAX)
-        for k in self.ks:
-            tr.topk(self.shard, k, out=self.loc[k])
-        tr.sync()
-        dist.barrier(group=self.group)  # every shard, bitmap word, popcount and candidate list is ready
-        # phase 2: the peers' shard bitmaps, unique counts and candidates
-        for r, p in enumerate(self.peers):
-            tr.peer_reduce([p[1]], 0, self.Sw, self._addr(self.bm_full, r * self.Sw))
-        tr.peer_reduce([p[2] for p in self.peers], 0, 1, self._addr(self.small_out, h.max_ids + T_UNIQUE_PAGES))
-        for i, k in enumerate(self.ks):
-            cp, cc = self.cand[k]
-            for r, p in enumerate(self.peers):
-                tr.peer_reduce([p[3 + 2 * i]], 0, k, self._addr(cp, r * k))
-                tr.peer_reduce([p[4 + 2 * i]], 0, k, self._addr(cc, r * k))
-        tr.sync()
-        dist.barrier(group=self.group)  # nobody reads this rank's buffers any more
-        h.small.copy_(self.small_out)
-        h.page_bitmap.copy_(self.bm_full[:h.words])
-        for k in self.ks:
-            cp, cc = self.cand[k]
-            tr.topk_merge(cp, cc, W, k, S, self.out[k])
+        tr = self.tr
+        with torch.cuda.stream(tr.stream):
+            self.pop.zero_()
+            self._barrier()  # every rank's local analyze is complete
+            tr.peer_reduce(self.src_shard, 0, self.S, self.shard, self.shard_bm, self.pop)
+            tr.peer_reduce_small(self.src_small, 0, self.n_small, self.slots, self.small_out)
+            for k in self.ks:
+                tr.topk(self.shard, k, out=self.loc[k])
+            self._barrier()  # every shard, bitmap word, count and candidate list is ready
+            tr.peer_gather(self.copies)
+            for k in self.ks:
+                cp, cc = self.cand[k]
+                tr.topk_merge(cp, cc, self.world, k, self.S, self.out[k])
+            self._barrier()  # nobody reads this rank's buffers any more
         return self.out
+
+    def close(self):
+        for ptr in self._opened:
+            try:
+                self.tr.ipc_close(ptr)
+            except Exception:
+                pass
+        self._opened = []

@@ -47,20 +47,31 @@ def test_our_arm_line_tiny():
 
 
 @pytest.mark.gpu
-def test_two_rank_bench_on_one_gpu():
-    """The N > 1 bench path (kernel-aligned shards, dist.PeerMerger through CUDA IPC,
-    max-over-ranks timing, e2e with the same merge) as two processes on one GPU with a
-    gloo group (PASTA_BENCH_GLOO=1; the driver's multi-GPU runs use NCCL)."""
+def test_two_rank_bench_on_one_gpu(tmp_path):
+    """The N > 1 bench path (kernel-aligned shards, dist.PeerMerger through libpasta's
+    CUDA IPC mappings, max-over-ranks timing, e2e with the same merge) as two processes
+    on one GPU with a gloo group (PASTA_BENCH_GLOO=1; the driver's multi-GPU runs use
+    NCCL), and EVERY merged output of both ranks (page shard, alloc counts, totals incl.
+    unique pages / WS_obj / the MAX_MEM_REFERENCED_KERNEL pair, bitmap, top-K) equal to
+    the oracle over the whole trace."""
     import socket
+
+    import numpy as np
+
+    import oracle
+    import paper_2602_22103_b200 as pb
+    import tracegen
 
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    env = dict(os.environ, PASTA_BENCH_GLOO="1")
+    n = 300_000_000
+    dump = str(tmp_path / "merged")
+    env = dict(os.environ, PASTA_BENCH_GLOO="1", PASTA_BENCH_DUMP=dump)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "gpt2m",
-           "--steps", "3", "--warmup", "3", "--no-cpu", "--e2e-records", "4194304"]
+           "--records", str(n), "--steps", "3", "--warmup", "3", "--no-cpu", "--e2e-records", "4194304"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
@@ -68,3 +79,34 @@ def test_two_rank_bench_on_one_gpu():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["merge"] == "peer" and d["value"] > 0
     assert d["phases_ms_per_step"]["merge"] > 0 and d["e2e"]["value"] > 0
+
+    p = tracegen.build_plan("gpt2m", 42, n)
+    o = oracle.OracleTrace(p.va_lo, p.va_hi, len(p.allocs), len(p.allocs))
+    for b, sz in p.allocs:
+        o.register_alloc(b, sz)
+    o.analyze_parallel(lambda j0, j1: tracegen.host_records(p, j0, j1), p.kernel_offsets, p.page_shift,
+                       kernel_rows=True)
+    bm, uniq = o.bitmap()
+    _, ws = o.footprints()
+    mk = o.max_kernel()
+    per = o.kernel_rows.sum(axis=1, dtype=np.uint64) + o.kun
+    A = len(p.allocs)
+    for r in range(2):
+        z = np.load(f"{dump}.rank{r}.npz")
+        S = int(z["S"])
+        pages = np.zeros(2 * S, dtype=np.uint64)
+        pages[:len(o.page_counts)] = o.page_counts
+        assert np.array_equal(z["shard"], pages[r * S:(r + 1) * S]), f"rank {r}: merged page shard"
+        small = z["small"]
+        assert np.array_equal(small[:A], o.alloc_counts), f"rank {r}: alloc counts"
+        tot = small[A:A + pb.TOTALS]
+        assert tot[:3].tolist() == o.totals.tolist(), f"rank {r}: records / unattributed / out of window"
+        assert int(tot[pb.T_UNIQUE_PAGES]) == uniq, f"rank {r}: unique pages"
+        assert int(tot[pb.T_WS_OBJ]) == ws, f"rank {r}: WS_obj"
+        assert int(tot[pb.T_MAX_KERNEL]) == mk and int(tot[pb.T_MAX_KERNEL_RECORDS]) == int(per[mk]), \
+            f"rank {r}: MAX_MEM_REFERENCED_KERNEL"
+        assert np.array_equal(z["bitmap"], bm), f"rank {r}: bitmap"
+        for k in p.topk:
+            rp, rc, rf = oracle.topk(o.page_counts, k)
+            assert int(z[f"top{k}_2"][0]) == rf, f"rank {r}: found top-{k}"
+            assert np.array_equal(z[f"top{k}_0"], rp) and np.array_equal(z[f"top{k}_1"], rc), f"rank {r}: top-{k}"

@@ -260,3 +260,90 @@ def test_enable_peer_status_codes():
             tr.enable_peer(bad)
         assert ei.value.status == pb.PASTA_EINVAL
     tr.close()
+
+
+def test_peer_reduce_small_slots():
+    """pasta_peer_reduce_small: SUM except MAX slots, an ARGMAX pair (ties to the lowest
+    index) and ZERO slots, over 1-16 sources, one launch; bad slots are EINVAL."""
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    rng = np.random.default_rng(11)
+    n = 70_001
+    for g in (1, 2, 5, 16):
+        srcs = [rng.integers(0, 1 << 62, size=n + 9, dtype=np.uint64) for _ in range(g)]
+        am = 777
+        for a in srcs:
+            a[3 + am + 1] = rng.integers(0, 3)  # tied values at the ARGMAX pair
+        dsrc = [_t(a) for a in srcs]
+        slots = [(5, pb.PASTA_PEER_MAX), (n - 1, pb.PASTA_PEER_MAX), (am, pb.PASTA_PEER_ARGMAX),
+                 (42, pb.PASTA_PEER_ZERO)]
+        out = torch.zeros(n, dtype=torch.int64, device=DEV)
+        tr.peer_reduce_small(dsrc, 3, n, slots, out)
+        tr.sync()
+        with np.errstate(over="ignore"):
+            ref = np.zeros(n, dtype=np.uint64)
+            for a in srcs:
+                ref += a[3:3 + n]
+        for i in (5, n - 1):
+            ref[i] = max(a[3 + i] for a in srcs)
+        best = max(range(g), key=lambda r: (int(srcs[r][3 + am + 1]), -int(srcs[r][3 + am])))
+        ref[am], ref[am + 1] = srcs[best][3 + am], srcs[best][3 + am + 1]
+        ref[42] = 0
+        assert np.array_equal(u64(out), ref), g
+    out = torch.zeros(8, dtype=torch.int64, device=DEV)
+    for bad in ([(8, pb.PASTA_PEER_MAX)], [(7, pb.PASTA_PEER_ARGMAX)], [(0, pb.PASTA_PEER_SUM)],
+                [(0, pb.PASTA_PEER_ZERO)] * 17):
+        with pytest.raises(pb.PastaError) as ei:
+            tr.peer_reduce_small(dsrc, 0, 8, bad, out)
+        assert ei.value.status == pb.PASTA_EINVAL
+    tr.close()
+
+
+def test_peer_gather_copies_and_ordered_adds():
+    """pasta_peer_gather: copies and atomic adds of many entries in one launch; one-word
+    entries into the same word apply in table order (a copy, then adds)."""
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    rng = np.random.default_rng(12)
+    srcs = [rng.integers(0, 1 << 40, size=int(m), dtype=np.uint64) for m in rng.integers(1, 50_000, size=40)]
+    dsrc = [_t(a) for a in srcs]
+    dst = torch.zeros(sum(a.size for a in srcs) + 1, dtype=torch.int64, device=DEV)
+    copies, off = [], 0
+    for a, d in zip(srcs, dsrc):
+        copies.append((d, dst.data_ptr() + 8 * off, a.size, pb.PASTA_COPY))
+        off += a.size
+    word = dst.data_ptr() + 8 * off
+    ones = [_t(np.array([v], dtype=np.uint64)) for v in (5, 7, 11, 13)]
+    copies.append((ones[0], word, 1, pb.PASTA_COPY))
+    copies += [(o, word, 1, pb.PASTA_COPY_ADD) for o in ones[1:]]
+    tr.peer_gather(copies)
+    tr.sync()
+    ref = np.concatenate(srcs + [np.array([5 + 7 + 11 + 13], dtype=np.uint64)])
+    assert np.array_equal(u64(dst), ref)
+    with pytest.raises(pb.PastaError):
+        tr.peer_gather(copies * 4)  # > 120 entries
+    with pytest.raises(pb.PastaError):
+        tr.peer_gather([(dsrc[0], dst, 4, 9)])  # bad op
+    tr.close()
+
+
+def test_ipc_export_status_codes():
+    """pasta_ipc_export of a caching-allocator tensor (an address inside a larger block):
+    offset recorded; a host pointer is EINVAL; opening one's own handle in the exporting
+    process is refused by the driver (ECUDA), closing an unknown pointer is ENOENT."""
+    import ctypes
+
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    big = torch.zeros(1 << 20, dtype=torch.int64, device=DEV)
+    hb = tr.ipc_export(big[1000:])
+    h = pb.pasta_ipc_handle.from_buffer_copy(hb)
+    assert h.offset >= 8000 and h.block_bytes >= 8 << 20 and h.device == (DEV.index or 0)
+    host = ctypes.create_string_buffer(64)
+    with pytest.raises(pb.PastaError) as ei:
+        tr.ipc_export(ctypes.addressof(host))
+    assert ei.value.status == pb.PASTA_EINVAL
+    with pytest.raises(pb.PastaError) as ei:
+        tr.ipc_open(hb)
+    assert ei.value.status == pb.PASTA_ECUDA
+    with pytest.raises(pb.PastaError) as ei:
+        tr.ipc_close(big.data_ptr())
+    assert ei.value.status == pb.PASTA_ENOENT
+    tr.close()
