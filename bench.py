@@ -488,11 +488,33 @@ def run_stream(args, plan, rec, n_loc, ko_loc, nk_loc, dev, expect_records):
     graph_ms = e0.elapsed_time(e1) / reps
     assert int(h.totals[0].item()) == expect_records
     calls = len(runner.calls)
+    # persistent ring consumer: one launch, the host publishing batch descriptors into a
+    # ring of 256 while it runs (events on the consumer's stream around open .. close)
+    from paper_2602_22103_b200.stream import StreamRing
+
+    ring_ms = []
+    ring = StreamRing(tr, h, rec, ko_loc.cpu().numpy(), n_loc - (n_loc % 2), args.stream_batch, plan.page_shift,
+                      slots=256)
+    for rep in range(1 + reps):
+        h.zero_()
+        torch.cuda.synchronize(dev)
+        e0.record(s)
+        ring.run()
+        e1.record(s)
+        ring.destroy()
+        s.synchronize()
+        if rep:
+            ring_ms.append(e0.elapsed_time(e1))
+    assert int(h.totals[0].item()) == n_loc - (n_loc % 2)
+    ring_t = sum(ring_ms) / len(ring_ms)
     tr.close()
     return {"batch_records": args.stream_batch, "calls": calls, "unit": "G rec/s",
             "graph_value": n_loc / (graph_ms / 1e3) / 1e9, "graph_ms": graph_ms,
             "eager_value": n_loc / (eager_ms / 1e3) / 1e9, "eager_ms": eager_ms,
-            "graph_us_per_call": graph_ms * 1e3 / calls}
+            "graph_us_per_call": graph_ms * 1e3 / calls,
+            "ring_value": (n_loc - n_loc % 2) / (ring_t / 1e3) / 1e9, "ring_ms": ring_t,
+            "ring_us_per_batch": ring_t * 1e3 / len(ring.batches), "ring_slots": 256,
+            "ring_path": "pasta_stream_open + pasta_stream_push (host publishes while the consumer runs) + close"}
 
 
 def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, k0, world, group, local, dev, top_out):

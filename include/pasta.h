@@ -375,6 +375,48 @@ typedef struct {
 } pasta_peer_copy;
 int pasta_peer_gather(pasta_trace* h, const pasta_peer_copy* table, uint32_t count);
 
+/* Streaming consumer (NEXT f2). The paper's profiler "records the
+ * instruction into a device buffer" that the analysis drains, the program stalling
+ * while the buffer is full, "e.g., 4MB" of it. pasta_stream_open launches
+ * ONE persistent consumer on the handle's stream; the producer then publishes batches
+ * (each a device buffer of records, e.g. 524,288 = 4 MB) with pasta_stream_push while it
+ * runs, and the consumer accumulates them into `out` exactly as pasta_analyze calls with
+ * PASTA_NO_FINALIZE would (counts are sums over any partition of the records, S:291-299;
+ * kernel rows at kernel_row0 + local kernel, so a kernel cut between batches accumulates
+ * into one row). At most `slots` batches are published and not yet read: push waits
+ * (host spin, up to ~30 s, then PASTA_ESTATE) until the consumer has read the batch
+ * `slots` places back, after which that batch's records and kernel offsets may be reused
+ * by the producer (pasta_stream_consumed tells how many batches have been read; a pushed
+ * batch's buffers must stay valid until then). pasta_stream_close publishes the end
+ * (asynchronous: later work on the handle's stream, e.g. pasta_finalize / pasta_topk, is
+ * ordered after the consumer drains); pasta_stream_destroy waits for the consumer and
+ * frees. The range table is the one current at open (snapshot, R13). out: page_counts,
+ * alloc_counts, totals required; kernel_alloc_counts / kernel_stats / kernel_page_bitmap
+ * optional (rows for every kernel_row0 + local kernel pushed); no hotness, no tensor level
+ * (EINVAL); out->flags ignored (never finalizes). Batches: addr 16-byte aligned, n even and
+ * <= max_batch (n = 0 is skipped), kernel_offsets NULL (one kernel) or [n_kernels + 1]
+ * batch-relative offsets with [0] = 0 and [n_kernels] = n (not checked: device memory).
+ * While a stream is open the handle's stream is busy with it: do not enqueue other calls
+ * of this handle until close. */
+typedef struct pasta_stream pasta_stream;
+typedef struct {
+  uint32_t page_shift;
+  uint32_t slots;      /* ring depth in batches, 2 .. 4096 */
+  uint64_t max_batch;  /* records per batch at most (even, >= 256) */
+} pasta_stream_params;
+typedef struct {
+  const uint64_t* addr;            /* device records */
+  uint64_t n;
+  const uint64_t* kernel_offsets;  /* device, batch-relative, or NULL */
+  uint32_t n_kernels;
+  uint32_t kernel_row0;
+} pasta_stream_batch;
+int pasta_stream_open(pasta_trace* h, const pasta_stream_params* p, const pasta_histograms* out, pasta_stream** s);
+int pasta_stream_push(pasta_stream* s, const pasta_stream_batch* batches, uint32_t count);
+int pasta_stream_consumed(pasta_stream* s, uint64_t* out_batches);
+int pasta_stream_close(pasta_stream* s);
+int pasta_stream_destroy(pasta_stream* s);
+
 /* CUDA IPC of device buffers between the ranks of one node, opened in the HANDLE's device
  * context (cudaIpcMemLazyEnablePeerAccess: NVLink / NVSwitch loads once mapped).
  * pasta_ipc_export: a handle for the device allocation holding ptr (any address inside a

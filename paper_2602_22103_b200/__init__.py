@@ -83,6 +83,15 @@ class pasta_ipc_handle(ctypes.Structure):
                 ("device", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
+class pasta_stream_params(ctypes.Structure):
+    _fields_ = [("page_shift", ctypes.c_uint32), ("slots", ctypes.c_uint32), ("max_batch", ctypes.c_uint64)]
+
+
+class pasta_stream_batch(ctypes.Structure):
+    _fields_ = [("addr", ctypes.c_void_p), ("n", ctypes.c_uint64), ("kernel_offsets", ctypes.c_void_p),
+                ("n_kernels", ctypes.c_uint32), ("kernel_row0", ctypes.c_uint32)]
+
+
 class pasta_rich_records(ctypes.Structure):
     _fields_ = [("records", ctypes.c_void_p), ("grid_lo", ctypes.c_uint32), ("grid_hi", ctypes.c_uint32)]
 
@@ -114,6 +123,12 @@ _SIGS = {
     "pasta_peer_reduce_small": (_int, [_vp, ctypes.POINTER(_vp), _u32, _u64, _u64, ctypes.POINTER(pasta_peer_slot),
                                        _u32, _vp]),
     "pasta_peer_gather": (_int, [_vp, ctypes.POINTER(pasta_peer_copy), _u32]),
+    "pasta_stream_open": (_int, [_vp, ctypes.POINTER(pasta_stream_params), ctypes.POINTER(pasta_histograms),
+                                 ctypes.POINTER(_vp)]),
+    "pasta_stream_push": (_int, [_vp, ctypes.POINTER(pasta_stream_batch), _u32]),
+    "pasta_stream_consumed": (_int, [_vp, ctypes.POINTER(_u64)]),
+    "pasta_stream_close": (_int, [_vp]),
+    "pasta_stream_destroy": (_int, [_vp]),
     "pasta_ipc_export": (_int, [_vp, _vp, ctypes.POINTER(pasta_ipc_handle)]),
     "pasta_ipc_open": (_int, [_vp, ctypes.POINTER(pasta_ipc_handle), ctypes.POINTER(_vp)]),
     "pasta_ipc_close": (_int, [_vp, _vp]),
@@ -268,6 +283,34 @@ def pasta_peer_gather(h, copies):
     """copies: [(src, dst, n_words, op)] (device addresses or tensors), one launch."""
     tab = (pasta_peer_copy * len(copies))(*[pasta_peer_copy(_ptr(a), _ptr(b), n, op, 0) for a, b, n, op in copies])
     _check(_lib.pasta_peer_gather(h, tab, len(copies)), "pasta_peer_gather")
+
+
+def pasta_stream_open(h, page_shift: int, slots: int, max_batch: int, hist):
+    out = _vp()
+    prm = pasta_stream_params(page_shift, slots, max_batch)
+    _check(_lib.pasta_stream_open(h, ctypes.byref(prm), ctypes.byref(hist), ctypes.byref(out)), "pasta_stream_open")
+    return out
+
+
+def pasta_stream_push(s, batches, count: int | None = None):
+    """batches: a ctypes array of pasta_stream_batch (or a list of them)."""
+    if not isinstance(batches, ctypes.Array):
+        batches = (pasta_stream_batch * len(batches))(*batches)
+    _check(_lib.pasta_stream_push(s, batches, len(batches) if count is None else count), "pasta_stream_push")
+
+
+def pasta_stream_consumed(s) -> int:
+    out = _u64()
+    _check(_lib.pasta_stream_consumed(s, ctypes.byref(out)), "pasta_stream_consumed")
+    return int(out.value)
+
+
+def pasta_stream_close(s):
+    _check(_lib.pasta_stream_close(s), "pasta_stream_close")
+
+
+def pasta_stream_destroy(s):
+    _check(_lib.pasta_stream_destroy(s), "pasta_stream_destroy")
 
 
 def pasta_ipc_export(h, ptr) -> bytes:

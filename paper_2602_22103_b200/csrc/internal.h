@@ -55,9 +55,10 @@ struct StreamDesc {          // one batch (32 B, a device ring slot)
   uint32_t k0;               // kernel row of the batch's first kernel
 };
 constexpr int kStreamMaxCtas = 256;
-struct StreamCtl {           // device
-  unsigned long long tail;   // batches published (stream-ordered host copies)
-  unsigned long long end;    // total batches once closed, else ~0
+struct StreamCtl {                              // device
+  unsigned long long tail;                      // batches published (stream-ordered host copies)
+  unsigned long long end;                       // total batches once closed, else ~0
+  unsigned long long cta_done[kStreamMaxCtas];  // per CTA: batches all its warps have read
 };
 struct StreamArgs {
   ScanArgs s;                   // table, window, outputs (rec / nbody / koffs unused)
@@ -65,8 +66,8 @@ struct StreamArgs {
   uint32_t slots;
   StreamCtl* ctl;
   uint64_t spb;                 // slices (256 records) per batch slot
-  unsigned* arrivals;           // [slots] CTAs done with the batch in that ring slot (zeroed)
   unsigned long long* consumed; // host-mapped: batches every CTA has read (flow control)
+  unsigned long long* prof;     // PASTA_STREAM_PROF builds: [ctas x warps x 5] counters, else unused
 };
 cudaError_t launch_stream_consumer(const StreamArgs& a, cudaStream_t st, int* ctas);
 

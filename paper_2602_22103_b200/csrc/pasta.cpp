@@ -11,7 +11,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -776,6 +779,232 @@ int pasta_peer_reduce(pasta_trace* h, const uint64_t* const* src, uint32_t g, ui
   cudaError_t e = launch_peer_reduce(s, g, lo, n, op, out, out_bitmap, out_popcount, h->sm_count * 8, h->stream);
   ++h->launches;
   return cuda_status(e);
+}
+
+// ---- streaming consumer (NEXT f2) ----
+struct pasta_stream {
+  pasta_trace* h = nullptr;
+  uint32_t slots = 0;
+  uint64_t max_batch = 0, spb = 0;
+  StreamDesc* d_ring = nullptr;        // [slots] device
+  StreamCtl* d_ctl = nullptr;          // device
+  StreamDesc* h_ring = nullptr;        // [slots] pinned staging of the descriptors
+  unsigned long long* h_vals = nullptr;  // [slots + 1] pinned: tail values, [slots] = end
+  unsigned long long* h_consumed = nullptr;  // pinned, mapped: batches read (GPU writes)
+  unsigned long long* d_consumed = nullptr;  // its device alias
+  cudaStream_t cs = nullptr;           // publishing copies (never behind the consumer)
+  uint64_t pushed = 0, seen = 0;
+  uint32_t vslot = 0;
+  bool closed = false;
+  int ctas = 0;
+  unsigned long long* d_prof = nullptr;  // PASTA_STREAM_PROF_OUT: per-warp counters
+};
+
+namespace {
+void stream_free(pasta_stream* s) {
+  if (s->cs) cudaStreamDestroy(s->cs);
+  if (s->d_ring) cudaFree(s->d_ring);
+  if (s->d_ctl) cudaFree(s->d_ctl);
+  if (s->h_ring) cudaFreeHost(s->h_ring);
+  if (s->h_vals) cudaFreeHost(s->h_vals);
+  if (s->h_consumed) cudaFreeHost(s->h_consumed);
+  delete s;
+}
+
+// Publish batches [first, s->pushed) from the pinned staging: the descriptor copies, then
+// the new tail (its own pinned word), in order on the publishing stream.
+int stream_publish(pasta_stream* s, uint64_t first) {
+  uint64_t b = first;
+  while (b < s->pushed) {
+    const uint32_t i = (uint32_t)(b % s->slots);
+    const uint64_t run = std::min<uint64_t>(s->pushed - b, s->slots - i);
+    if (cudaMemcpyAsync(s->d_ring + i, s->h_ring + i, run * sizeof(StreamDesc), cudaMemcpyHostToDevice, s->cs) !=
+        cudaSuccess)
+      return PASTA_ECUDA;
+    b += run;
+  }
+  unsigned long long* v = s->h_vals + s->vslot;
+  s->vslot = (s->vslot + 1) % s->slots;
+  *v = s->pushed;
+  if (cudaMemcpyAsync(&s->d_ctl->tail, v, 8, cudaMemcpyHostToDevice, s->cs) != cudaSuccess) return PASTA_ECUDA;
+  return PASTA_OK;
+}
+}  // namespace
+
+int pasta_stream_open(pasta_trace* h, const pasta_stream_params* p, const pasta_histograms* out, pasta_stream** ps) {
+  if (!h || !p || !out || !ps) return PASTA_EINVAL;
+  if (!out->page_counts || !out->alloc_counts || !out->totals) return PASTA_EINVAL;
+  if ((out->kernel_stats || out->kernel_page_bitmap) && !out->kernel_alloc_counts) return PASTA_EINVAL;
+  if (out->hotness || out->tensor_counts || out->kernel_tensor_counts || out->kernel_tensor_footprint)
+    return PASTA_EINVAL;
+  if (p->slots < 2 || p->slots > 4096 || p->max_batch < 256 || (p->max_batch & 1)) return PASTA_EINVAL;
+  int st = check_window(h, p->page_shift);
+  if (st) return st;
+  DeviceGuard g(h->device);
+  st = upload_table(h);
+  if (st) return st;
+  pasta_stream* s = new (std::nothrow) pasta_stream;
+  if (!s) return PASTA_ECUDA;
+  s->h = h;
+  s->slots = p->slots;
+  s->max_batch = p->max_batch;
+  s->spb = (p->max_batch + 255) / 256;
+  bool ok = cudaStreamCreateWithFlags(&s->cs, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMalloc(&s->d_ring, sizeof(StreamDesc) * s->slots) == cudaSuccess &&
+            cudaMalloc(&s->d_ctl, sizeof(StreamCtl)) == cudaSuccess &&
+            cudaMallocHost(&s->h_ring, sizeof(StreamDesc) * s->slots) == cudaSuccess &&
+            cudaMallocHost(&s->h_vals, 8ull * (s->slots + 1)) == cudaSuccess &&
+            cudaHostAlloc(&s->h_consumed, 8, cudaHostAllocMapped) == cudaSuccess &&
+            cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->d_consumed), s->h_consumed, 0) == cudaSuccess;
+  if (ok) {
+    *s->h_consumed = 0;
+    s->h_vals[s->slots] = ~0ull;  // ctl.end = "not closed"
+    ok = cudaMemsetAsync(s->d_ctl, 0, sizeof(StreamCtl), h->stream) == cudaSuccess &&
+         cudaMemcpyAsync(&s->d_ctl->end, s->h_vals + s->slots, 8, cudaMemcpyHostToDevice, h->stream) == cudaSuccess;
+    // the publishing copies must not overtake this initialization of the ring
+    cudaEvent_t ev = nullptr;
+    ok = ok && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventRecord(ev, h->stream) == cudaSuccess && cudaStreamWaitEvent(s->cs, ev, 0) == cudaSuccess;
+    if (ev) cudaEventDestroy(ev);
+  }
+  if (!ok) {
+    stream_free(s);
+    return PASTA_ECUDA;
+  }
+  const uint64_t P = (h->va_hi - h->va_lo) >> p->page_shift;
+  StreamArgs a{};
+  a.s.bounds = h->d_bounds;
+  a.s.ids = h->d_ids;
+  a.s.A = h->A_dev;
+  a.s.n_kernels = 1;
+  a.s.va_lo = h->va_lo;
+  a.s.va_hi = h->va_hi;
+  a.s.page_shift = p->page_shift;
+  a.s.words = (uint32_t)((P + 63) / 64);
+  a.s.max_ids = h->max_ids;
+  a.s.page_counts = out->page_counts;
+  a.s.alloc_counts = out->alloc_counts;
+  a.s.totals = out->totals;
+  a.s.kac = out->kernel_alloc_counts;
+  a.s.kstats = out->kernel_stats;
+  a.s.kpb = out->kernel_page_bitmap;
+  a.s.P = P;
+  a.s.window_kernels = 1;
+  a.s.log_ic = -1;
+  a.ring = s->d_ring;
+  a.slots = s->slots;
+  a.ctl = s->d_ctl;
+  a.spb = s->spb;
+  a.consumed = s->d_consumed;
+  a.prof = nullptr;
+  if (getenv("PASTA_STREAM_PROF_OUT")) {  // profiling builds only (PASTA_STREAM_PROF)
+    if (cudaMalloc(&s->d_prof, 8ull * 8 * kStreamMaxCtas * 32) == cudaSuccess) {
+      cudaMemsetAsync(s->d_prof, 0, 8ull * 8 * kStreamMaxCtas * 32, h->stream);
+      a.prof = s->d_prof;
+    }
+  }
+  {
+    Timed t(h, PASTA_PH_SCAN, h->stream);
+    const cudaError_t e = launch_stream_consumer(a, h->stream, &s->ctas);
+    ++h->launches;
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      stream_free(s);
+      return PASTA_ECUDA;
+    }
+  }
+  *ps = s;
+  return PASTA_OK;
+}
+
+int pasta_stream_push(pasta_stream* s, const pasta_stream_batch* batches, uint32_t count) {
+  if (!s || (count && !batches)) return PASTA_EINVAL;
+  if (s->closed) return PASTA_ESTATE;
+  for (uint32_t i = 0; i < count; ++i) {
+    const pasta_stream_batch& b = batches[i];
+    if (b.n > s->max_batch || (b.n & 1) || (b.n && (!b.addr || (reinterpret_cast<uintptr_t>(b.addr) & 15u))))
+      return PASTA_EINVAL;
+    if (b.kernel_offsets && b.n_kernels == 0) return PASTA_EINVAL;
+  }
+  DeviceGuard g(s->h->device);
+  uint64_t first = s->pushed;  // first batch not yet published
+  for (uint32_t i = 0; i < count; ++i) {
+    const uint64_t b = s->pushed;
+    const uint64_t quarter = std::max<uint64_t>(1, s->slots / 4);
+    if (b + 1 > s->seen + s->slots) {
+      // the ring slot still holds an unread batch: publish what is staged, then wait
+      // until a quarter of the ring (or what is left of this call) is free, so that each
+      // publication (three small copies) covers many batches
+      if (first < s->pushed) {
+        const int st = stream_publish(s, first);
+        if (st) return st;
+        first = s->pushed;
+      }
+      const uint64_t want = std::min<uint64_t>(quarter, count - i);
+      const auto t0 = std::chrono::steady_clock::now();
+      for (;;) {
+        const unsigned long long c = *reinterpret_cast<volatile unsigned long long*>(s->h_consumed);
+        if (c > s->seen) s->seen = c;  // GPU writes may land out of order: keep the max
+        if (b + want <= s->seen + s->slots) break;
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30)) return PASTA_ESTATE;
+      }
+    }
+    StreamDesc& d = s->h_ring[b % s->slots];
+    d.rec = batches[i].addr;
+    d.n = batches[i].n;
+    d.koffs = batches[i].kernel_offsets;
+    d.nk = batches[i].kernel_offsets ? batches[i].n_kernels : 1;
+    d.k0 = batches[i].kernel_row0;
+    s->pushed = b + 1;
+    // publish in runs of a quarter ring, so the consumer is fed while the host waits
+    if (s->pushed - first >= quarter) {
+      const int st = stream_publish(s, first);
+      if (st) return st;
+      first = s->pushed;
+    }
+  }
+  if (first < s->pushed) return stream_publish(s, first);
+  return PASTA_OK;
+}
+
+int pasta_stream_consumed(pasta_stream* s, uint64_t* out) {
+  if (!s || !out) return PASTA_EINVAL;
+  const unsigned long long c = *reinterpret_cast<volatile unsigned long long*>(s->h_consumed);
+  if (c > s->seen) s->seen = c;
+  *out = std::min<uint64_t>(s->seen, s->pushed);
+  return PASTA_OK;
+}
+
+int pasta_stream_close(pasta_stream* s) {
+  if (!s) return PASTA_EINVAL;
+  if (s->closed) return PASTA_OK;
+  DeviceGuard g(s->h->device);
+  s->closed = true;
+  s->h_vals[s->slots] = s->pushed;
+  return cuda_status(cudaMemcpyAsync(&s->d_ctl->end, s->h_vals + s->slots, 8, cudaMemcpyHostToDevice, s->cs));
+}
+
+int pasta_stream_destroy(pasta_stream* s) {
+  if (!s) return PASTA_OK;
+  DeviceGuard g(s->h->device);
+  int st = PASTA_OK;
+  if (!s->closed) st = pasta_stream_close(s);
+  if (cudaStreamSynchronize(s->h->stream) != cudaSuccess) st = PASTA_ECUDA;
+  if (s->d_prof) {
+    const char* path = getenv("PASTA_STREAM_PROF_OUT");
+    std::vector<unsigned long long> v(8ull * kStreamMaxCtas * 32);
+    cudaMemcpy(v.data(), s->d_prof, 8 * v.size(), cudaMemcpyDeviceToHost);
+    if (FILE* f = path ? fopen(path, "a") : nullptr) {
+      for (size_t i = 0; i + 7 < v.size(); i += 8)
+        if (v[i + 3])
+          fprintf(f, "%zu %llu %llu %llu %llu %llu %llu\n", i / 8, v[i], v[i + 1], v[i + 2], v[i + 3], v[i + 4],
+                  v[i + 5]);
+      fclose(f);
+    }
+    cudaFree(s->d_prof);
+  }
+  stream_free(s);
+  return st;
 }
 
 int pasta_peer_reduce_small(pasta_trace* h, const uint64_t* const* src, uint32_t g, uint64_t lo, uint64_t n,

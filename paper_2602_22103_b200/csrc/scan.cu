@@ -1144,8 +1144,20 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
 // host-mapped memory, so the host reuses a ring slot (and the batch's records) only
 // after every warp has read that batch.
 // ------------------------------------------------------------------------------------
-constexpr int kSlotInfoBytes = 48;  // per warp and ring stage: the slice in flight
-constexpr int kFrontBytes = kWarps * 8;
+constexpr int kSlotInfoBytes = 64;  // per warp and ring stage: the slice in flight
+constexpr int kStreamData = kWarps;  // data warps of the stream consumer; one more warp is the monitor
+constexpr int kStreamThreads = (kStreamData + 1) * 32;
+#ifndef PASTA_STREAM_CHUNK
+#define PASTA_STREAM_CHUNK 32  // consecutive slices of one batch per warp turn
+#endif
+constexpr uint32_t kStreamChunk = PASTA_STREAM_CHUNK;
+#ifndef PASTA_STREAM_PROF
+#define PASTA_STREAM_PROF 0  // per-warp clock64 counters (fill, TMA wait, total) into StreamArgs::prof
+#endif
+#ifndef PASTA_STREAM_MON_NS
+#define PASTA_STREAM_MON_NS 256  // the monitor warp's pause between progress reports
+#endif
+constexpr int kFrontBytes = ((kWarps + 1) * 8 + 15) / 16 * 16;  // data warps + monitor, 16-byte multiple
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -1159,92 +1171,192 @@ __device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsign
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-struct SlotInfo {   // 48 B in shared memory
-  uint64_t G;       // global slice index
+struct __align__(16) StreamTurn {  // lane 0's chunk state of one warp (shared memory)
+  uint64_t Q;          // the next chunk to start
+  uint64_t cb, cs, ce; // the current chunk: batch, slices [cs, ce)
+  const uint64_t* rec;
+  const uint64_t* koffs;
+  uint64_t n, kend, known_tail;
+  uint32_t nk, k0, kl, pad;
+};
+constexpr int kTurnBytes = kWarps * (int)sizeof(StreamTurn);
+
+struct __align__(16) SlotInfo {   // 64 B in shared memory
+  uint64_t G;       // global slice index b * spb + s
   const uint64_t* koffs;
   uint64_t n;       // records of the batch
   uint32_t nk, k0;
   uint32_t s, valid;
-  uint64_t pad;
+  uint32_t kl, pad; // batch-local kernel of the slice's first record
+  uint64_t kend;    // where that kernel ends (batch-relative), ~0 = never
+  uint64_t pad2;
 };
 
-// Lane 0 of warp 0: this CTA's progress to the producer. A batch is read when every
-// warp's lowest unread slice lies beyond it; each CTA adds one to the batch's arrival
-// counter when it is done with it, and the CTA that completes the count publishes
-// "batches < b + 1 are read" to the host (arrivals happen in batch order in every CTA,
-// so batches complete in order) and re-arms the counter for ring lap b + slots.
+// The monitor warp of each CTA (all 32 lanes): this CTA's progress to the producer. A
+// batch is read by the CTA once every data warp's lowest unread slice lies beyond it;
+// the CTA's count of read batches (only published ones: a warp's next slice may lie far
+// beyond them) goes to ctl->cta_done[cta]; the monitor of CTA 0 also folds every CTA's
+// count into the global minimum and writes it to the producer's host-mapped counter.
+// No per-batch atomics: one load per warp and per CTA per round.
 __device__ __forceinline__ void stream_report(const StreamArgs& ra, const volatile uint64_t* front,
-                                              unsigned long long& cta_last) {
-  uint64_t mn = ~0ull;
+                                              unsigned long long& cta_last, unsigned long long& glob_last) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint64_t mn = lane < (uint32_t)kWarps ? front[lane] : ~0ull;
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) mn = front[w] < mn ? front[w] : mn;
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t x = __shfl_xor_sync(kFull, mn, o);
+    mn = x < mn ? x : mn;
+  }
   unsigned long long done = mn == ~0ull ? ld_acquire_u64(&ra.ctl->end) : mn / ra.spb;
-  for (; cta_last < done; ++cta_last) {
-    unsigned* cnt = ra.arrivals + (cta_last % ra.slots);
-    if (atomicAdd(cnt, 1u) == gridDim.x - 1) {
-      *cnt = 0u;
-      __threadfence();
-      st_release_sys_u64(ra.consumed, cta_last + 1);
+  const unsigned long long tail = ld_acquire_u64(&ra.ctl->tail);
+  if (done > tail) done = tail;
+  if (done > cta_last) {
+    cta_last = done;
+    if (lane == 0) st_release_u64(&ra.ctl->cta_done[blockIdx.x], done);
+  }
+  if (blockIdx.x == 0) {
+    unsigned long long g = ~0ull;
+    for (uint32_t c = lane; c < gridDim.x; c += 32) {
+      const unsigned long long v = ld_acquire_u64(&ra.ctl->cta_done[c]);
+      g = v < g ? v : g;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(kFull, g, o);
+      g = x < g ? x : g;
+    }
+    if (g > glob_last) {
+      glob_last = g;
+      if (lane == 0) st_release_sys_u64(ra.consumed, g);
     }
   }
 }
 
 template <bool kBig, bool kRows, int kPages>
-__global__ void __launch_bounds__(kThreads, 1) stream_kernel(const __grid_constant__ StreamArgs ra, const int stages) {
+__global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_constant__ StreamArgs ra,
+                                                                     const int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   const ScanArgs& args = ra.s;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages));
   unsigned char* info_base = smem + ring_bytes(stages) + kBarBytes + kLaBytes;
   volatile uint64_t* front = reinterpret_cast<volatile uint64_t*>(info_base + kWarps * stages * kSlotInfoBytes);
-  uint64_t* sB = reinterpret_cast<uint64_t*>(info_base + kWarps * stages * kSlotInfoBytes + kFrontBytes);
+  StreamTurn* turns = reinterpret_cast<StreamTurn*>(info_base + kWarps * stages * kSlotInfoBytes + kFrontBytes);
+  uint64_t* sB = reinterpret_cast<uint64_t*>(info_base + kWarps * stages * kSlotInfoBytes + kFrontBytes + kTurnBytes);
   const uint32_t A = args.A;
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   SlotInfo* info = reinterpret_cast<SlotInfo*>(info_base) + warp * stages;
   const uint32_t ring_u32 = smem_u32(smem) + (uint32_t)(warp * stages) * kSliceBytes;
   const uint32_t bar_u32 = smem_u32(bars + warp * kMaxStages);
-  if (lane == 0) {
+  if (lane == 0 && warp < kStreamData) {
     for (int j = 0; j < stages; ++j) mbar_init(bars + warp * kMaxStages + j, 1);
     fence_mbar_init();
   }
   if (!kBig)
-    for (uint32_t i = threadIdx.x; i < 2 * A; i += kThreads) sB[i] = args.bounds[i];
-  const uint64_t W = (uint64_t)gridDim.x * kWarps;
-  uint64_t gnext = (uint64_t)blockIdx.x * kWarps + warp;  // next slice to look at (lane 0)
-  if (lane == 0) front[warp] = gnext;
+    for (uint32_t i = threadIdx.x; i < 2 * A; i += blockDim.x) sB[i] = args.bounds[i];
+  const uint64_t W = (uint64_t)gridDim.x * kStreamData;
+  const uint64_t gnext = (uint64_t)blockIdx.x * kStreamData + warp;  // the warp's first chunk
+  const uint64_t cpb = (ra.spb + kStreamChunk - 1) / kStreamChunk;  // chunks per batch slot
+  if (lane == 0)
+    front[warp] = warp < kStreamData ? (gnext / cpb) * ra.spb + (gnext % cpb) * kStreamChunk : ~0ull;
   __syncthreads();
+  if (warp == kStreamData) {
+    // the CTA's monitor warp (processes no slices): publishes the CTA's progress until
+    // every data warp has read its last slice (CTA 0's: until every CTA has), so the
+    // producer never waits on a warp that is busy reading records
+    unsigned long long cta_last = 0, glob_last = 0;
+    for (;;) {
+      stream_report(ra, front, cta_last, glob_last);
+      const unsigned long long end = ld_acquire_u64(&ra.ctl->end);
+      if (cta_last == end && (blockIdx.x != 0 || glob_last == end)) break;
+      __nanosleep(PASTA_STREAM_MON_NS);
+    }
+    return;
+  }
 
   const uint64_t pol = l2_evict_first_policy();
-  unsigned long long cta_last = 0;  // warp 0 lane 0: batches this CTA has reported read
-  // lane 0: the next non-empty published slice of this warp into ring slot `slot`
-  // (descriptor fields into the slot info, TMA issued); false when the stream has ended
-  auto issue = [&](uint32_t slot) -> bool {
-    for (;;) {
-      const uint64_t G = gnext, b = G / ra.spb, s = G % ra.spb;
-      while (ld_acquire_u64(&ra.ctl->tail) <= b) {
-        if (ld_acquire_u64(&ra.ctl->end) <= b) return false;
-        if (warp == 0) stream_report(ra, front, cta_last);
+  // lane 0: the warp's next non-empty slice into ring slot `slot`. Returns 1 when issued,
+  // 0 when its batch is not published yet (only if !block; with block it waits, reporting
+  // progress meanwhile if this is warp 0), 2 when the stream has ended before it.
+  // Warp turns: chunk Q = gw, gw + W, ... of the global chunk sequence (batch Q / cpb,
+  // slices [C (Q % cpb), C (Q % cpb + 1)) of it), so a warp reads one descriptor and
+  // locates one kernel segment per C consecutive slices, and the W warps together cover
+  // W / cpb batches at a time.
+  // lane 0's turn state lives in shared memory (registers are at the 80-per-thread limit)
+  StreamTurn& t = turns[warp];
+  if (lane == 0) {
+    t.Q = gnext;
+    t.cb = t.cs = t.ce = 0;
+    t.known_tail = 0;
+  }
+  // the lowest slice this warp has not issued yet (lane 0)
+  auto next_G = [&]() -> uint64_t {
+    return t.cs < t.ce ? t.cb * ra.spb + t.cs : (t.Q / cpb) * ra.spb + (t.Q % cpb) * kStreamChunk;
+  };
+  // lane 0: the warp's next slice into ring slot `slot`. Returns 1 when issued, 0 when its
+  // batch is not published yet (only if !block; with block it waits, reporting progress
+  // meanwhile if this is warp 0), 2 when the stream has ended before it.
+#if PASTA_STREAM_PROF
+  unsigned long long p_fill = 0, p_wait = 0, p_n = 0, p_t0 = clock64(), p_turns = 0, p_sleeps = 0;
+#endif
+  auto issue = [&](uint32_t slot, bool block) -> int {
+    while (t.cs == t.ce) {
+      const uint64_t b = t.Q / cpb, c0 = (t.Q % cpb) * kStreamChunk;
+      while (t.known_tail <= b) {
+        t.known_tail = ld_acquire_u64(&ra.ctl->tail);  // orders the descriptor loads below
+        if (t.known_tail > b) break;
+        if (ld_acquire_u64(&ra.ctl->end) <= b) return 2;
+        if (!block) return 0;
+        front[warp] = b * ra.spb + c0;  // nothing in flight: the warp's lowest unread slice
         __nanosleep(200);
+#if PASTA_STREAM_PROF
+        ++p_sleeps;
+#endif
       }
-      const StreamDesc* d = ra.ring + (b % ra.slots);
-      const uint64_t n = __ldcg(reinterpret_cast<const unsigned long long*>(&d->n));
-      gnext = G + W;
-      if (s * kSlice >= n) continue;  // past the end of a short batch
-      const uint64_t* rec = reinterpret_cast<const uint64_t*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d->rec)));
-      SlotInfo& si = info[slot];
-      si.G = G;
-      si.koffs = reinterpret_cast<const uint64_t*>(__ldcg(reinterpret_cast<const unsigned long long*>(&d->koffs)));
-      si.n = n;
-      const uint2 nkk = __ldcg(reinterpret_cast<const uint2*>(&d->nk));
-      si.nk = nkk.x;
-      si.k0 = nkk.y;
-      si.s = (uint32_t)s;
-      const uint64_t left = n - s * kSlice;
-      si.valid = left < (uint64_t)kSlice ? (uint32_t)left : (uint32_t)kSlice;
-      mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, si.valid * 8u);
-      tma_load_1d_u32(ring_u32 + slot * kSliceBytes, rec + s * kSlice, si.valid * 8u, bar_u32 + 8u * slot, pol);
-      return true;
+#if PASTA_STREAM_PROF
+      ++p_turns;
+#endif
+      // the 32-byte descriptor in two independent 16-byte loads (L2: written by copies)
+      const ulonglong2* d = reinterpret_cast<const ulonglong2*>(ra.ring + (b % ra.slots));
+      const ulonglong2 d0 = __ldcg(d), d1 = __ldcg(d + 1);
+      t.Q += W;
+      const uint64_t nsl = (d0.y + kSlice - 1) / kSlice;
+      if (c0 >= nsl) continue;  // past the end of a short batch
+      t.cb = b;
+      t.cs = c0;
+      t.ce = c0 + kStreamChunk < nsl ? c0 + kStreamChunk : nsl;
+      t.rec = reinterpret_cast<const uint64_t*>(d0.x);
+      t.n = d0.y;
+      t.koffs = reinterpret_cast<const uint64_t*>(d1.x);
+      t.nk = (uint32_t)d1.y;
+      t.k0 = (uint32_t)(d1.y >> 32);
+      t.kl = 0;
+      t.kend = ~0ull;
+      if (kRows && t.koffs != nullptr && t.nk > 1) {
+        t.kl = kernel_of(t.koffs, t.nk, t.cs * kSlice);
+        t.kend = t.kl + 1 < t.nk ? __ldg(t.koffs + t.kl + 1) : ~0ull;
+      }
     }
+    const uint64_t s = t.cs++;
+    const uint64_t r_lo = s * kSlice;
+    while (kRows && t.kend <= r_lo) {  // a kernel boundary since the last slice (rare)
+      ++t.kl;
+      t.kend = t.kl + 1 < t.nk ? __ldg(t.koffs + t.kl + 1) : ~0ull;
+    }
+    SlotInfo& si = info[slot];
+    si.G = t.cb * ra.spb + s;
+    si.koffs = t.koffs;
+    si.n = t.n;
+    si.nk = t.nk;
+    si.k0 = t.k0;
+    si.s = (uint32_t)s;
+    const uint64_t left = t.n - r_lo;
+    si.valid = left < (uint64_t)kSlice ? (uint32_t)left : (uint32_t)kSlice;
+    si.kl = t.kl;
+    si.kend = t.kend;
+    mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, si.valid * 8u);
+    tma_load_1d_u32(ring_u32 + slot * kSliceBytes, t.rec + r_lo, si.valid * 8u, bar_u32 + 8u * slot, pol);
+    return 1;
   };
 
   Ctx c;
@@ -1291,19 +1403,44 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const __grid_consta
   la.kbit = kOOW;
   uint32_t k = 0xFFFFFFFFu;  // kernel row of the warp's accumulators (none yet)
 
-  // prime the ring
-  uint32_t issued = 0;
-  if (lane == 0) {
-    while (issued < (uint32_t)stages && issue(issued)) ++issued;
-  }
-  issued = __shfl_sync(kFull, issued, 0);
-  __syncwarp();
-  bool more = issued == (uint32_t)stages;  // (lane 0's view; broadcast below)
-  uint32_t slot = 0, phase = 0;
-  for (uint32_t j = 0; j < issued; ++j) {
-    const SlotInfo si = info[slot];  // written by lane 0 before the __syncwarp that ended its issue
-    if (lane == 0) front[warp] = si.G;
-    mbar_wait_u32(bar_u32 + 8u * slot, phase);
+  // The warp's slots form a FIFO (filled at `tail`, consumed at `head`): it fills every
+  // free slot whose batch is published without waiting, and waits for a publication only
+  // when nothing is in flight -- a warp must never sit on a loaded slice while it waits
+  // for a later batch (the producer may be waiting for that slice to be read).
+  uint32_t head = 0, tail_slot = 0, inflight = 0, phases = 0;  // phases: bit i = parity of slot i
+  bool ended = false;
+
+  for (;;) {
+    int r = 1;
+#if PASTA_STREAM_PROF
+    const unsigned long long q0 = clock64();
+#endif
+    if (lane == 0) {
+      while (!ended && inflight < (uint32_t)stages) {
+        r = issue(tail_slot, inflight == 0);
+        if (r != 1) break;
+        tail_slot = tail_slot + 1 == (uint32_t)stages ? 0 : tail_slot + 1;
+        ++inflight;
+      }
+      if (r == 2) ended = true;
+      front[warp] = inflight ? info[head].G : (ended ? ~0ull : next_G());
+    }
+    inflight = __shfl_sync(kFull, inflight, 0);
+    __syncwarp();
+    if (inflight == 0) break;  // the stream ended and everything this warp took is done
+    const uint32_t slot = head;
+    const SlotInfo si = info[slot];  // written by lane 0 before the __syncwarp above
+#if PASTA_STREAM_PROF
+    const unsigned long long q1 = clock64();
+#endif
+    mbar_wait_u32(bar_u32 + 8u * slot, (phases >> slot) & 1u);
+    phases ^= 1u << slot;
+#if PASTA_STREAM_PROF
+    const unsigned long long q2 = clock64();
+    p_fill += q1 - q0;
+    p_wait += q2 - q1;
+    ++p_n;
+#endif
     uint64_t a[8];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -1312,14 +1449,11 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const __grid_consta
       a[2 * i + 1] = v.y;
     }
     if (si.s == 0 && lane == 0) red_add_u64(args.totals + 0, si.n);
-    // kernel segments of this slice (batch-relative record index r = 256 s + position)
+    // kernel segments of this slice (batch-relative record index r = 256 s + position);
+    // the slice's first kernel was located when it was issued
     const uint64_t r_lo = (uint64_t)si.s * kSlice;
-    uint32_t kl = 0;
-    uint64_t kend = ~0ull;
-    if (kRows && si.koffs != nullptr && si.nk > 1) {
-      kl = kernel_of(si.koffs, si.nk, r_lo);
-      kend = kl + 1 < si.nk ? __ldg(si.koffs + kl + 1) : ~0ull;
-    }
+    uint32_t kl = si.kl;
+    uint64_t kend = si.kend;
     if (kRows && si.k0 + kl != k) {
       if (k != 0xFFFFFFFFu) warp_flush<kRows, kPages>(w, la, o, k, lane);
       k = si.k0 + kl;
@@ -1350,41 +1484,30 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const __grid_consta
       }
     }
     __syncwarp();
-    // lowest unread slice: the next one in flight, else the one the refill looks for
-    if (lane == 0) front[warp] = issued > j + 1 ? info[slot + 1 == (uint32_t)stages ? 0 : slot + 1].G : gnext;
-    // refill this ring slot with the warp's next slice
-    uint32_t got = 0;
-    if (lane == 0 && more) got = issue(slot) ? 1u : 0u;
-    got = __shfl_sync(kFull, got, 0);
-    more = got != 0;
-    if (got) ++issued;
-    __syncwarp();
-    if (++slot == (uint32_t)stages) {
-      slot = 0;
-      phase ^= 1u;
-    }
-    if (warp == 0 && lane == 0) stream_report(ra, front, cta_last);
+    head = head + 1 == (uint32_t)stages ? 0 : head + 1;
+    --inflight;
   }
   if (k != 0xFFFFFFFFu || !kRows) warp_flush<kRows, kPages>(w, la, o, kRows ? k : 0u, lane);
   if (lane == 0) front[warp] = ~0ull;
-  __syncwarp();
-  if (warp == 0 && lane == 0) {
-    // keep reporting until every warp of this CTA has read its last slice (then every
-    // batch up to the end is reported)
-    for (;;) {
-      stream_report(ra, front, cta_last);
-      if (cta_last == ld_acquire_u64(&ra.ctl->end)) break;
-      __nanosleep(500);
-    }
+#if PASTA_STREAM_PROF
+  if (lane == 0 && ra.prof) {
+    unsigned long long* pr = ra.prof + 8ull * (blockIdx.x * kStreamData + warp);
+    pr[0] = p_fill;
+    pr[1] = p_wait;
+    pr[2] = clock64() - p_t0;
+    pr[3] = p_n;
+    pr[4] = p_turns;
+    pr[5] = p_sleeps;
   }
+#endif
 }
 
 int stream_smem_bytes(uint32_t A, bool big, int* stages_out) {
-  const long extra = (long)kWarps * kMaxStages * kSlotInfoBytes + kFrontBytes - kPfBytes;
+  const long extra = (long)kWarps * kMaxStages * kSlotInfoBytes + kFrontBytes + kTurnBytes - kPfBytes;
   int st = stages_for(A, big, extra);
   if (st > 4) st = 4;
   *stages_out = st;
-  return ring_bytes(st) + kBarBytes + kLaBytes + kWarps * st * kSlotInfoBytes + kFrontBytes +
+  return ring_bytes(st) + kBarBytes + kLaBytes + kWarps * st * kSlotInfoBytes + kFrontBytes + kTurnBytes +
          (big ? 0 : (int)(16ull * A));
 }
 
@@ -1398,14 +1521,14 @@ cudaError_t launch_stream_variant(const StreamArgs& a, cudaStream_t st, int* cta
   int dev = 0, sms = 0, nb = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kStreamThreads, smem);
   if (e != cudaSuccess) return e;
   int grid = sms * (nb < 1 ? 1 : (nb > 1 ? 1 : nb));
   if (grid > kStreamMaxCtas) grid = kStreamMaxCtas;
   *ctas = grid;
   void* args[] = {(void*)&a, (void*)&stages};
   // cooperative: every CTA is resident (a CTA that never ran could never report progress)
-  return cudaLaunchCooperativeKernel((void*)fn, dim3(grid), dim3(kThreads), args, smem, st);
+  return cudaLaunchCooperativeKernel((void*)fn, dim3(grid), dim3(kStreamThreads), args, smem, st);
 }
 
 

@@ -393,7 +393,8 @@ __device__ __forceinline__ u128 ld_key(const u128* p) {
 // Bitonic steps on n keys of a shared tile whose first key has global index gbase, for
 // sizes [size_lo, size_hi] and strides from min(size / 2, stride_cap) down to 1;
 // descending overall (pairs with (gbase + i) & size == 0 put the larger key first).
-__device__ void tile_bitonic(u128* t, uint32_t n, uint64_t gbase, uint64_t size_lo, uint64_t size_hi,
+template <typename T>
+__device__ void tile_bitonic(T* t, uint32_t n, uint64_t gbase, uint64_t size_lo, uint64_t size_hi,
                              uint64_t stride_cap) {
   for (uint64_t size = size_lo; size <= size_hi; size <<= 1) {
     uint64_t s0 = size >> 1;
@@ -403,7 +404,7 @@ __device__ void tile_bitonic(u128* t, uint32_t n, uint64_t gbase, uint64_t size_
         const uint32_t lo = q & (uint32_t)(stride - 1);
         const uint32_t i = ((q - lo) << 1) | lo, j = i | (uint32_t)stride;
         const bool desc = ((gbase + i) & size) == 0;
-        const u128 x = t[i], y = t[j];
+        const T x = t[i], y = t[j];
         if (desc ? x < y : x > y) {
           t[i] = y;
           t[j] = x;
@@ -417,6 +418,38 @@ __device__ void tile_bitonic(u128* t, uint32_t n, uint64_t gbase, uint64_t size_
 __device__ __forceinline__ void put_key(const TkArgs& a, uint64_t i, u128 k, uint64_t pmask) {
   a.out_count[i] = (uint64_t)(k >> a.pbits);
   a.out_page[i] = pmask - (uint64_t)(k & (u128)pmask);
+}
+
+// Block 0: sort tile[0, n2) (n2 a power of two <= kFastMax) descending and write the
+// first kprime keys to the outputs. When every key fits 64 bits (counts below
+// 2^(64 - pbits): every realistic trace) the keys are re-packed as u64 in the same
+// shared buffer first: half the shared-memory traffic and one compare per exchange.
+__device__ __noinline__ void block_sort_write(const TkArgs* a, u128* tile, uint32_t n2, uint64_t kprime,
+                                              uint64_t pmask) {
+  constexpr int kPer = kFastMax / kTB;
+  bool wide = false;
+  for (uint32_t i = threadIdx.x; i < n2; i += kTB) wide |= (uint64_t)(tile[i] >> 64) != 0;
+  if (__syncthreads_or(wide)) {
+    tile_bitonic(tile, n2, 0, 2, n2, n2);
+    for (uint32_t i = threadIdx.x; i < (uint32_t)kprime; i += kTB) put_key(*a, i, tile[i], pmask);
+    return;
+  }
+  uint64_t v[kPer];
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    const uint32_t i = threadIdx.x + (uint32_t)e * kTB;
+    v[e] = i < n2 ? (uint64_t)tile[i] : 0;
+  }
+  __syncthreads();
+  uint64_t* t64 = reinterpret_cast<uint64_t*>(tile);
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    const uint32_t i = threadIdx.x + (uint32_t)e * kTB;
+    if (i < n2) t64[i] = v[e];
+  }
+  __syncthreads();
+  tile_bitonic(t64, n2, 0, 2, n2, n2);
+  for (uint32_t i = threadIdx.x; i < (uint32_t)kprime; i += kTB) put_key(*a, i, (u128)t64[i], pmask);
 }
 
 __global__ void __launch_bounds__(kTB, 2) topk_kernel(const __grid_constant__ TkArgs a) {
@@ -480,8 +513,7 @@ __global__ void __launch_bounds__(kTB, 2) topk_kernel(const __grid_constant__ Tk
               for (uint32_t i = threadIdx.x; i < n2; i += kTB)
                 tile[i] = i < above ? ld_key(a.keys + i) : (i < n ? ld_key(a.compact + (i - above)) : (u128)0);
               __syncthreads();
-              tile_bitonic(tile, n2, 0, 2, n2, n2);
-              for (uint32_t i = threadIdx.x; i < (uint32_t)kprime; i += kTB) put_key(a, i, tile[i], pmask);
+              block_sort_write(&a, tile, n2, kprime, pmask);
             }
             fast = true;
             break;
@@ -514,8 +546,7 @@ __global__ void __launch_bounds__(kTB, 2) topk_kernel(const __grid_constant__ Tk
     if (blockIdx.x == 0) {
       for (uint32_t i = threadIdx.x; i < (uint32_t)kp2; i += kTB) tile[i] = i < kprime ? ld_key(a.keys + i) : (u128)0;
       __syncthreads();
-      tile_bitonic(tile, (uint32_t)kp2, 0, 2, kp2, kp2);
-      for (uint32_t i = threadIdx.x; i < (uint32_t)kprime; i += kTB) put_key(a, i, tile[i], pmask);
+      block_sort_write(&a, tile, (uint32_t)kp2, kprime, pmask);
     }
   } else {
     const uint64_t nthreads = (uint64_t)gridDim.x * kTB, tid = (uint64_t)blockIdx.x * kTB + threadIdx.x;

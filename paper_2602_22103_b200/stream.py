@@ -83,3 +83,55 @@ class BatchRunner:
         host synchronization). Nothing else may be enqueued on the trace's stream
         between the batches."""
         self._submit(self.tr.h, self.array, self.page_shift)
+
+
+class StreamRing:
+    """The same batches through ONE persistent consumer (pasta_stream_open / push /
+    close, include/pasta.h): the host publishes the batch descriptors of a resident trace
+    into a device ring of `slots` descriptors while the consumer runs; no launch per
+    batch. Outputs as BatchRunner (no finalize: call Trace.finalize after)."""
+
+    def __init__(self, trace, hist, records, kernel_offsets, n: int, batch: int, page_shift: int, slots: int = 64):
+        import torch
+
+        from . import pasta_stream_batch
+
+        if batch % 2 or n % 2:
+            raise ValueError("StreamRing: batches must hold an even number of records")
+        self.tr, self.hist, self.page_shift, self.slots, self.batch = trace, hist, page_shift, slots, batch
+        self.batches = plan_batches(kernel_offsets, n, batch)
+        flat = np.concatenate([s for _, _, _, s in self.batches])
+        self.offs = torch.from_numpy(flat).to(records.device)
+        arr = (pasta_stream_batch * len(self.batches))()
+        pos = 0
+        for i, (a, b, k0, sub) in enumerate(self.batches):
+            arr[i] = pasta_stream_batch(records.data_ptr() + 8 * a, b - a, self.offs.data_ptr() + 8 * pos,
+                                        len(sub) - 1, k0)
+            pos += len(sub)
+        self.array = arr
+        self.s = None
+
+    def start(self):
+        """Launch the consumer on the trace's stream (asynchronous)."""
+        from . import pasta_stream_open
+
+        self.s = pasta_stream_open(self.tr.h, self.page_shift, self.slots, self.batch, self.hist.struct())
+
+    def push_all(self):
+        """Publish every batch (the host waits whenever the ring is full), then the end."""
+        from . import pasta_stream_close, pasta_stream_push
+
+        pasta_stream_push(self.s, self.array)
+        pasta_stream_close(self.s)
+
+    def run(self):
+        self.start()
+        self.push_all()
+
+    def destroy(self):
+        """Wait for the consumer and free the ring."""
+        from . import pasta_stream_destroy
+
+        if self.s is not None:
+            pasta_stream_destroy(self.s)
+            self.s = None

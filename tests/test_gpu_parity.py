@@ -8,6 +8,7 @@ computes one by one, plus invariants that hold at any size.
 import json
 import os
 import random
+import time
 
 import numpy as np
 import pytest
@@ -611,6 +612,114 @@ def test_streaming_batches_equal_oracle(batch, stable):
     assert_parity(g, r, kernel_rows=True, kernel_pages=True, label=f"stream/{batch}")
     tr.close()
 
+
+
+@pytest.mark.parametrize("batch,slots,rows", [(4096, 2, True), (4096, 64, True), (65_536, 4, True), (10_002, 8, False)])
+def test_stream_ring_equals_oracle(batch, slots, rows):
+    """NEXT f2 persistent consumer: one launch, batch descriptors published into a ring of
+    `slots` while it runs (slots = 2: the host waits for the consumer after every other
+    batch), kernels cut between batches accumulating into one row, then one finalize ==
+    the oracle on every output."""
+    from paper_2602_22103_b200.stream import StreamRing
+
+    p = tracegen.build_plan("tiny", seed=22)
+    drec = torch.empty(p.n, dtype=torch.int64, device=DEV)
+    tracegen.device_records(tracegen.DevicePlan(p, DEV), drec)
+    tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs)
+    hist = tr.histograms(p.page_shift, n_kernels=p.n_kernels, kernel_rows=rows, kernel_pages=rows)
+    ring = StreamRing(tr, hist, drec, p.kernel_offsets, p.n, batch, p.page_shift, slots=slots)
+    try:
+        ring.run()
+    finally:
+        ring.destroy()  # publishes the end even on failure (the consumer always drains)
+    tr.finalize(p.page_shift, hist, n_kernels=p.n_kernels if rows else 0)
+    tr.sync()
+    o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
+    ko = [int(x) for x in p.kernel_offsets]
+    r = run_oracle(o, tracegen.host_records(p), p.page_shift, ko, kernel_rows=rows, kernel_pages=rows)
+    g = {"page_counts": u64(hist.page_counts), "alloc_counts": u64(hist.alloc_counts), "totals": u64(hist.totals),
+         "bitmap": u64(hist.page_bitmap), "topk": {}}
+    if rows:
+        g.update({"kac": u64(hist.kernel_alloc_counts).reshape(p.n_kernels, -1),
+                  "kstats": u64(hist.kernel_stats).reshape(p.n_kernels, 4),
+                  "kpb": u64(hist.kernel_page_bitmap).reshape(p.n_kernels, -1)})
+    assert_parity(g, r, kernel_rows=rows, kernel_pages=rows, label=f"ring/{batch}/{slots}")
+    tr.close()
+
+
+def test_stream_ring_reuses_producer_buffers():
+    """The paper's device buffer: the producer owns R = 3 record buffers of
+    one batch each and refills buffer i % R only after pasta_stream_consumed says batch
+    i - R has been read; the consumer's result equals the oracle over the whole trace."""
+    import paper_2602_22103_b200 as pbm
+
+    p = tracegen.build_plan("tiny", seed=23)
+    host = tracegen.host_records(p)
+    batch, R = 32_768, 3
+    bufs = [torch.empty(batch, dtype=torch.int64, device=DEV) for _ in range(R)]
+    # the trace gets its own stream: the producer's copies must not queue behind the
+    # persistent consumer (a synchronous copy on torch's default stream would)
+    tr = pb.Trace(DEV, p.va_lo, p.va_hi, len(p.allocs), len(p.allocs), stream=torch.cuda.Stream(DEV))
+    for b, sz in p.allocs:
+        tr.register_alloc(b, sz)
+    hist = tr.histograms(p.page_shift)
+    torch.cuda.synchronize()
+    s = pbm.pasta_stream_open(tr.h, p.page_shift, R, batch, hist.struct())
+    side = torch.cuda.Stream(DEV)
+    nb = p.n // batch
+    try:
+        for i in range(nb):
+            t0 = time.time()
+            while pbm.pasta_stream_consumed(s) < i - R + 1:
+                assert time.time() - t0 < 30, "consumer made no progress"
+            buf = bufs[i % R]
+            with torch.cuda.stream(side):
+                buf.copy_(torch.from_numpy(host[i * batch:(i + 1) * batch].view(np.int64)), non_blocking=False)
+            side.synchronize()
+            pbm.pasta_stream_push(s, [pbm.pasta_stream_batch(buf.data_ptr(), batch, None, 1, 0)])
+    finally:
+        pbm.pasta_stream_close(s)
+        pbm.pasta_stream_destroy(s)
+    tr.finalize(p.page_shift, hist)
+    tr.sync()
+    o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
+    r = run_oracle(o, host[:nb * batch], p.page_shift, None, kernel_rows=False, kernel_pages=False)
+    assert np.array_equal(u64(hist.page_counts), r["page_counts"])
+    assert np.array_equal(u64(hist.alloc_counts), r["alloc_counts"])
+    assert u64(hist.totals)[:3].tolist() == r["totals3"].tolist()
+    tr.close()
+
+
+def test_stream_ring_errors():
+    import paper_2602_22103_b200 as pbm
+
+    tr = pb.Trace(DEV, 0, 1 << 32, 4, 4)
+    tr.register_alloc(4096, 4096)
+    hist = tr.histograms(12)
+    for slots, mb in ((1, 1024), (8, 255), (8, 1025)):
+        with pytest.raises(pb.PastaError) as ei:
+            pbm.pasta_stream_open(tr.h, 12, slots, mb, hist.struct())
+        assert ei.value.status == pb.PASTA_EINVAL
+    rec = torch.full((2048,), 4096 + 8, dtype=torch.int64, device=DEV)
+    torch.cuda.synchronize()
+    # (nothing may be enqueued on the trace's stream -- here torch's default stream --
+    # while the consumer runs)
+    s = pbm.pasta_stream_open(tr.h, 12, 4, 1024, hist.struct())
+    for bad in (pbm.pasta_stream_batch(rec.data_ptr(), 2048, None, 1, 0),  # > max_batch
+                pbm.pasta_stream_batch(rec.data_ptr(), 3, None, 1, 0),  # odd
+                pbm.pasta_stream_batch(rec.data_ptr() + 8, 2, None, 1, 0)):  # not 16-byte aligned
+        with pytest.raises(pb.PastaError) as ei:
+            pbm.pasta_stream_push(s, [bad])
+        assert ei.value.status == pb.PASTA_EINVAL
+    pbm.pasta_stream_push(s, [pbm.pasta_stream_batch(rec.data_ptr(), 1024, None, 1, 0)])
+    pbm.pasta_stream_close(s)
+    with pytest.raises(pb.PastaError) as ei:
+        pbm.pasta_stream_push(s, [pbm.pasta_stream_batch(rec.data_ptr(), 2, None, 1, 0)])
+    assert ei.value.status == pb.PASTA_ESTATE
+    pbm.pasta_stream_destroy(s)
+    tr.sync()
+    assert int(u64(hist.totals)[0]) == 1024 and int(u64(hist.alloc_counts)[0]) == 1024
+    tr.close()
 
 def test_pdl_ordering_after_producer_kernels():
     """Programmatic dependent launch must not read stale data: each analyze follows, on
