@@ -73,12 +73,15 @@ __global__ void __launch_bounds__(kBlock) footprint_kernel(const uint64_t* __res
   for (uint64_t k = gw; k < K; k += nw) {
     const uint64_t* row = kac + k * max_ids;
     uint64_t f = 0;
-    for (uint64_t i0 = lane; i0 < max_ids; i0 += 32 * 4) {
-      uint64_t v[4];
+    // 16 loads in flight per lane: a warp streams one row (max_ids x 8 B, up to 512 KB at
+    // 65,536 ids) and few rows run at once, so the memory parallelism must come from here
+    constexpr int kFU = 16;
+    for (uint64_t i0 = lane; i0 < max_ids; i0 += 32 * kFU) {
+      uint64_t v[kFU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = i0 + 32 * u < max_ids ? __ldg(row + i0 + 32 * u) : 0;
+      for (int u = 0; u < kFU; ++u) v[u] = i0 + 32 * u < max_ids ? __ldg(row + i0 + 32 * u) : 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < kFU; ++u)
         if (v[u] != 0) f += __ldg(id_size + i0 + 32 * u);
     }
     f = warp_sum_u64(f);

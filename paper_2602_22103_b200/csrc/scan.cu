@@ -11,7 +11,7 @@
 //    slices (256 records) and every warp owns a contiguous run of slices; each warp
 //    runs its own TMA pipeline: lane 0 keeps S-1 slices in flight with 1-D bulk
 //    copies (cp.async.bulk + mbarrier complete_tx, L2 evict_first) into the warp's
-//    S-slot shared-memory ring (S = 6 or 7 by the table size), so warps never wait
+//    S-slot shared-memory ring (S = 4, or 3 for 1,545-4,616 ranges), so warps never wait
 //    on each other;
 //  * a slice is read with four conflict-free LDS.128 per lane (lane l holds slice
 //    positions 64i + 2l + {0,1}, i = 0..3, in position order);
@@ -1547,6 +1547,9 @@ cudaError_t launch_stream_variant(const StreamArgs& a, cudaStream_t st, int* cta
 // classification. Records outside A and B go straight to L2.
 // ------------------------------------------------------------------------------------
 constexpr int kRSlice = 128;
+#ifndef PASTA_RICH_BRANCHLESS
+#define PASTA_RICH_BRANCHLESS 0  // tier RC per-record classification with selects (A/B: slower, DESIGN 3.5)
+#endif
 #ifndef PASTA_RICH_WARPS
 #define PASTA_RICH_WARPS 24  // warps per CTA of the rich scan (A/B: 12-24 warps, more is faster)
 #endif
@@ -1806,6 +1809,26 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
       if (!inside(b0, IA)) IB = lookup<kBig>(oc, b0, c);
       cur = IB;
       uint32_t hA = 0, hT = 0, hR = 0, rest = 0, mAB = 0;
+#if PASTA_RICH_BRANCHLESS
+      // branch-free classification (selects, no per-record reconvergence blocks)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t hi = (uint32_t)(m[i] >> 32);
+        const bool an = !(hi & 0x20000u);
+        const uint32_t h = an ? (hi & 0x1FFFFu) + (1u << 24) : 0u;
+        const bool inA = inside(a[i], IA);
+        const bool inB = inside(a[i], IB);
+        const bool rs = an & !inA & !inB;
+        hT += h;
+        hA += inA ? h : 0u;
+        hR += rs ? h : 0u;
+        rest |= (rs ? 1u : 0u) << i;
+        if (kTwo && kRows) {
+          const uint32_t mi = an ? (mis >> i) & 1u : 0u;
+          mAB += inA ? mi : ((inB ? mi : 0u) << 8);
+        }
+      }
+#else
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t hi = (uint32_t)(m[i] >> 32);
@@ -1823,6 +1846,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rich_kernel(const RichArgs args,
           }
         }
       }
+#endif
       const bool any_rest = __any_sync(kFull, rest != 0);
       hA = __reduce_add_sync(kFull, hA);
       hT = __reduce_add_sync(kFull, hT);
