@@ -60,44 +60,56 @@ __global__ void __launch_bounds__(kBlock) bitmap_kernel(const uint64_t* __restri
   }
 }
 
+// One CTA per kernel row (grid-stride over rows): every thread strides over the row with
+// 4 loads in flight, block reduction of the footprint and of the row's page-bitmap
+// popcount. (A warp per row starved at wide rows: 3,000 x 65,536 ids = 1.6 GB streamed
+// by 3,000 warps at ~2 TB/s.)
 __global__ void __launch_bounds__(kBlock) footprint_kernel(const uint64_t* __restrict__ kac, uint32_t K,
                                                            uint64_t max_ids, const uint64_t* __restrict__ id_size,
                                                            const uint64_t* __restrict__ kpb, uint32_t words,
                                                            uint64_t* __restrict__ fp_out, uint32_t fp_stride,
                                                            uint64_t* __restrict__ up_out, uint32_t up_stride,
                                                            uint64_t* __restrict__ ws_out) {
-  const unsigned lane = threadIdx.x & 31;
-  const uint64_t gw = ((uint64_t)blockIdx.x * kBlock + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * kBlock) >> 5;
+  __shared__ uint64_t part[2][kBlock / 32];
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint64_t wmax = 0;
-  for (uint64_t k = gw; k < K; k += nw) {
+  for (uint64_t k = blockIdx.x; k < K; k += gridDim.x) {
     const uint64_t* row = kac + k * max_ids;
     uint64_t f = 0;
-    // 16 loads in flight per lane: a warp streams one row (max_ids x 8 B, up to 512 KB at
-    // 65,536 ids) and few rows run at once, so the memory parallelism must come from here
-    constexpr int kFU = 16;
-    for (uint64_t i0 = lane; i0 < max_ids; i0 += 32 * kFU) {
+    constexpr int kFU = 4;
+    for (uint64_t i0 = threadIdx.x; i0 < max_ids; i0 += (uint64_t)kBlock * kFU) {
       uint64_t v[kFU];
 #pragma unroll
-      for (int u = 0; u < kFU; ++u) v[u] = i0 + 32 * u < max_ids ? __ldg(row + i0 + 32 * u) : 0;
+      for (int u = 0; u < kFU; ++u) v[u] = i0 + (uint64_t)kBlock * u < max_ids ? __ldg(row + i0 + kBlock * u) : 0;
 #pragma unroll
       for (int u = 0; u < kFU; ++u)
-        if (v[u] != 0) f += __ldg(id_size + i0 + 32 * u);
+        if (v[u] != 0) f += __ldg(id_size + i0 + kBlock * u);
     }
-    f = warp_sum_u64(f);
     uint64_t up = 0;
     if (kpb) {
       const uint64_t* brow = kpb + k * words;
-      for (uint64_t w = lane; w < words; w += 32) up += __popcll(__ldg(brow + w));
-      up = warp_sum_u64(up);
+      for (uint64_t w = threadIdx.x; w < words; w += kBlock) up += __popcll(__ldg(brow + w));
     }
+    f = warp_sum_u64(f);
+    up = warp_sum_u64(up);
     if (lane == 0) {
-      fp_out[k * fp_stride] = f;
-      if (up_out) up_out[k * up_stride] = up;
+      part[0][wib] = f;
+      part[1][wib] = up;
     }
-    wmax = f > wmax ? f : wmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t F = 0, U = 0;
+      for (int i = 0; i < kBlock / 32; ++i) {
+        F += part[0][i];
+        U += part[1][i];
+      }
+      fp_out[k * fp_stride] = F;
+      if (up_out) up_out[k * up_stride] = U;
+      wmax = F > wmax ? F : wmax;
+    }
+    __syncthreads();
   }
-  if (lane == 0 && wmax) atomic_max_u64(ws_out, wmax);
+  if (threadIdx.x == 0 && wmax) atomic_max_u64(ws_out, wmax);
 }
 
 __global__ void __launch_bounds__(kBlock) bitmap_or_kernel(const uint64_t* gathered, uint32_t g,
@@ -198,7 +210,7 @@ cudaError_t launch_footprint(const uint64_t* kac, uint32_t n_kernels, uint64_t m
                              uint64_t* up_out, uint32_t up_stride, uint64_t* ws_out, int grid, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(ws_out, 0, sizeof(uint64_t), st);
   if (e != cudaSuccess) return e;
-  footprint_kernel<<<grid_for(n_kernels, kBlock / 32, grid), kBlock, 0, st>>>(
+  footprint_kernel<<<grid_for(n_kernels, 1, grid), kBlock, 0, st>>>(
       kac, n_kernels, max_ids, id_size, kpb, words, fp_out, fp_stride, up_out, up_stride, ws_out);
   return cudaGetLastError();
 }

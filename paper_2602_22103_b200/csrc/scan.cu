@@ -89,6 +89,9 @@ constexpr int kSlice = 256;                 // records per slice (8 per lane)
 #ifndef PASTA_TIER_S
 #define PASTA_TIER_S 1  // tier S (one owner, scattered pages) before tier L
 #endif
+#ifndef PASTA_ISSUE2
+#define PASTA_ISSUE2 0  // TMA refills in pairs
+#endif
 #ifndef PASTA_TIER_S_BATCH
 #define PASTA_TIER_S_BATCH 1  // tier S (kPages == 0): page REDs issued back to back
 #endif
@@ -1005,7 +1008,18 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
     // the slot is free again (every lane has consumed its values): refill it with the
     // slice `stages` ahead
     __syncwarp();
+#if PASTA_ISSUE2
+    // refills in pairs (every odd slice, this slot and the previous one): the issue path
+    // recomputes its shared-memory and source addresses (register pressure), and two
+    // issues share that work
+    if (lane == 0 && (j & 1u)) {
+      const uint32_t prev = slot == 0 ? (uint32_t)stages - 1u : slot - 1u;
+      if (j - 1 + stages < nmy) issue(j - 1 + stages, prev);
+      if (j + stages < nmy) issue(j + stages, slot);
+    }
+#else
     if (lane == 0 && j + stages < nmy) issue(j + stages, slot);
+#endif
     if (++slot == (uint32_t)stages) {
       slot = 0;
       phase ^= 1u;
