@@ -798,6 +798,8 @@ struct pasta_stream {
   bool closed = false;
   int ctas = 0;
   unsigned long long* d_prof = nullptr;  // PASTA_STREAM_PROF_OUT: per-warp counters
+  StreamArgs args{};                     // the consumer's arguments (deferred launch)
+  bool deferred = false;                 // PASTA_STREAM_DEFER_LAUNCH profiling hook
 };
 
 namespace {
@@ -903,7 +905,12 @@ int pasta_stream_open(pasta_trace* h, const pasta_stream_params* p, const pasta_
       a.prof = s->d_prof;
     }
   }
-  {
+  // Profiling hook (PASTA_STREAM_DEFER_LAUNCH set): launch the consumer only at close,
+  // after every batch is published (needs slots >= batches), so that a replaying profiler
+  // (ncu) sees a kernel whose inputs are all in device memory at launch.
+  s->args = a;
+  s->deferred = getenv("PASTA_STREAM_DEFER_LAUNCH") != nullptr;
+  if (!s->deferred) {
     Timed t(h, PASTA_PH_SCAN, h->stream);
     const cudaError_t e = launch_stream_consumer(a, h->stream, &s->ctas);
     ++h->launches;
@@ -981,7 +988,18 @@ int pasta_stream_close(pasta_stream* s) {
   DeviceGuard g(s->h->device);
   s->closed = true;
   s->h_vals[s->slots] = s->pushed;
-  return cuda_status(cudaMemcpyAsync(&s->d_ctl->end, s->h_vals + s->slots, 8, cudaMemcpyHostToDevice, s->cs));
+  cudaError_t e = cudaMemcpyAsync(&s->d_ctl->end, s->h_vals + s->slots, 8, cudaMemcpyHostToDevice, s->cs);
+  if (e == cudaSuccess && s->deferred) {  // profiling hook: everything is published now
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+      cudaEventRecord(ev, s->cs);
+      cudaStreamWaitEvent(s->h->stream, ev, 0);
+      cudaEventDestroy(ev);
+    }
+    e = launch_stream_consumer(s->args, s->h->stream, &s->ctas);
+    ++s->h->launches;
+  }
+  return cuda_status(e);
 }
 
 int pasta_stream_destroy(pasta_stream* s) {

@@ -760,3 +760,47 @@ def test_pdl_ordering_after_producer_kernels():
     with np.errstate(over="ignore"):
         assert np.array_equal(u64(got), refs[1] * np.uint64(4))
     tr.close()
+
+
+def test_arbitrary_cut_merge_then_finalize():
+    """Shards cut INSIDE kernels (not kernel-aligned): the straddling kernels' rows are
+    summed (what dist.merge_kernel_rows does across ranks), and pasta_finalize on the
+    merged rows recomputes every per-kernel footprint, WS_obj, the unique pages and the
+    MAX_MEM_REFERENCED_KERNEL pair exactly as the whole-trace oracle (WS does not merge
+    by MAX for such cuts)."""
+    p = tracegen.build_plan("tiny", seed=31)
+    drec = torch.empty(p.n, dtype=torch.int64, device=DEV)
+    tracegen.device_records(tracegen.DevicePlan(p, DEV), drec)
+    ko = np.asarray(p.kernel_offsets, dtype=np.int64)
+    cuts = [0, int(ko[3]) + 1001, int(ko[6]) - 77, p.n]  # inside kernels 3 and 5
+    tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs)
+    K = p.n_kernels
+    merged = tr.histograms(p.page_shift, n_kernels=K, kernel_rows=True, kernel_pages=True)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        k0 = int(np.searchsorted(ko, a, side="right")) - 1
+        k1 = int(np.searchsorted(ko, b, side="left"))
+        sub = np.concatenate([[0], np.clip(ko[k0 + 1:k1] - a, 0, b - a), [b - a]]).astype(np.int64)
+        h = tr.histograms(p.page_shift, n_kernels=len(sub) - 1, kernel_rows=True, kernel_pages=True)
+        tr.analyze(drec[a:b], p.page_shift, h, kernel_offsets=torch.from_numpy(sub).to(DEV), n=b - a)
+        tr.sync()
+        # merge: counts and rows SUM, per-kernel page bits OR (rows of the shard start at k0)
+        nk = len(sub) - 1
+        merged.page_counts += h.page_counts
+        merged.alloc_counts += h.alloc_counts
+        merged.totals[:3] += h.totals[:3]
+        merged.kernel_alloc_counts.view(K, -1)[k0:k0 + nk] += h.kernel_alloc_counts.view(nk, -1)
+        ks = merged.kernel_stats.view(K, 4)
+        ks[k0:k0 + nk, :2] += h.kernel_stats.view(nk, 4)[:, :2]
+        kp = merged.kernel_page_bitmap.view(K, -1)
+        kp[k0:k0 + nk] |= h.kernel_page_bitmap.view(nk, -1)
+    tr.finalize(p.page_shift, merged, n_kernels=K)
+    tr.sync()
+    o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
+    r = run_oracle(o, tracegen.host_records(p), p.page_shift, [int(x) for x in ko], kernel_rows=True,
+                   kernel_pages=True)
+    g = {"page_counts": u64(merged.page_counts), "alloc_counts": u64(merged.alloc_counts),
+         "totals": u64(merged.totals), "bitmap": u64(merged.page_bitmap),
+         "kac": u64(merged.kernel_alloc_counts).reshape(K, -1), "kstats": u64(merged.kernel_stats).reshape(K, 4),
+         "kpb": u64(merged.kernel_page_bitmap).reshape(K, -1), "topk": {}}
+    assert_parity(g, r, kernel_rows=True, kernel_pages=True, label="arbitrary cuts + finalize")
+    tr.close()
