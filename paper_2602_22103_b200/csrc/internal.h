@@ -66,6 +66,7 @@ struct StreamArgs {
   uint32_t slots;
   StreamCtl* ctl;
   uint64_t spb;                 // slices (256 records) per batch slot
+  uint64_t cpb;                 // chunks (warp turns) per batch slot, set by the launcher
   unsigned long long* consumed; // host-mapped: batches every CTA has read (flow control)
   unsigned long long* prof;     // PASTA_STREAM_PROF builds: [ctas x warps x 5] counters, else unused
 };

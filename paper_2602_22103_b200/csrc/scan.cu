@@ -92,6 +92,9 @@ constexpr int kSlice = 256;                 // records per slice (8 per lane)
 #ifndef PASTA_ISSUE2
 #define PASTA_ISSUE2 0  // TMA refills in pairs
 #endif
+#ifndef PASTA_FIXED_STAGES
+#define PASTA_FIXED_STAGES 0  // experiment: compile-time ring depth (the launch must pick the same)
+#endif
 #ifndef PASTA_TIER_S_BATCH
 #define PASTA_TIER_S_BATCH 1  // tier S (kPages == 0): page REDs issued back to back
 #endif
@@ -746,7 +749,14 @@ __device__ __forceinline__ uint32_t kernel_of(const uint64_t* __restrict__ koffs
 }
 
 template <bool kBig, bool kRows, int kPages, bool kIL>
-__global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages, const int cache_on) {
+__global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages_rt, const int cache_on) {
+#if PASTA_FIXED_STAGES
+  // experiment: the ring depth as a compile-time constant (constant shared offsets)
+  constexpr int stages = PASTA_FIXED_STAGES;
+  (void)stages_rt;
+#else
+  const int stages = stages_rt;
+#endif
   // Programmatic dependent launch: the next analyze call's scan may start its prologue
   // (barrier init, range table into shared memory) on free SMs while this one runs. A
   // chained scan (early == 2) triggers at entry: its predecessor is a scan that already
@@ -1169,7 +1179,7 @@ constexpr uint32_t kStreamChunk = PASTA_STREAM_CHUNK;
 #define PASTA_STREAM_PROF 0  // per-warp clock64 counters (fill, TMA wait, total) into StreamArgs::prof
 #endif
 #ifndef PASTA_STREAM_MON_NS
-#define PASTA_STREAM_MON_NS 256  // the monitor warp's pause between progress reports
+#define PASTA_STREAM_MON_NS 1000  // the monitor warp's pause between progress reports
 #endif
 constexpr int kFrontBytes = ((kWarps + 1) * 8 + 15) / 16 * 16;  // data warps + monitor, 16-byte multiple
 
@@ -1187,13 +1197,15 @@ __device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsign
 
 struct __align__(16) StreamTurn {  // lane 0's chunk state of one warp (shared memory)
   uint64_t Q;          // the next chunk to start
-  uint64_t cb, cs, ce; // the current chunk: batch, slices [cs, ce)
+  uint64_t cb, cs, ce; // the current chunk: batch (as its first global slice cb * spb), slices [cs, ce)
   const uint64_t* rec;
   const uint64_t* koffs;
   uint64_t n, kend, known_tail;
   uint32_t nk, k0, kl, pad;
 };
 constexpr int kTurnBytes = kWarps * (int)sizeof(StreamTurn);
+constexpr int kStreamHead = kWarps * kMaxStages * kSlotInfoBytes + kFrontBytes + kTurnBytes;  // see stream_kernel
+static_assert(kStreamHead % 16 == 0, "the ring after the head stays 16-byte aligned");
 
 struct __align__(16) SlotInfo {   // 64 B in shared memory
   uint64_t G;       // global slice index b * spb + s
@@ -1251,16 +1263,18 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
                                                                      const int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   const ScanArgs& args = ra.s;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(stages));
-  unsigned char* info_base = smem + ring_bytes(stages) + kBarBytes + kLaBytes;
-  volatile uint64_t* front = reinterpret_cast<volatile uint64_t*>(info_base + kWarps * stages * kSlotInfoBytes);
-  StreamTurn* turns = reinterpret_cast<StreamTurn*>(info_base + kWarps * stages * kSlotInfoBytes + kFrontBytes);
-  uint64_t* sB = reinterpret_cast<uint64_t*>(info_base + kWarps * stages * kSlotInfoBytes + kFrontBytes + kTurnBytes);
+  // dynamic shared memory: [slot infos | fronts | turn states] at fixed offsets (cheap
+  // addresses), then [ring | barriers | lane accumulators | range table]
+  volatile uint64_t* front = reinterpret_cast<volatile uint64_t*>(smem + kWarps * kMaxStages * kSlotInfoBytes);
+  StreamTurn* turns = reinterpret_cast<StreamTurn*>(smem + kWarps * kMaxStages * kSlotInfoBytes + kFrontBytes);
+  unsigned char* sm2 = smem + kStreamHead;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm2 + ring_bytes(stages));
+  uint64_t* sB = reinterpret_cast<uint64_t*>(sm2 + ring_bytes(stages) + kBarBytes + kLaBytes);
   const uint32_t A = args.A;
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
-  SlotInfo* info = reinterpret_cast<SlotInfo*>(info_base) + warp * stages;
-  const uint32_t ring_u32 = smem_u32(smem) + (uint32_t)(warp * stages) * kSliceBytes;
+  SlotInfo* info = reinterpret_cast<SlotInfo*>(smem) + warp * kMaxStages;
+  const uint32_t ring_u32 = smem_u32(sm2) + (uint32_t)(warp * stages) * kSliceBytes;
   const uint32_t bar_u32 = smem_u32(bars + warp * kMaxStages);
   if (lane == 0 && warp < kStreamData) {
     for (int j = 0; j < stages; ++j) mbar_init(bars + warp * kMaxStages + j, 1);
@@ -1270,7 +1284,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
     for (uint32_t i = threadIdx.x; i < 2 * A; i += blockDim.x) sB[i] = args.bounds[i];
   const uint64_t W = (uint64_t)gridDim.x * kStreamData;
   const uint64_t gnext = (uint64_t)blockIdx.x * kStreamData + warp;  // the warp's first chunk
-  const uint64_t cpb = (ra.spb + kStreamChunk - 1) / kStreamChunk;  // chunks per batch slot
+  const uint64_t cpb = ra.cpb;  // chunks per batch slot (a parameter: no division to rematerialise)
   if (lane == 0)
     front[warp] = warp < kStreamData ? (gnext / cpb) * ra.spb + (gnext % cpb) * kStreamChunk : ~0ull;
   __syncthreads();
@@ -1305,7 +1319,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
   }
   // the lowest slice this warp has not issued yet (lane 0)
   auto next_G = [&]() -> uint64_t {
-    return t.cs < t.ce ? t.cb * ra.spb + t.cs : (t.Q / cpb) * ra.spb + (t.Q % cpb) * kStreamChunk;
+    return t.cs < t.ce ? t.cb + t.cs : (t.Q / cpb) * ra.spb + (t.Q % cpb) * kStreamChunk;
   };
   // lane 0: the warp's next slice into ring slot `slot`. Returns 1 when issued, 0 when its
   // batch is not published yet (only if !block; with block it waits, reporting progress
@@ -1336,7 +1350,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
       t.Q += W;
       const uint64_t nsl = (d0.y + kSlice - 1) / kSlice;
       if (c0 >= nsl) continue;  // past the end of a short batch
-      t.cb = b;
+      t.cb = b * ra.spb;
       t.cs = c0;
       t.ce = c0 + kStreamChunk < nsl ? c0 + kStreamChunk : nsl;
       t.rec = reinterpret_cast<const uint64_t*>(d0.x);
@@ -1358,7 +1372,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
       t.kend = t.kl + 1 < t.nk ? __ldg(t.koffs + t.kl + 1) : ~0ull;
     }
     SlotInfo& si = info[slot];
-    si.G = t.cb * ra.spb + s;
+    si.G = t.cb + s;
     si.koffs = t.koffs;
     si.n = t.n;
     si.nk = t.nk;
@@ -1411,7 +1425,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
   w.own = A;
   w.pcnt = 0;
   w.ocnt = 0;
-  LaneAcc& la = reinterpret_cast<LaneAcc*>(smem + ring_bytes(stages) + kBarBytes)[threadIdx.x];
+  LaneAcc& la = reinterpret_cast<LaneAcc*>(sm2 + ring_bytes(stages) + kBarBytes)[threadIdx.x];
   la.own = A;
   la.ocnt = 0;
   la.kbit = kOOW;
@@ -1422,6 +1436,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
   // when nothing is in flight -- a warp must never sit on a loaded slice while it waits
   // for a later batch (the producer may be waiting for that slice to be read).
   uint32_t head = 0, tail_slot = 0, inflight = 0, phases = 0;  // phases: bit i = parity of slot i
+  uint32_t nit = 0;
   bool ended = false;
 
   for (;;) {
@@ -1437,7 +1452,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
         ++inflight;
       }
       if (r == 2) ended = true;
-      front[warp] = inflight ? info[head].G : (ended ? ~0ull : next_G());
+      // the warp's lowest unread slice, for the monitor; refreshed every 8 slices (a stale,
+      // lower value only delays the producer; a warp about to wait sets it in issue())
+      if ((++nit & 7u) == 0 || inflight == 0) front[warp] = inflight ? info[head].G : (ended ? ~0ull : next_G());
     }
     inflight = __shfl_sync(kFull, inflight, 0);
     __syncwarp();
@@ -1521,12 +1538,13 @@ int stream_smem_bytes(uint32_t A, bool big, int* stages_out) {
   int st = stages_for(A, big, extra);
   if (st > 4) st = 4;
   *stages_out = st;
-  return ring_bytes(st) + kBarBytes + kLaBytes + kWarps * st * kSlotInfoBytes + kFrontBytes + kTurnBytes +
-         (big ? 0 : (int)(16ull * A));
+  return kStreamHead + ring_bytes(st) + kBarBytes + kLaBytes + (big ? 0 : (int)(16ull * A));
 }
 
 template <bool kBig, bool kRows, int kPages>
-cudaError_t launch_stream_variant(const StreamArgs& a, cudaStream_t st, int* ctas) {
+cudaError_t launch_stream_variant(const StreamArgs& a0, cudaStream_t st, int* ctas) {
+  StreamArgs a = a0;
+  a.cpb = (a.spb + kStreamChunk - 1) / kStreamChunk;
   int stages = 0;
   const int smem = stream_smem_bytes(a.s.A, kBig, &stages);
   auto fn = stream_kernel<kBig, kRows, kPages>;
