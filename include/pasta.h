@@ -390,7 +390,8 @@ int pasta_peer_gather(pasta_trace* h, const pasta_peer_copy* table, uint32_t cou
  * batch's buffers must stay valid until then). pasta_stream_close publishes the end
  * (asynchronous: later work on the handle's stream, e.g. pasta_finalize / pasta_topk, is
  * ordered after the consumer drains); pasta_stream_destroy waits for the consumer and
- * frees. The range table is the one current at open (snapshot, R13). out: page_counts,
+ * frees (pasta_close does both for streams still open on the handle). The range table
+ * is the one current at open (snapshot, R13). out: page_counts,
  * alloc_counts, totals required; kernel_alloc_counts / kernel_stats / kernel_page_bitmap
  * optional (rows for every kernel_row0 + local kernel pushed); no hotness, no tensor level
  * (EINVAL); out->flags ignored (never finalizes). Batches: addr 16-byte aligned, n even and

@@ -72,6 +72,9 @@ struct pasta_trace {
   void* d_topk = nullptr;
   size_t topk_bytes = 0;
 
+  // streaming consumers opened on this handle and not destroyed yet (pasta_close ends them)
+  std::vector<pasta_stream*> streams;
+
   // CUDA IPC blocks opened in this handle's context: handle bytes -> (base, refs); and
   // every pointer handed out -> its block's handle bytes
   std::map<std::string, std::pair<void*, int>> ipc_blocks;
@@ -920,6 +923,7 @@ int pasta_stream_open(pasta_trace* h, const pasta_stream_params* p, const pasta_
       return PASTA_ECUDA;
     }
   }
+  h->streams.push_back(s);
   *ps = s;
   return PASTA_OK;
 }
@@ -1005,6 +1009,8 @@ int pasta_stream_close(pasta_stream* s) {
 int pasta_stream_destroy(pasta_stream* s) {
   if (!s) return PASTA_OK;
   DeviceGuard g(s->h->device);
+  auto& v = s->h->streams;
+  v.erase(std::remove(v.begin(), v.end(), s), v.end());
   int st = PASTA_OK;
   if (!s->closed) st = pasta_stream_close(s);
   if (cudaStreamSynchronize(s->h->stream) != cudaSuccess) st = PASTA_ECUDA;
@@ -1239,6 +1245,8 @@ int pasta_sync(pasta_trace* h) {
 int pasta_close(pasta_trace* h) {
   if (!h) return PASTA_OK;
   DeviceGuard g(h->device);
+  // a consumer still running would never finish: publish its end, then wait and free it
+  while (!h->streams.empty()) pasta_stream_destroy(h->streams.back());
   cudaStreamSynchronize(h->stream);
   if (h->copy_stream) {
     cudaStreamSynchronize(h->copy_stream);

@@ -92,9 +92,6 @@ constexpr int kSlice = 256;                 // records per slice (8 per lane)
 #ifndef PASTA_ISSUE2
 #define PASTA_ISSUE2 0  // TMA refills in pairs
 #endif
-#ifndef PASTA_FIXED_STAGES
-#define PASTA_FIXED_STAGES 0  // experiment: compile-time ring depth (the launch must pick the same)
-#endif
 #ifndef PASTA_TIER_S_BATCH
 #define PASTA_TIER_S_BATCH 1  // tier S (kPages == 0): page REDs issued back to back
 #endif
@@ -749,14 +746,7 @@ __device__ __forceinline__ uint32_t kernel_of(const uint64_t* __restrict__ koffs
 }
 
 template <bool kBig, bool kRows, int kPages, bool kIL>
-__global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages_rt, const int cache_on) {
-#if PASTA_FIXED_STAGES
-  // experiment: the ring depth as a compile-time constant (constant shared offsets)
-  constexpr int stages = PASTA_FIXED_STAGES;
-  (void)stages_rt;
-#else
-  const int stages = stages_rt;
-#endif
+__global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages, const int cache_on) {
   // Programmatic dependent launch: the next analyze call's scan may start its prologue
   // (barrier init, range table into shared memory) on free SMs while this one runs. A
   // chained scan (early == 2) triggers at entry: its predecessor is a scan that already

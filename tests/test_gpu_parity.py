@@ -719,6 +719,9 @@ def test_stream_ring_errors():
     pbm.pasta_stream_destroy(s)
     tr.sync()
     assert int(u64(hist.totals)[0]) == 1024 and int(u64(hist.alloc_counts)[0]) == 1024
+    # a stream left open: pasta_close publishes its end, waits for it and frees it
+    s = pbm.pasta_stream_open(tr.h, 12, 4, 1024, hist.struct())
+    pbm.pasta_stream_push(s, [pbm.pasta_stream_batch(rec.data_ptr(), 1024, None, 1, 0)])
     tr.close()
 
 def test_pdl_ordering_after_producer_kernels():
