@@ -2,6 +2,7 @@
 #   make            all libraries
 #   make clean
 NVCC    ?= nvcc
+CUDA_HOME ?= /usr/local/cuda
 ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -v --expt-relaxed-constexpr
 CC      ?= gcc
@@ -18,7 +19,12 @@ ifneq ($(PASTA_CU),)
 LIBS += $(PKG)/libpasta.so tracegen/libtracegen_dev.so
 endif
 
-all: $(LIBS)
+all: $(LIBS) examples/hand_worked
+
+# the C ABI from plain C (no Python): the hand-worked trace, checked on the GPU
+examples/hand_worked: examples/hand_worked.c include/pasta.h $(PKG)/libpasta.so
+	$(CC) -O2 -std=c11 -Iinclude -I$(CUDA_HOME)/include -o $@ $< -L$(PKG) -lpasta \
+	  -L$(CUDA_HOME)/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,$(CUDA_HOME)/lib64
 
 tracegen/libtracegen_host.so: tracegen/gen_host.c
 	$(CC) -O2 -std=c11 -fPIC -shared -o $@ $<
@@ -40,6 +46,6 @@ variants: $(PASTA_CU) $(PASTA_CPP) $(PASTA_H)
 	  $(NVCC) $(NVFLAGS) $$f -Iinclude -I$(CSRC) -shared -o build/variants/libpasta_$$n.so $(PASTA_CU) $(PASTA_CPP) 2>/dev/null || exit 1; done
 
 clean:
-	rm -f $(LIBS) build_ptxas.log
+	rm -f $(LIBS) examples/hand_worked build_ptxas.log
 
 .PHONY: all clean
