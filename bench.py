@@ -334,18 +334,18 @@ def run_ours(args):
                 print(f"bench: peer merge unavailable ({exc!r}); using the NCCL merge", file=sys.stderr)
         if merger is None:
             merger, merge_kind = pdist.ShardedMerger(tr, hist, plan.topk, group), "nccl"
-    K = max(plan.topk)
-    top_out = (torch.empty(K, dtype=torch.int64, device=dev), torch.empty(K, dtype=torch.int64, device=dev),
-               torch.empty(1, dtype=torch.int64, device=dev))
+    ks = list(dict.fromkeys(plan.topk))
+    top_outs = [(torch.empty(k, dtype=torch.int64, device=dev), torch.empty(k, dtype=torch.int64, device=dev),
+                 torch.empty(1, dtype=torch.int64, device=dev)) for k in ks]
+    top_out = top_outs[ks.index(max(ks))]
 
     def step():
         hist.zero_()
         tr.analyze(rec, plan.page_shift, hist, kernel_offsets=ko_loc, n=n_loc, finalize=True)
         if merger is not None:
             merger.merge()
-        else:
-            for k in plan.topk:
-                tr.topk(hist.page_counts, k, out=top_out)
+        else:  # every top-k list of the config from one selection (pasta_topk_many)
+            tr.topk_many(hist.page_counts, ks, top_outs)
 
     def barrier():
         if world > 1:
@@ -381,8 +381,8 @@ def run_ours(args):
             tops = {k: tuple(t.cpu().numpy().view(np.uint64).copy() for t in merger.out[k]) for k in plan.topk}
             shard, S = merger.shard.cpu().numpy().view(np.uint64).copy(), merger.S
         else:
-            tops = {k: tuple(t.cpu().numpy().view(np.uint64).copy() for t in tr.topk(hist.page_counts, k))
-                    for k in plan.topk}
+            tops = {k: tuple(t.cpu().numpy().view(np.uint64).copy() for t in o)
+                    for k, o in tr.topk_many(hist.page_counts, ks).items()}
             shard, S = hist.page_counts.cpu().numpy().view(np.uint64).copy(), P
         torch.cuda.synchronize()
         np.savez(f"{dump}.rank{rank}.npz", shard=shard, S=S, small=hist.small.cpu().numpy().view(np.uint64),
@@ -401,7 +401,7 @@ def run_ours(args):
         stream_res = run_stream(args, plan, rec, n_loc, ko_loc, nk_loc, dev, int(hist.totals[0].item()))
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, k0, world, group, local, dev, top_out)
+        e2e = run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, k0, world, group, local, dev, ks, top_outs)
     del rec
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -517,11 +517,13 @@ def run_stream(args, plan, rec, n_loc, ko_loc, nk_loc, dev, expect_records):
             "ring_path": "pasta_stream_open + pasta_stream_push (host publishes while the consumer runs) + close"}
 
 
-def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, k0, world, group, local, dev, top_out):
+def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, k0, world, group, local, dev, ks, top_outs):
     """End to end through the public API: every step copies its records from pinned
     host memory (inside pasta_analyze, chunked and overlapped with the scan), runs the
     whole path, and reads the results (totals + top-K) back to the host."""
     import torch
+
+    top_out = top_outs[ks.index(max(ks))]
 
     import paper_2602_22103_b200 as pb
 
@@ -568,8 +570,7 @@ def run_e2e(args, plan, tr, hist, rec, n_loc, ko_loc, j0, k0, world, group, loca
             outs = merger.merge()
             res = outs[max(plan.topk)]
         else:
-            for k in plan.topk:
-                tr.topk(h_e.page_counts, k, out=top_out)
+            tr.topk_many(h_e.page_counts, ks, top_outs)
             res = top_out
         T = pb.TOTALS
         res_host[:T].copy_(h_e.totals, non_blocking=True)

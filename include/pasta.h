@@ -307,6 +307,27 @@ int pasta_finalize(pasta_trace* h, uint32_t page_shift, uint32_t n_kernels, past
 int pasta_topk(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t k, uint64_t* out_page,
                uint64_t* out_count, uint64_t* out_found);
 
+/* Several top-K lists of the same counts (e.g. a config's top-16 and top-1024) with ONE
+ * selection: for every j < n_k, out_page[j], out_count[j], out_found[j] receive exactly
+ * what pasta_topk(h, page_counts, P, ks[j], ...) writes. R10's order (count desc, page
+ * asc) is total, so a top-k list is the first k entries of the top-k_max list
+ * (k_max = max_j ks[j]): the selection runs once for k_max into that entry's outputs and
+ * one launch copies the prefixes into the others (pasta_topk_prefix). ks, out_page,
+ * out_count, out_found are HOST arrays of n_k (1..16) entries; the pointers they hold are
+ * device pointers as in pasta_topk; outputs of different entries must not overlap.
+ * Every ks[j] >= 1. Asynchronous; PASTA_EINVAL on a bad argument. */
+int pasta_topk_many(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t n_k, const uint32_t* ks,
+                    uint64_t* const* out_page, uint64_t* const* out_count, uint64_t* const* out_found);
+
+/* The prefix step on its own (e.g. after pasta_topk_merge of the largest k in a
+ * multi-GPU merge): src_* is a top-k_src list as pasta_topk / pasta_topk_merge write it
+ * (device pointers); entry j (HOST arrays of n_k <= 16 entries) gets its first ks[j]
+ * entries and *out_found[j] = min(ks[j], *src_found). 1 <= ks[j] <= k_src, else
+ * PASTA_EINVAL. One launch, asynchronous on the handle's stream. */
+int pasta_topk_prefix(pasta_trace* h, const uint64_t* src_page, const uint64_t* src_count, const uint64_t* src_found,
+                      uint32_t k_src, uint32_t n_k, const uint32_t* ks, uint64_t* const* out_page,
+                      uint64_t* const* out_count, uint64_t* const* out_found);
+
 /* Multi-GPU merge helper (OR of bitmaps): out_bitmap[w] =
  * OR over r < g of gathered[r*words + w]; *out_popcount (device u64, may be NULL)
  * = number of set bits. NCCL has no bitwise-OR reduction, so shards all_gather their

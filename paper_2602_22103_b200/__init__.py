@@ -116,6 +116,10 @@ _SIGS = {
     "pasta_analyze_rich": (_int, [_vp, ctypes.POINTER(pasta_rich_records), _u64, _u32,
                                   ctypes.POINTER(pasta_histograms), ctypes.POINTER(pasta_rich_outputs)]),
     "pasta_topk": (_int, [_vp, _vp, _u64, _u32, _vp, _vp, _vp]),
+    "pasta_topk_many": (_int, [_vp, _vp, _u64, _u32, ctypes.POINTER(_u32), ctypes.POINTER(_vp),
+                               ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "pasta_topk_prefix": (_int, [_vp, _vp, _vp, _vp, _u32, _u32, ctypes.POINTER(_u32), ctypes.POINTER(_vp),
+                                 ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
     "pasta_bitmap_or": (_int, [_vp, _vp, _u32, _u64, _vp, _vp]),
     "pasta_topk_merge": (_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp]),
     "pasta_peer_reduce": (_int, [_vp, ctypes.POINTER(_vp), _u32, _u64, _u64, _u32, _vp, _vp, _vp]),
@@ -241,6 +245,25 @@ def pasta_finalize(h, page_shift: int, n_kernels: int, hist):
 def pasta_topk(h, page_counts, P: int, k: int, out_page, out_count, out_found):
     _check(_lib.pasta_topk(h, _ptr(page_counts), P, k, _ptr(out_page), _ptr(out_count), _ptr(out_found)),
            "pasta_topk")
+
+
+def _topk_arrays(ks, outs):
+    n = len(ks)
+    return ((_u32 * n)(*ks), (_vp * n)(*[_ptr(o[0]) for o in outs]), (_vp * n)(*[_ptr(o[1]) for o in outs]),
+            (_vp * n)(*[_ptr(o[2]) for o in outs]))
+
+
+def pasta_topk_many(h, page_counts, P: int, ks, outs):
+    """outs[j] = (out_page, out_count, out_found) for ks[j]."""
+    a_k, a_p, a_c, a_f = _topk_arrays(ks, outs)
+    _check(_lib.pasta_topk_many(h, _ptr(page_counts), P, len(ks), a_k, a_p, a_c, a_f), "pasta_topk_many")
+
+
+def pasta_topk_prefix(h, src, k_src: int, ks, outs):
+    """src = (page, count, found) of a top-k_src list; outs[j] = (page, count, found) for ks[j]."""
+    a_k, a_p, a_c, a_f = _topk_arrays(ks, outs)
+    _check(_lib.pasta_topk_prefix(h, _ptr(src[0]), _ptr(src[1]), _ptr(src[2]), k_src, len(ks), a_k, a_p, a_c, a_f),
+           "pasta_topk_prefix")
 
 
 def pasta_bitmap_or(h, gathered, g: int, words: int, out_bitmap, out_popcount=None):
@@ -517,6 +540,22 @@ class Trace:
                    torch.empty(1, dtype=torch.int64, device=self.device))
         pasta_topk(self.h, page_counts, page_counts.numel(), k, out[0], out[1], out[2])
         return out
+
+    def topk_many(self, page_counts, ks, outs=None):
+        """Every top-k list of ks with one selection (pasta_topk_many); returns {k: (page, count, found)}."""
+        import torch
+
+        ks = list(ks)
+        if outs is None:
+            outs = [(torch.empty(k, dtype=torch.int64, device=self.device),
+                     torch.empty(k, dtype=torch.int64, device=self.device),
+                     torch.empty(1, dtype=torch.int64, device=self.device)) for k in ks]
+        pasta_topk_many(self.h, page_counts, page_counts.numel(), ks, outs)
+        return dict(zip(ks, outs))
+
+    def topk_prefix(self, src, k_src: int, ks, outs):
+        pasta_topk_prefix(self.h, src, k_src, list(ks), outs)
+        return dict(zip(ks, outs))
 
     def bitmap_or(self, gathered, g: int, words: int, out_bitmap, out_popcount=None):
         pasta_bitmap_or(self.h, gathered, g, words, out_bitmap, out_popcount)

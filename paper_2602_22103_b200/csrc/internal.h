@@ -189,6 +189,24 @@ typedef void (*launch_hook)(void* ctx, int begin);
 cudaError_t run_topk(const uint64_t* page_counts, uint64_t P, uint32_t k, uint64_t* out_page, uint64_t* out_count,
                      uint64_t* out_found, void* scratch, int max_ctas, cudaStream_t st, int* n_launches);
 
+// Prefix copies of one top-k_max list into several top-k outputs (pasta_topk_many /
+// pasta_topk_prefix): entry j gets the first k_j entries and found_j = min(k_j, found).
+constexpr uint32_t kMaxTopkPrefix = 16;
+struct TopkPrefix {
+  uint64_t* dst_page;
+  uint64_t* dst_count;
+  uint64_t* dst_found;
+  uint64_t k;
+};
+struct TopkPrefixTable {
+  const uint64_t* src_page;
+  const uint64_t* src_count;
+  const uint64_t* src_found;
+  TopkPrefix e[kMaxTopkPrefix];
+  uint32_t count;
+};
+cudaError_t launch_topk_prefix(const TopkPrefixTable& t, int grid, cudaStream_t st);
+
 cudaError_t run_topk_merge(const uint64_t* cand_page, const uint64_t* cand_count, uint32_t g, uint32_t k,
                            uint64_t shard_pages, uint64_t* out_page, uint64_t* out_count, uint64_t* out_found,
                            void* scratch, int grid, cudaStream_t st, int* n_launches);

@@ -730,6 +730,54 @@ int pasta_topk(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t
   return cuda_status(e);
 }
 
+int pasta_topk_prefix(pasta_trace* h, const uint64_t* src_page, const uint64_t* src_count, const uint64_t* src_found,
+                      uint32_t k_src, uint32_t n_k, const uint32_t* ks, uint64_t* const* out_page,
+                      uint64_t* const* out_count, uint64_t* const* out_found) {
+  if (!h || !src_page || !src_count || !src_found || k_src == 0 || !ks || !out_page || !out_count || !out_found ||
+      n_k == 0 || n_k > kMaxTopkPrefix)
+    return PASTA_EINVAL;
+  TopkPrefixTable t{};
+  t.src_page = src_page;
+  t.src_count = src_count;
+  t.src_found = src_found;
+  for (uint32_t j = 0; j < n_k; ++j) {
+    if (ks[j] == 0 || ks[j] > k_src || !out_page[j] || !out_count[j] || !out_found[j]) return PASTA_EINVAL;
+    t.e[j] = TopkPrefix{out_page[j], out_count[j], out_found[j], ks[j]};
+  }
+  t.count = n_k;
+  DeviceGuard g(h->device);
+  Timed tm(h, PASTA_PH_TOPK, h->stream);
+  cudaError_t e = launch_topk_prefix(t, h->sm_count, h->stream);
+  if (e == cudaSuccess) h->launches += 1;
+  return cuda_status(e);
+}
+
+int pasta_topk_many(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t n_k, const uint32_t* ks,
+                    uint64_t* const* out_page, uint64_t* const* out_count, uint64_t* const* out_found) {
+  if (!h || !page_counts || P == 0 || !ks || !out_page || !out_count || !out_found || n_k == 0 ||
+      n_k > kMaxTopkPrefix)
+    return PASTA_EINVAL;
+  uint32_t jm = 0;
+  for (uint32_t j = 0; j < n_k; ++j) {
+    if (ks[j] == 0 || !out_page[j] || !out_count[j] || !out_found[j]) return PASTA_EINVAL;
+    if (ks[j] > ks[jm]) jm = j;
+  }
+  int rc = pasta_topk(h, page_counts, P, ks[jm], out_page[jm], out_count[jm], out_found[jm]);
+  if (rc != PASTA_OK || n_k == 1) return rc;
+  uint32_t kk[kMaxTopkPrefix];
+  uint64_t *op[kMaxTopkPrefix], *oc[kMaxTopkPrefix], *of[kMaxTopkPrefix];
+  uint32_t m = 0;
+  for (uint32_t j = 0; j < n_k; ++j) {
+    if (j == jm) continue;
+    kk[m] = ks[j];
+    op[m] = out_page[j];
+    oc[m] = out_count[j];
+    of[m] = out_found[j];
+    ++m;
+  }
+  return pasta_topk_prefix(h, out_page[jm], out_count[jm], out_found[jm], ks[jm], m, kk, op, oc, of);
+}
+
 int pasta_topk_merge(pasta_trace* h, const uint64_t* cand_page, const uint64_t* cand_count, uint32_t g, uint32_t k,
                      uint64_t shard_pages, uint64_t* out_page, uint64_t* out_count, uint64_t* out_found) {
   if (!h || !cand_page || !cand_count || !out_page || !out_count || !out_found || g == 0 || k == 0)

@@ -128,14 +128,17 @@ __device__ __forceinline__ u128 make_key(uint64_t c, uint64_t p, int pbits, uint
 // Streams the counts: f(p, c) for every page, called by every lane of every warp in step
 // (zero counts for lanes past the end), so f may use warp collectives. 16-byte loads,
 // kTU in flight per thread; an unaligned head element and an odd tail element are
-// visited by warp 0 of block 0 at the end.
-template <typename F>
+// visited by warp 0 of block 0 at the end. With `rev` the blocks of kTB * kTU pairs are
+// visited last to first: a pass that follows a forward pass then starts on the counts
+// the forward pass read last, which are still in L2 (126 MB; the llama counts are 134 MB).
+template <bool rev = false, typename F>
 __device__ __forceinline__ void tk_stream(const uint64_t* __restrict__ pc, uint64_t P, F&& f) {
   const uint64_t h = ((reinterpret_cast<uintptr_t>(pc) & 15u) != 0 && P > 0) ? 1 : 0;
   const ulonglong2* v2 = reinterpret_cast<const ulonglong2*>(pc + h);
   const uint64_t n2 = (P - h) / 2;
-  const uint64_t step = (uint64_t)gridDim.x * kTB * kTU;
-  for (uint64_t b0 = (uint64_t)blockIdx.x * kTB * kTU; b0 < n2; b0 += step) {
+  const uint64_t rows = (n2 + (uint64_t)kTB * kTU - 1) / ((uint64_t)kTB * kTU);
+  for (uint64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const uint64_t b0 = (rev ? rows - 1 - r : r) * (uint64_t)kTB * kTU;
     ulonglong2 v[kTU];
 #pragma unroll
     for (int u = 0; u < kTU; ++u) {
@@ -326,9 +329,16 @@ __device__ uint64_t tk_full_pass(const TkArgs& a, const Sel& s, int ps, unsigned
   // every key this pass acts on is >= rlo, i.e. has count >= rlo >> pbits (>= 1): a warp
   // whose counts are all below skips the key arithmetic (almost every count, every pass)
   const uint64_t cmin = (uint64_t)(s.rlo >> a.pbits);
-  tk_stream(a.pc, a.P, [&](uint64_t p, uint64_t c) {
+  auto visit = [&](uint64_t p, uint64_t c) {
     if (__any_sync(kFull, c >= cmin)) full_slow(&a, ctl, sh, sfill, p, c);
-  });
+  };
+#ifndef PASTA_TOPK_REV
+#define PASTA_TOPK_REV 1
+#endif
+  if (PASTA_TOPK_REV && (ps & 1))
+    tk_stream<true>(a.pc, a.P, visit);  // right after a forward pass: start on its L2-resident tail
+  else
+    tk_stream<false>(a.pc, a.P, visit);
   if (!rng) return 0;
   hist_publish(sh, hd->hist[ps], 1 << dw);  // (its barriers also complete every append)
   const uint64_t mine = *sfill;
@@ -703,6 +713,24 @@ __global__ void write_kernel(const State* st, const uint64_t* key_c, const uint6
   if (blockIdx.x == 0 && threadIdx.x == 0) *out_found = kp;
 }
 
+// Top-k lists as prefixes of one top-k_max list (R10's order is total, so the first k
+// entries of the top-k_max list ARE the top-k list, sentinels included): entry j copies
+// k_j entries and sets found_j = min(k_j, found_max). One launch for every entry.
+__global__ void topk_prefix_kernel(const __grid_constant__ TopkPrefixTable t) {
+  const uint64_t nt = (uint64_t)gridDim.x * blockDim.x, tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint32_t j = 0; j < t.count; ++j) {
+    const TopkPrefix& e = t.e[j];
+    for (uint64_t i = tid; i < e.k; i += nt) {
+      e.dst_page[i] = __ldg(t.src_page + i);
+      e.dst_count[i] = __ldg(t.src_count + i);
+    }
+    if (tid == 0) {
+      const uint64_t f = *t.src_found;
+      *e.dst_found = f < e.k ? f : e.k;
+    }
+  }
+}
+
 // Candidates of g shard-local top-K lists (rank-major, k entries each) -> sort keys with
 // global page ids (page + r * shard_pages); empty slots (count 0) become sentinels.
 __global__ void merge_load_kernel(const uint64_t* __restrict__ cand_page, const uint64_t* __restrict__ cand_count,
@@ -844,6 +872,16 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
   void* args[] = {(void*)&a};
   PASTA_TRY(cudaLaunchCooperativeKernel((void*)topk_kernel, dim3(g), dim3(kTB), args, kDynSmem, st));
   return cudaSuccess;
+}
+
+cudaError_t launch_topk_prefix(const TopkPrefixTable& t, int grid, cudaStream_t st) {
+  uint64_t most = 0;
+  for (uint32_t j = 0; j < t.count; ++j) most = t.e[j].k > most ? t.e[j].k : most;
+  uint64_t g = (most + 255) / 256;
+  if (g < 1) g = 1;
+  if (g > (uint64_t)grid) g = (uint64_t)grid;
+  topk_prefix_kernel<<<(unsigned)g, 256, 0, st>>>(t);
+  return cudaGetLastError();
 }
 
 cudaError_t run_topk_merge(const uint64_t* cand_page, const uint64_t* cand_count, uint32_t g, uint32_t k,

@@ -125,6 +125,27 @@ class Merger:
         h.totals[list(_WS_SLOTS)] = self.ws
 
 
+def _topk_buffers(self, ks, dev, alloc):
+    """Top-K buffers of a merger: ONE selection for k_max = max(ks) (local list, the g
+    gathered candidate lists, the merged list); the other k are prefixes of the merged
+    top-k_max list (R10's order is total), copied by pasta_topk_prefix."""
+    self.ks = tuple(dict.fromkeys(int(k) for k in ks))
+    self.kmax = max(self.ks)
+    km = self.kmax
+    self.loc = (alloc(km, dtype=torch.int64, device=dev), alloc(km, dtype=torch.int64, device=dev),
+                alloc(1, dtype=torch.int64, device=dev))
+    self.cand = (torch.empty(self.world * km, dtype=torch.int64, device=dev),
+                 torch.empty(self.world * km, dtype=torch.int64, device=dev))
+    self.out = {k: (torch.empty(k, dtype=torch.int64, device=dev), torch.empty(k, dtype=torch.int64, device=dev),
+                    torch.empty(1, dtype=torch.int64, device=dev)) for k in self.ks}
+
+
+def _topk_prefixes(self):
+    rest = [k for k in self.ks if k != self.kmax]
+    if rest:
+        self.tr.topk_prefix(self.out[self.kmax], self.kmax, rest, [self.out[k] for k in rest])
+
+
 class ShardedMerger:
     """Merge with the page counts left sharded (strong scaling):
 
@@ -149,13 +170,7 @@ class ShardedMerger:
         self.ws = torch.empty(len(_WS_SLOTS), dtype=torch.int64, device=dev)
         self.mk = torch.empty(2, dtype=torch.int64, device=dev)
         self.mk_all = torch.empty(2 * self.world, dtype=torch.int64, device=dev)
-        self.ks = tuple(ks)
-        self.loc = {k: (torch.empty(k, dtype=torch.int64, device=dev), torch.empty(k, dtype=torch.int64, device=dev),
-                        torch.empty(1, dtype=torch.int64, device=dev)) for k in self.ks}
-        self.cand = {k: (torch.empty(self.world * k, dtype=torch.int64, device=dev),
-                         torch.empty(self.world * k, dtype=torch.int64, device=dev)) for k in self.ks}
-        self.out = {k: (torch.empty(k, dtype=torch.int64, device=dev), torch.empty(k, dtype=torch.int64, device=dev),
-                        torch.empty(1, dtype=torch.int64, device=dev)) for k in self.ks}
+        _topk_buffers(self, ks, dev, torch.empty)
 
     def merge(self):
         from . import T_UNIQUE_PAGES
@@ -171,11 +186,12 @@ class ShardedMerger:
                           h.totals[T_UNIQUE_PAGES:T_UNIQUE_PAGES + 1])
         merge_max(self.ws, self.group)
         h.totals[list(_WS_SLOTS)] = self.ws
-        for k in self.ks:
-            lp, lc, _ = self.tr.topk(self.shard, k, out=self.loc[k])
-            cp, cc = self.cand[k]
-            gather_candidates(lp, lc, cp, cc, self.group)
-            self.tr.topk_merge(cp, cc, self.world, k, self.S, self.out[k])
+        km = self.kmax
+        lp, lc, _ = self.tr.topk(self.shard, km, out=self.loc)
+        cp, cc = self.cand
+        gather_candidates(lp, lc, cp, cc, self.group)
+        self.tr.topk_merge(cp, cc, self.world, km, self.S, self.out[km])
+        _topk_prefixes(self)
         return self.out
 
 
@@ -223,16 +239,8 @@ class PeerMerger:
         self.pop = torch.zeros(1, dtype=torch.int64, device=dev)
         self.small_out = torch.zeros_like(hist.small)
         self.flag = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.ks = tuple(ks)
-        self.loc = {k: (torch.zeros(k, dtype=torch.int64, device=dev), torch.zeros(k, dtype=torch.int64, device=dev),
-                        torch.zeros(1, dtype=torch.int64, device=dev)) for k in self.ks}
-        self.cand = {k: (torch.empty(self.world * k, dtype=torch.int64, device=dev),
-                         torch.empty(self.world * k, dtype=torch.int64, device=dev)) for k in self.ks}
-        self.out = {k: (torch.empty(k, dtype=torch.int64, device=dev), torch.empty(k, dtype=torch.int64, device=dev),
-                        torch.empty(1, dtype=torch.int64, device=dev)) for k in self.ks}
-        mine = [hist.packed, self.shard_bm, self.pop]
-        for k in self.ks:
-            mine += [self.loc[k][0], self.loc[k][1]]
+        _topk_buffers(self, ks, dev, torch.zeros)
+        mine = [hist.packed, self.shard_bm, self.pop, self.loc[0], self.loc[1]]
         torch.cuda.synchronize(dev)
         # own buffers are used directly; the others' through libpasta's IPC mappings
         handles = [trace.ipc_export(t) for t in mine] if self.world > 1 else []
@@ -287,11 +295,10 @@ class PeerMerger:
             cp.append((so + 8 * (u + 1), hs + 8 * (u + 1), self.n_small - u - 1, PASTA_COPY))
         for p in self.peers:
             cp.append((p[2], hs + 8 * u, 1, PASTA_COPY_ADD))
-        for i, k in enumerate(self.ks):
-            cpp, ccc = self.cand[k]
-            for r, p in enumerate(self.peers):
-                cp.append((p[3 + 2 * i], cpp.data_ptr() + 8 * r * k, k, PASTA_COPY))
-                cp.append((p[4 + 2 * i], ccc.data_ptr() + 8 * r * k, k, PASTA_COPY))
+        cpp, ccc, k = self.cand[0], self.cand[1], self.kmax
+        for r, p in enumerate(self.peers):
+            cp.append((p[3], cpp.data_ptr() + 8 * r * k, k, PASTA_COPY))
+            cp.append((p[4], ccc.data_ptr() + 8 * r * k, k, PASTA_COPY))
         assert len(cp) <= 120, "too many peer copies for one pasta_peer_gather"
         self.copies = cp
 
@@ -310,13 +317,11 @@ class PeerMerger:
             self._barrier()  # every rank's local analyze is complete
             tr.peer_reduce(self.src_shard, 0, self.S, self.shard, self.shard_bm, self.pop)
             tr.peer_reduce_small(self.src_small, 0, self.n_small, self.slots, self.small_out)
-            for k in self.ks:
-                tr.topk(self.shard, k, out=self.loc[k])
+            tr.topk(self.shard, self.kmax, out=self.loc)
             self._barrier()  # every shard, bitmap word, count and candidate list is ready
             tr.peer_gather(self.copies)
-            for k in self.ks:
-                cp, cc = self.cand[k]
-                tr.topk_merge(cp, cc, self.world, k, self.S, self.out[k])
+            tr.topk_merge(self.cand[0], self.cand[1], self.world, self.kmax, self.S, self.out[self.kmax])
+            _topk_prefixes(self)
             self._barrier()  # nobody reads this rank's buffers any more
         return self.out
 

@@ -50,10 +50,9 @@ def run_gpu(tr, records, page_shift, kernel_offsets=None, kernel_rows=False, ker
         ko = ko.pin_memory() if host else ko.to(tr.device)
     tr.analyze(records, page_shift, hist, kernel_offsets=ko, finalize=finalize, host=host, n=n)
     out = {"hist": hist}
-    tops = {}
-    for K in topk:
-        p, c, f = tr.topk(hist.page_counts, K)
-        tops[K] = (p, c, f)
+    # every requested list from one selection (pasta_topk_many: pasta_topk of the largest
+    # k, prefixes for the others); tests/test_gpu_parity.py covers pasta_topk per k
+    tops = tr.topk_many(hist.page_counts, list(dict.fromkeys(topk))) if topk else {}
     tr.sync()
     out["page_counts"] = u64(hist.page_counts)
     out["alloc_counts"] = u64(hist.alloc_counts)

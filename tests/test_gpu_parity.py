@@ -334,6 +334,43 @@ def test_topk_unaligned_tiny_and_k_above_p():
     tr.close()
 
 
+def test_topk_many_and_prefix():
+    """pasta_topk_many: each list equals pasta_topk / the oracle for its own k (k above
+    nnz and above P included, duplicates, 16 entries); pasta_topk_prefix of a merged list;
+    argument errors are status codes."""
+    rng = np.random.default_rng(77)
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    for P, ks in [(300_001, [16, 1024, 1, 5000, 1024]), (5, [1, 3, 8, 2]),
+                  (1_000_000, [1 << i for i in range(16)])]:
+        counts = rng.integers(0, 6, size=P).astype(np.uint64)
+        counts[rng.integers(0, P, 30)] = rng.integers(1 << 20, 1 << 40, 30).astype(np.uint64)
+        outs = [(torch.full((k,), 7, dtype=torch.int64, device=DEV), torch.full((k,), 7, dtype=torch.int64, device=DEV),
+                 torch.full((1,), 7, dtype=torch.int64, device=DEV)) for k in ks]
+        pb.pasta_topk_many(tr.h, _t(counts), P, ks, outs)
+        tr.sync()
+        for k, (p, c, f) in zip(ks, outs):
+            rp, rc, rf = oracle.topk(counts, k)
+            assert int(u64(f)[0]) == rf, (P, k)
+            assert np.array_equal(u64(p), rp) and np.array_equal(u64(c), rc), (P, k)
+    # prefix of a given list
+    counts = rng.integers(0, 1000, size=50_000).astype(np.uint64)
+    src = tr.topk(_t(counts), 700)
+    outs = {k: (torch.empty(k, dtype=torch.int64, device=DEV), torch.empty(k, dtype=torch.int64, device=DEV),
+                torch.empty(1, dtype=torch.int64, device=DEV)) for k in (1, 699, 700)}
+    tr.topk_prefix(src, 700, list(outs), list(outs.values()))
+    tr.sync()
+    for k, (p, c, f) in outs.items():
+        rp, rc, rf = oracle.topk(counts, k)
+        assert int(u64(f)[0]) == rf and np.array_equal(u64(p), rp) and np.array_equal(u64(c), rc), k
+    with pytest.raises(pb.PastaError):
+        tr.topk_prefix(src, 700, [701], [outs[700]])
+    with pytest.raises(pb.PastaError):
+        tr.topk_many(_t(counts), [1] * 17)
+    with pytest.raises(pb.PastaError):
+        tr.topk_many(_t(counts), [4, 0])
+    tr.close()
+
+
 def _topk_dists():
     rng = np.random.default_rng(2024)
     P = 3_000_017  # several CTAs' ranges, odd length
