@@ -1159,7 +1159,14 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
 // after every warp has read that batch.
 // ------------------------------------------------------------------------------------
 constexpr int kSlotInfoBytes = 64;  // per warp and ring stage: the slice in flight
-constexpr int kStreamData = kWarps;  // data warps of the stream consumer; one more warp is the monitor
+// Data warps of the stream consumer; one more warp is the monitor. 23 + 1 = 24 warps keep
+// 6 warps per SM sub-partition and so the scan's 80 registers per thread; 24 + 1 (7 on one
+// sub-partition) capped them at 72 with spills (ncu: an LDL per slice).
+#ifndef PASTA_STREAM_DATA_WARPS
+#define PASTA_STREAM_DATA_WARPS (kWarps - 1)
+#endif
+constexpr int kStreamData = PASTA_STREAM_DATA_WARPS;
+static_assert(kStreamData <= kWarps, "the slot, front and turn arrays hold kWarps warps");
 constexpr int kStreamThreads = (kStreamData + 1) * 32;
 #ifndef PASTA_STREAM_CHUNK
 #define PASTA_STREAM_CHUNK 32  // consecutive slices of one batch per warp turn
