@@ -1192,28 +1192,44 @@ __device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsign
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-struct __align__(16) StreamTurn {  // lane 0's chunk state of one warp (shared memory)
-  uint64_t Q;          // the next chunk to start
-  uint64_t cb, cs, ce; // the current chunk: batch (as its first global slice cb * spb), slices [cs, ce)
-  const uint64_t* rec;
+// Lane 0's chunk state of one warp (shared memory). The first 32 bytes are all the
+// per-slice fast path reads: slices [cs, cf) of the current chunk are full and lie inside
+// one kernel, so issuing one is two 16-byte loads, a tag store and the TMA copy.
+struct __align__(16) StreamTurn {
+  const uint64_t* rec;   // the current batch's records
+  uint32_t cs, cf;       // next slice to issue; end of the fast run
+  uint64_t G0;           // global slice index of the batch's slice 0 (b * spb)
+  uint32_t krow, eidx;   // kernel row of slice cs (k0 + kl); the chunk's entry (see SlotTag)
+  uint32_t ce, nk;       // end of the chunk (slices); kernels in the batch
+  uint32_t kl, k0;       // batch-local kernel of slice cs, the batch's first row
+  uint64_t kend;         // batch-relative record where kernel kl ends (~0: never)
   const uint64_t* koffs;
-  uint64_t n, kend, known_tail;
-  uint32_t nk, k0, kl, pad;
+  uint64_t n;            // records of the batch
+  uint64_t Q, known_tail;
+  uint32_t opened, pad;  // chunks opened (entry ring index)
 };
 constexpr int kTurnBytes = kWarps * (int)sizeof(StreamTurn);
 constexpr int kStreamHead = kWarps * kMaxStages * kSlotInfoBytes + kFrontBytes + kTurnBytes;  // see stream_kernel
 static_assert(kStreamHead % 16 == 0, "the ring after the head stays 16-byte aligned");
 
-struct __align__(16) SlotInfo {   // 64 B in shared memory
-  uint64_t G;       // global slice index b * spb + s
-  const uint64_t* koffs;
-  uint64_t n;       // records of the batch
-  uint32_t nk, k0;
-  uint32_t s, valid;
-  uint32_t kl, pad; // batch-local kernel of the slice's first record
-  uint64_t kend;    // where that kernel ends (batch-relative), ~0 = never
-  uint64_t pad2;
+// Per ring slot: what the processing side needs about the slice in it (one 16-byte store
+// by lane 0 when it issues the copy, one broadcast load per slice when it is processed).
+struct __align__(16) SlotTag {
+  uint64_t G;      // global slice index
+  uint32_t krow;   // kernel row of the slice's first record
+  uint32_t meta;   // bit 3: fast (full, one kernel); bits 0-2: the chunk entry
 };
+constexpr uint32_t kTagFast = 8u;
+// Per chunk the warp opened (ring of kMaxStages = 8 >= stages entries: the slices in
+// flight belong to at most `stages` consecutive chunks): what a slow slice needs.
+struct __align__(16) ChunkEntry {
+  const uint64_t* koffs;
+  uint64_t n;
+  uint64_t G0;
+  uint32_t nk, k0;
+};
+static_assert(sizeof(SlotTag) + sizeof(ChunkEntry) <= (size_t)kSlotInfoBytes, "tag + entry fit the slot info bytes");
+static_assert(kMaxStages == 8, "the entry index takes 3 tag bits");
 
 // The monitor warp of each CTA (all 32 lanes): this CTA's progress to the producer. A
 // batch is read by the CTA once every data warp's lowest unread slice lies beyond it;
@@ -1270,7 +1286,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
   const uint32_t A = args.A;
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
-  SlotInfo* info = reinterpret_cast<SlotInfo*>(smem) + warp * kMaxStages;
+  SlotTag* tags = reinterpret_cast<SlotTag*>(smem) + warp * kMaxStages;
+  ChunkEntry* ents = reinterpret_cast<ChunkEntry*>(smem + kWarps * kMaxStages * sizeof(SlotTag)) + warp * kMaxStages;
   const uint32_t ring_u32 = smem_u32(sm2) + (uint32_t)(warp * stages) * kSliceBytes;
   const uint32_t bar_u32 = smem_u32(bars + warp * kMaxStages);
   if (lane == 0 && warp < kStreamData) {
@@ -1311,20 +1328,24 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
   StreamTurn& t = turns[warp];
   if (lane == 0) {
     t.Q = gnext;
-    t.cb = t.cs = t.ce = 0;
+    t.cs = t.cf = t.ce = 0;
     t.known_tail = 0;
+    t.opened = 0;
   }
   // the lowest slice this warp has not issued yet (lane 0)
   auto next_G = [&]() -> uint64_t {
-    return t.cs < t.ce ? t.cb + t.cs : (t.Q / cpb) * ra.spb + (t.Q % cpb) * kStreamChunk;
+    return t.cs < t.ce ? t.G0 + t.cs : (t.Q / cpb) * ra.spb + (t.Q % cpb) * kStreamChunk;
   };
-  // lane 0: the warp's next slice into ring slot `slot`. Returns 1 when issued, 0 when its
-  // batch is not published yet (only if !block; with block it waits, reporting progress
-  // meanwhile if this is warp 0), 2 when the stream has ended before it.
 #if PASTA_STREAM_PROF
   unsigned long long p_fill = 0, p_wait = 0, p_n = 0, p_t0 = clock64(), p_turns = 0, p_sleeps = 0;
 #endif
-  auto issue = [&](uint32_t slot, bool block) -> int {
+  // lane 0, any slice: open the next non-empty chunk if the current one is done, locate
+  // the slice's kernel, tag it and issue its copy into ring slot `slot`. Returns 1 when
+  // issued, 0 when its batch is not published yet (only if !block; with block it waits),
+  // 2 when the stream has ended before it. The fast run [cs, cf) is set up for the
+  // following slices. Warp turns: chunk Q = gw, gw + W, ... of the global chunk sequence
+  // (batch Q / cpb, slices [C (Q % cpb), C (Q % cpb + 1)) of it).
+  auto issue_slow = [&](uint32_t slot, bool block) -> int {
     while (t.cs == t.ce) {
       const uint64_t b = t.Q / cpb, c0 = (t.Q % cpb) * kStreamChunk;
       while (t.known_tail <= b) {
@@ -1347,9 +1368,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
       t.Q += W;
       const uint64_t nsl = (d0.y + kSlice - 1) / kSlice;
       if (c0 >= nsl) continue;  // past the end of a short batch
-      t.cb = b * ra.spb;
-      t.cs = c0;
-      t.ce = c0 + kStreamChunk < nsl ? c0 + kStreamChunk : nsl;
+      if (c0 == 0 && d0.y) red_add_u64(args.totals + 0, d0.y);  // the batch's records, once
+      t.G0 = b * ra.spb;
+      t.cs = (uint32_t)c0;
+      t.ce = (uint32_t)(c0 + kStreamChunk < nsl ? c0 + kStreamChunk : nsl);
       t.rec = reinterpret_cast<const uint64_t*>(d0.x);
       t.n = d0.y;
       t.koffs = reinterpret_cast<const uint64_t*>(d1.x);
@@ -1358,30 +1380,62 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
       t.kl = 0;
       t.kend = ~0ull;
       if (kRows && t.koffs != nullptr && t.nk > 1) {
-        t.kl = kernel_of(t.koffs, t.nk, t.cs * kSlice);
+        t.kl = kernel_of(t.koffs, t.nk, (uint64_t)t.cs * kSlice);
         t.kend = t.kl + 1 < t.nk ? __ldg(t.koffs + t.kl + 1) : ~0ull;
       }
+      const uint32_t e = t.opened++ & (kMaxStages - 1);
+      t.eidx = e;
+      ChunkEntry& ce = ents[e];
+      ce.koffs = t.koffs;
+      ce.n = t.n;
+      ce.G0 = t.G0;
+      ce.nk = t.nk;
+      ce.k0 = t.k0;
     }
-    const uint64_t s = t.cs++;
-    const uint64_t r_lo = s * kSlice;
+    const uint32_t sl = t.cs++;
+    const uint64_t r_lo = (uint64_t)sl * kSlice;
     while (kRows && t.kend <= r_lo) {  // a kernel boundary since the last slice (rare)
       ++t.kl;
       t.kend = t.kl + 1 < t.nk ? __ldg(t.koffs + t.kl + 1) : ~0ull;
     }
-    SlotInfo& si = info[slot];
-    si.G = t.cb + s;
-    si.koffs = t.koffs;
-    si.n = t.n;
-    si.nk = t.nk;
-    si.k0 = t.k0;
-    si.s = (uint32_t)s;
     const uint64_t left = t.n - r_lo;
-    si.valid = left < (uint64_t)kSlice ? (uint32_t)left : (uint32_t)kSlice;
-    si.kl = t.kl;
-    si.kend = t.kend;
-    mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, si.valid * 8u);
-    tma_load_1d_u32(ring_u32 + slot * kSliceBytes, t.rec + r_lo, si.valid * 8u, bar_u32 + 8u * slot, pol);
+    const uint32_t valid = left < (uint64_t)kSlice ? (uint32_t)left : (uint32_t)kSlice;
+    const bool fast = valid == (uint32_t)kSlice && (!kRows || t.kend - r_lo >= (uint64_t)kSlice);
+    t.krow = t.k0 + t.kl;
+    // the fast run after this slice: full slices inside kernel kl and inside the chunk
+    {
+      uint64_t f = t.ce;
+      const uint64_t nfull = t.n / kSlice;
+      if (nfull < f) f = nfull;
+      if (kRows && t.kend != ~0ull && t.kend / kSlice < f) f = t.kend / kSlice;
+      t.cf = f > t.cs ? (uint32_t)f : t.cs;
+    }
+    SlotTag tg;
+    tg.G = t.G0 + sl;
+    tg.krow = t.krow;
+    tg.meta = t.eidx | (fast ? kTagFast : 0u);
+    tags[slot] = tg;
+    mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, valid * 8u);
+    tma_load_1d_u32(ring_u32 + slot * kSliceBytes, t.rec + r_lo, valid * 8u, bar_u32 + 8u * slot, pol);
     return 1;
+  };
+  // lane 0: the next slice into `slot`: the fast run (full slice, same kernel, same
+  // chunk) or issue_slow
+  auto issue = [&](uint32_t slot, bool block) -> int {
+    const uint32_t cs = t.cs;
+    if (cs < t.cf) {
+      t.cs = cs + 1;
+      SlotTag tg;
+      tg.G = t.G0 + cs;
+      tg.krow = t.krow;
+      tg.meta = t.eidx | kTagFast;
+      tags[slot] = tg;
+      mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, kSliceBytes);
+      tma_load_1d_u32(ring_u32 + slot * kSliceBytes, t.rec + (uint64_t)cs * kSlice, kSliceBytes, bar_u32 + 8u * slot,
+                      pol);
+      return 1;
+    }
+    return issue_slow(slot, block);
   };
 
   Ctx c;
@@ -1451,13 +1505,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
       if (r == 2) ended = true;
       // the warp's lowest unread slice, for the monitor; refreshed every 8 slices (a stale,
       // lower value only delays the producer; a warp about to wait sets it in issue())
-      if ((++nit & 7u) == 0 || inflight == 0) front[warp] = inflight ? info[head].G : (ended ? ~0ull : next_G());
+      if ((++nit & 7u) == 0 || inflight == 0) front[warp] = inflight ? tags[head].G : (ended ? ~0ull : next_G());
     }
     inflight = __shfl_sync(kFull, inflight, 0);
     __syncwarp();
     if (inflight == 0) break;  // the stream ended and everything this warp took is done
     const uint32_t slot = head;
-    const SlotInfo si = info[slot];  // written by lane 0 before the __syncwarp above
+    const SlotTag tg = tags[slot];  // written by lane 0 before the __syncwarp above
 #if PASTA_STREAM_PROF
     const unsigned long long q1 = clock64();
 #endif
@@ -1476,23 +1530,24 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
       a[2 * i] = v.x;
       a[2 * i + 1] = v.y;
     }
-    if (si.s == 0 && lane == 0) red_add_u64(args.totals + 0, si.n);
-    // kernel segments of this slice (batch-relative record index r = 256 s + position);
-    // the slice's first kernel was located when it was issued
-    const uint64_t r_lo = (uint64_t)si.s * kSlice;
-    uint32_t kl = si.kl;
-    uint64_t kend = si.kend;
-    if (kRows && si.k0 + kl != k) {
+    if (kRows && tg.krow != k) {  // the slice starts in another kernel row than the warp's run
       if (k != 0xFFFFFFFFu) warp_flush<kRows, kPages>(w, la, o, k, lane);
-      k = si.k0 + kl;
+      k = tg.krow;
     }
     const uint32_t sa = ring_u32 + slot * kSliceBytes;
-    if (si.valid == (uint32_t)kSlice && kend - r_lo >= (uint64_t)kSlice) {
+    if (tg.meta & kTagFast) {
       process_full<kBig, kRows, kPages>(a, sa, cur, oc, la, w, c, o, kRows ? k : 0u, lane);
     } else {
+      // a partial slice or one holding a kernel boundary: segments as the scan does
+      const ChunkEntry e = ents[tg.meta & 7u];
+      const uint64_t r_lo = (tg.G - e.G0) * kSlice;
+      const uint64_t left = e.n - r_lo;
+      const uint32_t valid = left < (uint64_t)kSlice ? (uint32_t)left : (uint32_t)kSlice;
+      uint32_t kl = tg.krow - e.k0;
+      uint64_t kend = (kRows && kl + 1 < e.nk) ? __ldg(e.koffs + kl + 1) : ~0ull;
       uint32_t r0 = 0;
       for (;;) {
-        uint32_t r1 = si.valid;
+        uint32_t r1 = valid;
         if (kRows && kend - r_lo < (uint64_t)r1) r1 = (uint32_t)(kend - r_lo);
         uint32_t vm = 0;
 #pragma unroll
@@ -1502,13 +1557,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
         }
         process_lane<kBig, kRows, kPages>(a, vm, oc, la, w, c, o, kRows ? k : 0u, lane);
         r0 = r1;
-        if (r0 >= si.valid) break;
+        if (r0 >= valid) break;
         // the next kernel of the batch starts inside this slice
         warp_flush<kRows, kPages>(w, la, o, k, lane);
         ++kl;
-        while (kl + 1 < si.nk && __ldg(si.koffs + kl + 1) <= r_lo + r0) ++kl;
-        kend = kl + 1 < si.nk ? __ldg(si.koffs + kl + 1) : ~0ull;
-        k = si.k0 + kl;
+        while (kl + 1 < e.nk && __ldg(e.koffs + kl + 1) <= r_lo + r0) ++kl;
+        kend = kl + 1 < e.nk ? __ldg(e.koffs + kl + 1) : ~0ull;
+        k = e.k0 + kl;
       }
     }
     __syncwarp();
