@@ -89,6 +89,19 @@ __device__ __forceinline__ ulonglong2 lds128(uint32_t a) {
   return v;
 }
 
+// Ordered variants ("memory" clobber): mixed with C++ accesses to the same shared data.
+__device__ __forceinline__ ulonglong2 lds128_o(uint32_t a) {
+  ulonglong2 v;
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts128_o(uint32_t a, uint64_t x, uint64_t y) {
+  asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(x), "l"(y) : "memory");
+}
+__device__ __forceinline__ void sts32_o(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ uint64_t lds64(uint32_t a) {
   uint64_t v;
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));

@@ -38,6 +38,7 @@
 //    at kernel-segment boundaries (per warp, no CTA barrier) and at the end; the
 //    per-kernel page bit is set with atom.or at the page flush.
 #include <cstdint>
+#include <cstddef>
 #include <type_traits>
 
 #include "common.cuh"
@@ -1208,6 +1209,9 @@ struct __align__(16) StreamTurn {
   uint64_t Q, known_tail;
   uint32_t opened, pad;  // chunks opened (entry ring index)
 };
+static_assert(offsetof(StreamTurn, cs) == 8 && offsetof(StreamTurn, G0) == 16 && offsetof(StreamTurn, krow) == 24 &&
+                  offsetof(StreamTurn, eidx) == 28,
+              "the fast issue path reads the turn state as two 16-byte words");
 constexpr int kTurnBytes = kWarps * (int)sizeof(StreamTurn);
 constexpr int kStreamHead = kWarps * kMaxStages * kSlotInfoBytes + kFrontBytes + kTurnBytes;  // see stream_kernel
 static_assert(kStreamHead % 16 == 0, "the ring after the head stays 16-byte aligned");
@@ -1421,18 +1425,19 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
   };
   // lane 0: the next slice into `slot`: the fast run (full slice, same kernel, same
   // chunk) or issue_slow
+  // (shared-memory addresses as 32-bit offsets: no generic-to-shared conversion per slice)
+  const uint32_t t_u32 = smem_u32(&t);
+  const uint32_t tag_u32 = smem_u32(tags);
   auto issue = [&](uint32_t slot, bool block) -> int {
-    const uint32_t cs = t.cs;
-    if (cs < t.cf) {
-      t.cs = cs + 1;
-      SlotTag tg;
-      tg.G = t.G0 + cs;
-      tg.krow = t.krow;
-      tg.meta = t.eidx | kTagFast;
-      tags[slot] = tg;
+    const ulonglong2 h0 = lds128_o(t_u32);  // rec | cs, cf
+    const uint32_t cs = (uint32_t)h0.y;
+    if (cs < (uint32_t)(h0.y >> 32)) {
+      sts32_o(t_u32 + 8u, cs + 1);
+      const ulonglong2 h1 = lds128_o(t_u32 + 16u);  // G0 | krow, eidx
+      sts128_o(tag_u32 + 16u * slot, h1.x + cs, h1.y | ((uint64_t)kTagFast << 32));
       mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, kSliceBytes);
-      tma_load_1d_u32(ring_u32 + slot * kSliceBytes, t.rec + (uint64_t)cs * kSlice, kSliceBytes, bar_u32 + 8u * slot,
-                      pol);
+      tma_load_1d_u32(ring_u32 + slot * kSliceBytes, reinterpret_cast<const uint64_t*>(h0.x) + (uint64_t)cs * kSlice,
+                      kSliceBytes, bar_u32 + 8u * slot, pol);
       return 1;
     }
     return issue_slow(slot, block);
@@ -1505,13 +1510,20 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
       if (r == 2) ended = true;
       // the warp's lowest unread slice, for the monitor; refreshed every 8 slices (a stale,
       // lower value only delays the producer; a warp about to wait sets it in issue())
-      if ((++nit & 7u) == 0 || inflight == 0) front[warp] = inflight ? tags[head].G : (ended ? ~0ull : next_G());
+      if ((++nit & 7u) == 0 || inflight == 0)
+        front[warp] = inflight ? lds128_o(tag_u32 + 16u * head).x : (ended ? ~0ull : next_G());
     }
     inflight = __shfl_sync(kFull, inflight, 0);
     __syncwarp();
     if (inflight == 0) break;  // the stream ended and everything this warp took is done
     const uint32_t slot = head;
-    const SlotTag tg = tags[slot];  // written by lane 0 before the __syncwarp above
+    SlotTag tg;  // written by lane 0 before the __syncwarp above
+    {
+      const ulonglong2 v = lds128_o(tag_u32 + 16u * slot);
+      tg.G = v.x;
+      tg.krow = (uint32_t)v.y;
+      tg.meta = (uint32_t)(v.y >> 32);
+    }
 #if PASTA_STREAM_PROF
     const unsigned long long q1 = clock64();
 #endif
