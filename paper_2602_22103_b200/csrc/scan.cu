@@ -90,6 +90,9 @@ constexpr int kSlice = 256;                 // records per slice (8 per lane)
 #ifndef PASTA_TIER_S
 #define PASTA_TIER_S 1  // tier S (one owner, scattered pages) before tier L
 #endif
+#ifndef PASTA_TMA_PAIR
+#define PASTA_TMA_PAIR 1  // one 4 KiB bulk copy per two slices when the ring has an even depth
+#endif
 #ifndef PASTA_ISSUE2
 #define PASTA_ISSUE2 0  // TMA refills in pairs
 #endif
@@ -746,7 +749,7 @@ __device__ __forceinline__ uint32_t kernel_of(const uint64_t* __restrict__ koffs
   return lo;
 }
 
-template <bool kBig, bool kRows, int kPages, bool kIL>
+template <bool kBig, bool kRows, int kPages, bool kIL, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, const int stages, const int cache_on) {
   // Programmatic dependent launch: the next analyze call's scan may start its prologue
   // (barrier init, range table into shared memory) on free SMs while this one runs. A
@@ -833,8 +836,26 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
     mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, bytes);
     tma_load_1d_u32(ring_u32 + slot * kSliceBytes, args.rec + gsl(j) * kSlice, bytes, bar_u32 + 8u * slot, pol);
   };
-  if (lane == 0)
-    for (uint32_t j = 0; j < (uint32_t)stages && j < nmy; ++j) issue(j, j);
+  // kPair: double slots, relative slices 2p, 2p + 1 in one 4 KiB copy (contiguous in both
+  // schedules: interleaved chunks hold an even number of slices, the partial tail is the
+  // trace's last slice). Half as many bulk copies in flight for the same bytes: llama
+  // 13.55 -> 13.22 ms (B200 A/B; the read microbenchmark scripts/micro/read_bw.cu shows
+  // fewer, larger copies per SM reaching more of HBM). Used when the ring depth is even.
+  const uint32_t S2 = (uint32_t)stages / 2u;
+  auto issue_pair = [&](uint32_t p, uint32_t s2) {
+    const uint32_t j = 2u * p;
+    uint32_t bytes = j < nfull ? kSliceBytes : tail_valid * 8u;
+    if (j + 1 < nmy) bytes += j + 1 < nfull ? kSliceBytes : tail_valid * 8u;
+    mbar_arrive_expect_tx_u32(bar_u32 + 8u * s2, bytes);
+    tma_load_1d_u32(ring_u32 + s2 * 2u * kSliceBytes, args.rec + gsl(j) * kSlice, bytes, bar_u32 + 8u * s2, pol);
+  };
+  if (lane == 0) {
+    if constexpr (kPair) {
+      for (uint32_t p = 0; p < S2 && 2u * p < nmy; ++p) issue_pair(p, p);
+    } else {
+      for (uint32_t j = 0; j < (uint32_t)stages && j < nmy; ++j) issue(j, j);
+    }
+  }
   if (args.early == 1) {
     grid_dep_wait();
     grid_dep_launch_dependents();
@@ -960,8 +981,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
 
   uint32_t slot = 0, phase = 0;
   for (uint32_t j = 0; j < nmy; ++j) {
-    const uint32_t sa = ring_u32 + slot * kSliceBytes;
-    mbar_wait_u32(bar_u32 + 8u * slot, phase);
+    const uint32_t sa = ring_u32 + slot * (kPair ? 2u : 1u) * kSliceBytes + (kPair ? (j & 1u) * kSliceBytes : 0u);
+    if (!kPair || (j & 1u) == 0) mbar_wait_u32(bar_u32 + 8u * slot, phase);
 #if PASTA_TRACE_TIMING
     if (lane == 0 && j == 0) g_warp_times[tslot + 1] = gtimer();
     if (lane == 0 && j == nmy / 4) g_warp_times[tslot + 2] = gtimer();
@@ -1009,6 +1030,15 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
     // the slot is free again (every lane has consumed its values): refill it with the
     // slice `stages` ahead
     __syncwarp();
+    if constexpr (kPair) {
+      if ((j & 1u) || j + 1 == nmy) {  // both slices of the double slot consumed
+        if (lane == 0 && 2u * ((j >> 1) + S2) < nmy) issue_pair((j >> 1) + S2, slot);
+        if (++slot == S2) {
+          slot = 0;
+          phase ^= 1u;
+        }
+      }
+    } else {
 #if PASTA_ISSUE2
     // refills in pairs (every odd slice, this slot and the previous one): the issue path
     // recomputes its shared-memory and source addresses (register pressure), and two
@@ -1019,11 +1049,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
       if (j + stages < nmy) issue(j + stages, slot);
     }
 #else
-    if (lane == 0 && j + stages < nmy) issue(j + stages, slot);
+      if (lane == 0 && j + stages < nmy) issue(j + stages, slot);
 #endif
-    if (++slot == (uint32_t)stages) {
-      slot = 0;
-      phase ^= 1u;
+      if (++slot == (uint32_t)stages) {
+        slot = 0;
+        phase ^= 1u;
+      }
     }
   }
   warp_flush<kRows, kPages>(w, la, o, k, lane);
@@ -1124,7 +1155,11 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
   const int stages = stages_for(a.A, kBig, cache_on ? kCacheBytes : 0);
   const int smem = ring_bytes(stages) + kBarBytes + kLaBytes + kPfBytes + (kBig ? 0 : (int)(16ull * a.A)) +
                    (cache_on ? kCacheBytes : 0);
-  auto fn = a.log_ic >= 0 ? scan_kernel<kBig, kRows, kPages, true> : scan_kernel<kBig, kRows, kPages, false>;
+  // paired 4 KiB copies need an even ring depth and (interleaved) chunks of >= 2 slices
+  const bool pair = PASTA_TMA_PAIR && stages % 2 == 0 && a.log_ic != 0;
+  auto fn = a.log_ic >= 0 ? (pair ? scan_kernel<kBig, kRows, kPages, true, true> : scan_kernel<kBig, kRows, kPages, true, false>)
+                          : (pair ? scan_kernel<kBig, kRows, kPages, false, true>
+                                  : scan_kernel<kBig, kRows, kPages, false, false>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   // launched as a programmatic dependent of the stream's previous kernel (the kernel

@@ -1,0 +1,9 @@
+# usage: bash scripts/ab_rich2.sh v1 v2 ...  (rich-record scan A/B: clean, 5 % singles, 5 % in 32-record bursts; gpt2m 2e9)
+for rep in 1 2; do
+for v in "$@"; do
+  lib=build/variants/libpasta_$v.so; [ "$v" = base ] && lib=paper_2602_22103_b200/libpasta.so
+  for mb in "0 0" "0.05 0" "0.05 5"; do
+    echo "$v $mb: $(PASTA_LIB=$lib timeout 300 python scripts/rich_bench.py gpt2m 2000000000 $mb 2>&1 | tail -1)"
+  done
+done
+done
