@@ -186,8 +186,11 @@ size_t topk_merge_scratch_bytes(uint64_t n, int grid);
 // Enqueues the whole radix-select + gather + sort pipeline; `launch` is called once
 // per kernel launch with the phase's cudaError_t (for counting / timing hooks).
 typedef void (*launch_hook)(void* ctx, int begin);
+// *head_state: 0 = unknown (the scratch is fresh or pasta_topk_merge used it), 1 / 2 =
+// head 0 / head 1 is zero; run_topk updates it (the caller keeps it per scratch buffer).
 cudaError_t run_topk(const uint64_t* page_counts, uint64_t P, uint32_t k, uint64_t* out_page, uint64_t* out_count,
-                     uint64_t* out_found, void* scratch, int max_ctas, cudaStream_t st, int* n_launches);
+                     uint64_t* out_found, void* scratch, int max_ctas, cudaStream_t st, int* n_launches,
+                     int* head_state);
 
 // Prefix copies of one top-k_max list into several top-k outputs (pasta_topk_many /
 // pasta_topk_prefix): entry j gets the first k_j entries and found_j = min(k_j, found).

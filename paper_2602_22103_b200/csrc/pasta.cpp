@@ -71,6 +71,7 @@ struct pasta_trace {
   // top-K scratch
   void* d_topk = nullptr;
   size_t topk_bytes = 0;
+  int topk_heads = 0;  // run_topk's head state for d_topk (0 = unknown)
 
   // streaming consumers opened on this handle and not destroyed yet (pasta_close ends them)
   std::vector<pasta_stream*> streams;
@@ -720,12 +721,15 @@ int pasta_topk(pasta_trace* h, const uint64_t* page_counts, uint64_t P, uint32_t
     }
     h->d_topk = nullptr;
     h->topk_bytes = 0;
+    h->topk_heads = 0;
     if (cudaMalloc(&h->d_topk, need) != cudaSuccess) return PASTA_ECUDA;
     h->topk_bytes = need;
   }
   int nl = 0;
   Timed t(h, PASTA_PH_TOPK, h->stream);
-  cudaError_t e = run_topk(page_counts, P, k, out_page, out_count, out_found, h->d_topk, max_ctas, h->stream, &nl);
+  cudaError_t e =
+      run_topk(page_counts, P, k, out_page, out_count, out_found, h->d_topk, max_ctas, h->stream, &nl, &h->topk_heads);
+  if (e != cudaSuccess) h->topk_heads = 0;
   h->launches += (uint64_t)nl;
   return cuda_status(e);
 }
@@ -792,11 +796,13 @@ int pasta_topk_merge(pasta_trace* h, const uint64_t* cand_page, const uint64_t* 
     }
     h->d_topk = nullptr;
     h->topk_bytes = 0;
+    h->topk_heads = 0;
     if (cudaMalloc(&h->d_topk, need) != cudaSuccess) return PASTA_ECUDA;
     h->topk_bytes = need;
   }
   int nl = 0;
   Timed t(h, PASTA_PH_MERGE, h->stream);
+  h->topk_heads = 0;  // the merge carves the same scratch: the next pasta_topk zeroes a head first
   cudaError_t e = run_topk_merge(cand_page, cand_count, g, k, shard_pages, out_page, out_count, out_found, h->d_topk,
                                  grid, h->stream, &nl);
   h->launches += (uint64_t)nl;

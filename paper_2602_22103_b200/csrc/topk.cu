@@ -96,10 +96,14 @@ struct TkHead {  // zeroed before every call
   unsigned long long cfill;           // keys of the first range copied to the compact list
 };
 
+constexpr size_t kHeadBytes = (sizeof(TkHead) + 255) / 256 * 256;  // a head's slot in the scratch
+constexpr uint32_t kHeadWords = (uint32_t)(kHeadBytes / 16);
+
 struct TkArgs {
   const uint64_t* pc;
   uint64_t P, K;
-  TkHead* head;
+  TkHead* head;       // zero on entry (zeroed by the previous call or a memset)
+  TkHead* next_head;  // the other head: zeroed by this launch for the next call
   u128* buf;     // candidate buffer: CTA c appends to its own region [c * rcap, (c + 1) * rcap)
   uint64_t rcap; // region capacity (keys)
   u128* keys;    // gathered keys [kcap]
@@ -472,6 +476,11 @@ __global__ void __launch_bounds__(kTB, 2) topk_kernel(const __grid_constant__ Tk
   extern __shared__ u128 tile[];  // [kFastMax] (dynamic): sort tiles, the fast finish
   for (int i = threadIdx.x; i < kBins; i += kTB) sh[i] = 0;
   if (threadIdx.x == 0) sfill = 0;
+  {  // the next call's head (no memset launch per call); nothing in this launch uses it
+    uint4* nh = reinterpret_cast<uint4*>(a.next_head);
+    for (uint32_t i = blockIdx.x * kTB + threadIdx.x; i < kHeadWords; i += gridDim.x * kTB)
+      nh[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
   __syncthreads();
   TkHead* hd = a.head;
   const uint64_t pmask = a.pbits ? ((~0ull) >> (64 - a.pbits)) : 0ull;
@@ -786,8 +795,7 @@ uint64_t topk_region_cap(uint64_t P, int max_ctas) {
 size_t topk_scratch_bytes(uint64_t k, uint64_t P, int max_ctas) {
   const uint64_t m = k < P ? k : P;
   const uint64_t Kp = pow2_ceil(m < 2 ? 2 : m);
-  return (sizeof(TkHead) + 255) / 256 * 256 + 16ull * kFastMax + 16 * topk_region_cap(P, max_ctas) * (uint64_t)max_ctas +
-         16 * Kp;
+  return 2 * kHeadBytes + 16ull * kFastMax + 16 * topk_region_cap(P, max_ctas) * (uint64_t)max_ctas + 16 * Kp;
 }
 
 size_t topk_merge_scratch_bytes(uint64_t n, int grid) {
@@ -827,15 +835,22 @@ cudaError_t sort_keys(uint64_t* key_c, uint64_t* key_p, uint64_t Kp, int grid, c
 }
 
 cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_page, uint64_t* out_count,
-                     uint64_t* out_found, void* scratch, int max_ctas, cudaStream_t st, int* n_launches) {
+                     uint64_t* out_found, void* scratch, int max_ctas, cudaStream_t st, int* n_launches,
+                     int* head_state) {
   const uint64_t m = (uint64_t)k < P ? (uint64_t)k : P;
   TkArgs a;
   a.pc = pc;
   a.P = P;
   a.K = k;
   char* b = static_cast<char*>(scratch);
-  a.head = reinterpret_cast<TkHead*>(b);
-  b += (sizeof(TkHead) + 255) / 256 * 256;
+  // two heads: each call uses the one the previous call zeroed and zeroes the other;
+  // *head_state = 0 (unknown: fresh scratch, or the merge used it) -> memset head 0
+  TkHead* h0 = reinterpret_cast<TkHead*>(b);
+  TkHead* h1 = reinterpret_cast<TkHead*>(b + kHeadBytes);
+  const bool use1 = *head_state == 2;
+  a.head = use1 ? h1 : h0;
+  a.next_head = use1 ? h0 : h1;
+  b += 2 * kHeadBytes;
   a.compact = reinterpret_cast<u128*>(b);
   b += 16ull * kFastMax;
   a.rcap = topk_region_cap(P, max_ctas);
@@ -847,8 +862,11 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
   a.out_count = out_count;
   a.out_found = out_found;
   a.pbits = P > 1 ? 64 - __builtin_clzll(P - 1) : 0;
-  cudaError_t e = cudaMemsetAsync(a.head, 0, sizeof(TkHead), st);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (*head_state == 0) {
+    e = cudaMemsetAsync(a.head, 0, sizeof(TkHead), st);
+    if (e != cudaSuccess) return e;
+  }
   constexpr int kDynSmem = 16 * kFastMax;
   static int coop_blocks = 0;  // co-resident blocks per SM for the cooperative launch
   if (coop_blocks == 0) {
@@ -871,6 +889,7 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
   if (g > max_ctas) g = max_ctas;
   void* args[] = {(void*)&a};
   PASTA_TRY(cudaLaunchCooperativeKernel((void*)topk_kernel, dim3(g), dim3(kTB), args, kDynSmem, st));
+  *head_state = use1 ? 1 : 2;  // the head zeroed by this launch is the next call's
   return cudaSuccess;
 }
 
