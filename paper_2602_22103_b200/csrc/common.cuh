@@ -98,6 +98,11 @@ __device__ __forceinline__ ulonglong2 lds128_o(uint32_t a) {
 __device__ __forceinline__ void sts128_o(uint32_t a, uint64_t x, uint64_t y) {
   asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(x), "l"(y) : "memory");
 }
+__device__ __forceinline__ uint32_t lds32_o(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ void sts32_o(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }

@@ -37,6 +37,7 @@ struct ScanArgs {
   uint64_t wk_magic;         // ceil(2^64 / window_kernels) for window_kernels >= 2
   const ulonglong2* chunk_k; // [chunks] (k, koffs[k+1]) of each interleaved chunk's first record (scratch)
   int32_t log_ic;            // log2 slices per interleaved chunk, -1 = contiguous (scan_schedule)
+  unsigned long long* chunk_ctr;  // interleaved: the dynamic schedule's chunk counter (scratch, reset by the pre-pass)
   // tensor level (NEXT f3): all nullptr when off
   const uint32_t* tids;      // [A] tensor id of table interval r, kNoTensor = none
   uint64_t* tensor_counts;   // [max_tids]

@@ -281,6 +281,11 @@ int scan_range(pasta_trace* h, const uint64_t* rec, uint64_t n, uint64_t g0, Sca
       h->scan_bytes = sneed;
     }
     a.chunk_k = reinterpret_cast<const ulonglong2*>(h->d_scan);
+    a.chunk_ctr = nullptr;
+    if (a.log_ic >= 0) {  // the counter follows the chunk map (scan_scratch_bytes)
+      const uint64_t nch = ((cnt + 255) / 256 + (1ull << a.log_ic) - 1) >> a.log_ic;
+      a.chunk_ctr = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(h->d_scan) + 16 * nch);
+    }
     Timed t(h, PASTA_PH_SCAN, st);
     int nl = 0;
     cudaError_t e = launch_scan(a, grid, st, &nl);

@@ -105,8 +105,11 @@ constexpr int kSlice = 256;                 // records per slice (8 per lane)
 #ifndef PASTA_IL_LOG_CHUNK
 #define PASTA_IL_LOG_CHUNK 6  // log2 slices per interleaved chunk
 #endif
+#ifndef PASTA_IL_DYNAMIC
+#define PASTA_IL_DYNAMIC 1  // interleaved schedule: chunks after the first taken from a global counter
+#endif
 #ifndef PASTA_IL_MIN_CHUNKS
-#define PASTA_IL_MIN_CHUNKS 16  // interleave only when every warp gets this many chunks
+#define PASTA_IL_MIN_CHUNKS 4  // interleave only when every warp gets this many chunks (dynamic: rn50 +2.7 %)
 #endif
 constexpr uint32_t kSliceBytes = kSlice * 8;  // 2 KiB
 constexpr int kMaxStages = 8;
@@ -779,16 +782,36 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   //  * interleaved schedule (kIL): chunks of 2^lc slices, warp gw takes chunks gw,
   //    gw + W, ..., so every warp samples the whole trace (cheap sweeps, tiled jumps and
   //    scattered records alike) and no warp straggles behind an expensive region.
+  //  * dynamic interleaved (kIL, PASTA_IL_DYNAMIC): the warp's first chunk is gw, every
+  //    later one comes from a global counter (lane 0, one atomic per chunk, taken when the
+  //    previous chunk starts), so warps that drew cheap chunks take more and all warps end
+  //    within about one chunk of each other (static interleaving: the last warp ended
+  //    5-8 % after the median one, scripts/warp_times.py).
   uint32_t lc = 0, icm = 0, nmy;
   uint64_t s0 = 0;
   bool tail_mine;
+  uint32_t nch = 0;
+  const uint32_t ring_u32 = smem_u32(sm) + (uint32_t)(warp * stages) * kSliceBytes;
+  const uint32_t bar_u32 = smem_u32(bars + warp * kMaxStages);
+  // the ids of this warp's m-th chunk live in its spare barrier slots 6 and 7 (stages <= 6):
+  // cid(m) = slot 6 + (m & 1)
+  const uint32_t cid_u32 = bar_u32 + 8u * 6u;
+  auto clen = [&](uint32_t q) -> uint32_t { return q + 1 == nch ? (uint32_t)(nsl - ((uint64_t)q << lc)) : icm + 1u; };
   if constexpr (kIL) {
     lc = args.log_ic;
     icm = (1u << lc) - 1u;
-    const uint64_t nch = (nsl + icm) >> lc;
+    nch = (uint32_t)((nsl + icm) >> lc);
+#if PASTA_IL_DYNAMIC
+    // until chunk 0 starts (and takes chunk 1's id) the warp knows only its first chunk
+    tail_mine = gwarp + 1 == nch;
+    nmy = gwarp < nch ? clen(gwarp) : 0u;
+    if (lane == 0) sts32_o(cid_u32, gwarp);
+    __syncwarp();
+#else
     const uint64_t nct = gwarp < nch ? (nch - gwarp + nwarp - 1) / nwarp : 0;  // my chunks
     tail_mine = nct > 0 && (gwarp + (nct - 1) * nwarp == nch - 1);            // I own the last chunk
-    nmy = (uint32_t)((nct << lc) - (tail_mine ? (nch << lc) - nsl : 0));
+    nmy = (uint32_t)((nct << lc) - (tail_mine ? ((uint64_t)nch << lc) - nsl : 0));
+#endif
   } else {
     s0 = (uint64_t)gwarp * nsl / nwarp;
     const uint64_t s1 = (uint64_t)(gwarp + 1) * nsl / nwarp;
@@ -797,13 +820,17 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   }
   auto gsl = [&](uint32_t j) -> uint64_t {
     // chunk index < 2^32 (a launch holds < 2^32 slices)
-    if constexpr (kIL) return ((uint64_t)((j >> lc) * nwarp + gwarp) << lc) + (j & icm);
-    else return s0 + j;
+    if constexpr (kIL) {
+#if PASTA_IL_DYNAMIC
+      return ((uint64_t)lds32_o(cid_u32 + 4u * ((j >> lc) & 1u)) << lc) + (j & icm);
+#else
+      return ((uint64_t)((j >> lc) * nwarp + gwarp) << lc) + (j & icm);
+#endif
+    } else {
+      return s0 + j;
+    }
   };
-  const uint32_t nfull = (tail_mine && nmy > 0 && tail_valid != (uint32_t)kSlice) ? nmy - 1 : nmy;
-
-  const uint32_t ring_u32 = smem_u32(sm) + (uint32_t)(warp * stages) * kSliceBytes;
-  const uint32_t bar_u32 = smem_u32(bars + warp * kMaxStages);
+  uint32_t nfull = (tail_mine && nmy > 0 && tail_valid != (uint32_t)kSlice) ? nmy - 1 : nmy;
 
   if (lane == 0) {
     for (int j = 0; j < stages; ++j) mbar_init(bars + warp * kMaxStages + j, 1);
@@ -922,6 +949,24 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
     if (kRows && K > 1 && j < nmy && lane == 0) cp_async_16(pf_u32, args.chunk_k + (gsl(j) >> lc));
   };
   auto enter_chunk = [&](uint32_t j) {
+#if PASTA_IL_DYNAMIC
+    if constexpr (kIL) {
+      // take the chunk after this one (all lanes: nmy / nfull are warp-uniform)
+      const uint32_t m = j >> lc;
+      uint32_t qn = 0;
+      if (lane == 0) {
+        qn = nwarp + (uint32_t)atomicAdd(args.chunk_ctr, 1ull);
+        sts32_o(cid_u32 + 4u * ((m + 1u) & 1u), qn);
+      }
+      __syncwarp();
+      qn = __shfl_sync(kFull, qn, 0);
+      const uint32_t qm = lds32_o(cid_u32 + 4u * (m & 1u));
+      const bool more = qn < nch;
+      nmy = j + clen(qm) + (more ? clen(qn) : 0u);
+      tail_mine = (more ? qn : qm) + 1 == nch;
+      nfull = (tail_mine && tail_valid != (uint32_t)kSlice) ? nmy - 1 : nmy;
+    }
+#endif
     if (kRows && K > 1) {
       if (lane == 0) cp_async_wait_all();
       __syncwarp();
@@ -941,7 +986,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   auto next_event_after = [&](uint32_t j) -> uint32_t {
     if constexpr (kIL) {
       const uint32_t jb = j & ~icm;
-      uint64_t e = (kRows && K > 1) ? (uint64_t)jb + icm + 1 : nfull;
+      // chunk starts are events (the chunk map; with the dynamic schedule also the next grab)
+      uint64_t e = ((kRows && K > 1) || PASTA_IL_DYNAMIC) ? (uint64_t)jb + icm + 1 : nfull;
       if (nfull < e) e = nfull;
       if (kRows && kend != ~0ull) {
         const uint64_t gb = args.gidx0 + gsl(jb) * kSlice;
@@ -963,7 +1009,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   uint32_t jev;
   if constexpr (kIL) {
     prefetch_chunk(0);
-    if (nmy > 0) enter_chunk(0);
+    if (nmy > 0) enter_chunk(0);  // (dynamic: takes chunk 1's id, extends nmy)
     jev = nmy > 0 ? next_event_after(0) : 0;
     if (kRows && K > 1 && nmy > 0) {
       // the first slice itself may hold a boundary
@@ -1131,7 +1177,7 @@ int stages_for(uint32_t A, bool big, long extra = 0) {
   const long table = big ? 0 : 16l * A;
   const long avail = (long)kSmemLimit - kBarBytes - kLaBytes - kPfBytes - table - extra;
   long st = avail / ring_bytes(1);
-  if (st > kMaxStages) st = kMaxStages;
+  if (st > 6) st = 6;  // barrier slots 6 and 7 of each warp hold the dynamic schedule's chunk ids
   return (int)st;
 }
 
@@ -1141,10 +1187,13 @@ int stages_for(uint32_t A, bool big, long extra = 0) {
 #endif
 bool cache_fits(uint32_t A, bool big) { return kCacheBits && stages_for(A, big, kCacheBytes) >= PASTA_PCACHE_MIN_STAGES; }
 
-// chunk_k[c] = (kernel segment k of interleaved chunk c's first record, koffs[k + 1]).
-__global__ void chunk_kernel_map(const __grid_constant__ ScanArgs a, ulonglong2* chunk_k, uint64_t nch) {
+// chunk_k[c] = (kernel segment k of interleaved chunk c's first record, koffs[k + 1])
+// (fill: kernel rows with several kernels); thread 0 also resets the dynamic schedule's
+// chunk counter. Runs before every interleaved scan.
+__global__ void chunk_kernel_map(const __grid_constant__ ScanArgs a, ulonglong2* chunk_k, uint64_t nch, int fill) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nch) return;
+  if (i == 0 && a.chunk_ctr) *a.chunk_ctr = 0;
+  if (!fill || i >= nch) return;
   const uint32_t k = kernel_of(a.koffs, a.n_kernels, a.gidx0 + (i << a.log_ic) * kSlice);
   chunk_k[i] = make_ulonglong2(k, k + 1 < a.n_kernels ? a.koffs[k + 1] : ~0ull);
 }
@@ -1157,6 +1206,8 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
                    (cache_on ? kCacheBytes : 0);
   // paired 4 KiB copies need an even ring depth and (interleaved) chunks of >= 2 slices
   const bool pair = PASTA_TMA_PAIR && stages % 2 == 0 && a.log_ic != 0;
+  // the dynamic interleaved schedule needs chunks of more than a ring depth of slices
+  if (PASTA_IL_DYNAMIC && a.log_ic >= 0 && (1 << a.log_ic) < 2 * stages) return cudaErrorInvalidValue;
   auto fn = a.log_ic >= 0 ? (pair ? scan_kernel<kBig, kRows, kPages, true, true> : scan_kernel<kBig, kRows, kPages, true, false>)
                           : (pair ? scan_kernel<kBig, kRows, kPages, false, true>
                                   : scan_kernel<kBig, kRows, kPages, false, false>);
@@ -2173,14 +2224,17 @@ int scan_schedule(uint64_t nbody, int grid, uint32_t force) {
   const uint64_t nwarp = (uint64_t)grid * kWarps;
   if (force == PASTA_SCHED_CONTIGUOUS) return -1;
   if (force == PASTA_SCHED_INTERLEAVED) {
-    // the largest chunk (<= PASTA_IL_LOG_CHUNK) that still gives every warp one
-    int lc = 0;
+    // the largest chunk (<= PASTA_IL_LOG_CHUNK) that still gives every warp one; the
+    // dynamic schedule needs chunks of >= 8 slices (a warp's refills run up to a ring
+    // depth, <= 6 slices, ahead, and only the next chunk's id is known in advance)
+    int lc = PASTA_IL_DYNAMIC ? 3 : 0;
     while (lc < PASTA_IL_LOG_CHUNK && (nsl >> (lc + 1)) >= nwarp) ++lc;
     return lc;
   }
   return (PASTA_IL && (nsl >> PASTA_IL_LOG_CHUNK) >= nwarp * PASTA_IL_MIN_CHUNKS) ? PASTA_IL_LOG_CHUNK : -1;
 }
 
+// [chunk map: 16 B per chunk | 256 B: the dynamic schedule's chunk counter at offset 0]
 size_t scan_scratch_bytes(uint64_t nbody, int log_ic) {
   if (log_ic < 0) return 256;
   const uint64_t nsl = (nbody + kSlice - 1) / kSlice;
@@ -2207,10 +2261,12 @@ int scan_smem_bytes(uint32_t A, bool big_table) {
 cudaError_t launch_scan(const ScanArgs& a, int grid, cudaStream_t st, int* launches) {
   const bool big = !scan_table_fits_smem(a.A);
   const bool rows = a.kac != nullptr;  // per-kernel outputs all require kernel rows
-  if (a.log_ic >= 0 && rows && a.n_kernels > 1 && a.nbody > 0) {
+  const bool fill = a.log_ic >= 0 && rows && a.n_kernels > 1 && a.nbody > 0;
+  if (fill || (PASTA_IL_DYNAMIC && a.log_ic >= 0 && a.nbody > 0)) {
     const uint64_t nsl = (a.nbody + kSlice - 1) / kSlice;
     const uint64_t nch = (nsl + (1ull << a.log_ic) - 1) >> a.log_ic;
-    chunk_kernel_map<<<(unsigned)((nch + 255) / 256), 256, 0, st>>>(a, const_cast<ulonglong2*>(a.chunk_k), nch);
+    chunk_kernel_map<<<fill ? (unsigned)((nch + 255) / 256) : 1u, 256, 0, st>>>(
+        a, const_cast<ulonglong2*>(a.chunk_k), nch, fill ? 1 : 0);
     const cudaError_t e0 = cudaGetLastError();
     if (e0 != cudaSuccess) return e0;
     ++*launches;
