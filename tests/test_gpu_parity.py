@@ -485,6 +485,29 @@ def test_full_config_bit_exact(name):
     assert_parity(g, r, kernel_rows=True, kernel_pages=p.want_kernel_pages, label=name)
 
 
+@pytest.mark.parametrize("name,n", [("gpt2m", 1 << 24), ("llama", 1 << 26), ("uvm", 1 << 25), ("rn50", 3 << 23)])
+def test_dynamic_interleaved_schedule_prefixes(name, n):
+    """The interleaved schedule with dynamically taken chunks (forced, so the chunk size is
+    the largest that gives every warp one: 16-64 slices here, a few hundred chunks taken
+    from the counter after the static first round), on plan prefixes cut inside kernels,
+    every output against the whole-prefix oracle; 4 KiB paired copies (4-stage rings) and
+    single copies (uvm's 3-stage ring)."""
+    p = tracegen.build_plan(name)
+    ko = [int(x) for x in p.kernel_offsets if int(x) < n] + [n]
+    drec = torch.empty(n, dtype=torch.int64, device=DEV)
+    tracegen.device_records(tracegen.DevicePlan(p, DEV), drec, 0, n)
+    tr = gpu_trace(DEV, p.va_lo, p.va_hi, p.allocs, schedule="interleaved")
+    g = run_gpu(tr, drec, p.page_shift, ko, kernel_rows=True, kernel_pages=p.want_kernel_pages, topk=(1, 1024))
+    tr.close()
+    del drec
+    o = oracle_trace(p.va_lo, p.va_hi, p.allocs)
+    o.analyze_parallel(lambda j0, j1: tracegen.host_records(p, j0, j1), ko, p.page_shift, kernel_rows=True,
+                       kernel_pages=p.want_kernel_pages)
+    r = oracle_results(o, kernel_rows=True, kernel_pages=p.want_kernel_pages, topk=(1, 1024))
+    assert int(r["totals3"][0]) == n
+    assert_parity(g, r, kernel_rows=True, kernel_pages=p.want_kernel_pages, label=f"{name}/{n}/dynamic")
+
+
 def _table(rng, A, va_lo, page_shift):
     """A live ranges packed upward from va_lo: sizes 1 B .. 6 pages, half of them adjacent
     to their predecessor, the rest after a gap of up to 2 pages."""
