@@ -120,7 +120,7 @@ int scan_warps();
 // Scan schedule of a launch over nbody records on `grid` CTAs: log2 slices per
 // interleaved chunk, or -1 for contiguous per-warp ranges; and the chunk map scratch.
 // force: 0 = automatic, else PASTA_SCHED_CONTIGUOUS / PASTA_SCHED_INTERLEAVED.
-int scan_schedule(uint64_t nbody, int grid, uint32_t force);
+int scan_schedule(uint64_t nbody, int grid, uint32_t force, uint32_t A);
 size_t scan_scratch_bytes(uint64_t nbody, int log_ic);
 
 cudaError_t launch_finalize_bitmap(const uint64_t* page_counts, uint64_t P, uint64_t* bitmap, uint64_t* unique_out,

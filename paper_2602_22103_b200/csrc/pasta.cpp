@@ -267,7 +267,7 @@ int scan_range(pasta_trace* h, const uint64_t* rec, uint64_t n, uint64_t g0, Sca
     // calls spread over every SM (lowest latency for one call).
     const uint64_t wpc = (uint64_t)scan_warps() * (a.early == 2 ? kChainSlicesPerWarp : 1u);
     const int grid = (int)std::min<uint64_t>((uint64_t)h->sm_count, std::max<uint64_t>(1, (slices + wpc - 1) / wpc));
-    a.log_ic = scan_schedule(cnt, grid, h->sched);
+    a.log_ic = scan_schedule(cnt, grid, h->sched, a.A);
     if (a.log_ic >= 0 && a.early == 2) a.early = 1;  // the chunk-map pre-pass is this scan's predecessor
     const size_t sneed = scan_scratch_bytes(cnt, a.log_ic);
     if (sneed > h->scan_bytes) {
