@@ -524,7 +524,8 @@ __global__ void __launch_bounds__(kTB, 2) topk_kernel(const __grid_constant__ Tk
           // fast finish: the keys above the first range and the range itself (compacted)
           // are few: block 0 sorts them all and keeps the first K'; the others are done
           const uint64_t above = __ldcg(&hd->slots), total = __ldcg(&hd->fill[1]);
-          if (total <= kFastMax && above + total <= kFastMax) {
+          // (only if no CTA's region overflowed: the compact list holds whole regions)
+          if (total <= kFastMax && above + total <= kFastMax && __ldcg(&hd->overflow[1]) == 0u) {
             if (blockIdx.x == 0) {
               const uint32_t n = (uint32_t)(above + total);
               uint32_t n2 = 2;
@@ -887,6 +888,10 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
   if (w < 1) w = 1;
   if ((uint64_t)g > w) g = (int)w;
   if (g > max_ctas) g = max_ctas;
+  // the candidate buffer (sized for max_ctas regions) split over the CTAs actually
+  // launched: regions of >= min(P, 2^20) / g keys, so a pass over P <= 2^20 counts
+  // never overflows a region (a small P runs on few CTAs)
+  a.rcap = topk_region_cap(P, max_ctas) * (uint64_t)max_ctas / (uint64_t)g;
   void* args[] = {(void*)&a};
   PASTA_TRY(cudaLaunchCooperativeKernel((void*)topk_kernel, dim3(g), dim3(kTB), args, kDynSmem, st));
   *head_state = use1 ? 1 : 2;  // the head zeroed by this launch is the next call's

@@ -61,8 +61,20 @@ for i in range(n_topk):
     p, cc, f = tr.topk(tp._t(c), K)
     tr.sync()
     rp, rc, rf = oracle.topk(c, K)
-    assert int(tp.u64(f)[0]) == rf and np.array_equal(tp.u64(cc), rc) and np.array_equal(tp.u64(p), rp), \
-        f"stress topk {i}: P={P} kind={kind} K={K}"
+    ok = int(tp.u64(f)[0]) == rf and np.array_equal(tp.u64(cc), rc) and np.array_equal(tp.u64(p), rp)
+    if not ok:
+        print(f"stress topk {i}: P={P} kind={kind} K={K} counts[:8]={c[:8]} found gpu/oracle {int(tp.u64(f)[0])}/{rf}"
+              f" gpu pages {tp.u64(p)[:8]} counts {tp.u64(cc)[:8]} oracle pages {rp[:8]} counts {rc[:8]}", flush=True)
+        # the same input again, and once more after a fresh handle
+        p2, cc2, f2 = tr.topk(tp._t(c), K)
+        tr.sync()
+        print("  again:", int(tp.u64(f2)[0]), tp.u64(p2)[:8], tp.u64(cc2)[:8], flush=True)
+        t2 = pb.Trace(tp.DEV, 0, 1 << 32, 1, 1)
+        p3, cc3, f3 = t2.topk(tp._t(c), K)
+        t2.sync()
+        print("  fresh handle:", int(tp.u64(f3)[0]), tp.u64(p3)[:8], tp.u64(cc3)[:8], flush=True)
+        t2.close()
+        raise AssertionError(f"stress topk {i}")
 tr.close()
 print(f"topk: {n_topk} cases ok ({time.time() - t0:.0f} s)", flush=True)
 

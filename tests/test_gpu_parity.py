@@ -334,6 +334,27 @@ def test_topk_unaligned_tiny_and_k_above_p():
     tr.close()
 
 
+@pytest.mark.parametrize("P", [1000, 5000, 70_000, 1 << 20])
+def test_topk_small_arrays_few_ctas(P):
+    """Small count arrays run on few CTAs, so one CTA can hold every key of the selected
+    range: all counts equal (the whole array is the range), two values, sparse. Every K
+    against the oracle (a region overflow once sent the fast finish garbage)."""
+    rng = np.random.default_rng(P)
+    tr = pb.Trace(DEV, 0, 1 << 32, 1, 1)
+    cases = [np.full(P, 8, dtype=np.uint64), np.full(P, 1, dtype=np.uint64),
+             rng.integers(7, 9, size=P).astype(np.uint64)]
+    sparse = np.zeros(P, dtype=np.uint64)
+    sparse[rng.integers(0, P, 3000)] = 5
+    cases.append(sparse)
+    for i, counts in enumerate(cases):
+        for K in (1, 3, 1000, 4096, 5000):
+            p, c, f = tr.topk(_t(counts), K)
+            tr.sync()
+            rp, rc, rf = oracle.topk(counts, K)
+            assert int(u64(f)[0]) == rf and np.array_equal(u64(c), rc) and np.array_equal(u64(p), rp), (P, i, K)
+    tr.close()
+
+
 def test_topk_many_and_prefix():
     """pasta_topk_many: each list equals pasta_topk / the oracle for its own k (k above
     nnz and above P included, duplicates, 16 entries); pasta_topk_prefix of a merged list;
