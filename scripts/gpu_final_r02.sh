@@ -7,4 +7,4 @@ bash scripts/gpu_round2.sh $T
 PASTA_STREAM_DEFER_LAUNCH=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_kernel -c 1 \
   -o gpurun_out/${T}_stream_full python scripts/stream_ring_bench.py 536870912 524288:1024 > gpurun_out/${T}_stream_ncu.log 2>&1; echo ncu stream rc=$?
 python scripts/ncu_summary.py gpurun_out/${T}_stream_full.ncu-rep 25 > gpurun_out/${T}_stream_ncu_summary.txt 2>&1
-bash scripts/gpu_sanitize.sh $T
+# (compute-sanitizer is closed on this GPU pool since mid-round 2: scripts/gpu_sanitize.sh not run)
