@@ -108,6 +108,9 @@ constexpr int kSlice = 256;                 // records per slice (8 per lane)
 #ifndef PASTA_IL_DYNAMIC
 #define PASTA_IL_DYNAMIC 1  // interleaved schedule: chunks after the first taken from a global counter
 #endif
+#ifndef PASTA_IL_LOG_CHUNK_MIN
+#define PASTA_IL_LOG_CHUNK_MIN 6  // smallest chunk of the automatic interleaved schedule (>= 3)
+#endif
 #ifndef PASTA_IL_MIN_CHUNKS
 #define PASTA_IL_MIN_CHUNKS 4  // interleave only when every warp gets this many chunks (dynamic: rn50 +2.7 %)
 #endif
@@ -2234,7 +2237,12 @@ int scan_schedule(uint64_t nbody, int grid, uint32_t force, uint32_t A) {
   // a global-memory range table keeps its lookups cheap through each warp's locality:
   // medium launches stay contiguous there (S-manyranges: 0.78 contiguous vs 1.01 ms)
   const uint64_t min_chunks = scan_table_fits_smem(A) ? PASTA_IL_MIN_CHUNKS : 16;
-  return (PASTA_IL && (nsl >> PASTA_IL_LOG_CHUNK) >= nwarp * min_chunks) ? PASTA_IL_LOG_CHUNK : -1;
+  if (!PASTA_IL || (nsl >> PASTA_IL_LOG_CHUNK) < nwarp * min_chunks) return -1;
+  // medium launches: smaller chunks (down to 2^PASTA_IL_LOG_CHUNK_MIN slices) so that every
+  // warp still takes about 16, and the dynamic schedule's end spread (one chunk) shrinks
+  int lc = PASTA_IL_LOG_CHUNK;
+  while (lc > PASTA_IL_LOG_CHUNK_MIN && (nsl >> lc) < nwarp * 16) --lc;
+  return lc;
 }
 
 // [chunk map: 16 B per chunk | 256 B: the dynamic schedule's chunk counter at offset 0]
