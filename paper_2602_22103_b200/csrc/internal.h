@@ -38,6 +38,7 @@ struct ScanArgs {
   const ulonglong2* chunk_k; // [chunks] (k, koffs[k+1]) of each interleaved chunk's first record (scratch)
   int32_t log_ic;            // log2 slices per interleaved chunk, -1 = contiguous (scan_schedule)
   unsigned long long* chunk_ctr;  // interleaved: the dynamic schedule's chunk counter (scratch, reset by the pre-pass)
+  uint64_t chunk_perm;            // PASTA_IL_PERMUTE builds: a multiplier coprime with the dynamic chunk count - 1
   // tensor level (NEXT f3): all nullptr when off
   const uint32_t* tids;      // [A] tensor id of table interval r, kNoTensor = none
   uint64_t* tensor_counts;   // [max_tids]

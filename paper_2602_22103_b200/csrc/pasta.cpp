@@ -285,6 +285,13 @@ int scan_range(pasta_trace* h, const uint64_t* rec, uint64_t n, uint64_t g0, Sca
     if (a.log_ic >= 0) {  // the counter follows the chunk map (scan_scratch_bytes)
       const uint64_t nch = ((cnt + 255) / 256 + (1ull << a.log_ic) - 1) >> a.log_ic;
       a.chunk_ctr = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(h->d_scan) + 16 * nch);
+      // a multiplier near 0.618 (M - 1) coprime with M - 1, M = the dynamically handed-out chunks
+      const uint64_t nwarp = (uint64_t)grid * scan_warps();
+      const uint64_t m1 = nch > nwarp + 1 ? nch - nwarp - 1 : 1;
+      uint64_t mul = m1 * 618 / 1000 | 1;
+      auto gcd = [](uint64_t x, uint64_t y) { while (y) { const uint64_t t = x % y; x = y; y = t; } return x; };
+      while (m1 > 1 && gcd(mul, m1) != 1) ++mul;
+      a.chunk_perm = m1 > 1 ? mul : 1;
     }
     Timed t(h, PASTA_PH_SCAN, st);
     int nl = 0;

@@ -108,6 +108,9 @@ constexpr int kSlice = 256;                 // records per slice (8 per lane)
 #ifndef PASTA_IL_DYNAMIC
 #define PASTA_IL_DYNAMIC 1  // interleaved schedule: chunks after the first taken from a global counter
 #endif
+#ifndef PASTA_IL_PERMUTE
+#define PASTA_IL_PERMUTE 0  // A/B: dynamic chunks handed out in a permuted order
+#endif
 #ifndef PASTA_IL_LOG_CHUNK_MIN
 #define PASTA_IL_LOG_CHUNK_MIN 6  // smallest chunk of the automatic interleaved schedule (>= 3)
 #endif
@@ -958,7 +961,16 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
       const uint32_t m = j >> lc;
       uint32_t qn = 0;
       if (lane == 0) {
-        qn = nwarp + (uint32_t)atomicAdd(args.chunk_ctr, 1ull);
+        const uint64_t c = atomicAdd(args.chunk_ctr, 1ull);
+#if PASTA_IL_PERMUTE
+        // grab order permuted over the dynamic chunks except the trace's last one (always
+        // drawn last, so a warp's partial tail slice is its final slice): the last grabs
+        // land anywhere in the trace instead of on its final region
+        const uint64_t M1 = nch > nwarp + 1 ? (uint64_t)(nch - nwarp - 1) : 0;
+        qn = nwarp + (uint32_t)(c < M1 ? (c * args.chunk_perm) % M1 : c);
+#else
+        qn = nwarp + (uint32_t)c;
+#endif
         sts32_o(cid_u32 + 4u * ((m + 1u) & 1u), qn);
       }
       __syncwarp();

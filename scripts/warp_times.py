@@ -31,5 +31,9 @@ rel = (t - t[:, 0].min()) / 1000.0
 q = [0, 10, 50, 90, 99, 100]
 for i, name in enumerate(["start", "first data", "quarter", "end"]):
     print(f"{cfg} {name:10s} us pct{q}: {np.percentile(rel[:, i], q).round(1)}")
+# per-SM view: the last warp of each CTA (one CTA per SM) and the spread inside CTAs
+endc = rel[:, 3].reshape(-1, W)
+print(f"{cfg} per-CTA last end us pct{q}: {np.percentile(endc.max(1), q).round(1)}")
+print(f"{cfg} per-CTA (last - first end) us pct{q}: {np.percentile(endc.max(1) - endc.min(1), q).round(1)}")
 work = rel[:, 3] - rel[:, 1]
 print(f"{cfg} per-warp busy (end - first data) us pct{q}: {np.percentile(work, q).round(1)}")
