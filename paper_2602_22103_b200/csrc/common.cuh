@@ -3,6 +3,28 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Device-side bounds checks of a debug build (make variants VARIANTS="chk:-DPASTA_CHECKS=1"),
+// the stand-in for compute-sanitizer where it is not available: a failed check prints the
+// site and traps (the launch fails with an error, the process reports it).
+#ifndef PASTA_CHECKS
+#define PASTA_CHECKS 0
+#endif
+#if PASTA_CHECKS
+#include <cstdio>
+#define PASTA_DCHECK(cond)                                                                       \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("PASTA_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                                 \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define PASTA_DCHECK(cond) \
+  do {                     \
+  } while (0)
+#endif
+
 namespace pasta {
 namespace dev {
 

@@ -866,6 +866,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   // TMA for relative slice j into ring slot `slot` (lane 0 only)
   auto issue = [&](uint32_t j, uint32_t slot) {
     const uint32_t bytes = j < nfull ? kSliceBytes : tail_valid * 8u;
+    PASTA_DCHECK(slot < (uint32_t)stages && j < nmy && gsl(j) * kSlice * 8 + bytes <= args.nbody * 8);
     mbar_arrive_expect_tx_u32(bar_u32 + 8u * slot, bytes);
     tma_load_1d_u32(ring_u32 + slot * kSliceBytes, args.rec + gsl(j) * kSlice, bytes, bar_u32 + 8u * slot, pol);
   };
@@ -879,6 +880,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
     const uint32_t j = 2u * p;
     uint32_t bytes = j < nfull ? kSliceBytes : tail_valid * 8u;
     if (j + 1 < nmy) bytes += j + 1 < nfull ? kSliceBytes : tail_valid * 8u;
+    PASTA_DCHECK(s2 < S2 && j < nmy && gsl(j) * kSlice * 8 + bytes <= args.nbody * 8 &&
+                 (j + 1 >= nmy || gsl(j + 1) == gsl(j) + 1));
     mbar_arrive_expect_tx_u32(bar_u32 + 8u * s2, bytes);
     tma_load_1d_u32(ring_u32 + s2 * 2u * kSliceBytes, args.rec + gsl(j) * kSlice, bytes, bar_u32 + 8u * s2, pol);
   };
@@ -977,6 +980,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
       qn = __shfl_sync(kFull, qn, 0);
       const uint32_t qm = lds32_o(cid_u32 + 4u * (m & 1u));
       const bool more = qn < nch;
+      PASTA_DCHECK(qm < nch && (j & icm) == 0 && lc >= 3);
       nmy = j + clen(qm) + (more ? clen(qn) : 0u);
       tail_mine = (more ? qn : qm) + 1 == nch;
       nfull = (tail_mine && tail_valid != (uint32_t)kSlice) ? nmy - 1 : nmy;
@@ -1515,6 +1519,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
       if (kRows && t.kend != ~0ull && t.kend / kSlice < f) f = t.kend / kSlice;
       t.cf = f > t.cs ? (uint32_t)f : t.cs;
     }
+    PASTA_DCHECK(slot < (uint32_t)stages && sl < t.ce && r_lo < t.n && t.eidx < 8u && t.kl < t.nk);
     SlotTag tg;
     tg.G = t.G0 + sl;
     tg.krow = t.krow;
@@ -1533,6 +1538,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
     const ulonglong2 h0 = lds128_o(t_u32);  // rec | cs, cf
     const uint32_t cs = (uint32_t)h0.y;
     if (cs < (uint32_t)(h0.y >> 32)) {
+      PASTA_DCHECK(slot < (uint32_t)stages && cs < t.ce && (uint64_t)(cs + 1) * kSlice <= t.n && t.eidx < 8u);
       sts32_o(t_u32 + 8u, cs + 1);
       const ulonglong2 h1 = lds128_o(t_u32 + 16u);  // G0 | krow, eidx
       sts128_o(tag_u32 + 16u * slot, h1.x + cs, h1.y | ((uint64_t)kTagFast << 32));
@@ -1654,6 +1660,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) stream_kernel(const __grid_
       // a partial slice or one holding a kernel boundary: segments as the scan does
       const ChunkEntry e = ents[tg.meta & 7u];
       const uint64_t r_lo = (tg.G - e.G0) * kSlice;
+      PASTA_DCHECK(tg.G >= e.G0 && r_lo < e.n && tg.krow >= e.k0 && tg.krow - e.k0 < e.nk);
       const uint64_t left = e.n - r_lo;
       const uint32_t valid = left < (uint64_t)kSlice ? (uint32_t)left : (uint32_t)kSlice;
       uint32_t kl = tg.krow - e.k0;

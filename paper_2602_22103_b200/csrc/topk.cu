@@ -356,6 +356,7 @@ __device__ uint64_t tk_full_pass(const TkArgs& a, const Sel& s, int ps, unsigned
     __syncthreads();
     const uint64_t off = *sfill;
     if (mine <= a.rcap && off + mine <= kFastMax) {
+      PASTA_DCHECK((uint64_t)(blockIdx.x + 1) * a.rcap * 16 <= a.rcap * 16 * gridDim.x);
       const u128* region = a.buf + (uint64_t)blockIdx.x * a.rcap;
       for (uint64_t i = threadIdx.x; i < mine; i += kTB) a.compact[off + i] = region[i];
     }
@@ -730,6 +731,7 @@ __global__ void topk_prefix_kernel(const __grid_constant__ TopkPrefixTable t) {
   const uint64_t nt = (uint64_t)gridDim.x * blockDim.x, tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (uint32_t j = 0; j < t.count; ++j) {
     const TopkPrefix& e = t.e[j];
+    PASTA_DCHECK(t.count <= kMaxTopkPrefix);
     for (uint64_t i = tid; i < e.k; i += nt) {
       e.dst_page[i] = __ldg(t.src_page + i);
       e.dst_count[i] = __ldg(t.src_count + i);
