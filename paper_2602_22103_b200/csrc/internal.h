@@ -38,7 +38,7 @@ struct ScanArgs {
   const ulonglong2* chunk_k; // [chunks] (k, koffs[k+1]) of each interleaved chunk's first record (scratch)
   int32_t log_ic;            // log2 slices per interleaved chunk, -1 = contiguous (scan_schedule)
   unsigned long long* chunk_ctr;  // interleaved: the dynamic schedule's chunk counter (scratch, reset by the pre-pass)
-  uint64_t chunk_perm;            // PASTA_IL_PERMUTE builds: a multiplier coprime with the dynamic chunk count - 1
+  uint64_t chunk_perm;            // 0, or a multiplier coprime with (dynamic chunks - 1): permuted hand-out
   // tensor level (NEXT f3): all nullptr when off
   const uint32_t* tids;      // [A] tensor id of table interval r, kNoTensor = none
   uint64_t* tensor_counts;   // [max_tids]
@@ -122,6 +122,7 @@ int scan_warps();
 // interleaved chunk, or -1 for contiguous per-warp ranges; and the chunk map scratch.
 // force: 0 = automatic, else PASTA_SCHED_CONTIGUOUS / PASTA_SCHED_INTERLEAVED.
 int scan_schedule(uint64_t nbody, int grid, uint32_t force, uint32_t A);
+int scan_permute_below();  // chunks per warp under which the dynamic hand-out is permuted
 size_t scan_scratch_bytes(uint64_t nbody, int log_ic);
 
 cudaError_t launch_finalize_bitmap(const uint64_t* page_counts, uint64_t P, uint64_t* bitmap, uint64_t* unique_out,

@@ -108,8 +108,8 @@ constexpr int kSlice = 256;                 // records per slice (8 per lane)
 #ifndef PASTA_IL_DYNAMIC
 #define PASTA_IL_DYNAMIC 1  // interleaved schedule: chunks after the first taken from a global counter
 #endif
-#ifndef PASTA_IL_PERMUTE
-#define PASTA_IL_PERMUTE 0  // A/B: dynamic chunks handed out in a permuted order
+#ifndef PASTA_IL_PERMUTE_BELOW
+#define PASTA_IL_PERMUTE_BELOW 128  // permuted hand-out when warps take fewer chunks than this
 #endif
 #ifndef PASTA_IL_LOG_CHUNK_MIN
 #define PASTA_IL_LOG_CHUNK_MIN 6  // smallest chunk of the automatic interleaved schedule (>= 3)
@@ -965,15 +965,11 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
       uint32_t qn = 0;
       if (lane == 0) {
         const uint64_t c = atomicAdd(args.chunk_ctr, 1ull);
-#if PASTA_IL_PERMUTE
-        // grab order permuted over the dynamic chunks except the trace's last one (always
-        // drawn last, so a warp's partial tail slice is its final slice): the last grabs
-        // land anywhere in the trace instead of on its final region
+        // chunk_perm != 0: the grab order is permuted over the dynamic chunks except the
+        // trace's last one (always drawn last, so a warp's partial tail slice is its final
+        // slice): the last grabs land anywhere in the trace instead of on its final region
         const uint64_t M1 = nch > nwarp + 1 ? (uint64_t)(nch - nwarp - 1) : 0;
-        qn = nwarp + (uint32_t)(c < M1 ? (c * args.chunk_perm) % M1 : c);
-#else
-        qn = nwarp + (uint32_t)c;
-#endif
+        qn = nwarp + (uint32_t)(args.chunk_perm && c < M1 ? (c * args.chunk_perm) % M1 : c);
         sts32_o(cid_u32 + 4u * ((m + 1u) & 1u), qn);
       }
       __syncwarp();
@@ -2240,6 +2236,7 @@ cudaError_t launch_rich_variant(const RichArgs& a, int grid, cudaStream_t st) {
 }  // namespace
 
 int scan_warps() { return kWarps; }
+int scan_permute_below() { return PASTA_IL_PERMUTE_BELOW; }
 
 int scan_schedule(uint64_t nbody, int grid, uint32_t force, uint32_t A) {
   const uint64_t nsl = (nbody + kSlice - 1) / kSlice;
