@@ -105,10 +105,12 @@ typedef struct {
 } pasta_open_params;
 
 /* Scan schedule (pasta_open_params.flags). By default a launch over few records per
- * warp gives each warp one contiguous range of 2 KiB slices, and a long launch
- * (>= ~0.9e9 records on 148 SMs) interleaves chunks of 64 slices across warps so that
- * no warp straggles behind an expensive region of the trace. Results are identical
- * under every schedule; the flags force one (for tests and tuning). */
+ * warp gives each warp one contiguous range of 2 KiB slices, and a longer launch
+ * (>= ~0.23e9 records on 148 SMs; >= ~0.9e9 when the range table is too large for shared
+ * memory) hands out chunks of 64 slices dynamically: each warp's first chunk is fixed,
+ * later ones come from a device counter, so no warp straggles behind an expensive region
+ * of the trace. Results are identical under every schedule; the flags force one (for
+ * tests and tuning; forced interleaving uses chunks of 8-64 slices). */
 enum { PASTA_SCHED_CONTIGUOUS = 1u, PASTA_SCHED_INTERLEAVED = 2u };
 
 /* Input records. By default both arrays are DEVICE memory, read-only, never copied
