@@ -383,8 +383,9 @@ class Histograms:
     """Output arrays as int64 CUDA tensors (u64 bit patterns).
 
     ``packed`` = [page_counts (P) | alloc_counts (max_ids) | totals (9) | tensor_counts
-    (max_tensor_ids)] is one buffer, so the merge across ranks is one all_reduce(SUM)
-    (DESIGN.md section 5). Per-kernel arrays and the bitmap are separate tensors."""
+    (max_tensor_ids)] is one contiguous part, so the merge across ranks is one
+    all_reduce(SUM); it and every other output are views of one
+    zero-initialised arena (zero_() is one fill)."""
 
     def __init__(self, P: int, max_ids: int, device, n_kernels: int = 0, kernel_rows: bool = False,
                  kernel_pages: bool = False, bitmap: bool = True, pad_pages_to: int = 1, window_kernels: int = 0,
@@ -397,35 +398,45 @@ class Histograms:
         # the page part is padded with zero pages to a multiple of `pad_pages_to` so it
         # can be reduce-scattered in equal shards (dist.ShardedMerger)
         self.P_pad = (P + pad_pages_to - 1) // pad_pages_to * pad_pages_to
-        self.packed = torch.zeros(self.P_pad + max_ids + TOTALS + max_tensor_ids, dtype=torch.int64, device=device)
+        # every output lives in ONE zero-initialised arena (256-byte aligned parts), so a
+        # step's reset is one fill launch instead of one per array
+        sizes = {"packed": self.P_pad + max_ids + TOTALS + max_tensor_ids,
+                 "page_bitmap": self.words if bitmap else 0,
+                 "kernel_alloc_counts": n_kernels * max_ids if kernel_rows else 0,
+                 "kernel_stats": n_kernels * KSTATS if kernel_rows else 0,
+                 "kernel_tensor_counts": n_kernels * max_tensor_ids if (kernel_rows and max_tensor_ids) else 0,
+                 "kernel_tensor_footprint": n_kernels if (kernel_rows and max_tensor_ids) else 0,
+                 "kernel_page_bitmap": n_kernels * self.words if kernel_pages else 0}
+        self.window_kernels = window_kernels
+        self.n_windows = (n_kernels + window_kernels - 1) // window_kernels if window_kernels else 0
+        sizes["hotness"] = self.n_windows * P
+        offs, total = {}, 0
+        for name, n in sizes.items():
+            offs[name] = total
+            total += (n + 31) // 32 * 32
+        self.arena = torch.zeros(max(total, 1), dtype=torch.int64, device=device)
+
+        def part(name, present=True):
+            n = sizes[name]
+            return self.arena[offs[name]:offs[name] + n] if present else None
+
+        self.packed = part("packed")
         self.page_counts = self.packed[:P]
         self.pages_padded = self.packed[:self.P_pad]
         self.small = self.packed[self.P_pad:]  # [alloc_counts | totals | tensor_counts]
         self.alloc_counts = self.packed[self.P_pad:self.P_pad + max_ids]
         self.totals = self.packed[self.P_pad + max_ids:self.P_pad + max_ids + TOTALS]
         self.tensor_counts = self.packed[self.P_pad + max_ids + TOTALS:] if max_tensor_ids else None
-        self.page_bitmap = torch.zeros(self.words, dtype=torch.int64, device=device) if bitmap else None
-        self.kernel_alloc_counts = self.kernel_stats = self.kernel_page_bitmap = None
-        self.kernel_tensor_counts = self.kernel_tensor_footprint = None
-        if kernel_rows:
-            self.kernel_alloc_counts = torch.zeros(n_kernels * max_ids, dtype=torch.int64, device=device)
-            self.kernel_stats = torch.zeros(n_kernels * KSTATS, dtype=torch.int64, device=device)
-            if max_tensor_ids:
-                self.kernel_tensor_counts = torch.zeros(n_kernels * max_tensor_ids, dtype=torch.int64, device=device)
-                self.kernel_tensor_footprint = torch.zeros(n_kernels, dtype=torch.int64, device=device)
-        if kernel_pages:
-            self.kernel_page_bitmap = torch.zeros(n_kernels * self.words, dtype=torch.int64, device=device)
-        self.window_kernels = window_kernels
-        self.hotness = None
-        if window_kernels:
-            self.n_windows = (n_kernels + window_kernels - 1) // window_kernels
-            self.hotness = torch.zeros(self.n_windows * P, dtype=torch.int64, device=device)
+        self.page_bitmap = part("page_bitmap", bitmap)
+        self.kernel_alloc_counts = part("kernel_alloc_counts", kernel_rows)
+        self.kernel_stats = part("kernel_stats", kernel_rows)
+        self.kernel_tensor_counts = part("kernel_tensor_counts", kernel_rows and bool(max_tensor_ids))
+        self.kernel_tensor_footprint = part("kernel_tensor_footprint", kernel_rows and bool(max_tensor_ids))
+        self.kernel_page_bitmap = part("kernel_page_bitmap", kernel_pages)
+        self.hotness = part("hotness", bool(window_kernels))
 
     def zero_(self):
-        for t in (self.packed, self.page_bitmap, self.kernel_alloc_counts, self.kernel_stats,
-                  self.kernel_page_bitmap, self.hotness, self.kernel_tensor_counts, self.kernel_tensor_footprint):
-            if t is not None:
-                t.zero_()
+        self.arena.zero_()
         return self
 
     def struct(self, flags: int = 0) -> pasta_histograms:
