@@ -884,7 +884,10 @@ cudaError_t run_topk(const uint64_t* pc, uint64_t P, uint32_t k, uint64_t* out_p
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int g = sms * (coop_blocks < 2 ? coop_blocks : 2);
   // no more CTAs than the counts (or the sort) give work to
-  const uint64_t want = (P + 2ull * kTB * kTU - 1) / (2ull * kTB * kTU);
+#ifndef PASTA_TOPK_PER_CTA
+#define PASTA_TOPK_PER_CTA (2ull * kTB * kTU)  // counts per CTA below which fewer CTAs are launched
+#endif
+  const uint64_t want = (P + PASTA_TOPK_PER_CTA - 1) / PASTA_TOPK_PER_CTA;
   const uint64_t want_sort = a.kcap / kSortTile;
   uint64_t w = want > want_sort ? want : want_sort;
   if (w < 1) w = 1;
