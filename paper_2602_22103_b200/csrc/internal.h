@@ -16,6 +16,7 @@ struct ScanArgs {
   uint64_t nbody;            // even count of body records
   uint64_t gidx0;            // global record index of rec[0] (for kernel offsets)
   const uint64_t* bounds;    // [2A] sorted boundary array of the live ranges
+  uint32_t samp_n, samp_sh;  // global-memory table: samp_n samples bounds[i << samp_sh] in shared memory (0: none)
   const uint32_t* ids;       // [A] alloc id of live range r
   uint32_t A;                // live ranges
   uint32_t n_kernels;        // >= 1

@@ -108,6 +108,9 @@ constexpr int kSlice = 256;                 // records per slice (8 per lane)
 #ifndef PASTA_IL_DYNAMIC
 #define PASTA_IL_DYNAMIC 1  // interleaved schedule: chunks after the first taken from a global counter
 #endif
+#ifndef PASTA_BIG_SAMPLES
+#define PASTA_BIG_SAMPLES 1  // global range table: every 2^sh-th boundary sampled into shared memory
+#endif
 #ifndef PASTA_IL_PERMUTE_BELOW
 #define PASTA_IL_PERMUTE_BELOW 128  // permuted hand-out when warps take fewer chunks than this
 #endif
@@ -135,6 +138,10 @@ struct Ctx {
   uint32_t s;
   uint32_t A;
   const uint64_t* B;  // boundary array (shared or global)
+  // global table only: samples S[i] = B[i << sh] (i < nS) in shared memory narrow the
+  // search to 2^sh entries of B (nS = 0: plain search of B)
+  const uint64_t* S = nullptr;
+  uint32_t nS = 0, sh = 0;
 };
 
 struct Ival {           // one interval: [lo, lo + span]
@@ -180,7 +187,19 @@ template <bool kBig>
 __device__ __forceinline__ void own_lookup(OwnCache& oc, uint64_t a, const Ctx& c) {
   if (a - oc.olo > oc.ospan) {
     const uint32_t m = 2 * c.A;
-    const uint32_t cc = count_le<kBig>(c.B, m, a);
+    uint32_t cc;
+    if (kBig && c.nS) {
+      // B[(j - 1) << sh] <= a < B[j << sh]: the count lies in ((j - 1) << sh, j << sh]
+      const uint32_t j = count_le<false>(c.S, c.nS, a);
+      if (j == 0) {
+        cc = 0;
+      } else {
+        const uint32_t lo = (j - 1) << c.sh, hi = min(j << c.sh, m);
+        cc = lo + 1 + count_le<true>(c.B + lo + 1, hi - lo - 1, a);
+      }
+    } else {
+      cc = count_le<kBig>(c.B, m, a);
+    }
     const uint64_t olo = cc ? (kBig ? __ldg(c.B + cc - 1) : c.B[cc - 1]) : 0ull;
     const uint64_t olast = (cc == m) ? ~0ull : (kBig ? __ldg(c.B + cc) : c.B[cc]) - 1;
     oc.olo = olo;
@@ -845,6 +864,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   // the range table is only ever written by stream-ordered copies, never by a kernel
   if (!kBig)
     for (uint32_t i = threadIdx.x; i < 2 * A; i += kThreads) sB[i] = args.bounds[i];
+  else  // the global table's shared-memory samples (where the table would otherwise sit)
+    for (uint32_t i = threadIdx.x; i < args.samp_n; i += kThreads) sB[i] = args.bounds[(uint64_t)i << args.samp_sh];
   const bool cache = kPages == 0 && kCacheBits && cache_on;
   if (cache)
     for (uint32_t i = threadIdx.x; i + 1 <= kCacheSlots; i += kThreads) sts64(cache_base() + 8u * i, kCacheEmptySlot);
@@ -905,6 +926,11 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanArgs args, 
   c.s = args.page_shift;
   c.A = A;
   c.B = kBig ? args.bounds : sB;
+  if (kBig) {
+    c.S = sB;
+    c.nS = args.samp_n;
+    c.sh = args.samp_sh;
+  }
   Out o;
   o.page_counts = args.page_counts;
   o.alloc_counts = args.alloc_counts;
@@ -1217,7 +1243,17 @@ template <bool kBig, bool kRows, int kPages>
 cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
   const int cache_on = (kPages == 0 && cache_fits(a.A, kBig)) ? 1 : 0;
   const int stages = stages_for(a.A, kBig, cache_on ? kCacheBytes : 0);
-  const int smem = ring_bytes(stages) + kBarBytes + kLaBytes + kPfBytes + (kBig ? 0 : (int)(16ull * a.A)) +
+  ScanArgs b = a;
+  b.samp_n = b.samp_sh = 0;
+  if (kBig && PASTA_BIG_SAMPLES) {  // samples of the global table in the free shared memory
+    const long base = (long)ring_bytes(stages) + kBarBytes + kLaBytes + kPfBytes + (cache_on ? kCacheBytes : 0);
+    const uint64_t room = (uint64_t)((long)kSmemLimit - base) / 8, m = 2ull * a.A;
+    uint32_t sh = 3;
+    while (((m + (1ull << sh) - 1) >> sh) > room) ++sh;
+    b.samp_sh = sh;
+    b.samp_n = (uint32_t)((m + (1ull << sh) - 1) >> sh);
+  }
+  const int smem = ring_bytes(stages) + kBarBytes + kLaBytes + kPfBytes + (kBig ? 8 * (int)b.samp_n : (int)(16ull * a.A)) +
                    (cache_on ? kCacheBytes : 0);
   // paired 4 KiB copies need an even ring depth and (interleaved) chunks of >= 2 slices
   const bool pair = PASTA_TMA_PAIR && stages % 2 == 0 && a.log_ic != 0;
@@ -1240,7 +1276,7 @@ cudaError_t launch_variant(const ScanArgs& a, int grid, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = PASTA_PDL;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fn, a, stages, cache_on);
+  return cudaLaunchKernelEx(&cfg, fn, b, stages, cache_on);
 }
 
 // ------------------------------------------------------------------------------------
